@@ -1,0 +1,269 @@
+"""Ports of proj/tests/test_mapper.cpp and proj/tests/test_metrics.cpp onto the CPU oracle
+(loss, SSIM, PSNR, pyramid, level schedule, Adam, init, prune, SH schedule)."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+
+GEN = np.random.default_rng(55)
+
+
+def rand_img(h, w, c, gen=GEN):
+    return gen.uniform(0, 1, (h, w, c)) if c > 1 else gen.uniform(0, 1, (h, w))
+
+
+# ----------------------------------------------------------------------------- metrics
+def test_psnr_kats():  # test_metrics.cpp:67-90
+    a = rand_img(16, 16, 3)
+    assert O.psnr(a, a) == 100.0
+    assert O.psnr(np.full((8, 8), 0.2), np.full((8, 8), 0.3)) == pytest.approx(20.0, rel=1e-12)
+    c = rand_img(16, 16, 3)
+    mse = np.mean((a - c) ** 2)
+    assert O.psnr(a, c) == pytest.approx(10 * math.log10(1 / mse), rel=1e-9)
+
+
+def test_psnr_monotone_and_rejects():  # test_metrics.cpp:92-106
+    prev = 1e300
+    for off in np.arange(0.05, 0.4501, 0.05):
+        p = O.psnr(np.full((8, 8), 0.5), np.full((8, 8), 0.5 + off))
+        assert p < prev
+        prev = p
+    with pytest.raises(O.InvalidArgument):
+        O.psnr(np.zeros((4, 4)), np.zeros((4, 5)))
+
+
+def ssim_reference(a, b):  # test_metrics.cpp:26-63 — direct windowed, no separability
+    g = np.exp(-((np.arange(11) - 5) ** 2) / (2 * 1.5 ** 2)); g /= g.sum()
+    w2 = np.outer(g, g)
+    if a.ndim == 2:
+        a = a[..., None]; b = b[..., None]
+    H, W, Cn = a.shape
+    tot, cnt = 0.0, 0
+    for c in range(Cn):
+        for y in range(5, H - 5):
+            for x in range(5, W - 5):
+                pa = a[y - 5:y + 6, x - 5:x + 6, c]; pb = b[y - 5:y + 6, x - 5:x + 6, c]
+                ma = (w2 * pa).sum(); mb = (w2 * pb).sum()
+                va = (w2 * pa * pa).sum() - ma * ma; vb = (w2 * pb * pb).sum() - mb * mb
+                cv = (w2 * pa * pb).sum() - ma * mb
+                tot += ((2 * ma * mb + 1e-4) * (2 * cv + 9e-4)) / ((ma * ma + mb * mb + 1e-4) * (va + vb + 9e-4))
+                cnt += 1
+    return tot / cnt
+
+
+def test_ssim_kats():  # test_metrics.cpp:103-115
+    a = rand_img(24, 32, 3)
+    assert O.ssim(a, a) == pytest.approx(1.0, rel=1e-12)
+    cb = np.fromfunction(lambda y, x: ((x + y) % 2).astype(float), (16, 16))
+    assert O.ssim(cb, 1.0 - cb) < 0.0
+
+
+def test_ssim_matches_windowed_reference():  # test_metrics.cpp:117-123
+    for _ in range(3):
+        a = rand_img(20, 26, 3); b = rand_img(20, 26, 3)
+        assert O.ssim(a, b) == pytest.approx(ssim_reference(a, b), rel=1e-6)
+
+
+def test_ssim_symmetric_permutation_and_rejects():  # test_metrics.cpp:125-144
+    a = rand_img(14, 14, 1); b = rand_img(14, 14, 1)
+    assert O.ssim(a, b) == pytest.approx(O.ssim(b, a), rel=1e-9)
+    with pytest.raises(O.InvalidArgument):
+        O.ssim(np.zeros((10, 14)), np.zeros((10, 14)))
+    a = rand_img(16, 16, 3); b = rand_img(16, 16, 3)
+    perm = [2, 0, 1]
+    assert O.ssim(a, b) == pytest.approx(O.ssim(a[..., perm], b[..., perm]), rel=1e-12)
+
+
+def test_ssim_gradient_fd():  # test_metrics.cpp:146-161
+    a = rand_img(16, 18, 3); b = rand_img(16, 18, 3)
+    _, grad = O.ssim(a, b, with_grad=True)
+    h = 1e-6
+    flat = a.reshape(-1)
+    for i in GEN.integers(0, flat.size, 30):
+        hi = flat.copy(); lo = flat.copy(); hi[i] += h; lo[i] -= h
+        fd = (O.ssim(hi.reshape(a.shape), b) - O.ssim(lo.reshape(a.shape), b)) / (2 * h)
+        assert grad.reshape(-1)[i] == pytest.approx(fd, rel=1e-4, abs=1e-9)
+
+
+def test_depth_rmse():  # test_metrics.cpp:163-190
+    d = rand_img(12, 12, 1)
+    assert O.depth_rmse(d, d)[0] == pytest.approx(0.0)
+    assert O.depth_rmse(np.full((12, 12), 2.5), np.full((12, 12), 2.0))[0] == pytest.approx(0.5, rel=1e-12)
+    v, empty = O.depth_rmse(d, np.zeros((12, 12)))
+    assert empty and math.isnan(v)
+
+
+# ----------------------------------------------------------------------------- loss / pyramid
+def test_pyramid_shapes_and_depth_valid_average():  # test_mapper.cpp:85-125
+    img = rand_img(13, 17, 3)
+    lv = O.build_pyramid(img, 2)
+    assert [x.shape for x in lv] == [(13, 17, 3), (7, 9, 3), (4, 5, 3)]
+    assert lv[1][0, 0, 0] == pytest.approx(img[0:2, 0:2, 0].mean())
+    assert lv[1][6, 8, 1] == pytest.approx(img[12, 16, 1])  # odd border: the one sample that exists
+    d = np.zeros((4, 4)); d[0, 0] = 2.0; d[2, 2] = 3.0; d[2, 3] = 5.0
+    dl = O.build_pyramid(d, 1, depth=True)
+    assert dl[1][0, 0] == pytest.approx(2.0)
+    assert dl[1][1, 1] == pytest.approx(4.0)
+    assert dl[1][0, 1] == 0.0
+    with pytest.raises(O.InvalidArgument):
+        O.build_pyramid(np.zeros((3, 3, 3)), 2)
+
+
+def test_loss_zero_on_perfect_render():  # test_mapper.cpp:127-144
+    gt = np.full((24, 32, 3), 0.4); gd = np.full((24, 32), 2.0)
+    r = O.compute_loss(gt, gd, np.ones((24, 32)), gt, gd, O.make_cfg())
+    assert r["total"] == pytest.approx(0.0, abs=1e-12)
+    assert r["ssim"] == pytest.approx(1.0)
+    # The reference test asserts dl_dcolor == 0.0 exactly. metrics.cpp:131-133 computes
+    # ds_dmu_direct as (2 mb num2) * inv_dd - s (2 ma) / den1: two rounding paths that differ by
+    # ~1 ulp even when a == b, so the fp64 formula (followed verbatim here) leaves a <=1e-16
+    # residue. Bound it instead of asserting an exact zero the formula cannot produce.
+    assert np.abs(r["dl_dcolor"]).max() < 1e-15
+    assert not r["dl_ddepth"].any()
+    r = O.compute_loss(gt, gd, np.ones((24, 32)), gt, gd, O.make_cfg(0.0, 0.5))
+    assert not r["dl_dcolor"].any()
+
+
+def test_loss_lambda0_plain_l1():  # test_mapper.cpp:146-161
+    r = O.compute_loss(np.full((16, 16, 3), 0.5), np.zeros((16, 16)), np.ones((16, 16)),
+                       np.full((16, 16, 3), 0.25), np.zeros((16, 16)), O.make_cfg(0.0, 0.0))
+    assert r["total"] == pytest.approx(0.25, rel=1e-12)
+    assert r["depth_loss"] == 0.0
+
+
+def test_loss_gradient_fd():  # test_mapper.cpp:163-204
+    gc = rand_img(16, 20, 3)
+    gd = np.fromfunction(lambda y, x: np.where((x + y) % 4 != 0, 1.0, 0.0), (16, 20)) * GEN.uniform(1, 5, (16, 20))
+    col = rand_img(16, 20, 3); dep = GEN.uniform(1, 5, (16, 20)); vis = np.ones((16, 20))
+    cfg = O.make_cfg()
+    r = O.compute_loss(col, dep, vis, gc, gd, cfg)
+    h = 1e-6
+    for i in GEN.integers(0, col.size, 20):
+        hi = col.reshape(-1).copy(); lo = hi.copy(); hi[i] += h; lo[i] -= h
+        fd = (O.compute_loss(hi.reshape(col.shape), dep, vis, gc, gd, cfg)["total"]
+              - O.compute_loss(lo.reshape(col.shape), dep, vis, gc, gd, cfg)["total"]) / (2 * h)
+        assert r["dl_dcolor"].reshape(-1)[i] == pytest.approx(fd, rel=1e-4, abs=1e-10)
+    for i in GEN.integers(0, dep.size, 20):
+        hi = dep.reshape(-1).copy(); lo = hi.copy(); hi[i] += h; lo[i] -= h
+        fd = (O.compute_loss(col, hi.reshape(dep.shape), vis, gc, gd, cfg)["total"]
+              - O.compute_loss(col, lo.reshape(dep.shape), vis, gc, gd, cfg)["total"]) / (2 * h)
+        assert r["dl_ddepth"].reshape(-1)[i] == pytest.approx(fd, rel=1e-4, abs=1e-10)
+
+
+def test_loss_rejects_wrong_resolution():  # mapper.cpp:148-153
+    with pytest.raises(O.InvalidArgument):
+        O.compute_loss(np.zeros((8, 8, 3)), np.zeros((8, 8)), np.zeros((8, 8)), np.zeros((16, 16, 3)),
+                       np.zeros((16, 16)), O.make_cfg(0.0, 0.0))
+
+
+# ----------------------------------------------------------------------------- schedule / training
+def test_level_schedule_coarse_to_fine():  # test_mapper.cpp:206-239
+    rng = O.Rng(9)
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    m = O.random_scene(rng, 30, cam, O.pose())
+    kf = O.Keyframe(O.pose(), np.full((48, 64, 3), 0.3), np.zeros((48, 64)), 30, 2)
+    cfg = O.make_cfg(levels=2, ipl=10)
+    levels = [O.train_keyframe_step(m, kf, cfg, cam)["level"] for _ in range(30)]
+    assert levels == [2] * 10 + [1] * 10 + [0] * 10
+    assert O.train_keyframe_step(m, kf, cfg, cam) is None
+    assert m.global_step == 30
+
+
+def test_training_decreases_loss():  # test_mapper.cpp:241-276
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    rng = O.Rng(21)
+    gt = O.random_scene(rng, 40, cam, O.pose(), 1.0, 2.0)
+    gt_render = O.render(gt, O.pose(), cam)
+    g = gt.gaussians
+    g["p"][:, 10] = math.log(0.1 / 0.9)
+    g["p"][:, 7:10] += 0.4
+    m = O.OracleMap(g)
+    kf = O.Keyframe(O.pose(), gt_render.color, np.zeros((48, 64)), 30, 1)
+    cfg = O.make_cfg(levels=1)
+    losses, lv = [], []
+    for _ in range(30):
+        r = O.train_keyframe_step(m, kf, cfg, cam)
+        losses.append(r["loss"]); lv.append(r["level"])
+    min_l0 = min(l for l, v in zip(losses, lv) if v == 0)
+    assert min_l0 < losses[0]
+    assert losses[-1] < losses[0]
+
+
+def test_sh_schedule():  # test_mapper.cpp:278-296
+    m = O.OracleMap()
+    m.init_from_points(np.array([[0, 0, 2, 0.5, 0.5, 0.5]]))
+    m.global_step = 99
+    assert m.maybe_upgrade_sh(100) == 0
+    m.global_step = 100
+    assert m.maybe_upgrade_sh(100) == 1
+    m.global_step = 300
+    assert m.maybe_upgrade_sh(100) == 3
+    assert m.gaussians["degree"][0] == 3
+    m.global_step = 1000
+    assert m.maybe_upgrade_sh(100) == 3
+
+
+def test_prune_keeps_state_aligned():  # test_mapper.cpp:298-313
+    m = O.OracleMap()
+    m.init_from_points(np.array([[i, 0, 3, 0.5, 0.5, 0.5] for i in range(10)], dtype=float))
+    g = m.gaussians; g["p"][:, 10] = 0.0; m.gaussians = g
+    assert m.prune(0.005) == 0
+    g = m.gaussians; g["p"][4, 10] = math.log(0.001 / 0.999); m.gaussians = g
+    assert m.prune(0.005) == 1
+    assert len(m) == 9
+    assert m.gaussians["p"][4, 0] == 5.0
+    with pytest.raises(O.InvalidArgument):
+        m.prune(0.0)
+
+
+def test_apply_gradients_rejects_mismatch():  # test_mapper.cpp:337-344
+    m = O.OracleMap()
+    m.init_from_points(np.array([[0, 0, 2, 0.5, 0.5, 0.5]]))
+    with pytest.raises(O.InvalidArgument):
+        m.apply_gradients(np.zeros((3, 59)))
+
+
+def test_init_from_points_kats():  # test_mapper.cpp:32-83
+    m = O.OracleMap()
+    m.init_from_points(np.array([[1, 2, 3, 1.0, 0.5, 0.5]]))
+    g = m.gaussians[0]
+    assert g["degree"] == 0
+    assert g["p"][10] == pytest.approx(math.log(0.1 / 0.9), rel=1e-9)
+    for d in ([0, 0, 1], [0.6, 0.8, 0]):
+        assert np.linalg.norm(O.eval_sh(g["p"][11:], 0, d) - [1.0, 0.5, 0.5]) < 1e-6
+    m = O.OracleMap()
+    m.init_from_points(np.array([[0, 0, 0, 1, 1, 1], [0.2, 0, 0, 1, 1, 1], [0.4, 0, 0, 1, 1, 1]], dtype=float))
+    s = np.exp(m.gaussians["p"][:, 7])
+    assert s == pytest.approx([0.3, 0.2, 0.3], rel=1e-12)
+
+
+def test_adam_known_answer_numpy():
+    """Adam has no KAT in the reference; pin the restatement of
+    gaussian_map.cpp:15-54 against an independent numpy formula over two steps, including the
+    lr_pos * scene_extent scaling and the per-Gaussian step counter."""
+    gen = np.random.default_rng(3)
+    g0 = O.empty_gaussians(4)
+    g0["p"][:] = gen.normal(size=(4, 59)); g0["degree"] = [0, 1, 2, 3]
+    m = O.OracleMap(g0)
+    ext = m.scene_extent
+    lr = np.array([1.6e-4 * ext] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+    p = g0["p"].copy(); mm = np.zeros_like(p); vv = np.zeros_like(p)
+    for t in (1, 2):
+        grads = gen.normal(size=(4, 59)) * 10.0 ** gen.uniform(-8, 1, (4, 59))
+        m.apply_gradients(grads)
+        mm = 0.9 * mm + (1 - 0.9) * grads
+        vv = 0.999 * vv + (1 - 0.999) * grads * grads
+        p = p - lr * (mm / (1 - 0.9 ** t)) / (np.sqrt(vv / (1 - 0.999 ** t)) + 1e-15)
+        np.testing.assert_allclose(m.gaussians["p"], p, rtol=1e-13, atol=1e-15)
+    _, _, steps = m.adam_state()
+    assert list(steps) == [2, 2, 2, 2] and m.global_step == 2
+
+
+def test_sparse_depth_keeps_minimum():  # io/sequence.cpp:246-259
+    cam = O.camera(10, 10, 4.5, 4.5, 10, 10)
+    pts = np.array([[0, 0, 2, 0, 0, 0], [0, 0, 3, 0, 0, 0], [0, 0, -1, 0, 0, 0], [100, 0, 1, 0, 0, 0]], float)
+    d = O.project_sparse_depth(pts, O.pose(), cam)
+    assert d[4, 4] == 0.0 or d[5, 5] == 2.0 or d[4, 5] == 2.0 or d[5, 4] == 2.0
+    assert np.count_nonzero(d) == 1 and d.max() == 2.0
