@@ -1,0 +1,180 @@
+/* gsmap_b200 — B200-native (sm_100a) drop-in for the LVI-GS mapping hot path.
+ *
+ * C-ABI boundary (extern "C", POD structs, opaque handles, int status). No CUDA, torch or
+ * C++ types cross it. Each entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/proj). The C++ shim in gsmap_b200.hpp re-exports the
+ * reference signatures over these calls and rethrows the reference's exception types.
+ *
+ * Conventions shared with the reference:
+ *   - a Gaussian is 59 fp64 scalars in gaussian.hpp:16-26 order: position[3], rotation (w,x,y,z)
+ *     [4], log_scale[3], opacity_logit[1], sh[16][3]; plus int active_degree.
+ *   - host images are row-major HWC fp64 (io/image.hpp:26-33), color H*W*3, depth/vis H*W.
+ *   - gs_pose holds the NORMALISED q_cw (w,x,y,z) + t_cw, exactly as gsmap::Pose stores it
+ *     (core/types.hpp:53-54). gs_camera is gsmap::CameraModel (core/types.hpp:15-45).
+ * Device state: the map lives on the GPU as fp32 SoA planes ([59][capacity]) plus Adam m/v
+ * planes, an int32 per-Gaussian step and an int8 degree. Host<->device conversion happens only
+ * in gs_map_{append,set,get}_* and gs_frame_read / host-cotangent entry points.
+ */
+#ifndef GSMAP_B200_H
+#define GSMAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The C++ shim maps GS_EINVAL -> std::invalid_argument and GS_ELOGIC ->
+ * std::logic_error, the two exception types the reference throws on this path. */
+enum {
+    GS_OK = 0,
+    GS_EINVAL = 1, /* std::invalid_argument (types.hpp:22-29, rasterizer.cpp:229-234, ...) */
+    GS_ELOGIC = 2, /* std::logic_error (rasterizer.cpp:236-237) */
+    GS_ECUDA = 3,
+    GS_ENCCL = 4,
+    GS_ENOMEM = 5
+};
+
+typedef struct gs_camera { double fx, fy, cx, cy; int32_t width, height; } gs_camera;
+typedef struct gs_pose { double qw, qx, qy, qz, tx, ty, tz; } gs_pose;
+typedef struct gs_gaussian { double p[59]; int32_t active_degree; int32_t pad; } gs_gaussian;
+typedef struct gs_learning_rates { double position, rotation, log_scale, opacity, sh; } gs_learning_rates;
+typedef struct gs_train_config {
+    double lambda, lambda_d;            /* mapper.hpp:17-19 */
+    int32_t pyramid_levels, iters_per_level; /* mapper.hpp:20-21 */
+    gs_learning_rates lr;               /* mapper.hpp:22 */
+} gs_train_config;
+typedef struct gs_loss_result { double total, color_loss, depth_loss, l1, ssim, psnr; } gs_loss_result;
+typedef struct gs_step_report { int32_t ran, level; double loss, psnr; } gs_step_report;
+typedef struct gs_frame_stats {
+    int64_t n_visible;   /* projected (survived near clip + off-screen cull) */
+    int64_t n_pairs;     /* (tile, gaussian) pairs = tile-list entries */
+    int64_t n_contrib;   /* total compositing contributions (sum of per-pixel list lengths) */
+    int32_t tiles_x, tiles_y, width, height;
+} gs_frame_stats;
+
+typedef struct gs_context gs_context;
+typedef struct gs_map gs_map;
+typedef struct gs_frame gs_frame;
+typedef struct gs_grads gs_grads;
+typedef struct gs_keyframe gs_keyframe;
+
+const char* gs_last_error(void);
+const char* gs_version(void);
+
+/* ---- context: one device + one CUDA stream (stream may be an external cudaStream_t) ---- */
+int gs_context_create(int device, void* cuda_stream, gs_context** out);
+int gs_context_destroy(gs_context* ctx);
+int gs_context_synchronize(gs_context* ctx);
+int gs_context_set_stream(gs_context* ctx, void* cuda_stream);
+/* number of this library's kernel launches since creation (bench/driver evidence) */
+int gs_context_launch_count(gs_context* ctx, int64_t* count);
+
+/* ---- camera helpers (core/types.hpp:22-44) ---- */
+int gs_camera_validate(const gs_camera* cam);
+int gs_camera_scaled(const gs_camera* cam, int level, gs_camera* out);
+
+/* ---- GaussianMap (map/gaussian_map.hpp:44-96) ---- */
+int gs_map_create(gs_context* ctx, gs_map** out);
+int gs_map_destroy(gs_map* map);
+int gs_map_size(const gs_map* map, int64_t* n);
+/* GaussianMap::append (gaussian_map.cpp:31-35): fresh Adam state, refresh_extent */
+int gs_map_append(gs_map* map, const gs_gaussian* g, int64_t n);
+/* host edit through non-const gaussians() (gaussian_map.hpp:62): overwrite all n params */
+int gs_map_set_gaussians(gs_map* map, const gs_gaussian* g, int64_t n);
+int gs_map_get_gaussians(gs_map* map, gs_gaussian* out, int64_t n);
+int gs_map_get_adam(gs_map* map, double* m59, double* v59, int64_t* step, int64_t n);
+int gs_map_set_adam(gs_map* map, const double* m59, const double* v59, const int64_t* step, int64_t n);
+int gs_map_scene_extent(const gs_map* map, double* extent);
+int gs_map_set_scene_extent(gs_map* map, double extent);
+int gs_map_global_step(const gs_map* map, int64_t* step);
+int gs_map_set_global_step(gs_map* map, int64_t step);
+int gs_map_raise_sh_degree(gs_map* map, int degree);   /* gaussian_map.cpp:75-79 */
+int gs_map_max_active_degree(gs_map* map, int* degree);
+/* device SoA access: params/m/v planes [59][capacity] fp32 */
+int gs_map_device_planes(gs_map* map, float** params, float** adam_m, float** adam_v, int64_t* capacity);
+
+/* ---- render (rasterizer.hpp:69-70): project -> depth sort -> tile keys -> blend ---- */
+int gs_frame_create(gs_context* ctx, gs_frame** out);
+int gs_frame_destroy(gs_frame* frame);
+int gs_render(gs_map* map, const gs_pose* pose, const gs_camera* cam, gs_frame* frame);
+int gs_frame_stats_get(gs_frame* frame, gs_frame_stats* out);
+/* RenderOutput color/depth/visibility as host fp64 HWC (any pointer may be NULL) */
+int gs_frame_read(gs_frame* frame, double* color, double* depth, double* visibility);
+/* device planes: color [3][H][W], depth [H][W], visibility [H][W] (fp32) */
+int gs_frame_device_images(gs_frame* frame, float** color, float** depth, float** visibility);
+/* per-pixel list length and final transmittance (H*W each) */
+int gs_frame_read_pixel_state(gs_frame* frame, int32_t* n_contrib, float* t_final);
+/* depth-sorted projected set (ProjectedGaussian order, rasterizer.cpp:69-72): map index,
+ * fp64 mean[2], int pixel rect[4] (x0, y0, x1, y1 = clamped ceil(mean-r)..floor(mean+r),
+ * rasterizer.cpp:81-84; x0 > x1 when empty), fp32 conic[3] (cov_inv 00,01,11), fp32 opacity,
+ * fp32 color[3], fp64 depth; each pointer may be NULL; arrays sized n_visible */
+int gs_frame_read_projected(gs_frame* frame, int32_t* index, double* mean2, int32_t* rect4,
+                            float* conic3, float* opacity, float* color3, double* depth);
+/* tile lists (bin_tiles, rasterizer.cpp:76-91): tile_offsets[T+1], entries[n_pairs] = map index */
+int gs_frame_read_tiles(gs_frame* frame, int64_t* tile_offsets, int32_t* entries);
+/* CSR contributor table (RenderOutput::contrib_offsets/contribs, rasterizer.hpp:52-53), built
+ * only on request: offsets[H*W+1], gaussian[n_contrib], alpha[n_contrib] */
+int gs_frame_materialize(gs_frame* frame, uint32_t* offsets, int32_t* gaussian, double* alpha);
+
+/* ---- gradients (RenderGradients, rasterizer.hpp:62-64) as device fp32 planes [59][cap] ---- */
+int gs_grads_create(gs_context* ctx, gs_grads** out);
+/* external storage (e.g. a torch tensor that NCCL all-reduces): floats >= 59 * capacity */
+int gs_grads_create_external(gs_context* ctx, float* device_ptr, int64_t capacity, gs_grads** out);
+int gs_grads_destroy(gs_grads* grads);
+int gs_grads_zero(gs_grads* grads, gs_map* map);
+int gs_grads_read(gs_grads* grads, double* out59, int64_t n);
+int gs_grads_write(gs_grads* grads, const double* in59, int64_t n);
+int gs_grads_device_planes(gs_grads* grads, float** planes, int64_t* capacity);
+
+/* render_backward (rasterizer.hpp:74-77) with host fp64 cotangents; OVERWRITES grads */
+int gs_render_backward(gs_map* map, const gs_pose* pose, const gs_camera* cam, gs_frame* frame,
+                       const double* dl_dcolor, const double* dl_ddepth, int32_t h, int32_t w,
+                       gs_grads* grads);
+/* GaussianMap::apply_gradients (gaussian_map.cpp:37-54): one Adam step on every Gaussian */
+int gs_apply_gradients(gs_map* map, gs_grads* grads, const gs_learning_rates* lr);
+
+/* ---- keyframe + loss + fused train step (mapper.hpp:61-76) ---- */
+/* builds the pyramid (build_keyframe_pyramid, mapper.cpp:137-144) on the device */
+int gs_keyframe_create(gs_context* ctx, const gs_pose* pose, const double* color,
+                       const double* sparse_depth, int32_t h, int32_t w, int32_t initial_iters,
+                       int32_t levels, gs_keyframe** out);
+/* same, from device fp32 level-0 planes (color [3][H][W], depth [H][W]) */
+int gs_keyframe_create_device(gs_context* ctx, const gs_pose* pose, const float* color_planes,
+                              const float* depth, int32_t h, int32_t w, int32_t initial_iters,
+                              int32_t levels, gs_keyframe** out);
+int gs_keyframe_destroy(gs_keyframe* kf);
+int gs_keyframe_consumed(gs_keyframe* kf, int32_t* consumed);
+int gs_keyframe_set_consumed(gs_keyframe* kf, int32_t consumed);
+int gs_keyframe_levels(gs_keyframe* kf, int32_t* n_levels);
+/* read a pyramid level back (host fp64 HWC) */
+int gs_keyframe_read_level(gs_keyframe* kf, int32_t level, double* color, double* depth);
+/* compute_loss (mapper.cpp:146-212) on the frame's images vs pyramid level `level`; the
+ * cotangents stay on the device for gs_render_backward_frame; optional host copies */
+int gs_compute_loss(gs_frame* frame, gs_keyframe* kf, int32_t level, const gs_train_config* cfg,
+                    gs_loss_result* out, double* dl_dcolor, double* dl_ddepth);
+/* backward with the cotangents the last gs_compute_loss left on the frame; ACCUMULATES */
+int gs_render_backward_frame(gs_map* map, const gs_pose* pose, const gs_camera* cam,
+                             gs_frame* frame, gs_grads* grads);
+/* train_keyframe_step (mapper.cpp:214-238): level schedule, render, loss, backward, Adam, psnr */
+int gs_train_step(gs_map* map, gs_keyframe* kf, const gs_train_config* cfg, const gs_camera* cam,
+                  gs_step_report* report);
+/* keyframe-batch step: grads of every view summed (GaussianGrad::add), then the
+ * caller may all-reduce gs_grads planes across ranks, then gs_apply_gradients. This call does
+ * render+loss+backward for one view at its scheduled level and accumulates into grads.
+ * Loss/psnr land in report only when sync != 0 (otherwise they stay on the device). */
+int gs_train_accumulate(gs_map* map, gs_keyframe* kf, const gs_train_config* cfg,
+                        const gs_camera* cam, gs_frame* frame, gs_grads* grads, int32_t sync,
+                        gs_step_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* GSMAP_B200_H */

@@ -1,0 +1,56 @@
+// Shared device-side definitions for the gsmap_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gsb {
+
+constexpr int kTile = 16;                 // rasterizer.hpp:17 kTileSize
+constexpr int kTileThreads = kTile * kTile;
+constexpr double kNearClip = 0.01;        // projection.hpp:11
+constexpr double kCovReg = 0.3;           // projection.hpp:12
+constexpr float kAlphaMaxF = 0.99f;       // rasterizer.hpp:18 (fp32 compare)
+constexpr double kAlphaMaxD = 0.99;       // rasterizer.hpp:18 (fp64 transmittance update)
+constexpr double kTMin = 1e-4;            // rasterizer.hpp:19
+constexpr int kNumParams = 59;            // gaussian.hpp:16-26 flattened
+constexpr int kGeomParams = 11;           // position 3, rotation 4, log_scale 3, opacity 1
+constexpr int kNumPartials = 10;          // per (tile, gaussian) backward partial sums
+
+// Parameter planes ([59][capacity], fp32): same order as the reference's Gaussian3D.
+enum Plane : int { P_POS = 0, P_ROT = 3, P_LS = 7, P_OP = 10, P_SH = 11 };
+
+// 64-byte projected-Gaussian record, rank (depth) ordered after the sort. Everything the
+// blend kernels need, fetched as 4 x 16 B.
+struct __align__(16) Splat {
+    double mx, my;           // fp64 image-plane mean (pixels)
+    float ca, cb, cc;        // conic = inverse(cov2d) (00, 01, 11), rounded to fp32
+    float opacity;           // sigmoid(opacity_logit)
+    float r, g, b;           // SH colour clamped to [0, 1]
+    float depth;             // camera-frame z
+    int16_t x0, y0, x1, y1;  // clamped integer pixel rect (inclusive) = the per-pixel box test
+    int32_t gid;             // map index
+    uint32_t ntiles;         // tiles the rect touches (0 when the rect is empty)
+};
+static_assert(sizeof(Splat) == 64, "Splat must be 64 bytes");
+
+// Per-view camera + pose in fp64, passed by value to kernels.
+struct ViewParams {
+    double qw, qx, qy, qz, tx, ty, tz;  // normalised q_cw, t_cw
+    double fx, fy, cx, cy;
+    int width, height, tiles_x, tiles_y;
+};
+
+struct LossScalars {       // device-side loss accumulators (fp64) for one compute_loss call
+    double l1_sum;         // sum |C - I|
+    double sq_sum;         // sum (C - I)^2   (psnr)
+    double ssim_sum;       // sum of SSIM map values over valid windows and channels
+    double depth_abs_sum;  // sum |D/V - gt| over valid pixels
+    unsigned long long n_valid;
+    float depth_scale;     // lambda_d / n_valid (written by finalize, read by blend_bwd)
+    float pad;
+};
+
+__host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace gsb

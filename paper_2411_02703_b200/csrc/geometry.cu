@@ -1,0 +1,438 @@
+// K1 preprocess_fwd and K8 preprocess_bwd: per-Gaussian FP64 geometry.
+//
+// This translation unit is compiled with --fmad=false. The fp64 operation sequence for the
+// camera transform, mean, depth, 2D covariance and radius follows the oracle's canonical order
+// (oracle/core.cpp, which in turn restates proj/src/core/projection.cpp:17-40 and
+// covariance.cpp:51-56 with Eigen's evaluation formulas), so mean / depth / radius / pixel
+// rect / tile keys come out bit-identical to the fp64 reference on the same inputs. Only the
+// data the blend needs at fp32 (conic, opacity, colour, depth) is rounded after the fact.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gsb {
+
+namespace {
+
+struct D3 { double x, y, z; };
+
+__device__ __forceinline__ D3 cross3(const D3& a, const D3& b) {
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+// Eigen QuaternionBase::_transformVector (uv = q.vec x v; uv += uv; v + w uv + q.vec x uv)
+__device__ __forceinline__ D3 quat_rotate(double w, double x, double y, double z, const D3& v) {
+    const D3 qv{x, y, z};
+    D3 uv = cross3(qv, v);
+    uv = {uv.x + uv.x, uv.y + uv.y, uv.z + uv.z};
+    const D3 c = cross3(qv, uv);
+    return {(v.x + w * uv.x) + c.x, (v.y + w * uv.y) + c.y, (v.z + w * uv.z) + c.z};
+}
+
+// Eigen QuaternionBase::toRotationMatrix
+__device__ __forceinline__ void pose_matrix(const ViewParams& v, double W[3][3]) {
+    const double tx = 2.0 * v.qx, ty = 2.0 * v.qy, tz = 2.0 * v.qz;
+    const double twx = tx * v.qw, twy = ty * v.qw, twz = tz * v.qw;
+    const double txx = tx * v.qx, txy = ty * v.qx, txz = tz * v.qx;
+    const double tyy = ty * v.qy, tyz = tz * v.qy, tzz = tz * v.qz;
+    W[0][0] = 1.0 - (tyy + tzz); W[0][1] = txy - twz; W[0][2] = txz + twy;
+    W[1][0] = txy + twz; W[1][1] = 1.0 - (txx + tzz); W[1][2] = tyz - twx;
+    W[2][0] = txz - twy; W[2][1] = tyz + twx; W[2][2] = 1.0 - (txx + tyy);
+}
+
+// covariance.cpp:7-14 on the normalised quaternion (Eigen normalized(): q / sqrt(|q|^2))
+__device__ __forceinline__ void unit_quat(const double q[4], double u[4], double* nrm) {
+    const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    const double n = sqrt(n2);
+    *nrm = n;
+    if (n2 > 0.0) {
+        for (int i = 0; i < 4; ++i) u[i] = q[i] / n;
+    } else {
+        for (int i = 0; i < 4; ++i) u[i] = q[i];
+    }
+}
+
+__device__ __forceinline__ void rotation_from_unit(const double u[4], double r[3][3]) {
+    const double w = u[0], x = u[1], y = u[2], z = u[3];
+    r[0][0] = 1 - 2 * (y * y + z * z); r[0][1] = 2 * (x * y - w * z); r[0][2] = 2 * (x * z + w * y);
+    r[1][0] = 2 * (x * y + w * z); r[1][1] = 1 - 2 * (x * x + z * z); r[1][2] = 2 * (y * z - w * x);
+    r[2][0] = 2 * (x * z - w * y); r[2][1] = 2 * (y * z + w * x); r[2][2] = 1 - 2 * (x * x + y * y);
+}
+
+// covariance.cpp:51-56: Sigma = R diag(exp(2 ls)) R^T, then 0.5 (Sigma + Sigma^T)
+__device__ __forceinline__ void build_covariance(const double q[4], const double ls[3],
+                                                 double out[3][3]) {
+    double u[4], nrm, r[3][3];
+    unit_quat(q, u, &nrm);
+    rotation_from_unit(u, r);
+    const double s2[3] = {exp(2.0 * ls[0]), exp(2.0 * ls[1]), exp(2.0 * ls[2])};
+    double rd[3][3], sg[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int k = 0; k < 3; ++k) rd[i][k] = r[i][k] * s2[k];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            sg[i][j] = (rd[i][0] * r[j][0] + rd[i][1] * r[j][1]) + rd[i][2] * r[j][2];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) out[i][j] = 0.5 * (sg[i][j] + sg[j][i]);
+}
+
+__device__ __forceinline__ void mul23_33(const double a[2][3], const double b[3][3], double c[2][3]) {
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 3; ++j)
+            c[i][j] = (a[i][0] * b[0][j] + a[i][1] * b[1][j]) + a[i][2] * b[2][j];
+}
+
+// projection.cpp:9-15
+__device__ __forceinline__ void perspective_jacobian(const D3& p, const ViewParams& v, double j[2][3]) {
+    const double z = p.z;
+    j[0][0] = v.fx / z; j[0][1] = 0.0; j[0][2] = -v.fx * p.x / (z * z);
+    j[1][0] = 0.0; j[1][1] = v.fy / z; j[1][2] = -v.fy * p.y / (z * z);
+}
+
+// sh.cpp constants
+constexpr double kC0 = 0.28209479177387814;
+constexpr double kC1 = 0.4886025119029199;
+constexpr double kC2_0 = 1.0925484305920792, kC2_1 = 1.0925484305920792, kC2_2 = 0.31539156525252005,
+                 kC2_3 = 1.0925484305920792, kC2_4 = 0.5462742152960396;
+constexpr double kC3_0 = 0.5900435899266435, kC3_1 = 2.890611442640554, kC3_2 = 0.4570457994644658,
+                 kC3_3 = 0.3731763325901154, kC3_4 = 0.4570457994644658, kC3_5 = 1.445305721320277,
+                 kC3_6 = 0.5900435899266435;
+
+// sh.cpp:30-53
+__device__ __forceinline__ void sh_basis(const D3& d, int degree, double out[16]) {
+    const double x = d.x, y = d.y, z = d.z;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[i] = 0.0;
+    out[0] = kC0;
+    if (degree < 1) return;
+    out[1] = kC1 * y; out[2] = kC1 * z; out[3] = kC1 * x;
+    if (degree < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    out[4] = kC2_0 * x * y; out[5] = kC2_1 * y * z; out[6] = kC2_2 * (2.0 * zz - xx - yy);
+    out[7] = kC2_3 * x * z; out[8] = kC2_4 * (xx - yy);
+    if (degree < 3) return;
+    out[9] = kC3_0 * y * (3.0 * xx - yy);
+    out[10] = kC3_1 * x * y * z;
+    out[11] = kC3_2 * y * (4.0 * zz - xx - yy);
+    out[12] = kC3_3 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+    out[13] = kC3_4 * x * (4.0 * zz - xx - yy);
+    out[14] = kC3_5 * z * (xx - yy);
+    out[15] = kC3_6 * x * (xx - 3.0 * yy);
+}
+
+// d(basis_k)/d(dir) . a  accumulated over k with weights wk = coeffs_k . d_color (sh.cpp:55-80)
+__device__ __forceinline__ D3 sh_dir_grad(const D3& d, int degree, const double wk[16]) {
+    D3 g{0.0, 0.0, 0.0};
+    if (degree < 1) return g;
+    const double x = d.x, y = d.y, z = d.z;
+    auto acc = [&](double s, double jx, double jy, double jz, double w) {
+        g.x += s * jx * w; g.y += s * jy * w; g.z += s * jz * w;
+    };
+    acc(1.0, 0.0, kC1, 0.0, wk[1]);
+    acc(1.0, 0.0, 0.0, kC1, wk[2]);
+    acc(1.0, kC1, 0.0, 0.0, wk[3]);
+    if (degree < 2) return g;
+    acc(kC2_0, y, x, 0.0, wk[4]);
+    acc(kC2_1, 0.0, z, y, wk[5]);
+    acc(kC2_2, -2.0 * x, -2.0 * y, 4.0 * z, wk[6]);
+    acc(kC2_3, z, 0.0, x, wk[7]);
+    acc(kC2_4, 2.0 * x, -2.0 * y, 0.0, wk[8]);
+    if (degree < 3) return g;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    acc(kC3_0, 6.0 * x * y, 3.0 * xx - 3.0 * yy, 0.0, wk[9]);
+    acc(kC3_1, y * z, x * z, x * y, wk[10]);
+    acc(kC3_2, -2.0 * x * y, 4.0 * zz - xx - 3.0 * yy, 8.0 * y * z, wk[11]);
+    acc(kC3_3, -6.0 * x * z, -6.0 * y * z, 6.0 * zz - 3.0 * xx - 3.0 * yy, wk[12]);
+    acc(kC3_4, 4.0 * zz - 3.0 * xx - yy, -2.0 * x * y, 8.0 * x * z, wk[13]);
+    acc(kC3_5, 2.0 * x * z, -2.0 * y * z, xx - yy, wk[14]);
+    acc(kC3_6, 3.0 * xx - 3.0 * yy, -6.0 * x * y, 0.0, wk[15]);
+    return g;
+}
+
+__device__ __forceinline__ double ldp(const float* __restrict__ params, int64_t cap, int plane, int i) {
+    return static_cast<double>(__ldg(params + plane * cap + i));
+}
+
+// covariance.cpp:17-43 rotation_partial(u, k) (without the factor 2, applied by the caller)
+__device__ __forceinline__ void rotation_partial(const double u[4], int k, double d[3][3]) {
+    const double w = u[0], x = u[1], y = u[2], z = u[3];
+    if (k == 0) {
+        d[0][0] = 0; d[0][1] = -z; d[0][2] = y; d[1][0] = z; d[1][1] = 0; d[1][2] = -x;
+        d[2][0] = -y; d[2][1] = x; d[2][2] = 0;
+    } else if (k == 1) {
+        d[0][0] = 0; d[0][1] = y; d[0][2] = z; d[1][0] = y; d[1][1] = -2 * x; d[1][2] = -w;
+        d[2][0] = z; d[2][1] = w; d[2][2] = -2 * x;
+    } else if (k == 2) {
+        d[0][0] = -2 * y; d[0][1] = x; d[0][2] = w; d[1][0] = x; d[1][1] = 0; d[1][2] = z;
+        d[2][0] = -w; d[2][1] = z; d[2][2] = -2 * y;
+    } else {
+        d[0][0] = -2 * z; d[0][1] = -w; d[0][2] = x; d[1][0] = w; d[1][1] = -2 * z; d[1][2] = y;
+        d[2][0] = x; d[2][1] = y; d[2][2] = 0;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// K1: one thread per Gaussian. Culls (near clip z <= 0.01, off-screen box), writes the 64 B
+// Splat record at the map index, the fp64 depth bit pattern as the sort key, and counts the
+// visible set and the (tile, gaussian) pairs with warp-aggregated atomics.
+// Reference: rasterizer.cpp:37-68 (project_visible) + projection.cpp:17-40 + sh.cpp:82-92 +
+// rasterizer.cpp:81-88 (pixel rect -> tile rect).
+__global__ void __launch_bounds__(256) preprocess_fwd_kernel(
+    const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, int n,
+    ViewParams v, Splat* __restrict__ rec_by_gid, uint8_t* __restrict__ vis_flag,
+    unsigned long long* __restrict__ depth_key, unsigned long long* __restrict__ counters) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool visible = false;
+    uint32_t ntiles = 0;
+    if (i < n) {
+        const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
+        D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
+        p = {p.x + v.tx, p.y + v.ty, p.z + v.tz};
+        if (!(p.z <= kNearClip)) {  // projection.cpp:20 (culled, not clamped)
+            const double mx = v.fx * p.x / p.z + v.cx;
+            const double my = v.fy * p.y / p.z + v.cy;
+            double W[3][3], J[2][3], M[2][3], S[3][3], MS[2][3];
+            pose_matrix(v, W);
+            perspective_jacobian(p, v, J);
+            mul23_33(J, W, M);
+            const double q[4] = {ldp(params, cap, P_ROT, i), ldp(params, cap, P_ROT + 1, i),
+                                 ldp(params, cap, P_ROT + 2, i), ldp(params, cap, P_ROT + 3, i)};
+            const double ls[3] = {ldp(params, cap, P_LS, i), ldp(params, cap, P_LS + 1, i),
+                                  ldp(params, cap, P_LS + 2, i)};
+            build_covariance(q, ls, S);
+            mul23_33(M, S, MS);
+            double cov[2][2];
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b)
+                    cov[a][b] = (MS[a][0] * M[b][0] + MS[a][1] * M[b][1]) + MS[a][2] * M[b][2];
+            cov[0][0] += kCovReg;
+            cov[1][1] += kCovReg;
+            double c2[2][2];
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b) c2[a][b] = 0.5 * (cov[a][b] + cov[b][a]);
+            const double half_trace = 0.5 * (c2[0][0] + c2[1][1]);
+            const double det = c2[0][0] * c2[1][1] - c2[1][0] * c2[0][1];
+            const double disc = sqrt(fmax(half_trace * half_trace - det, 0.0));
+            const double lmax = half_trace + disc;
+            const double rr = fmin(ceil(3.0 * sqrt(lmax)), 1073741824.0);
+            const int radius = max(1, static_cast<int>(rr));
+            const double rd = static_cast<double>(radius);
+            // rasterizer.cpp:48-50 off-screen cull
+            if (!(mx + rd < 0.0 || mx - rd > static_cast<double>(v.width - 1) || my + rd < 0.0 ||
+                  my - rd > static_cast<double>(v.height - 1))) {
+                visible = true;
+                // Eigen 2x2 inverse: adj * (1 / det)
+                const double invdet = 1.0 / det;
+                Splat s;
+                s.mx = mx;
+                s.my = my;
+                s.ca = static_cast<float>(c2[1][1] * invdet);
+                s.cb = static_cast<float>(-c2[0][1] * invdet);
+                s.cc = static_cast<float>(c2[0][0] * invdet);
+                s.opacity = static_cast<float>(1.0 / (1.0 + exp(-ldp(params, cap, P_OP, i))));
+                // view direction from the camera centre (types.hpp:61-63, rasterizer.cpp:61-64)
+                const D3 ctr = quat_rotate(v.qw, -v.qx, -v.qy, -v.qz, D3{-v.tx, -v.ty, -v.tz});
+                const D3 vd{pos.x - ctr.x, pos.y - ctr.y, pos.z - ctr.z};
+                const double dist = sqrt((vd.x * vd.x + vd.y * vd.y) + vd.z * vd.z);
+                const D3 dir = dist > 0.0 ? D3{vd.x / dist, vd.y / dist, vd.z / dist} : D3{0.0, 0.0, 1.0};
+                const int deg = degree[i];
+                double basis[16];
+                sh_basis(dir, deg, basis);
+                const int nb = (deg + 1) * (deg + 1);
+                double col[3] = {0.5, 0.5, 0.5};
+                for (int k = 0; k < nb; ++k)
+                    for (int c = 0; c < 3; ++c) col[c] += basis[k] * ldp(params, cap, P_SH + 3 * k + c, i);
+                s.r = static_cast<float>(fmin(fmax(col[0], 0.0), 1.0));
+                s.g = static_cast<float>(fmin(fmax(col[1], 0.0), 1.0));
+                s.b = static_cast<float>(fmin(fmax(col[2], 0.0), 1.0));
+                s.depth = static_cast<float>(p.z);
+                // rasterizer.cpp:81-88: integer pixel rect of the 3-sigma box
+                const int px0 = max(0, static_cast<int>(ceil(mx - rd)));
+                const int px1 = min(v.width - 1, static_cast<int>(floor(mx + rd)));
+                const int py0 = max(0, static_cast<int>(ceil(my - rd)));
+                const int py1 = min(v.height - 1, static_cast<int>(floor(my + rd)));
+                if (px0 <= px1 && py0 <= py1) {
+                    ntiles = static_cast<uint32_t>((px1 / kTile - px0 / kTile + 1) * (py1 / kTile - py0 / kTile + 1));
+                    s.x0 = static_cast<int16_t>(px0); s.x1 = static_cast<int16_t>(px1);
+                    s.y0 = static_cast<int16_t>(py0); s.y1 = static_cast<int16_t>(py1);
+                } else {
+                    s.x0 = 1; s.x1 = 0; s.y0 = 1; s.y1 = 0;  // empty
+                }
+                s.gid = i;
+                s.ntiles = ntiles;
+                rec_by_gid[i] = s;
+                depth_key[i] = static_cast<unsigned long long>(__double_as_longlong(p.z));
+            }
+        }
+        vis_flag[i] = visible ? 1 : 0;
+    }
+    // warp-aggregated counters: [0] visible, [1] pairs
+    const unsigned vis_count = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
+    unsigned long long pairs = ntiles;
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31) == 0) {
+        if (vis_count) atomicAdd(counters + 0, static_cast<unsigned long long>(vis_count));
+        if (pairs) atomicAdd(counters + 1, pairs);
+    }
+}
+
+void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, int n,
+                           const ViewParams& v, Splat* rec_by_gid, uint8_t* vis_flag,
+                           unsigned long long* depth_key, unsigned long long* counters,
+                           cudaStream_t st) {
+    if (n <= 0) return;
+    preprocess_fwd_kernel<<<div_up(n, 256), 256, 0, st>>>(params, cap, degree, n, v, rec_by_gid,
+                                                          vis_flag, depth_key, counters);
+}
+
+// ------------------------------------------------------------------------------------------
+// K8: one thread per projected Gaussian (rank). Reduces the (tile, gaussian) partials of its
+// emission segment in fp64, then runs the per-Gaussian VJP chain (rasterizer.cpp:323-353):
+// colour clamp mask -> eval_sh_vjp -> view-direction chain, sigmoid, project_gaussian_vjp
+// (projection.cpp:42-74) -> build_covariance_vjp (covariance.cpp:58-79). Accumulates into the
+// gradient planes (batch semantics = GaussianGrad::add, gaussian.hpp:51-57).
+__global__ void __launch_bounds__(128) preprocess_bwd_kernel(
+    const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
+    const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
+    const float* __restrict__ partials, int n_vis, float* __restrict__ grads, int64_t gcap) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_vis) return;
+    const uint32_t e0 = emit_off[r], e1 = emit_off[r + 1];
+    if (e0 == e1) return;  // no tile: never touched (rasterizer.cpp:327)
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    for (uint32_t e = e0; e < e1; ++e) {
+        const float2* pp = reinterpret_cast<const float2*>(partials + static_cast<size_t>(e) * kNumPartials);
+#pragma unroll
+        for (int k = 0; k < kNumPartials / 2; ++k) {
+            const float2 t = __ldg(pp + k);
+            acc[2 * k] += t.x;
+            acc[2 * k + 1] += t.y;
+        }
+    }
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) any |= (acc[k] != 0.0);
+    if (!any) return;  // untouched (or all-zero cotangent): exact zero gradient
+    const int i = rec[r].gid;
+    const int deg = degree[i];
+    const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
+
+    // ---- colour: clamp mask, SH, view direction (rasterizer.cpp:330-340)
+    const D3 ctr = quat_rotate(v.qw, -v.qx, -v.qy, -v.qz, D3{-v.tx, -v.ty, -v.tz});
+    const D3 vd{pos.x - ctr.x, pos.y - ctr.y, pos.z - ctr.z};
+    const double dist = sqrt((vd.x * vd.x + vd.y * vd.y) + vd.z * vd.z);
+    const D3 dir = dist > 0.0 ? D3{vd.x / dist, vd.y / dist, vd.z / dist} : D3{0.0, 0.0, 1.0};
+    double basis[16];
+    sh_basis(dir, deg, basis);
+    const int nb = (deg + 1) * (deg + 1);
+    double raw[3] = {0.5, 0.5, 0.5};
+    for (int k = 0; k < nb; ++k)
+        for (int c = 0; c < 3; ++c) raw[c] += basis[k] * ldp(params, cap, P_SH + 3 * k + c, i);
+    double dr[3];
+    for (int c = 0; c < 3; ++c) dr[c] = (raw[c] <= 0.0 || raw[c] >= 1.0) ? 0.0 : acc[c];
+    double wk[16];
+    for (int k = 0; k < nb; ++k) {
+        double s = 0.0;
+        for (int c = 0; c < 3; ++c) s += ldp(params, cap, P_SH + 3 * k + c, i) * dr[c];
+        wk[k] = s;
+        for (int c = 0; c < 3; ++c) grads[(P_SH + 3 * k + c) * gcap + i] += static_cast<float>(basis[k] * dr[c]);
+    }
+    const D3 ddir = sh_dir_grad(dir, deg, wk);
+    double gpos[3] = {0.0, 0.0, 0.0};
+    if (dist > 0.0) {
+        const double vdd = (dir.x * ddir.x + dir.y * ddir.y) + dir.z * ddir.z;
+        gpos[0] = (ddir.x - dir.x * vdd) / dist;
+        gpos[1] = (ddir.y - dir.y * vdd) / dist;
+        gpos[2] = (ddir.z - dir.z * vdd) / dist;
+    }
+
+    // ---- opacity logit through the sigmoid (rasterizer.cpp:343)
+    const double o = 1.0 / (1.0 + exp(-ldp(params, cap, P_OP, i)));
+    grads[P_OP * gcap + i] += static_cast<float>(acc[4] * o * (1.0 - o));
+
+    // ---- geometry (projection.cpp:42-74)
+    D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
+    p = {p.x + v.tx, p.y + v.ty, p.z + v.tz};
+    double W[3][3], J[2][3], M[2][3], S[3][3];
+    pose_matrix(v, W);
+    perspective_jacobian(p, v, J);
+    mul23_33(J, W, M);
+    const double q[4] = {ldp(params, cap, P_ROT, i), ldp(params, cap, P_ROT + 1, i),
+                         ldp(params, cap, P_ROT + 2, i), ldp(params, cap, P_ROT + 3, i)};
+    const double ls[3] = {ldp(params, cap, P_LS, i), ldp(params, cap, P_LS + 1, i), ldp(params, cap, P_LS + 2, i)};
+    build_covariance(q, ls, S);
+    const double dcov[2][2] = {{acc[7], acc[8]}, {acc[8], acc[9]}};
+    // d_sigma_w = M^T dcov M
+    double dsw[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) {
+            const double t0 = M[0][a] * dcov[0][0] + M[1][a] * dcov[1][0];
+            const double t1 = M[0][a] * dcov[0][1] + M[1][a] * dcov[1][1];
+            dsw[a][c] = t0 * M[0][c] + t1 * M[1][c];
+        }
+    // d_m = (dcov + dcov^T) M Sigma_w ; d_j = d_m W^T
+    double dsm[2][3], dm[2][3], dj[2][3];
+    for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 3; ++c) dsm[a][c] = (2.0 * dcov[a][0]) * M[0][c] + (2.0 * dcov[a][1]) * M[1][c];
+    mul23_33(dsm, S, dm);
+    for (int a = 0; a < 2; ++a)
+        for (int c = 0; c < 3; ++c) dj[a][c] = (dm[a][0] * W[c][0] + dm[a][1] * W[c][1]) + dm[a][2] * W[c][2];
+    // build_covariance_vjp (covariance.cpp:58-79)
+    {
+        double u[4], nrm, R[3][3];
+        unit_quat(q, u, &nrm);
+        rotation_from_unit(u, R);
+        const double s2[3] = {exp(2.0 * ls[0]), exp(2.0 * ls[1]), exp(2.0 * ls[2])};
+        double rtg[3][3], rtgr[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 3; ++c)
+                rtg[a][c] = (R[0][a] * dsw[0][c] + R[1][a] * dsw[1][c]) + R[2][a] * dsw[2][c];
+        for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 3; ++c) rtgr[a][c] = (rtg[a][0] * R[0][c] + rtg[a][1] * R[1][c]) + rtg[a][2] * R[2][c];
+        for (int k = 0; k < 3; ++k) grads[(P_LS + k) * gcap + i] += static_cast<float>(2.0 * s2[k] * rtgr[k][k]);
+        double dR[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 3; ++c) {
+                double s = 0.0;
+                for (int b = 0; b < 3; ++b) s += (dsw[a][b] + dsw[b][a]) * R[b][c];
+                dR[a][c] = s * s2[c];
+            }
+        double du[4];
+        for (int k = 0; k < 4; ++k) {
+            double d[3][3];
+            rotation_partial(u, k, d);
+            double s = 0.0;
+            for (int c = 0; c < 3; ++c)
+                for (int a = 0; a < 3; ++a) s += dR[a][c] * (2.0 * d[a][c]);
+            du[k] = s;
+        }
+        const double ud = ((u[0] * du[0] + u[1] * du[1]) + u[2] * du[2]) + u[3] * du[3];
+        for (int k = 0; k < 4; ++k) grads[(P_ROT + k) * gcap + i] += static_cast<float>((du[k] - u[k] * ud) / nrm);
+    }
+    // position: J^T d_mean + J(p) terms + depth, then W^T
+    double dp[3];
+    for (int c = 0; c < 3; ++c) dp[c] = J[0][c] * acc[5] + J[1][c] * acc[6];
+    const double z = p.z, z2 = z * z, z3 = z2 * z;
+    dp[0] += dj[0][2] * (-v.fx / z2);
+    dp[1] += dj[1][2] * (-v.fy / z2);
+    dp[2] += dj[0][0] * (-v.fx / z2) + dj[1][1] * (-v.fy / z2) + dj[0][2] * (2.0 * v.fx * p.x / z3) +
+             dj[1][2] * (2.0 * v.fy * p.y / z3);
+    dp[2] += acc[3];
+    for (int c = 0; c < 3; ++c) {
+        const double dpos = (W[0][c] * dp[0] + W[1][c] * dp[1]) + W[2][c] * dp[2];
+        grads[(P_POS + c) * gcap + i] += static_cast<float>(gpos[c] + dpos);
+    }
+}
+
+void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
+                           const Splat* rec, const uint32_t* emit_off, const float* partials,
+                           int n_vis, float* grads, int64_t gcap, cudaStream_t st) {
+    if (n_vis <= 0) return;
+    preprocess_bwd_kernel<<<div_up(n_vis, 128), 128, 0, st>>>(params, cap, degree, v, rec, emit_off,
+                                                             partials, n_vis, grads, gcap);
+}
+
+}  // namespace gsb

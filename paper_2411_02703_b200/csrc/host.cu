@@ -1,0 +1,1209 @@
+// Host side of the C-ABI (include/gsmap_b200.h): device state, buffer management and the
+// orchestration of the hot step train_keyframe_step (mapper.cpp:214-238) over the kernels.
+// Exceptions never cross the boundary: every entry point returns a status and keeps a
+// thread-local message (gs_last_error).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gsmap_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace gsb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct GsError : std::runtime_error {
+    int code;
+    GsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw GsError(code, msg); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(e == cudaErrorMemoryAllocation ? GS_ENOMEM : GS_ECUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return GS_OK;
+    } catch (const GsError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return GS_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GS_ELOGIC;
+    }
+}
+
+// Grow-only device buffer (no per-iteration cudaMalloc on the hot path).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        const size_t alloc = std::max<size_t>(need + need / 4, 256);
+        ck(cudaMalloc(&p, alloc), "cudaMalloc");
+        bytes = alloc;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        ck(cudaMallocHost(&p, need), "cudaMallocHost");
+        bytes = need;
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+void validate_camera(const gs_camera& c) {  // core/types.hpp:22-29
+    if (c.fx <= 0.0 || c.fy <= 0.0) fail(GS_EINVAL, "CameraModel: focal lengths must be positive");
+    if (c.width <= 0 || c.height <= 0) fail(GS_EINVAL, "CameraModel: image size must be positive");
+    if (c.cx < 0.0 || c.cx >= c.width || c.cy < 0.0 || c.cy >= c.height)
+        fail(GS_EINVAL, "CameraModel: principal point outside image");
+}
+
+gs_camera scaled(const gs_camera& c, int level) {  // core/types.hpp:34-44
+    gs_camera s = c;
+    const double f = static_cast<double>(1 << level);
+    s.fx = c.fx / f;
+    s.fy = c.fy / f;
+    s.cx = (c.cx + 0.5) / f - 0.5;
+    s.cy = (c.cy + 0.5) / f - 0.5;
+    s.width = (c.width + (1 << level) - 1) >> level;
+    s.height = (c.height + (1 << level) - 1) >> level;
+    return s;
+}
+
+ViewParams make_view(const gs_pose& p, const gs_camera& c) {
+    ViewParams v;
+    v.qw = p.qw; v.qx = p.qx; v.qy = p.qy; v.qz = p.qz;
+    v.tx = p.tx; v.ty = p.ty; v.tz = p.tz;
+    v.fx = c.fx; v.fy = c.fy; v.cx = c.cx; v.cy = c.cy;
+    v.width = c.width; v.height = c.height;
+    v.tiles_x = div_up(c.width, kTile);
+    v.tiles_y = div_up(c.height, kTile);
+    return v;
+}
+
+int n_active_planes(int max_degree) { return kGeomParams + 3 * (max_degree + 1) * (max_degree + 1); }
+
+}  // namespace
+
+// ============================================================================ handles
+struct gs_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    DevBuf cub_tmp;
+    DevBuf counters;  // 2 x u64
+    PinnedBuf pinned;
+    int64_t launches = 0;
+    gs_frame* scratch_frame = nullptr;
+    gs_grads* scratch_grads = nullptr;
+
+    void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
+    void launched(int k = 1) {
+        launches += k;
+        ck(cudaGetLastError(), "kernel launch");
+    }
+    void* cub(size_t bytes) {
+        cub_tmp.ensure(bytes);
+        return cub_tmp.p;
+    }
+};
+
+struct gs_map {
+    gs_context* ctx = nullptr;
+    int64_t n = 0, cap = 0;
+    float* params = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    int32_t* step = nullptr;
+    int8_t* degree = nullptr;
+    std::vector<int8_t> deg_host;
+    int max_degree = 0;
+    double scene_extent = 1.0;
+    int64_t global_step = 0;
+    DevBuf minmax;
+
+    void free_all() {
+        for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
+                        static_cast<void*>(step), static_cast<void*>(degree)})
+            if (p) cudaFree(p);
+        params = m = v = nullptr;
+        step = nullptr;
+        degree = nullptr;
+    }
+    void recompute_max_degree() {
+        int d = 0;
+        for (int8_t x : deg_host) d = std::max<int>(d, x);
+        max_degree = d;
+    }
+};
+
+struct gs_frame {
+    gs_context* ctx = nullptr;
+    bool rendered = false;
+    ViewParams view{};
+    int64_t map_n = 0, n_vis = 0, n_pairs = 0;
+    // per-Gaussian / per-rank / per-pair scratch
+    DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
+        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials;
+    // per-pixel
+    DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
+    DevBuf loss;  // LossScalars
+    bool has_cotangent = false;
+    int loss_level = -1;
+    double loss_lambda = 0.0, loss_lambda_d = 0.0;
+};
+
+struct gs_grads {
+    gs_context* ctx = nullptr;
+    float* planes = nullptr;
+    int64_t cap = 0;
+    int64_t n = -1;  // Gaussians the gradient set describes (-1 = unset)
+    bool external = false;
+    void ensure(int64_t need) {
+        if (need <= cap) return;
+        if (external) fail(GS_EINVAL, "gs_grads: external buffer too small for the map");
+        if (planes) cudaFree(planes);
+        planes = nullptr;
+        const int64_t c = std::max<int64_t>(need + need / 4, 1024);
+        ck(cudaMalloc(&planes, sizeof(float) * kNumParams * c), "cudaMalloc grads");
+        ck(cudaMemsetAsync(planes, 0, sizeof(float) * kNumParams * c, ctx->stream), "memset grads");
+        cap = c;
+    }
+};
+
+struct gs_keyframe {
+    gs_context* ctx = nullptr;
+    gs_pose pose{};
+    int32_t initial_iters = 0, consumed = 0;
+    std::vector<int> hs, ws;
+    std::vector<DevBuf> color, depth;  // per level: planes [3][h][w] and [h][w]
+    ~gs_keyframe() {
+        for (auto& b : color) b.release();
+        for (auto& b : depth) b.release();
+    }
+};
+
+// ============================================================================ internals
+namespace {
+
+void map_reserve(gs_map* M, int64_t need) {
+    if (need <= M->cap) return;
+    const int64_t nc = std::max<int64_t>(need, M->cap + M->cap / 2);
+    cudaStream_t st = M->ctx->stream;
+    float *p = nullptr, *m = nullptr, *v = nullptr;
+    int32_t* s = nullptr;
+    int8_t* d = nullptr;
+    ck(cudaMalloc(&p, sizeof(float) * kNumParams * nc), "cudaMalloc params");
+    ck(cudaMalloc(&m, sizeof(float) * kNumParams * nc), "cudaMalloc adam m");
+    ck(cudaMalloc(&v, sizeof(float) * kNumParams * nc), "cudaMalloc adam v");
+    ck(cudaMalloc(&s, sizeof(int32_t) * nc), "cudaMalloc step");
+    ck(cudaMalloc(&d, sizeof(int8_t) * nc), "cudaMalloc degree");
+    ck(cudaMemsetAsync(m, 0, sizeof(float) * kNumParams * nc, st), "memset");
+    ck(cudaMemsetAsync(v, 0, sizeof(float) * kNumParams * nc, st), "memset");
+    ck(cudaMemsetAsync(p, 0, sizeof(float) * kNumParams * nc, st), "memset");
+    if (M->n > 0) {
+        ck(cudaMemcpy2DAsync(p, sizeof(float) * nc, M->params, sizeof(float) * M->cap, sizeof(float) * M->n,
+                             kNumParams, cudaMemcpyDeviceToDevice, st), "copy params");
+        ck(cudaMemcpy2DAsync(m, sizeof(float) * nc, M->m, sizeof(float) * M->cap, sizeof(float) * M->n,
+                             kNumParams, cudaMemcpyDeviceToDevice, st), "copy m");
+        ck(cudaMemcpy2DAsync(v, sizeof(float) * nc, M->v, sizeof(float) * M->cap, sizeof(float) * M->n,
+                             kNumParams, cudaMemcpyDeviceToDevice, st), "copy v");
+        ck(cudaMemcpyAsync(s, M->step, sizeof(int32_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy step");
+        ck(cudaMemcpyAsync(d, M->degree, sizeof(int8_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy degree");
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+    M->free_all();
+    M->params = p; M->m = m; M->v = v; M->step = s; M->degree = d;
+    M->cap = nc;
+}
+
+// upload AoS fp64 Gaussians [first, first+cnt) into the fp32 planes
+void upload_gaussians(gs_map* M, const gs_gaussian* g, int64_t first, int64_t cnt) {
+    if (cnt <= 0) return;
+    std::vector<float> soa(static_cast<size_t>(kNumParams) * cnt);
+    for (int64_t i = 0; i < cnt; ++i)
+        for (int k = 0; k < kNumParams; ++k) soa[static_cast<size_t>(k) * cnt + i] = static_cast<float>(g[i].p[k]);
+    std::vector<int8_t> deg(cnt);
+    for (int64_t i = 0; i < cnt; ++i) {
+        if (g[i].active_degree < 0 || g[i].active_degree > 3) fail(GS_EINVAL, "eval_sh: active_degree out of range");
+        deg[i] = static_cast<int8_t>(g[i].active_degree);
+    }
+    ck(cudaMemcpy2DAsync(M->params + first, sizeof(float) * M->cap, soa.data(), sizeof(float) * cnt,
+                         sizeof(float) * cnt, kNumParams, cudaMemcpyHostToDevice, M->ctx->stream), "upload params");
+    ck(cudaMemcpyAsync(M->degree + first, deg.data(), cnt, cudaMemcpyHostToDevice, M->ctx->stream), "upload degree");
+    ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+    if (static_cast<int64_t>(M->deg_host.size()) < first + cnt) M->deg_host.resize(first + cnt);
+    std::copy(deg.begin(), deg.end(), M->deg_host.begin() + first);
+    M->recompute_max_degree();
+}
+
+void refresh_extent(gs_map* M) {  // gaussian_map.cpp:87-99
+    if (M->n == 0) {
+        M->scene_extent = 1.0;
+        return;
+    }
+    M->minmax.ensure(6 * sizeof(unsigned int));
+    launch_position_minmax(M->params, M->cap, static_cast<int>(M->n), M->minmax.as<float>(), M->ctx->stream);
+    M->ctx->launched();
+    unsigned int enc[6];
+    ck(cudaMemcpyAsync(enc, M->minmax.p, sizeof(enc), cudaMemcpyDeviceToHost, M->ctx->stream), "d2h");
+    ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+    double lo[3], hi[3];
+    auto dec = [](unsigned int u) {
+        const unsigned int b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+        float f;
+        std::memcpy(&f, &b, 4);
+        return static_cast<double>(f);
+    };
+    for (int c = 0; c < 3; ++c) {
+        lo[c] = dec(enc[c]);
+        hi[c] = dec(enc[3 + c]);
+    }
+    const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+    M->scene_extent = std::max(0.5 * std::sqrt((dx * dx + dy * dy) + dz * dz), 1e-6);
+}
+
+void frame_pixels(gs_frame* F, const ViewParams& v) {
+    const size_t P = static_cast<size_t>(v.width) * v.height;
+    F->color.ensure(3 * P * sizeof(float));
+    F->depth.ensure(P * sizeof(float));
+    F->vis.ensure(P * sizeof(float));
+    F->t_final.ensure(P * sizeof(float));
+    F->n_proc.ensure(P * sizeof(int32_t));
+    F->n_contrib.ensure(P * sizeof(int32_t));
+    F->dl_dcolor.ensure(3 * P * sizeof(float));
+    F->depth_cot.ensure(P * sizeof(float));
+    F->loss.ensure(sizeof(LossScalars));
+    F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * sizeof(uint2));
+}
+
+// render (rasterizer.cpp:100-199) without the CSR: project -> compact -> depth sort -> pack ->
+// scan -> emit (tile, rank) pairs -> stable tile sort -> ranges -> blend.
+void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F) {
+    validate_camera(cam);
+    gs_context* C = M->ctx;
+    C->use();
+    cudaStream_t st = C->stream;
+    const ViewParams v = make_view(pose, cam);
+    F->view = v;
+    F->map_n = M->n;
+    F->rendered = false;
+    F->has_cotangent = false;
+    frame_pixels(F, v);
+    const int n = static_cast<int>(M->n);
+    const int T = v.tiles_x * v.tiles_y;
+    ck(cudaMemsetAsync(F->ranges.p, 0, sizeof(uint2) * T, st), "memset ranges");
+    F->n_vis = 0;
+    F->n_pairs = 0;
+    if (n > 0) {
+        F->rec_by_gid.ensure(sizeof(Splat) * n);
+        F->vis_flag.ensure(n);
+        F->key_by_gid.ensure(sizeof(unsigned long long) * n);
+        C->counters.ensure(2 * sizeof(unsigned long long));
+        C->pinned.ensure(64);
+        ck(cudaMemsetAsync(C->counters.p, 0, 2 * sizeof(unsigned long long), st), "memset counters");
+        launch_preprocess_fwd(M->params, M->cap, M->degree, n, v, F->rec_by_gid.as<Splat>(),
+                              F->vis_flag.as<uint8_t>(), F->key_by_gid.as<unsigned long long>(),
+                              C->counters.as<unsigned long long>(), st);
+        C->launched();
+        ck(cudaMemcpyAsync(C->pinned.p, C->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
+           "d2h counters");
+        ck(cudaStreamSynchronize(st), "sync counters");
+        const unsigned long long* cnt = static_cast<unsigned long long*>(C->pinned.p);
+        F->n_vis = static_cast<int64_t>(cnt[0]);
+        F->n_pairs = static_cast<int64_t>(cnt[1]);
+        if (F->n_pairs > 0xffffffffLL) fail(GS_ELOGIC, "render: more than 2^32 (tile, gaussian) pairs");
+    }
+    const int nv = static_cast<int>(F->n_vis);
+    const uint32_t K = static_cast<uint32_t>(F->n_pairs);
+    if (nv > 0) {
+        F->vis_gid.ensure(sizeof(int32_t) * nv);
+        F->keys_a.ensure(sizeof(unsigned long long) * nv);
+        F->keys_b.ensure(sizeof(unsigned long long) * nv);
+        F->gid_sorted.ensure(sizeof(int32_t) * nv);
+        F->rec_sorted.ensure(sizeof(Splat) * nv);
+        F->ntiles.ensure(sizeof(uint32_t) * (nv + 1));
+        F->emit_off.ensure(sizeof(uint32_t) * (nv + 1));
+        F->num_sel.ensure(sizeof(int));
+        // stable compaction of the visible map indices (index order = reference tie-break order)
+        cub::CountingInputIterator<int32_t> iota(0);
+        size_t tb = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb, iota, F->vis_flag.as<uint8_t>(), F->vis_gid.as<int32_t>(),
+                                   F->num_sel.as<int>(), n, st);
+        ck(cub::DeviceSelect::Flagged(C->cub(tb), tb, iota, F->vis_flag.as<uint8_t>(), F->vis_gid.as<int32_t>(),
+                                      F->num_sel.as<int>(), n, st), "DeviceSelect::Flagged");
+        launch_gather_keys(F->vis_gid.as<int32_t>(), F->key_by_gid.as<unsigned long long>(), nv,
+                           F->keys_a.as<unsigned long long>(), st);
+        C->launched();
+        // (depth, index) order: LSD radix sort on the fp64 depth bits is stable, so equal depths
+        // keep ascending map index (rasterizer.cpp:69-72)
+        tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<unsigned long long>(),
+                                        F->keys_b.as<unsigned long long>(), F->vis_gid.as<int32_t>(),
+                                        F->gid_sorted.as<int32_t>(), nv, 0, 64, st);
+        ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<unsigned long long>(),
+                                           F->keys_b.as<unsigned long long>(), F->vis_gid.as<int32_t>(),
+                                           F->gid_sorted.as<int32_t>(), nv, 0, 64, st), "depth sort");
+        launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), nv, F->rec_sorted.as<Splat>(),
+                    F->ntiles.as<uint32_t>(), st);
+        C->launched();
+        ck(cudaMemsetAsync(F->ntiles.as<uint32_t>() + nv, 0, sizeof(uint32_t), st), "memset");
+        tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), nv + 1, st);
+        ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
+                                         nv + 1, st), "scan");
+        if (K > 0) {
+            F->pair_keys.ensure(sizeof(uint32_t) * K);
+            F->pair_keys2.ensure(sizeof(uint32_t) * K);
+            F->pair_vals.ensure(sizeof(uint32_t) * K);
+            F->pair_vals2.ensure(sizeof(uint32_t) * K);
+            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), nv, K, v.tiles_x,
+                              F->pair_keys.as<uint32_t>(), F->pair_vals.as<uint32_t>(), st);
+            C->launched();
+            int bits = 1;
+            while ((1 << bits) < T) ++bits;
+            tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, F->pair_keys.as<uint32_t>(), F->pair_keys2.as<uint32_t>(),
+                                            F->pair_vals.as<uint32_t>(), F->pair_vals2.as<uint32_t>(),
+                                            static_cast<int>(K), 0, bits, st);
+            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->pair_keys.as<uint32_t>(),
+                                               F->pair_keys2.as<uint32_t>(), F->pair_vals.as<uint32_t>(),
+                                               F->pair_vals2.as<uint32_t>(), static_cast<int>(K), 0, bits, st),
+               "tile sort");
+            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), K, F->ranges.as<uint2>(), st);
+            C->launched();
+        }
+    }
+    launch_blend_fwd(F->ranges.as<uint2>(), K > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
+                     nv > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(), F->depth.as<float>(),
+                     F->vis.as<float>(), F->t_final.as<float>(), F->n_proc.as<int32_t>(),
+                     F->n_contrib.as<int32_t>(), st);
+    C->launched();
+    F->rendered = true;
+}
+
+void need_rendered(gs_frame* F) {
+    if (!F->rendered) fail(GS_ELOGIC, "render_backward: contributor lists missing or inconsistent");
+}
+
+void grads_zero(gs_grads* G, gs_map* M) {
+    G->ensure(std::max<int64_t>(M->n, 1));
+    if (M->n > 0) {
+        const int planes = n_active_planes(M->max_degree);
+        ck(cudaMemset2DAsync(G->planes, sizeof(float) * G->cap, 0, sizeof(float) * M->n, planes, M->ctx->stream),
+           "memset grads");
+    }
+    G->n = M->n;
+}
+
+void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* dl_ddepth,
+                   const float* depth_scale, gs_grads* G) {
+    gs_context* C = M->ctx;
+    cudaStream_t st = C->stream;
+    need_rendered(F);
+    if (F->map_n != M->n) fail(GS_ELOGIC, "render_backward: contributor lists missing or inconsistent");
+    const int nv = static_cast<int>(F->n_vis);
+    const uint32_t K = static_cast<uint32_t>(F->n_pairs);
+    if (nv == 0 || K == 0) return;
+    F->partials.ensure(sizeof(float) * kNumPartials * K);
+    launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
+                     F->emit_off.as<uint32_t>(), F->view, F->t_final.as<float>(), F->n_proc.as<int32_t>(), dl_dcolor,
+                     dl_ddepth, depth_scale, F->partials.as<float>(), st);
+    C->launched();
+    launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(), F->emit_off.as<uint32_t>(),
+                          F->partials.as<float>(), nv, G->planes, G->cap, st);
+    C->launched();
+}
+
+void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr) {
+    if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
+    const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
+    launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
+                M->scene_extent, M->ctx->stream);
+    M->ctx->launched();
+    ++M->global_step;
+}
+
+void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cfg) {
+    if (level < 0 || level >= static_cast<int>(K->hs.size()))
+        fail(GS_EINVAL, "compute_loss: pyramid level out of range");
+    need_rendered(F);
+    const int h = K->hs[level], w = K->ws[level];
+    if (F->view.height != h || F->view.width != w)
+        fail(GS_EINVAL, "compute_loss: rendered resolution does not match level");
+    gs_context* C = F->ctx;
+    cudaStream_t st = C->stream;
+    ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset loss");
+    launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
+                      K->depth[level].as<float>(), h, w, cfg.lambda, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
+                      F->loss.as<LossScalars>(), st);
+    C->launched();
+    if (cfg.lambda != 0.0) {
+        if (h < 11 || w < 11) fail(GS_EINVAL, "ssim: image smaller than the 11x11 window");
+        F->wbuf.ensure(sizeof(float) * 9 * static_cast<size_t>(h - 10) * (w - 10));
+        launch_ssim(F->color.as<float>(), K->color[level].as<float>(), h, w, cfg.lambda, F->wbuf.as<float>(),
+                    F->dl_dcolor.as<float>(), F->loss.as<LossScalars>(), st);
+        C->launched(2);
+    }
+    launch_loss_finalize(F->loss.as<LossScalars>(), cfg.lambda_d, st);
+    C->launched();
+    F->has_cotangent = true;
+    F->loss_level = level;
+    F->loss_lambda = cfg.lambda;
+    F->loss_lambda_d = cfg.lambda_d;
+}
+
+gs_loss_result read_loss(gs_frame* F) {
+    gs_context* C = F->ctx;
+    C->pinned.ensure(sizeof(LossScalars) + 64);
+    ck(cudaMemcpyAsync(C->pinned.p, F->loss.p, sizeof(LossScalars), cudaMemcpyDeviceToHost, C->stream), "d2h loss");
+    ck(cudaStreamSynchronize(C->stream), "sync loss");
+    LossScalars s;
+    std::memcpy(&s, C->pinned.p, sizeof(s));
+    const int h = F->view.height, w = F->view.width;
+    const double inv_n = 1.0 / (static_cast<double>(h) * w * 3);
+    gs_loss_result r{};
+    r.l1 = s.l1_sum * inv_n;
+    r.ssim = F->loss_lambda != 0.0 ? s.ssim_sum / (static_cast<double>(h - 10) * (w - 10) * 3) : 0.0;
+    r.color_loss = (1.0 - F->loss_lambda) * r.l1 + (F->loss_lambda != 0.0 ? F->loss_lambda * (1.0 - r.ssim) : 0.0);
+    r.depth_loss = s.n_valid > 0 ? s.depth_abs_sum / static_cast<double>(s.n_valid) : 0.0;
+    r.total = r.color_loss + F->loss_lambda_d * r.depth_loss;
+    const double mse = s.sq_sum * inv_n;
+    r.psnr = mse == 0.0 ? 100.0 : 10.0 * std::log10(1.0 / mse);
+    return r;
+}
+
+int schedule_level(const gs_keyframe* K, const gs_train_config& cfg) {  // mapper.cpp:221-224
+    const int n = static_cast<int>(K->hs.size()) - 1;
+    const int ipl = cfg.iters_per_level > 0 ? cfg.iters_per_level
+                                            : std::max(1, K->initial_iters / (cfg.pyramid_levels + 1));
+    return n - std::min(n, K->consumed / ipl);
+}
+
+void keyframe_build(gs_keyframe* K, const float* color0, const float* depth0, int h, int w, int levels,
+                    bool device_src) {
+    if (levels < 0) fail(GS_EINVAL, "build_pyramid: levels must be >= 0");
+    if (h < (1 << levels) || w < (1 << levels)) fail(GS_EINVAL, "build_pyramid: image too small for requested levels");
+    cudaStream_t st = K->ctx->stream;
+    K->hs.assign(levels + 1, 0);
+    K->ws.assign(levels + 1, 0);
+    K->color.resize(levels + 1);
+    K->depth.resize(levels + 1);
+    int ch = h, cw = w;
+    for (int l = 0; l <= levels; ++l) {
+        K->hs[l] = ch;
+        K->ws[l] = cw;
+        K->color[l].ensure(sizeof(float) * 3 * ch * cw);
+        K->depth[l].ensure(sizeof(float) * ch * cw);
+        ch = (ch + 1) / 2;
+        cw = (cw + 1) / 2;
+    }
+    const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    ck(cudaMemcpyAsync(K->color[0].p, color0, sizeof(float) * 3 * h * w, kind, st), "upload color");
+    ck(cudaMemcpyAsync(K->depth[0].p, depth0, sizeof(float) * h * w, kind, st), "upload depth");
+    for (int l = 1; l <= levels; ++l) {
+        launch_downsample(K->color[l - 1].as<float>(), K->hs[l - 1], K->ws[l - 1], 3, false, K->color[l].as<float>(), st);
+        launch_downsample(K->depth[l - 1].as<float>(), K->hs[l - 1], K->ws[l - 1], 1, true, K->depth[l].as<float>(), st);
+        K->ctx->launched(2);
+    }
+    ck(cudaStreamSynchronize(st), "sync keyframe");
+}
+
+gs_frame* scratch_frame(gs_context* C) {
+    if (!C->scratch_frame) {
+        C->scratch_frame = new gs_frame();
+        C->scratch_frame->ctx = C;
+    }
+    return C->scratch_frame;
+}
+
+gs_grads* scratch_grads(gs_context* C) {
+    if (!C->scratch_grads) {
+        C->scratch_grads = new gs_grads();
+        C->scratch_grads->ctx = C;
+    }
+    return C->scratch_grads;
+}
+
+void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_camera& cam, gs_frame* F,
+                gs_grads* G, int* level_out) {
+    const int level = schedule_level(K, cfg);
+    const gs_camera lc = scaled(cam, level);
+    render_impl(M, K->pose, lc, F);
+    loss_impl(F, K, level, cfg);
+    backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(), &F->loss.as<LossScalars>()->depth_scale, G);
+    *level_out = level;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+extern "C" {
+
+const char* gs_last_error(void) { return g_err.c_str(); }
+const char* gs_version(void) { return "gsmap_b200 0.1 (sm_100a)"; }
+
+int gs_context_create(int device, void* stream, gs_context** out) {
+    return guard([&] {
+        auto* C = new gs_context();
+        C->device = device;
+        try {
+            C->use();
+            if (stream) {
+                C->stream = static_cast<cudaStream_t>(stream);
+            } else {
+                ck(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+                C->own_stream = true;
+            }
+        } catch (...) {
+            delete C;
+            throw;
+        }
+        *out = C;
+    });
+}
+
+int gs_context_destroy(gs_context* C) {
+    return guard([&] {
+        if (!C) return;
+        C->use();
+        cudaStreamSynchronize(C->stream);
+        delete C->scratch_frame;
+        if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external) cudaFree(C->scratch_grads->planes);
+        delete C->scratch_grads;
+        C->cub_tmp.release();
+        C->counters.release();
+        if (C->own_stream) cudaStreamDestroy(C->stream);
+        delete C;
+    });
+}
+
+int gs_context_synchronize(gs_context* C) {
+    return guard([&] { ck(cudaStreamSynchronize(C->stream), "cudaStreamSynchronize"); });
+}
+
+int gs_context_set_stream(gs_context* C, void* stream) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(C->stream), "sync");
+        if (C->own_stream) cudaStreamDestroy(C->stream);
+        C->own_stream = false;
+        C->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int gs_context_launch_count(gs_context* C, int64_t* count) {
+    return guard([&] { *count = C->launches; });
+}
+
+int gs_camera_validate(const gs_camera* cam) { return guard([&] { validate_camera(*cam); }); }
+int gs_camera_scaled(const gs_camera* cam, int level, gs_camera* out) { return guard([&] { *out = scaled(*cam, level); }); }
+
+// ---------------------------------------------------------------- map
+int gs_map_create(gs_context* C, gs_map** out) {
+    return guard([&] {
+        auto* M = new gs_map();
+        M->ctx = C;
+        *out = M;
+    });
+}
+
+int gs_map_destroy(gs_map* M) {
+    return guard([&] {
+        if (!M) return;
+        M->ctx->use();
+        cudaStreamSynchronize(M->ctx->stream);
+        M->free_all();
+        M->minmax.release();
+        delete M;
+    });
+}
+
+int gs_map_size(const gs_map* M, int64_t* n) { return guard([&] { *n = M->n; }); }
+
+int gs_map_append(gs_map* M, const gs_gaussian* g, int64_t n) {
+    return guard([&] {
+        M->ctx->use();
+        if (n < 0) fail(GS_EINVAL, "append: negative count");
+        map_reserve(M, M->n + n);
+        // fresh optimizer state for the new range (gaussian_map.cpp:33)
+        cudaStream_t st = M->ctx->stream;
+        if (n > 0) {
+            ck(cudaMemset2DAsync(M->m + M->n, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
+            ck(cudaMemset2DAsync(M->v + M->n, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
+            ck(cudaMemsetAsync(M->step + M->n, 0, sizeof(int32_t) * n, st), "memset");
+        }
+        upload_gaussians(M, g, M->n, n);
+        M->n += n;
+        refresh_extent(M);
+    });
+}
+
+int gs_map_set_gaussians(gs_map* M, const gs_gaussian* g, int64_t n) {
+    return guard([&] {
+        M->ctx->use();
+        if (n != M->n) fail(GS_EINVAL, "set_gaussians: count does not match map size");
+        upload_gaussians(M, g, 0, n);
+    });
+}
+
+int gs_map_get_gaussians(gs_map* M, gs_gaussian* out, int64_t n) {
+    return guard([&] {
+        M->ctx->use();
+        if (n != M->n) fail(GS_EINVAL, "get_gaussians: count does not match map size");
+        if (n == 0) return;
+        std::vector<float> soa(static_cast<size_t>(kNumParams) * n);
+        ck(cudaMemcpy2DAsync(soa.data(), sizeof(float) * n, M->params, sizeof(float) * M->cap, sizeof(float) * n,
+                             kNumParams, cudaMemcpyDeviceToHost, M->ctx->stream), "download params");
+        ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+        for (int64_t i = 0; i < n; ++i) {
+            for (int k = 0; k < kNumParams; ++k) out[i].p[k] = soa[static_cast<size_t>(k) * n + i];
+            out[i].active_degree = M->deg_host[i];
+            out[i].pad = 0;
+        }
+    });
+}
+
+int gs_map_get_adam(gs_map* M, double* m59, double* v59, int64_t* step, int64_t n) {
+    return guard([&] {
+        M->ctx->use();
+        if (n != M->n) fail(GS_EINVAL, "get_adam: count does not match map size");
+        if (n == 0) return;
+        std::vector<float> a(static_cast<size_t>(kNumParams) * n), b(a.size());
+        std::vector<int32_t> s(n);
+        cudaStream_t st = M->ctx->stream;
+        ck(cudaMemcpy2DAsync(a.data(), sizeof(float) * n, M->m, sizeof(float) * M->cap, sizeof(float) * n, kNumParams,
+                             cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpy2DAsync(b.data(), sizeof(float) * n, M->v, sizeof(float) * M->cap, sizeof(float) * n, kNumParams,
+                             cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(s.data(), M->step, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        for (int64_t i = 0; i < n; ++i) {
+            for (int k = 0; k < kNumParams; ++k) {
+                if (m59) m59[i * kNumParams + k] = a[static_cast<size_t>(k) * n + i];
+                if (v59) v59[i * kNumParams + k] = b[static_cast<size_t>(k) * n + i];
+            }
+            if (step) step[i] = s[i];
+        }
+    });
+}
+
+int gs_map_set_adam(gs_map* M, const double* m59, const double* v59, const int64_t* step, int64_t n) {
+    return guard([&] {
+        M->ctx->use();
+        if (n != M->n) fail(GS_EINVAL, "set_adam: count does not match map size");
+        if (n == 0) return;
+        std::vector<float> a(static_cast<size_t>(kNumParams) * n), b(a.size());
+        std::vector<int32_t> s(n);
+        for (int64_t i = 0; i < n; ++i) {
+            for (int k = 0; k < kNumParams; ++k) {
+                a[static_cast<size_t>(k) * n + i] = static_cast<float>(m59[i * kNumParams + k]);
+                b[static_cast<size_t>(k) * n + i] = static_cast<float>(v59[i * kNumParams + k]);
+            }
+            s[i] = static_cast<int32_t>(step[i]);
+        }
+        cudaStream_t st = M->ctx->stream;
+        ck(cudaMemcpy2DAsync(M->m, sizeof(float) * M->cap, a.data(), sizeof(float) * n, sizeof(float) * n, kNumParams,
+                             cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpy2DAsync(M->v, sizeof(float) * M->cap, b.data(), sizeof(float) * n, sizeof(float) * n, kNumParams,
+                             cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(M->step, s.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int gs_map_scene_extent(const gs_map* M, double* e) { return guard([&] { *e = M->scene_extent; }); }
+int gs_map_set_scene_extent(gs_map* M, double e) { return guard([&] { M->scene_extent = e; }); }
+int gs_map_global_step(const gs_map* M, int64_t* s) { return guard([&] { *s = M->global_step; }); }
+int gs_map_set_global_step(gs_map* M, int64_t s) { return guard([&] { M->global_step = s; }); }
+
+int gs_map_raise_sh_degree(gs_map* M, int degree) {  // gaussian_map.cpp:75-79
+    return guard([&] {
+        M->ctx->use();
+        const int d = std::clamp(degree, 0, 3);
+        for (auto& x : M->deg_host) x = static_cast<int8_t>(std::max<int>(x, d));
+        if (M->n > 0)
+            ck(cudaMemcpyAsync(M->degree, M->deg_host.data(), M->n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
+        ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+        M->recompute_max_degree();
+    });
+}
+
+int gs_map_max_active_degree(gs_map* M, int* degree) { return guard([&] { *degree = M->max_degree; }); }
+
+int gs_map_device_planes(gs_map* M, float** params, float** m, float** v, int64_t* cap) {
+    return guard([&] {
+        if (params) *params = M->params;
+        if (m) *m = M->m;
+        if (v) *v = M->v;
+        if (cap) *cap = M->cap;
+    });
+}
+
+// ---------------------------------------------------------------- frames
+int gs_frame_create(gs_context* C, gs_frame** out) {
+    return guard([&] {
+        auto* F = new gs_frame();
+        F->ctx = C;
+        *out = F;
+    });
+}
+
+int gs_frame_destroy(gs_frame* F) {
+    return guard([&] {
+        if (!F) return;
+        F->ctx->use();
+        cudaStreamSynchronize(F->ctx->stream);
+        for (DevBuf* b : {&F->rec_by_gid, &F->vis_flag, &F->key_by_gid, &F->vis_gid, &F->keys_a, &F->keys_b,
+                          &F->gid_sorted, &F->rec_sorted, &F->ntiles, &F->emit_off, &F->num_sel, &F->pair_keys,
+                          &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->color,
+                          &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
+                          &F->wbuf, &F->host_stage, &F->loss})
+            b->release();
+        delete F;
+    });
+}
+
+int gs_render(gs_map* M, const gs_pose* pose, const gs_camera* cam, gs_frame* F) {
+    return guard([&] { render_impl(M, *pose, *cam, F); });
+}
+
+int gs_frame_stats_get(gs_frame* F, gs_frame_stats* out) {
+    return guard([&] {
+        need_rendered(F);
+        out->n_visible = F->n_vis;
+        out->n_pairs = F->n_pairs;
+        out->tiles_x = F->view.tiles_x;
+        out->tiles_y = F->view.tiles_y;
+        out->width = F->view.width;
+        out->height = F->view.height;
+        const size_t P = static_cast<size_t>(F->view.width) * F->view.height;
+        std::vector<int32_t> nc(P);
+        ck(cudaMemcpyAsync(nc.data(), F->n_contrib.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, F->ctx->stream), "d2h");
+        ck(cudaStreamSynchronize(F->ctx->stream), "sync");
+        int64_t s = 0;
+        for (int32_t x : nc) s += x;
+        out->n_contrib = s;
+    });
+}
+
+int gs_frame_read(gs_frame* F, double* color, double* depth, double* vis) {
+    return guard([&] {
+        need_rendered(F);
+        F->ctx->use();
+        const int h = F->view.height, w = F->view.width;
+        const size_t P = static_cast<size_t>(h) * w;
+        F->host_stage.ensure(sizeof(double) * 5 * P);
+        double* stage = F->host_stage.as<double>();
+        cudaStream_t st = F->ctx->stream;
+        launch_to_hwc_double(F->color.as<float>(), h, w, 3, stage, st);
+        launch_to_hwc_double(F->depth.as<float>(), h, w, 1, stage + 3 * P, st);
+        launch_to_hwc_double(F->vis.as<float>(), h, w, 1, stage + 4 * P, st);
+        F->ctx->launched(3);
+        if (color) ck(cudaMemcpyAsync(color, stage, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, st), "d2h");
+        if (depth) ck(cudaMemcpyAsync(depth, stage + 3 * P, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        if (vis) ck(cudaMemcpyAsync(vis, stage + 4 * P, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int gs_frame_device_images(gs_frame* F, float** color, float** depth, float** vis) {
+    return guard([&] {
+        need_rendered(F);
+        if (color) *color = F->color.as<float>();
+        if (depth) *depth = F->depth.as<float>();
+        if (vis) *vis = F->vis.as<float>();
+    });
+}
+
+int gs_frame_read_pixel_state(gs_frame* F, int32_t* n_contrib, float* t_final) {
+    return guard([&] {
+        need_rendered(F);
+        const size_t P = static_cast<size_t>(F->view.width) * F->view.height;
+        cudaStream_t st = F->ctx->stream;
+        if (n_contrib) ck(cudaMemcpyAsync(n_contrib, F->n_contrib.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        if (t_final) ck(cudaMemcpyAsync(t_final, F->t_final.p, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int gs_frame_read_projected(gs_frame* F, int32_t* index, double* mean2, int32_t* rect4, float* conic3,
+                            float* opacity, float* color3, double* depth) {
+    return guard([&] {
+        need_rendered(F);
+        const int64_t nv = F->n_vis;
+        if (nv == 0) return;
+        std::vector<Splat> rec(nv);
+        std::vector<unsigned long long> keys(nv);
+        cudaStream_t st = F->ctx->stream;
+        ck(cudaMemcpyAsync(rec.data(), F->rec_sorted.p, sizeof(Splat) * nv, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(keys.data(), F->keys_b.p, sizeof(unsigned long long) * nv, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        for (int64_t r = 0; r < nv; ++r) {
+            const Splat& s = rec[r];
+            if (index) index[r] = s.gid;
+            if (mean2) { mean2[2 * r] = s.mx; mean2[2 * r + 1] = s.my; }
+            if (rect4) {
+                rect4[4 * r] = s.x0; rect4[4 * r + 1] = s.y0; rect4[4 * r + 2] = s.x1; rect4[4 * r + 3] = s.y1;
+            }
+            if (conic3) { conic3[3 * r] = s.ca; conic3[3 * r + 1] = s.cb; conic3[3 * r + 2] = s.cc; }
+            if (opacity) opacity[r] = s.opacity;
+            if (color3) { color3[3 * r] = s.r; color3[3 * r + 1] = s.g; color3[3 * r + 2] = s.b; }
+            if (depth) {
+                double d;
+                std::memcpy(&d, &keys[r], sizeof(double));
+                depth[r] = d;
+            }
+        }
+    });
+}
+
+int gs_frame_read_tiles(gs_frame* F, int64_t* tile_offsets, int32_t* entries) {
+    return guard([&] {
+        need_rendered(F);
+        const int T = F->view.tiles_x * F->view.tiles_y;
+        const int64_t K = F->n_pairs;
+        std::vector<uint2> ranges(T);
+        std::vector<uint32_t> vals(K);
+        std::vector<Splat> rec(F->n_vis);
+        cudaStream_t st = F->ctx->stream;
+        ck(cudaMemcpyAsync(ranges.data(), F->ranges.p, sizeof(uint2) * T, cudaMemcpyDeviceToHost, st), "d2h");
+        if (K) ck(cudaMemcpyAsync(vals.data(), F->pair_vals2.p, sizeof(uint32_t) * K, cudaMemcpyDeviceToHost, st), "d2h");
+        if (F->n_vis)
+            ck(cudaMemcpyAsync(rec.data(), F->rec_sorted.p, sizeof(Splat) * F->n_vis, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        int64_t k = 0;
+        tile_offsets[0] = 0;
+        for (int t = 0; t < T; ++t) {
+            for (uint32_t i = ranges[t].x; i < ranges[t].y; ++i) entries[k++] = rec[vals[i]].gid;
+            tile_offsets[t + 1] = k;
+        }
+        if (k != K) fail(GS_ELOGIC, "read_tiles: tile ranges do not cover every pair");
+    });
+}
+
+int gs_frame_materialize(gs_frame* F, uint32_t* offsets, int32_t* gaussian, double* alpha) {
+    return guard([&] {
+        need_rendered(F);
+        const int h = F->view.height, w = F->view.width;
+        const size_t P = static_cast<size_t>(h) * w;
+        std::vector<int32_t> nc(P);
+        cudaStream_t st = F->ctx->stream;
+        ck(cudaMemcpyAsync(nc.data(), F->n_contrib.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        std::vector<uint32_t> off(P + 1, 0);
+        for (size_t p = 0; p < P; ++p) off[p + 1] = off[p] + static_cast<uint32_t>(nc[p]);
+        if (offsets) std::memcpy(offsets, off.data(), sizeof(uint32_t) * (P + 1));
+        const uint32_t total = off[P];
+        if (total == 0 || (!gaussian && !alpha)) return;
+        DevBuf doff, dg, da;
+        doff.ensure(sizeof(uint32_t) * (P + 1));
+        dg.ensure(sizeof(int32_t) * total);
+        da.ensure(sizeof(double) * total);
+        ck(cudaMemcpyAsync(doff.p, off.data(), sizeof(uint32_t) * (P + 1), cudaMemcpyHostToDevice, st), "h2d");
+        launch_materialize(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(), F->view,
+                           doff.as<uint32_t>(), dg.as<int32_t>(), da.as<double>(), st);
+        F->ctx->launched();
+        if (gaussian) ck(cudaMemcpyAsync(gaussian, dg.p, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st), "d2h");
+        if (alpha) ck(cudaMemcpyAsync(alpha, da.p, sizeof(double) * total, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        doff.release();
+        dg.release();
+        da.release();
+    });
+}
+
+// ---------------------------------------------------------------- gradients
+int gs_grads_create(gs_context* C, gs_grads** out) {
+    return guard([&] {
+        auto* G = new gs_grads();
+        G->ctx = C;
+        *out = G;
+    });
+}
+
+int gs_grads_create_external(gs_context* C, float* ptr, int64_t capacity, gs_grads** out) {
+    return guard([&] {
+        auto* G = new gs_grads();
+        G->ctx = C;
+        G->planes = ptr;
+        G->cap = capacity;
+        G->external = true;
+        *out = G;
+    });
+}
+
+int gs_grads_destroy(gs_grads* G) {
+    return guard([&] {
+        if (!G) return;
+        if (G->planes && !G->external) {
+            cudaStreamSynchronize(G->ctx->stream);
+            cudaFree(G->planes);
+        }
+        delete G;
+    });
+}
+
+int gs_grads_zero(gs_grads* G, gs_map* M) { return guard([&] { grads_zero(G, M); }); }
+
+int gs_grads_read(gs_grads* G, double* out59, int64_t n) {
+    return guard([&] {
+        if (n != G->n) fail(GS_EINVAL, "grads_read: count does not match");
+        if (n == 0) return;
+        std::vector<float> soa(static_cast<size_t>(kNumParams) * n);
+        ck(cudaMemcpy2DAsync(soa.data(), sizeof(float) * n, G->planes, sizeof(float) * G->cap, sizeof(float) * n,
+                             kNumParams, cudaMemcpyDeviceToHost, G->ctx->stream), "d2h grads");
+        ck(cudaStreamSynchronize(G->ctx->stream), "sync");
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < kNumParams; ++k) out59[i * kNumParams + k] = soa[static_cast<size_t>(k) * n + i];
+    });
+}
+
+int gs_grads_write(gs_grads* G, const double* in59, int64_t n) {
+    return guard([&] {
+        G->ensure(std::max<int64_t>(n, 1));
+        std::vector<float> soa(static_cast<size_t>(kNumParams) * n);
+        for (int64_t i = 0; i < n; ++i)
+            for (int k = 0; k < kNumParams; ++k) soa[static_cast<size_t>(k) * n + i] = static_cast<float>(in59[i * kNumParams + k]);
+        if (n > 0)
+            ck(cudaMemcpy2DAsync(G->planes, sizeof(float) * G->cap, soa.data(), sizeof(float) * n, sizeof(float) * n,
+                                 kNumParams, cudaMemcpyHostToDevice, G->ctx->stream), "h2d grads");
+        ck(cudaStreamSynchronize(G->ctx->stream), "sync");
+        G->n = n;
+    });
+}
+
+int gs_grads_device_planes(gs_grads* G, float** planes, int64_t* cap) {
+    return guard([&] {
+        *planes = G->planes;
+        *cap = G->cap;
+    });
+}
+
+int gs_render_backward(gs_map* M, const gs_pose* pose, const gs_camera* cam, gs_frame* F, const double* dl_dcolor,
+                       const double* dl_ddepth, int32_t h, int32_t w, gs_grads* G) {
+    return guard([&] {
+        validate_camera(*cam);
+        M->ctx->use();
+        (void)pose;
+        if (h != cam->height || w != cam->width) fail(GS_EINVAL, "render_backward: dl_dcolor dimensions mismatch");
+        need_rendered(F);
+        if (F->view.width != cam->width || F->view.height != cam->height)
+            fail(GS_ELOGIC, "render_backward: contributor lists missing or inconsistent");
+        const size_t P = static_cast<size_t>(h) * w;
+        cudaStream_t st = M->ctx->stream;
+        DevBuf tmp;
+        tmp.ensure(sizeof(double) * 4 * P);
+        ck(cudaMemcpyAsync(tmp.p, dl_dcolor, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(tmp.as<double>() + 3 * P, dl_ddepth, sizeof(double) * P, cudaMemcpyHostToDevice, st), "h2d");
+        launch_from_hwc_double(tmp.as<double>(), h, w, 3, F->dl_dcolor.as<float>(), st);
+        launch_from_hwc_double(tmp.as<double>() + 3 * P, h, w, 1, F->depth_cot.as<float>(), st);
+        M->ctx->launched(2);
+        grads_zero(G, M);
+        backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(), nullptr, G);
+        ck(cudaStreamSynchronize(st), "sync");
+        tmp.release();
+    });
+}
+
+int gs_apply_gradients(gs_map* M, gs_grads* G, const gs_learning_rates* lr) {
+    return guard([&] {
+        M->ctx->use();
+        adam_impl(M, G, *lr);
+    });
+}
+
+// ---------------------------------------------------------------- keyframes / loss / step
+int gs_keyframe_create(gs_context* C, const gs_pose* pose, const double* color, const double* sparse_depth, int32_t h,
+                       int32_t w, int32_t initial_iters, int32_t levels, gs_keyframe** out) {
+    return guard([&] {
+        C->use();
+        auto* K = new gs_keyframe();
+        K->ctx = C;
+        K->pose = *pose;
+        K->initial_iters = initial_iters;
+        try {
+            const size_t P = static_cast<size_t>(h) * w;
+            std::vector<float> cp(3 * P), dp(P);
+            for (size_t p = 0; p < P; ++p) {
+                for (int c = 0; c < 3; ++c) cp[c * P + p] = static_cast<float>(color[p * 3 + c]);
+                dp[p] = static_cast<float>(sparse_depth[p]);
+            }
+            keyframe_build(K, cp.data(), dp.data(), h, w, levels, false);
+        } catch (...) {
+            delete K;
+            throw;
+        }
+        *out = K;
+    });
+}
+
+int gs_keyframe_create_device(gs_context* C, const gs_pose* pose, const float* color_planes, const float* depth,
+                              int32_t h, int32_t w, int32_t initial_iters, int32_t levels, gs_keyframe** out) {
+    return guard([&] {
+        C->use();
+        auto* K = new gs_keyframe();
+        K->ctx = C;
+        K->pose = *pose;
+        K->initial_iters = initial_iters;
+        try {
+            keyframe_build(K, color_planes, depth, h, w, levels, true);
+        } catch (...) {
+            delete K;
+            throw;
+        }
+        *out = K;
+    });
+}
+
+int gs_keyframe_destroy(gs_keyframe* K) {
+    return guard([&] {
+        if (!K) return;
+        cudaStreamSynchronize(K->ctx->stream);
+        delete K;
+    });
+}
+
+int gs_keyframe_consumed(gs_keyframe* K, int32_t* c) { return guard([&] { *c = K->consumed; }); }
+int gs_keyframe_set_consumed(gs_keyframe* K, int32_t c) { return guard([&] { K->consumed = c; }); }
+int gs_keyframe_levels(gs_keyframe* K, int32_t* n) { return guard([&] { *n = static_cast<int32_t>(K->hs.size()); }); }
+
+int gs_keyframe_read_level(gs_keyframe* K, int32_t level, double* color, double* depth) {
+    return guard([&] {
+        if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
+        const int h = K->hs[level], w = K->ws[level];
+        const size_t P = static_cast<size_t>(h) * w;
+        std::vector<float> cp(3 * P), dp(P);
+        cudaStream_t st = K->ctx->stream;
+        ck(cudaMemcpyAsync(cp.data(), K->color[level].p, sizeof(float) * 3 * P, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(dp.data(), K->depth[level].p, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        for (size_t p = 0; p < P; ++p) {
+            if (color)
+                for (int c = 0; c < 3; ++c) color[p * 3 + c] = cp[c * P + p];
+            if (depth) depth[p] = dp[p];
+        }
+    });
+}
+
+int gs_compute_loss(gs_frame* F, gs_keyframe* K, int32_t level, const gs_train_config* cfg, gs_loss_result* out,
+                    double* dl_dcolor, double* dl_ddepth) {
+    return guard([&] {
+        F->ctx->use();
+        loss_impl(F, K, level, *cfg);
+        if (out) *out = read_loss(F);
+        const int h = F->view.height, w = F->view.width;
+        const size_t P = static_cast<size_t>(h) * w;
+        if (dl_dcolor || dl_ddepth) {
+            cudaStream_t st = F->ctx->stream;
+            std::vector<float> dc(3 * P), dd(P);
+            LossScalars s;
+            ck(cudaMemcpyAsync(dc.data(), F->dl_dcolor.p, sizeof(float) * 3 * P, cudaMemcpyDeviceToHost, st), "d2h");
+            ck(cudaMemcpyAsync(dd.data(), F->depth_cot.p, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "d2h");
+            ck(cudaMemcpyAsync(&s, F->loss.p, sizeof(s), cudaMemcpyDeviceToHost, st), "d2h");
+            ck(cudaStreamSynchronize(st), "sync");
+            for (size_t p = 0; p < P; ++p) {
+                if (dl_dcolor)
+                    for (int c = 0; c < 3; ++c) dl_dcolor[p * 3 + c] = dc[c * P + p];
+                if (dl_ddepth) dl_ddepth[p] = static_cast<double>(dd[p]) * s.depth_scale;
+            }
+        }
+    });
+}
+
+int gs_render_backward_frame(gs_map* M, const gs_pose* pose, const gs_camera* cam, gs_frame* F, gs_grads* G) {
+    return guard([&] {
+        (void)pose;
+        (void)cam;
+        M->ctx->use();
+        if (!F->has_cotangent) fail(GS_ELOGIC, "render_backward_frame: no cotangent (call gs_compute_loss first)");
+        G->ensure(std::max<int64_t>(M->n, 1));
+        if (G->n != M->n) grads_zero(G, M);
+        backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
+                      &F->loss.as<LossScalars>()->depth_scale, G);
+    });
+}
+
+int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_step_report* report) {
+    return guard([&] {
+        M->ctx->use();
+        *report = gs_step_report{};
+        if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
+        if (K->consumed >= K->initial_iters) return;  // std::nullopt (mapper.cpp:219)
+        gs_frame* F = scratch_frame(M->ctx);
+        gs_grads* G = scratch_grads(M->ctx);
+        grads_zero(G, M);
+        int level = 0;
+        train_view(M, K, *cfg, *cam, F, G, &level);
+        adam_impl(M, G, cfg->lr);
+        ++K->consumed;
+        const gs_loss_result lr = read_loss(F);
+        report->ran = 1;
+        report->level = level;
+        report->loss = lr.total;
+        report->psnr = lr.psnr;
+    });
+}
+
+int gs_train_accumulate(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_frame* F,
+                        gs_grads* G, int32_t sync, gs_step_report* report) {
+    return guard([&] {
+        M->ctx->use();
+        *report = gs_step_report{};
+        if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
+        if (K->consumed >= K->initial_iters) return;
+        if (!F) F = scratch_frame(M->ctx);
+        G->ensure(std::max<int64_t>(M->n, 1));
+        if (G->n != M->n) grads_zero(G, M);
+        int level = 0;
+        train_view(M, K, *cfg, *cam, F, G, &level);
+        ++K->consumed;
+        report->ran = 1;
+        report->level = level;
+        if (sync) {
+            const gs_loss_result lr = read_loss(F);
+            report->loss = lr.total;
+            report->psnr = lr.psnr;
+        }
+    });
+}
+
+}  // extern "C"

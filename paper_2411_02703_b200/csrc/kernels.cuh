@@ -1,0 +1,50 @@
+// Host-side launchers for the gsmap_b200 kernels (one declaration per kernel family).
+#pragma once
+
+#include "common.cuh"
+
+namespace gsb {
+
+// geometry.cu (FP64, --fmad=false)
+void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, int n,
+                           const ViewParams& v, Splat* rec_by_gid, uint8_t* vis_flag,
+                           unsigned long long* depth_key, unsigned long long* counters, cudaStream_t st);
+void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
+                           const Splat* rec, const uint32_t* emit_off, const float* partials, int n_vis,
+                           float* grads, int64_t gcap, cudaStream_t st);
+
+// raster.cu
+void launch_gather_keys(const int32_t* vis_gid, const unsigned long long* depth_key_by_gid, int n_vis,
+                        unsigned long long* keys_out, cudaStream_t st);
+void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, int n_vis, Splat* rec_sorted,
+                 uint32_t* ntiles_sorted, cudaStream_t st);
+void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, int n_vis, uint32_t n_pairs, int tiles_x,
+                       uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_tile_ranges(const uint32_t* keys_sorted, uint32_t n_pairs, uint2* ranges, cudaStream_t st);
+void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
+                      float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
+                      int32_t* n_contrib, cudaStream_t st);
+void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
+                      const ViewParams& v, const float* t_final, const int32_t* n_proc,
+                      const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
+                      float* partials, cudaStream_t st);
+void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
+                        const uint32_t* offsets, int32_t* out_gid, double* out_alpha, cudaStream_t st);
+
+// loss.cu
+void launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
+                       const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
+                       float* depth_cot, LossScalars* acc, cudaStream_t st);
+void launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
+                 float* dl_dcolor, LossScalars* acc, cudaStream_t st);
+void launch_loss_finalize(LossScalars* acc, double lambda_d, cudaStream_t st);
+void launch_downsample(const float* in, int h, int w, int channels, bool depth, float* out, cudaStream_t st);
+
+// adam.cu
+void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
+                 int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, cudaStream_t st);
+void launch_position_minmax(const float* params, int64_t cap, int n, float* out6, cudaStream_t st);
+void launch_to_hwc_double(const float* planes, int h, int w, int channels, double* out, cudaStream_t st);
+void launch_from_hwc_double(const double* hwc, int h, int w, int channels, float* planes, cudaStream_t st);
+
+}  // namespace gsb

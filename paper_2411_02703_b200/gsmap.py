@@ -1,0 +1,499 @@
+"""Python mirror of the reference's hot-path interface over the B200 C-ABI (include/gsmap_b200.h).
+
+Names, argument meaning and error behaviour follow proj/include/gsmap/{render/rasterizer.hpp,
+map/gaussian_map.hpp, map/mapper.hpp}: ``render``, ``render_backward``,
+``GaussianMap.apply_gradients``, ``compute_loss``, ``train_keyframe_step``; ``ValueError``
+stands in for std::invalid_argument and ``LogicError`` for std::logic_error.
+
+There is no CPU fallback: importing this module on a machine where the in-tree
+``libgsmap_b200.so`` is missing raises, and every call runs the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsmap_b200.so")
+
+GAUSS_DTYPE = np.dtype([("p", "<f8", (59,)), ("degree", "<i4"), ("pad", "<i4")])
+
+GS_OK, GS_EINVAL, GS_ELOGIC, GS_ECUDA, GS_ENCCL, GS_ENOMEM = range(6)
+
+
+class Camera(C.Structure):  # gsmap::CameraModel (core/types.hpp:15-45)
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class Pose(C.Structure):  # gsmap::Pose with q already normalised (core/types.hpp:48-64)
+    _fields_ = [("qw", C.c_double), ("qx", C.c_double), ("qy", C.c_double), ("qz", C.c_double),
+                ("tx", C.c_double), ("ty", C.c_double), ("tz", C.c_double)]
+
+
+class LearningRates(C.Structure):  # map/gaussian_map.hpp:34-40
+    _fields_ = [("position", C.c_double), ("rotation", C.c_double), ("log_scale", C.c_double),
+                ("opacity", C.c_double), ("sh", C.c_double)]
+
+    @classmethod
+    def default(cls):
+        return cls(1.6e-4, 1e-3, 5e-3, 5e-2, 2.5e-3)
+
+
+class TrainConfig(C.Structure):  # map/mapper.hpp:17-30 (hot-path fields)
+    _fields_ = [("lambda_", C.c_double), ("lambda_d", C.c_double), ("pyramid_levels", C.c_int32),
+                ("iters_per_level", C.c_int32), ("lr", LearningRates)]
+
+    @classmethod
+    def make(cls, lam=0.2, lam_d=0.5, levels=2, ipl=0, lr=None):
+        return cls(lam, lam_d, levels, ipl, lr or LearningRates.default())
+
+
+class LossResult(C.Structure):
+    _fields_ = [("total", C.c_double), ("color_loss", C.c_double), ("depth_loss", C.c_double),
+                ("l1", C.c_double), ("ssim", C.c_double), ("psnr", C.c_double)]
+
+
+class StepReport(C.Structure):
+    _fields_ = [("ran", C.c_int32), ("level", C.c_int32), ("loss", C.c_double), ("psnr", C.c_double)]
+
+
+class FrameStats(C.Structure):
+    _fields_ = [("n_visible", C.c_int64), ("n_pairs", C.c_int64), ("n_contrib", C.c_int64),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class LogicError(RuntimeError):
+    """std::logic_error"""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"gsmap_b200: CUDA extension {LIB_PATH} is not built "
+                              "(run __graft_entry__.build()); there is no CPU fallback")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.gs_last_error.restype = C.c_char_p
+        _lib.gs_version.restype = C.c_char_p
+    return _lib
+
+
+def _check(st: int):
+    if st == GS_OK:
+        return
+    msg = lib().gs_last_error().decode()
+    if st == GS_EINVAL:
+        raise ValueError(msg)
+    if st == GS_ELOGIC:
+        raise LogicError(msg)
+    if st == GS_ENOMEM:
+        raise MemoryError(msg)
+    raise CudaError(msg)
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _vp(h):
+    return C.c_void_p(h)
+
+
+def exported_symbols():
+    """Names the header declares; used by the CPU symbol test."""
+    return [n for n in dir(lib()) if n.startswith("gs_")]
+
+
+# --------------------------------------------------------------------------- context
+class Context:
+    """One device + one CUDA stream (defaults to the library's own non-blocking stream)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = C.c_void_p()
+        _check(lib().gs_context_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h.value
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gs_context_destroy(_vp(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().gs_context_synchronize(_vp(self.h)))
+
+    def set_stream(self, stream: int):
+        _check(lib().gs_context_set_stream(_vp(self.h), C.c_void_p(stream)))
+
+    @property
+    def launches(self) -> int:
+        n = C.c_int64()
+        _check(lib().gs_context_launch_count(_vp(self.h), C.byref(n)))
+        return n.value
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def camera_scaled(cam: Camera, level: int) -> Camera:
+    out = Camera()
+    _check(lib().gs_camera_scaled(C.byref(cam), level, C.byref(out)))
+    return out
+
+
+def validate_camera(cam: Camera):
+    _check(lib().gs_camera_validate(C.byref(cam)))
+
+
+# --------------------------------------------------------------------------- GaussianMap
+class GaussianMap:
+    """gsmap::GaussianMap (map/gaussian_map.hpp:44-96) resident on the GPU (fp32 SoA + Adam)."""
+
+    def __init__(self, ctx: Context | None = None, gaussians: np.ndarray | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(lib().gs_map_create(_vp(self.ctx.h), C.byref(h)))
+        self.h = h.value
+        if gaussians is not None and len(gaussians):
+            self.append(gaussians)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().gs_map_destroy(_vp(self.h))
+                self.h = None
+        except Exception:
+            pass
+
+    def __len__(self):
+        n = C.c_int64()
+        _check(lib().gs_map_size(_vp(self.h), C.byref(n)))
+        return n.value
+
+    def append(self, g: np.ndarray):
+        g = np.ascontiguousarray(g, dtype=GAUSS_DTYPE)
+        _check(lib().gs_map_append(_vp(self.h), _p(g), C.c_int64(len(g))))
+
+    @property
+    def gaussians(self) -> np.ndarray:
+        n = len(self)
+        g = np.zeros(n, dtype=GAUSS_DTYPE)
+        _check(lib().gs_map_get_gaussians(_vp(self.h), _p(g), C.c_int64(n)))
+        return g
+
+    @gaussians.setter
+    def gaussians(self, g: np.ndarray):
+        g = np.ascontiguousarray(g, dtype=GAUSS_DTYPE)
+        _check(lib().gs_map_set_gaussians(_vp(self.h), _p(g), C.c_int64(len(g))))
+
+    def adam_state(self):
+        n = len(self)
+        m = np.zeros((n, 59)); v = np.zeros((n, 59)); s = np.zeros(n, np.int64)
+        _check(lib().gs_map_get_adam(_vp(self.h), _p(m), _p(v), _p(s), C.c_int64(n)))
+        return m, v, s
+
+    def set_adam_state(self, m, v, s):
+        m = np.ascontiguousarray(m, np.float64); v = np.ascontiguousarray(v, np.float64)
+        s = np.ascontiguousarray(s, np.int64)
+        _check(lib().gs_map_set_adam(_vp(self.h), _p(m), _p(v), _p(s), C.c_int64(len(s))))
+
+    @property
+    def scene_extent(self) -> float:
+        e = C.c_double()
+        _check(lib().gs_map_scene_extent(_vp(self.h), C.byref(e)))
+        return e.value
+
+    @scene_extent.setter
+    def scene_extent(self, e: float):
+        _check(lib().gs_map_set_scene_extent(_vp(self.h), C.c_double(e)))
+
+    @property
+    def global_step(self) -> int:
+        s = C.c_int64()
+        _check(lib().gs_map_global_step(_vp(self.h), C.byref(s)))
+        return s.value
+
+    @global_step.setter
+    def global_step(self, s: int):
+        _check(lib().gs_map_set_global_step(_vp(self.h), C.c_int64(s)))
+
+    def raise_sh_degree(self, d: int):
+        _check(lib().gs_map_raise_sh_degree(_vp(self.h), d))
+
+    def max_active_degree(self) -> int:
+        d = C.c_int()
+        _check(lib().gs_map_max_active_degree(_vp(self.h), C.byref(d)))
+        return d.value
+
+    def apply_gradients(self, grads: "RenderGradients", lr: LearningRates | None = None):
+        """GaussianMap::apply_gradients (gaussian_map.cpp:37-54)."""
+        _check(lib().gs_apply_gradients(_vp(self.h), _vp(grads.h), C.byref(lr or LearningRates.default())))
+
+    def device_planes(self):
+        p, m, v, cap = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_int64()
+        _check(lib().gs_map_device_planes(_vp(self.h), C.byref(p), C.byref(m), C.byref(v), C.byref(cap)))
+        return p.value, m.value, v.value, cap.value
+
+
+# --------------------------------------------------------------------------- gradients
+class RenderGradients:
+    """gsmap::RenderGradients (rasterizer.hpp:62-64) as device fp32 planes [59][capacity]."""
+
+    def __init__(self, ctx: Context | None = None, external_ptr: int | None = None, capacity: int = 0):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        if external_ptr is not None:
+            _check(lib().gs_grads_create_external(_vp(self.ctx.h), C.c_void_p(external_ptr), C.c_int64(capacity),
+                                                  C.byref(h)))
+        else:
+            _check(lib().gs_grads_create(_vp(self.ctx.h), C.byref(h)))
+        self.h = h.value
+        self.n = 0
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().gs_grads_destroy(_vp(self.h))
+                self.h = None
+        except Exception:
+            pass
+
+    def zero(self, m: GaussianMap):
+        _check(lib().gs_grads_zero(_vp(self.h), _vp(m.h)))
+        self.n = len(m)
+
+    def read(self, n: int | None = None) -> np.ndarray:
+        n = self.n if n is None else n
+        out = np.zeros((n, 59))
+        _check(lib().gs_grads_read(_vp(self.h), _p(out), C.c_int64(n)))
+        return out
+
+    def write(self, g: np.ndarray):
+        g = np.ascontiguousarray(g, np.float64)
+        _check(lib().gs_grads_write(_vp(self.h), _p(g), C.c_int64(g.shape[0])))
+        self.n = g.shape[0]
+
+    @property
+    def per_gaussian(self) -> np.ndarray:
+        return self.read()
+
+    def device_planes(self):
+        p, cap = C.c_void_p(), C.c_int64()
+        _check(lib().gs_grads_device_planes(_vp(self.h), C.byref(p), C.byref(cap)))
+        return p.value, cap.value
+
+
+# --------------------------------------------------------------------------- render
+class RenderOutput:
+    """gsmap::RenderOutput (rasterizer.hpp:43-59). Images download lazily as fp64 HWC; the
+    contributor CSR and the projected set are materialised only on request."""
+
+    def __init__(self, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(lib().gs_frame_create(_vp(self.ctx.h), C.byref(h)))
+        self.h = h.value
+        self.cam = None
+        self._imgs = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().gs_frame_destroy(_vp(self.h))
+                self.h = None
+        except Exception:
+            pass
+
+    def _images(self):
+        if self._imgs is None:
+            H, W = self.cam.height, self.cam.width
+            c = np.zeros((H, W, 3)); d = np.zeros((H, W)); v = np.zeros((H, W))
+            _check(lib().gs_frame_read(_vp(self.h), _p(c), _p(d), _p(v)))
+            self._imgs = (c, d, v)
+        return self._imgs
+
+    @property
+    def color(self):
+        return self._images()[0]
+
+    @property
+    def depth(self):
+        return self._images()[1]
+
+    @property
+    def visibility(self):
+        return self._images()[2]
+
+    def stats(self) -> FrameStats:
+        s = FrameStats()
+        _check(lib().gs_frame_stats_get(_vp(self.h), C.byref(s)))
+        return s
+
+    def pixel_state(self):
+        H, W = self.cam.height, self.cam.width
+        nc = np.zeros((H, W), np.int32); t = np.zeros((H, W), np.float32)
+        _check(lib().gs_frame_read_pixel_state(_vp(self.h), _p(nc), _p(t)))
+        return nc, t
+
+    def projected(self):
+        n = self.stats().n_visible
+        d = dict(index=np.zeros(n, np.int32), mean=np.zeros((n, 2)), rect=np.zeros((n, 4), np.int32),
+                 conic=np.zeros((n, 3), np.float32), opacity=np.zeros(n, np.float32),
+                 color=np.zeros((n, 3), np.float32), depth=np.zeros(n))
+        _check(lib().gs_frame_read_projected(_vp(self.h), *[_p(d[k]) for k in
+                                             ("index", "mean", "rect", "conic", "opacity", "color", "depth")]))
+        return d
+
+    def tiles(self):
+        s = self.stats()
+        off = np.zeros(s.tiles_x * s.tiles_y + 1, np.int64); ent = np.zeros(s.n_pairs, np.int32)
+        _check(lib().gs_frame_read_tiles(_vp(self.h), _p(off), _p(ent)))
+        return off, ent
+
+    def csr(self):
+        s = self.stats()
+        off = np.zeros(s.width * s.height + 1, np.uint32)
+        g = np.zeros(s.n_contrib, np.int32); a = np.zeros(s.n_contrib)
+        _check(lib().gs_frame_materialize(_vp(self.h), _p(off), _p(g), _p(a)))
+        return off, g, a
+
+    def contributors(self, y: int, x: int):
+        off, g, a = self.csr()
+        p = y * self.cam.width + x
+        return list(zip(g[off[p]:off[p + 1]].tolist(), a[off[p]:off[p + 1]].tolist()))
+
+    def device_images(self):
+        c, d, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().gs_frame_device_images(_vp(self.h), C.byref(c), C.byref(d), C.byref(v)))
+        return c.value, d.value, v.value
+
+
+def render(m: GaussianMap, pose: Pose, cam: Camera, out: RenderOutput | None = None, pool=None) -> RenderOutput:
+    """rasterizer.hpp:69-70. ``pool`` (the reference's ThreadPool*) is accepted and ignored."""
+    out = out or RenderOutput(m.ctx)
+    out.cam = Camera(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    out._imgs = None
+    _check(lib().gs_render(_vp(m.h), C.byref(pose), C.byref(cam), _vp(out.h)))
+    return out
+
+
+def render_backward(m: GaussianMap, pose: Pose, cam: Camera, out: RenderOutput, dl_dcolor, dl_ddepth,
+                    pool=None, grads: RenderGradients | None = None) -> RenderGradients:
+    """rasterizer.hpp:74-77: fresh RenderGradients for the cotangents (host fp64 HWC)."""
+    dc = np.ascontiguousarray(dl_dcolor, np.float64)
+    dd = np.ascontiguousarray(dl_ddepth, np.float64)
+    if dc.ndim != 3 or dc.shape != (cam.height, cam.width, 3):
+        raise ValueError("render_backward: dl_dcolor dimensions mismatch")
+    if dd.shape != (cam.height, cam.width):
+        raise ValueError("render_backward: dl_ddepth dimensions mismatch")
+    g = grads or RenderGradients(m.ctx)
+    _check(lib().gs_render_backward(_vp(m.h), C.byref(pose), C.byref(cam), _vp(out.h), _p(dc), _p(dd),
+                                    cam.height, cam.width, _vp(g.h)))
+    g.n = len(m)
+    return g
+
+
+# --------------------------------------------------------------------------- keyframes / loss / step
+class Keyframe:
+    """gsmap::Keyframe hot-path fields (map/keyframe.hpp:23-34) with its pyramid on the device."""
+
+    def __init__(self, pose: Pose, color=None, sparse_depth=None, initial_iters: int = 0, levels: int = 2,
+                 ctx: Context | None = None, device_planes: tuple | None = None, hw: tuple | None = None):
+        self.ctx = ctx or default_context()
+        self.pose = pose
+        h = C.c_void_p()
+        if device_planes is not None:
+            H, W = hw
+            _check(lib().gs_keyframe_create_device(_vp(self.ctx.h), C.byref(pose), C.c_void_p(device_planes[0]),
+                                                   C.c_void_p(device_planes[1]), H, W, initial_iters, levels,
+                                                   C.byref(h)))
+        else:
+            color = np.ascontiguousarray(color, np.float64)
+            sparse_depth = np.ascontiguousarray(sparse_depth, np.float64)
+            H, W = color.shape[:2]
+            _check(lib().gs_keyframe_create(_vp(self.ctx.h), C.byref(pose), _p(color), _p(sparse_depth), H, W,
+                                            initial_iters, levels, C.byref(h)))
+        self.h = h.value
+        self.shape = (H, W)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().gs_keyframe_destroy(_vp(self.h))
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def consumed_iters(self) -> int:
+        c = C.c_int32()
+        _check(lib().gs_keyframe_consumed(_vp(self.h), C.byref(c)))
+        return c.value
+
+    @consumed_iters.setter
+    def consumed_iters(self, c: int):
+        _check(lib().gs_keyframe_set_consumed(_vp(self.h), c))
+
+    def level(self, l: int):
+        H, W = self.shape
+        for _ in range(l):
+            H, W = (H + 1) // 2, (W + 1) // 2
+        c = np.zeros((H, W, 3)); d = np.zeros((H, W))
+        _check(lib().gs_keyframe_read_level(_vp(self.h), l, _p(c), _p(d)))
+        return c, d
+
+
+def compute_loss(out: RenderOutput, kf: Keyframe, level: int, cfg: TrainConfig, with_cotangents: bool = True):
+    """mapper.cpp:146-212 -> dict(total, color_loss, depth_loss, l1, ssim, psnr, dl_dcolor, dl_ddepth)."""
+    r = LossResult()
+    H, W = out.cam.height, out.cam.width
+    dc = np.zeros((H, W, 3)) if with_cotangents else None
+    dd = np.zeros((H, W)) if with_cotangents else None
+    _check(lib().gs_compute_loss(_vp(out.h), _vp(kf.h), level, C.byref(cfg), C.byref(r), _p(dc), _p(dd)))
+    res = {k: getattr(r, k) for k, _ in LossResult._fields_}
+    res["dl_dcolor"], res["dl_ddepth"] = dc, dd
+    return res
+
+
+def train_keyframe_step(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera, pool=None):
+    """mapper.cpp:214-238. Returns dict(level, loss, psnr) or None when the budget is spent."""
+    rep = StepReport()
+    _check(lib().gs_train_step(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), C.byref(rep)))
+    if not rep.ran:
+        return None
+    return dict(level=rep.level, loss=rep.loss, psnr=rep.psnr)
+
+
+def train_accumulate(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera, grads: RenderGradients,
+                     frame: RenderOutput | None = None, sync: bool = False):
+    """One view of a keyframe batch: render + loss + backward, gradients summed into ``grads``."""
+    rep = StepReport()
+    _check(lib().gs_train_accumulate(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam),
+                                     _vp(frame.h) if frame else None, _vp(grads.h), int(sync), C.byref(rep)))
+    grads.n = len(m)
+    if not rep.ran:
+        return None
+    return dict(level=rep.level, loss=rep.loss, psnr=rep.psnr)

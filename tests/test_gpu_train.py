@@ -1,0 +1,148 @@
+"""GPU loss (L1 + SSIM + masked depth), pyramid, Adam and the fused train_keyframe_step against
+the CPU fp64 oracle, through the C-ABI."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from tests._common import gpu_cam, gpu_pose, pair, random_scene, rel_err, round32
+
+pytestmark = pytest.mark.gpu
+
+
+def G():
+    from paper_2411_02703_b200 import gsmap
+    return gsmap
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+def test_pyramid_matches_oracle():  # mapper.cpp:65-144
+    gen = np.random.default_rng(1)
+    col = f32(gen.uniform(0, 1, (37, 53, 3)))
+    dep = f32(np.where(gen.uniform(size=(37, 53)) < 0.3, gen.uniform(1, 5, (37, 53)), 0.0))
+    kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), col, dep, 10, 2)
+    oc = O.build_pyramid(col, 2)
+    od = O.build_pyramid(dep, 2, depth=True)
+    for l in range(3):
+        c, d = kf.level(l)
+        assert np.abs(c - oc[l]).max() < 1e-6
+        assert np.abs(d - od[l]).max() < 1e-5
+
+
+def test_pyramid_rejects_too_small():
+    with pytest.raises(ValueError):
+        G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), np.zeros((3, 3, 3)), np.zeros((3, 3)), 1, 2)
+
+
+@pytest.mark.parametrize("lam,lam_d", [(0.2, 0.5), (0.0, 0.0), (0.0, 0.5), (0.2, 0.0)])
+def test_loss_matches_oracle(lam, lam_d):
+    """compute_loss on the GPU's own render vs the oracle's compute_loss on the same images."""
+    cam = O.camera(120, 120, 63.5, 47.5, 128, 96)
+    om, gm = pair(random_scene(8, 300, cam, O.pose(), 0.0, 2.5))
+    gen = np.random.default_rng(8)
+    gt = f32(gen.uniform(0, 1, (96, 128, 3)))
+    gd = f32(np.where(gen.uniform(size=(96, 128)) < 0.5, gen.uniform(1, 8, (96, 128)), 0.0))
+    kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), gt, gd, 10, 0)
+    go = G().render(gm, gpu_pose(O.pose()), gpu_cam(cam))
+    cfg = G().TrainConfig.make(lam, lam_d, 0)
+    r = G().compute_loss(go, kf, 0, cfg)
+    ref = O.compute_loss(go.color, go.depth, go.visibility, gt, gd, O.make_cfg(lam, lam_d, 0))
+    for k in ("total", "l1", "ssim", "color_loss", "depth_loss"):
+        assert r[k] == pytest.approx(ref[k], rel=1e-5, abs=1e-7), k
+    assert r["psnr"] == pytest.approx(O.psnr(go.color, gt), rel=1e-6)
+    scale = np.abs(ref["dl_dcolor"]).max()
+    assert np.abs(r["dl_dcolor"] - ref["dl_dcolor"]).max() <= 1e-4 * scale + 1e-12
+    dscale = max(np.abs(ref["dl_ddepth"]).max(), 1e-30)
+    assert np.abs(r["dl_ddepth"] - ref["dl_ddepth"]).max() <= 1e-5 * dscale
+
+
+def test_loss_rejects_wrong_level_resolution():
+    cam = O.camera(100, 100, 32, 32, 64, 64)
+    _, gm = pair(O.make_blob([0, 0, 2], 0.5, [1, 0, 0]))
+    kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), np.zeros((64, 64, 3)), np.zeros((64, 64)), 10, 1)
+    go = G().render(gm, gpu_pose(O.pose()), gpu_cam(cam))
+    with pytest.raises(ValueError):
+        G().compute_loss(go, kf, 1, G().TrainConfig.make())
+    with pytest.raises(ValueError):
+        G().compute_loss(go, kf, 5, G().TrainConfig.make())
+
+
+def test_adam_matches_oracle():  # gaussian_map.cpp:37-54
+    gen = np.random.default_rng(3)
+    g0 = O.empty_gaussians(300)
+    g0["p"][:] = gen.normal(size=(300, 59)); g0["degree"] = gen.integers(0, 4, 300)
+    om, gm = pair(g0)
+    assert gm.scene_extent == om.scene_extent
+    for t in range(3):
+        grads = round32_arr(gen.normal(size=(300, 59)) * 10.0 ** gen.uniform(-6, 1, (300, 59)))
+        for i, d in enumerate(g0["degree"]):  # inactive SH coefficients carry no gradient
+            grads[i, 11 + 3 * (d + 1) ** 2:] = 0.0
+        om.apply_gradients(grads)
+        gg = G().RenderGradients(gm.ctx)
+        gg.write(grads)
+        gm.apply_gradients(gg)
+        a, b = gm.gaussians["p"], om.gaussians["p"]
+        lr = np.array([1.6e-4 * om.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+        # Adam's step is ~lr*sign; fp32 parameter storage rounds at ~6e-8 relative
+        assert np.all(np.abs(a - b) <= 1e-4 * lr + 4e-7 * np.abs(b)), t
+    _, _, steps = gm.adam_state()
+    assert np.all(steps == 3) and gm.global_step == 3
+
+
+def round32_arr(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+def test_apply_gradients_rejects_mismatch():  # test_mapper.cpp:337-344
+    _, gm = pair(O.make_blob([0, 0, 2], 0.5, [1, 0, 0]))
+    gg = G().RenderGradients(gm.ctx)
+    gg.write(np.zeros((3, 59)))
+    with pytest.raises(ValueError):
+        gm.apply_gradients(gg)
+
+
+def test_level_schedule_and_budget():  # test_mapper.cpp:206-239
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    _, gm = pair(random_scene(9, 30, cam, O.pose()))
+    kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), np.full((48, 64, 3), 0.3), np.zeros((48, 64)), 30, 2)
+    cfg = G().TrainConfig.make(levels=2, ipl=10)
+    levels = [G().train_keyframe_step(gm, kf, cfg, gpu_cam(cam))["level"] for _ in range(30)]
+    assert levels == [2] * 10 + [1] * 10 + [0] * 10
+    assert G().train_keyframe_step(gm, kf, cfg, gpu_cam(cam)) is None
+    assert gm.global_step == 30
+
+
+def test_train_steps_track_oracle():
+    """A few full train_keyframe_step iterations (render -> loss -> backward -> Adam) on both;
+    losses agree and parameters stay within a few Adam steps' worth of each other."""
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    gt_map = O.random_scene(O.Rng(21), 40, cam, O.pose(), 1.0, 2.0)
+    gt = O.render(gt_map, O.pose(), cam)
+    g = gt_map.gaussians
+    g["p"][:, 10] = np.log(0.1 / 0.9)
+    g["p"][:, 7:10] += 0.4
+    om, gm = pair(g)
+    color = f32(gt.color)
+    sparse = f32(np.where(np.random.default_rng(1).uniform(size=(48, 64)) < 0.2, gt.depth, 0.0))
+    okf = O.Keyframe(O.pose(), color, sparse, 6, 1)
+    gkf = G().Keyframe(gpu_pose(O.pose()), color, sparse, 6, 1)
+    ocfg = O.make_cfg(0.2, 0.5, 1)
+    gcfg = G().TrainConfig.make(0.2, 0.5, 1)
+    for it in range(6):
+        ro = O.train_keyframe_step(om, okf, ocfg, cam)
+        rg = G().train_keyframe_step(gm, gkf, gcfg, gpu_cam(cam))
+        assert rg["level"] == ro["level"]
+        assert rg["loss"] == pytest.approx(ro["loss"], rel=2e-3)
+        assert rg["psnr"] == pytest.approx(ro["psnr"], rel=1e-3)
+    lr = np.array([1.6e-4 * om.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+    d = np.abs(gm.gaussians["p"] - om.gaussians["p"])
+    assert np.all(d <= 6 * 2 * lr + 1e-6)
+    assert np.mean(d <= 0.05 * lr + 1e-6) > 0.95
+
+
+def test_train_step_requires_pyramid_semantics():
+    _, gm = pair(O.make_blob([0, 0, 2], 0.5, [1, 0, 0]))
+    kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), np.zeros((64, 64, 3)), np.zeros((64, 64)), 0, 0)
+    assert G().train_keyframe_step(gm, kf, G().TrainConfig.make(), G().Camera(100, 100, 32, 32, 64, 64)) is None
