@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark of the LVI-GS mapping hot path on B200 (BASELINE.json metric).
+
+Metric: training iterations/s (render -> L1+SSIM+depth loss -> backward -> Adam, one keyframe
+view per iteration at its scheduled pyramid level) and Mpix/s, 1M Gaussians at 1280x1024,
+3-level pyramid (levels 2,1,0 = 320x256 / 640x512 / 1280x1024), lambda=0.2, lambda_d=0.5.
+
+  python bench.py [--steps K] [--warmup W] [--impl ours|reference] [--sh-degree 0|3]
+  torchrun --nproc-per-node N bench.py --gpus N      (C4: 8-view batch sharded over N GPUs,
+                                                      NCCL all-reduce of the gradient SoA)
+
+Workload: synthetic scene = proj/src/io/synthetic.cpp restated (fixtures/),
+focal 0.8125*W, extent 18, line trajectory, 8 frames, seed 1, LiDAR noise 0.06 m; the
+training map is the colourised-LiDAR initialisation (all 1M GT centres displaced along the
+frame-0 beam, 3-NN isotropic scale, opacity 0.1, SH degree 0). GT colour = the GT map
+rendered at level 0; LiDAR depth = project_sparse_depth of each frame's cloud. Eight
+keyframes, each consumes its pyramid coarse-to-fine (iters_per_level = 1) and is then
+recycled, so every 3 consecutive iterations cover levels 2, 1, 0 once (K multiple of 3).
+Inputs (1M-Gaussian params + Adam state ~ 240 MB at d=0) exceed the 126 MB L2: no flush.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training iters/sec (fwd+bwd+Adam) and Mpix/s at 1M Gaussians 1280×1024, 1/2/4/8 B200"
+N_GAUSS, W0, H0, N_FRAMES, LEVELS = 1_000_000, 1280, 1024, 8, 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sh-degree", type=int, default=0)
+    ap.add_argument("--n-gaussians", type=int, default=N_GAUSS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workload
+def build_fixture(n_gauss):
+    from fixtures import pyfixture as F
+    t = time.time()
+    scene = F.Scene(n_gaussians=n_gauss, width=W0, height=H0, n_frames=N_FRAMES, seed=1)
+    train = scene.training_map(seed=2, noise=0.06)
+    return scene, train, time.time() - t
+
+
+def level_shapes():
+    out, h, w = [], H0, W0
+    for _ in range(LEVELS + 1):
+        out.append((h, w)); h, w = (h + 1) // 2, (w + 1) // 2
+    return out
+
+
+def schedule(step):
+    """(keyframe index, level) of iteration `step` (3 iterations per keyframe, coarse first)."""
+    return (step // 3) % N_FRAMES, LEVELS - (step % 3)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device_index=0):
+        self.proc = None
+        self.dev = device_index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0])); mx = max(mx, float(f[1]))
+                for n, v in zip(names, f[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- roofline model
+def algorithmic(stats_by_level, n, sp):
+    """Algorithmic bytes / flops / ex2 per launch of each kernel family, averaged over the
+    three levels. stats_by_level[l] = (n_vis, pairs, pixels, contribs, tiles)."""
+    out = {}
+    for l, (nv, K, P, SC, T) in stats_by_level.items():
+        per = {
+            "preprocess_fwd": (4 * sp * n + 64 * nv, 300 * n, 0),
+            "depth_sort_pack_scan": (24 * nv + 136 * nv, 0, 0),
+            "tile_keys_sort_ranges": (36 * K, 0, 0),
+            "blend_fwd": (64 * K + 28 * P, 22 * SC, SC),
+            "loss_l1_ssim_depth": (52 * P, 650 * P, 0),
+            "blend_bwd": (64 * K + 24 * P + 40 * K, 70 * SC, SC),
+            "preprocess_bwd": (40 * K + 40 * nv + 8 * sp * nv, 600 * nv, 0),
+            "adam": ((28 * sp + 8) * n, 10 * sp * n, 0),
+        }
+        for k, v in per.items():
+            acc = out.setdefault(k, [0.0, 0.0, 0.0])
+            for i in range(3):
+                acc[i] += v[i] / len(stats_by_level)
+    return out
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world):
+    import torch
+    from paper_2411_02703_b200 import gsmap as G
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    ctx = G.Context(dev, stream.cuda_stream)
+    scene, train, t_fix = build_fixture(args.n_gaussians)
+    fx, fy, cx, cy, W, H = scene.camera
+    cam = G.Camera(fx, fy, cx, cy, W, H)
+    poses = [G.Pose(*p) for p in scene.poses]
+
+    # GT colour = the GT map rendered at level 0 by the same renderer (setup, untimed)
+    gt_map = G.GaussianMap(ctx, scene.gaussians)
+    gt_frame = G.RenderOutput(ctx)
+    kfs, host_levels = [], []
+    for f in range(N_FRAMES):
+        G.render(gt_map, poses[f], cam, gt_frame)
+        color = gt_frame.color.copy()
+        sparse = scene.sparse_depth(f)
+        kfs.append(G.Keyframe(poses[f], color, sparse, initial_iters=3, levels=LEVELS, ctx=ctx))
+        lv = []
+        for l in range(LEVELS + 1):  # pinned fp64 HWC copies of the pyramid for the e2e leg
+            c, d = kfs[-1].level(l)
+            pc = torch.empty(c.shape, dtype=torch.float64, pin_memory=True).numpy(); pc[...] = c
+            pd = torch.empty(d.shape, dtype=torch.float64, pin_memory=True).numpy(); pd[...] = d
+            lv.append((pc, pd))
+        host_levels.append(lv)
+    del gt_map, gt_frame
+    m = G.GaussianMap(ctx, train)
+    if args.sh_degree:
+        m.raise_sh_degree(args.sh_degree)
+    cfg = G.TrainConfig.make(0.2, 0.5, LEVELS, 1)
+    lvl_cams = [G.camera_scaled(cam, l) for l in range(LEVELS + 1)]
+    shapes = level_shapes()
+
+    batch = world > 1
+    views_per_rank = 1
+    if batch:  # C4: 8-view batch sharded over ranks, NCCL all-reduce of the gradient SoA
+        import torch.distributed as dist
+        cap = len(m) + 1024
+        gbuf = torch.zeros(59 * cap, dtype=torch.float32, device=f"cuda:{dev}")
+        grads = G.RenderGradients(ctx, external_ptr=gbuf.data_ptr(), capacity=cap)
+        views_per_rank = N_FRAMES // world
+        frame = G.RenderOutput(ctx)
+
+    def step(s, e2e=False):
+        if not batch:
+            k, lvl = schedule(s)
+            kf = kfs[k]
+            if kf.consumed_iters >= 3:
+                kf.consumed_iters = 0
+            if e2e:
+                kf.upload_level(lvl, *host_levels[k][lvl])
+            rep = G.train_keyframe_step(m, kf, cfg, cam)
+            assert rep is not None and rep["level"] == lvl
+            return 1, shapes[lvl][0] * shapes[lvl][1]
+        lvl = LEVELS - (s % 3)
+        grads.zero(m)
+        px = 0
+        for v in range(views_per_rank):
+            k = rank * views_per_rank + v
+            kf = kfs[k]
+            kf.consumed_iters = (LEVELS - lvl)
+            if e2e:
+                kf.upload_level(lvl, *host_levels[k][lvl])
+            G.train_accumulate(m, kf, cfg, cam, grads, frame, sync=False)
+            px += shapes[lvl][0] * shapes[lvl][1]
+        dist.all_reduce(gbuf[: 59 * cap])
+        m.apply_gradients(grads, cfg.lr)
+        torch.cuda.current_stream().synchronize()
+        return views_per_rank, px
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        step(s)
+    barrier()
+    launches0 = ctx.launches
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        views = pix = 0
+        for s in range(args.steps):
+            v, p = step(args.warmup + s)
+            views += v; pix += p
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    total_views = views * world
+    total_pix = pix * world
+    value = total_views / (ms_max / 1e3)
+
+    result = {"metric": METRIC, "value": round(value, 3), "unit": "iters/s", "n_gpus": world,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+              "higher_is_better": True, "scaling": "strong" if batch else "weak", "vs_baseline": None,
+              "dtype": "f32 (fp64 geometry, fp64 transmittance)",
+              "data": "synthetic (reference synthetic.cpp scene, colourised-LiDAR-initialised map)",
+              "mpix_per_s": round(total_pix / (ms_max / 1e3) / 1e6, 3),
+              "config": {"workload": ("C4: 8-keyframe batch sharded over ranks, NCCL all-reduce" if batch else
+                                      "C3: 1M Gaussians 1280x1024, 3-level pyramid (L2,L1,L0 in turn), L1+SSIM+depth loss"),
+                         "n_gaussians": len(m), "width": W0, "height": H0, "pyramid_levels": LEVELS + 1,
+                         "sh_degree": args.sh_degree, "lambda": 0.2, "lambda_d": 0.5, "keyframes": N_FRAMES,
+                         "l2": "inputs larger than L2 (params+Adam+grads > 126 MB)",
+                         "parallelism": f"dp{world}" if batch else "single-view"},
+              "gpu_launches": launches, "clocks": clk.summary(), "fixture_s": round(t_fix, 2)}
+
+    # ---------------- per-kernel profile pass (separate from the headline timing)
+    ctx.profile(True)
+    for s in range(args.steps):
+        step(args.warmup + args.steps + s)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    # per-level workload counters for the algorithmic model
+    stats = {}
+    fr = G.RenderOutput(ctx)
+    for l in range(LEVELS + 1):
+        G.render(m, poses[0], lvl_cams[l], fr)
+        st = fr.stats()
+        stats[l] = (st.n_visible, st.n_pairs, st.width * st.height, st.n_contrib, st.tiles_x * st.tiles_y)
+    sp = 11 + 3 * (args.sh_degree + 1) ** 2
+    alg = algorithmic(stats, len(m), sp)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    import ctypes as C
+    fp32 = C.c_double(); ex2 = C.c_double()
+    G._check(G.lib().gs_microbench(dev, 0, C.byref(fp32)))
+    G._check(G.lib().gs_microbench(dev, 1, C.byref(ex2)))
+    kernels = {}
+    for k, (tot_ms, cnt) in prof.items():
+        avg = tot_ms / max(cnt, 1) * 1e-3
+        b, fl, x = alg.get(k, (0, 0, 0))
+        kernels[k] = {"share": round(tot_ms / sum(v[0] for v in prof.values()), 4), "avg_ms": round(avg * 1e3, 4),
+                      "launches": cnt, "gbs": round(b / avg / 1e9, 1) if b else None,
+                      "tflops": round(fl / avg / 1e12, 3) if fl else None}
+    dom = max(prof, key=lambda k: prof[k][0])
+    avg = prof[dom][0] / prof[dom][1] * 1e-3
+    b, fl, x = alg.get(dom, (0, 0, 0))
+    t_hbm, t_fp, t_ex = b / (hbm * 1e9), fl / fp32.value, x / ex2.value
+    if t_hbm >= max(t_fp, t_ex):
+        roof = {"bound": "hbm", "achieved": round(b / avg / 1e9, 1), "peak": hbm, "unit": "GB/s"}
+    else:
+        roof = {"bound": "fp32" if t_fp >= t_ex else "mufu.ex2",
+                "achieved": round((fl / avg if t_fp >= t_ex else x / avg) / 1e12, 3),
+                "peak": round((fp32.value if t_fp >= t_ex else ex2.value) / 1e12, 3),
+                "unit": "TFLOP/s" if t_fp >= t_ex else "Tex2/s"}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["kernel"] = dom
+    roof["traffic"] = None
+    roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm"
+                           else "gs_microbench on this device (FP32 FMA / MUFU.EX2 issue rate)")
+    roof["model"] = "SURVEY §8d algorithmic bytes/flops per launch, averaged over the 3 pyramid levels"
+    result["roofline"] = roof
+    result["kernels"] = kernels
+    result["workload_counters"] = {f"L{l}": dict(zip(["n_visible", "pairs", "pixels", "contribs", "tiles"], v))
+                                   for l, v in stats.items()}
+
+    # ---------------- e2e: same metric through the C-ABI with host buffers each step
+    if not args.no_e2e:
+        for s in range(3):
+            step(s, e2e=True)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        views = 0
+        h2d = 0
+        for s in range(args.steps):
+            v, _ = step(s, e2e=True)
+            views += v
+            lvl = LEVELS - (s % 3)
+            h2d += 32 * shapes[lvl][0] * shapes[lvl][1] * (views_per_rank if batch else 1)
+        t1.record(stream)
+        barrier()
+        e_ms = t0.elapsed_time(t1)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e_ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        result["e2e"] = {"value": round(views * world / (e_ms / 1e3), 3), "unit": "iters/s",
+                         "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 24,
+                         "path": "gs_keyframe_upload_level (host fp64 HWC pyramid level, pinned) + gs_train_step"}
+    return result, (scene, train, kfs, host_levels)
+
+
+# ----------------------------------------------------------------------------- CPU (oracle) arm
+def cpu_sample(scene, train, gt_levels, threads=0):
+    """The oracle restatement of train_keyframe_step (fp64, ThreadPool with every host thread)
+    over one coarse-to-fine cycle of keyframe 0 (levels 2, 1, 0): 3 iterations."""
+    from oracle import pyoracle as O
+    fx, fy, cx, cy, W, H = scene.camera
+    cam = O.camera(fx, fy, cx, cy, W, H)
+    p = scene.poses[0]
+    pose = O.Pose(*p)
+    om = O.OracleMap(train)
+    color0, depth0 = gt_levels
+    kf = O.Keyframe(pose, color0, depth0, 3, LEVELS)
+    cfg = O.make_cfg(0.2, 0.5, LEVELS, 1)
+    pool = O.ThreadPool(threads)
+    t = time.time()
+    px = 0
+    for it in range(3):
+        r = O.train_keyframe_step(om, kf, cfg, cam, pool)
+        h, w = level_shapes()[r["level"]]
+        px += h * w
+    dt = time.time() - t
+    return {"value": round(3 / dt, 5), "unit": "iters/s", "cores": pool.threads, "kind": "port",
+            "mpix_per_s": round(px / dt / 1e6, 4),
+            "sample": "oracle restatement (oracle/, fp64, -O3 -ffp-contract=off) of train_keyframe_step: one "
+                      "L2->L1->L0 cycle (3 iterations) of keyframe 0 of the same 1M-Gaussian workload",
+            "seconds": round(dt, 2)}
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference's CPU path (oracle restatement; the C++ reference itself
+    cannot be built here: no Eigen/libpng/doctest) on this host's cores."""
+    if rank != 0:
+        return None
+    from oracle import pyoracle as O
+    scene, train, t_fix = build_fixture(args.n_gaussians)
+    fx, fy, cx, cy, W, H = scene.camera
+    cam = O.camera(fx, fy, cx, cy, W, H)
+    pose = O.Pose(*scene.poses[0])
+    pool = O.ThreadPool(0)
+    gt = O.render(O.OracleMap(scene.gaussians), pose, cam, threads=pool.threads)
+    color = gt.color.copy()
+    depth = scene.sparse_depth(0)
+    del gt
+    om = O.OracleMap(train)
+    kf = O.Keyframe(pose, color, depth, 3, LEVELS)
+    cfg = O.make_cfg(0.2, 0.5, LEVELS, 1)
+    warm = min(args.warmup, 1)
+    timed = min(args.steps, 3)
+    for _ in range(warm):
+        O.train_keyframe_step(om, kf, cfg, cam, pool)
+    kf.consumed_iters = 0
+    t = time.time()
+    px = 0
+    for _ in range(timed):
+        r = O.train_keyframe_step(om, kf, cfg, cam, pool)
+        h, w = level_shapes()[r["level"]]
+        px += h * w
+    dt = time.time() - t
+    v = timed / dt
+    sample = (f"oracle restatement of train_keyframe_step (fp64, ThreadPool({pool.threads})), {timed} iterations "
+              f"(levels 2,1,0) of keyframe 0 after {warm} warm-up; same fixture as --impl ours")
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "iters/s", "n_gpus": 0,
+            "steps": timed, "warmup": warm, "ms_per_step": round(dt / timed * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "mpix_per_s": round(px / dt / 1e6, 4),
+            "config": {"workload": "C3: 1M Gaussians 1280x1024, 3-level pyramid, L1+SSIM+depth loss",
+                       "n_gaussians": len(train), "width": W0, "height": H0},
+            "cpu_baseline": {"kind": "port", "cores": pool.threads, "sample": sample, "value": round(v, 5),
+                             "unit": "iters/s"},
+            "e2e": {"value": round(v, 5), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    result, ctxdata = run_ours(args, rank, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
+        scene, train, kfs, host_levels = ctxdata
+        c0, d0 = host_levels[0][0]
+        result["cpu_baseline"] = cpu_sample(scene, train, (np.array(c0), np.array(d0)))
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

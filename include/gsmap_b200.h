@@ -73,6 +73,14 @@ int gs_context_synchronize(gs_context* ctx);
 int gs_context_set_stream(gs_context* ctx, void* cuda_stream);
 /* number of this library's kernel launches since creation (bench/driver evidence) */
 int gs_context_launch_count(gs_context* ctx, int64_t* count);
+/* per-kernel CUDA-event timing on the context stream (enable != 0 resets the table) */
+int gs_context_profile(gs_context* ctx, int enable);
+/* reads the table: names as one '\n'-separated string, per-name total ms and launch counts */
+int gs_context_profile_read(gs_context* ctx, char* names, int32_t names_len, double* total_ms,
+                            int64_t* launches, int32_t max_entries, int32_t* n_entries);
+
+/* roofline denominators measured on this device: kind 0 = FP32 FMA flop/s, 1 = MUFU.EX2/s */
+int gs_microbench(int device, int kind, double* per_second);
 
 /* ---- camera helpers (core/types.hpp:22-44) ---- */
 int gs_camera_validate(const gs_camera* cam);
@@ -151,6 +159,8 @@ int gs_keyframe_destroy(gs_keyframe* kf);
 int gs_keyframe_consumed(gs_keyframe* kf, int32_t* consumed);
 int gs_keyframe_set_consumed(gs_keyframe* kf, int32_t consumed);
 int gs_keyframe_levels(gs_keyframe* kf, int32_t* n_levels);
+/* overwrite one pyramid level from host fp64 HWC images (the reference's ImageD) */
+int gs_keyframe_upload_level(gs_keyframe* kf, int32_t level, const double* color, const double* depth);
 /* read a pyramid level back (host fp64 HWC) */
 int gs_keyframe_read_level(gs_keyframe* kf, int32_t level, double* color, double* depth);
 /* compute_loss (mapper.cpp:146-212) on the frame's images vs pyramid level `level`; the

@@ -135,7 +135,24 @@ struct gs_context {
     int64_t launches = 0;
     gs_frame* scratch_frame = nullptr;
     gs_grads* scratch_grads = nullptr;
+    // optional per-kernel event timing (bench roofline); events are pooled
+    bool profile = false;
+    struct ProfRec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_next = 0;
 
+    cudaEvent_t ev() {
+        if (ev_next == ev_pool.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_next++];
+    }
     void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
     void launched(int k = 1) {
         launches += k;
@@ -146,6 +163,28 @@ struct gs_context {
         return cub_tmp.p;
     }
 };
+
+namespace {
+// Brackets one kernel family with CUDA events on the context stream when profiling is on.
+struct Scope {
+    gs_context* C;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    Scope(gs_context* c, const char* n) : C(c), name(n) {
+        if (C->profile) {
+            a = C->ev();
+            cudaEventRecord(a, C->stream);
+        }
+    }
+    ~Scope() {
+        if (C->profile && a) {
+            cudaEvent_t b = C->ev();
+            cudaEventRecord(b, C->stream);
+            C->prof.push_back({name, a, b});
+        }
+    }
+};
+}  // namespace
 
 struct gs_map {
     gs_context* ctx = nullptr;
@@ -216,9 +255,11 @@ struct gs_keyframe {
     int32_t initial_iters = 0, consumed = 0;
     std::vector<int> hs, ws;
     std::vector<DevBuf> color, depth;  // per level: planes [3][h][w] and [h][w]
+    DevBuf stage;                      // fp64 HWC staging for host uploads
     ~gs_keyframe() {
         for (auto& b : color) b.release();
         for (auto& b : depth) b.release();
+        stage.release();
     }
 };
 
@@ -341,10 +382,13 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
         C->counters.ensure(2 * sizeof(unsigned long long));
         C->pinned.ensure(64);
         ck(cudaMemsetAsync(C->counters.p, 0, 2 * sizeof(unsigned long long), st), "memset counters");
-        launch_preprocess_fwd(M->params, M->cap, M->degree, n, v, F->rec_by_gid.as<Splat>(),
-                              F->vis_flag.as<uint8_t>(), F->key_by_gid.as<unsigned long long>(),
-                              C->counters.as<unsigned long long>(), st);
-        C->launched();
+        {
+            Scope sc(C, "preprocess_fwd");
+            launch_preprocess_fwd(M->params, M->cap, M->degree, n, v, F->rec_by_gid.as<Splat>(),
+                                  F->vis_flag.as<uint8_t>(), F->key_by_gid.as<unsigned long long>(),
+                                  C->counters.as<unsigned long long>(), st);
+            C->launched();
+        }
         ck(cudaMemcpyAsync(C->pinned.p, C->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
            "d2h counters");
         ck(cudaStreamSynchronize(st), "sync counters");
@@ -365,6 +409,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
         F->emit_off.ensure(sizeof(uint32_t) * (nv + 1));
         F->num_sel.ensure(sizeof(int));
         // stable compaction of the visible map indices (index order = reference tie-break order)
+        Scope sc_sort(C, "depth_sort_pack_scan");
         cub::CountingInputIterator<int32_t> iota(0);
         size_t tb = 0;
         cub::DeviceSelect::Flagged(nullptr, tb, iota, F->vis_flag.as<uint8_t>(), F->vis_gid.as<int32_t>(),
@@ -392,6 +437,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
         ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
                                          nv + 1, st), "scan");
         if (K > 0) {
+            Scope sc_keys(C, "tile_keys_sort_ranges");
             F->pair_keys.ensure(sizeof(uint32_t) * K);
             F->pair_keys2.ensure(sizeof(uint32_t) * K);
             F->pair_vals.ensure(sizeof(uint32_t) * K);
@@ -413,11 +459,14 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
             C->launched();
         }
     }
-    launch_blend_fwd(F->ranges.as<uint2>(), K > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
-                     nv > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(), F->depth.as<float>(),
-                     F->vis.as<float>(), F->t_final.as<float>(), F->n_proc.as<int32_t>(),
-                     F->n_contrib.as<int32_t>(), st);
-    C->launched();
+    {
+        Scope sc(C, "blend_fwd");
+        launch_blend_fwd(F->ranges.as<uint2>(), K > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
+                         nv > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
+                         F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
+                         F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), st);
+        C->launched();
+    }
     F->rendered = true;
 }
 
@@ -445,18 +494,25 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     const uint32_t K = static_cast<uint32_t>(F->n_pairs);
     if (nv == 0 || K == 0) return;
     F->partials.ensure(sizeof(float) * kNumPartials * K);
-    launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
-                     F->emit_off.as<uint32_t>(), F->view, F->t_final.as<float>(), F->n_proc.as<int32_t>(), dl_dcolor,
-                     dl_ddepth, depth_scale, F->partials.as<float>(), st);
-    C->launched();
-    launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(), F->emit_off.as<uint32_t>(),
-                          F->partials.as<float>(), nv, G->planes, G->cap, st);
-    C->launched();
+    {
+        Scope sc(C, "blend_bwd");
+        launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
+                         F->emit_off.as<uint32_t>(), F->view, F->t_final.as<float>(), F->n_proc.as<int32_t>(),
+                         dl_dcolor, dl_ddepth, depth_scale, F->partials.as<float>(), st);
+        C->launched();
+    }
+    {
+        Scope sc(C, "preprocess_bwd");
+        launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
+                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), nv, G->planes, G->cap, st);
+        C->launched();
+    }
 }
 
 void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr) {
     if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
+    Scope sc(M->ctx, "adam");
     launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
                 M->scene_extent, M->ctx->stream);
     M->ctx->launched();
@@ -473,6 +529,7 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     gs_context* C = F->ctx;
     cudaStream_t st = C->stream;
     ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset loss");
+    Scope sc(C, "loss_l1_ssim_depth");
     launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
                       K->depth[level].as<float>(), h, w, cfg.lambda, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
                       F->loss.as<LossScalars>(), st);
@@ -632,6 +689,49 @@ int gs_context_set_stream(gs_context* C, void* stream) {
 
 int gs_context_launch_count(gs_context* C, int64_t* count) {
     return guard([&] { *count = C->launches; });
+}
+
+int gs_context_profile(gs_context* C, int enable) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(C->stream), "sync");
+        C->profile = enable != 0;
+        C->prof.clear();
+        C->ev_next = 0;
+    });
+}
+
+int gs_context_profile_read(gs_context* C, char* names, int32_t names_len, double* total_ms, int64_t* launches,
+                            int32_t max_entries, int32_t* n_entries) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(C->stream), "sync");
+        std::vector<std::string> keys;
+        std::vector<double> ms;
+        std::vector<int64_t> cnt;
+        for (const auto& r : C->prof) {
+            float t = 0.f;
+            ck(cudaEventElapsedTime(&t, r.a, r.b), "cudaEventElapsedTime");
+            size_t k = 0;
+            while (k < keys.size() && keys[k] != r.name) ++k;
+            if (k == keys.size()) {
+                keys.emplace_back(r.name);
+                ms.push_back(0.0);
+                cnt.push_back(0);
+            }
+            ms[k] += t;
+            cnt[k] += 1;
+        }
+        std::string joined;
+        const int n = std::min<int>(static_cast<int>(keys.size()), max_entries);
+        for (int i = 0; i < n; ++i) {
+            joined += keys[i];
+            joined += '\n';
+            total_ms[i] = ms[i];
+            launches[i] = cnt[i];
+        }
+        if (static_cast<int>(joined.size()) + 1 > names_len) fail(GS_EINVAL, "profile_read: names buffer too small");
+        std::memcpy(names, joined.c_str(), joined.size() + 1);
+        *n_entries = n;
+    });
 }
 
 int gs_camera_validate(const gs_camera* cam) { return guard([&] { validate_camera(*cam); }); }
@@ -1105,6 +1205,22 @@ int gs_keyframe_destroy(gs_keyframe* K) {
 int gs_keyframe_consumed(gs_keyframe* K, int32_t* c) { return guard([&] { *c = K->consumed; }); }
 int gs_keyframe_set_consumed(gs_keyframe* K, int32_t c) { return guard([&] { K->consumed = c; }); }
 int gs_keyframe_levels(gs_keyframe* K, int32_t* n) { return guard([&] { *n = static_cast<int32_t>(K->hs.size()); }); }
+
+int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
+    return guard([&] {
+        if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
+        const int h = K->hs[level], w = K->ws[level];
+        const size_t P = static_cast<size_t>(h) * w;
+        cudaStream_t st = K->ctx->stream;
+        K->stage.ensure(sizeof(double) * 4 * P);
+        ck(cudaMemcpyAsync(K->stage.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d color");
+        ck(cudaMemcpyAsync(K->stage.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st),
+           "h2d depth");
+        launch_from_hwc_double(K->stage.as<double>(), h, w, 3, K->color[level].as<float>(), st);
+        launch_from_hwc_double(K->stage.as<double>() + 3 * P, h, w, 1, K->depth[level].as<float>(), st);
+        K->ctx->launched(2);
+    });
+}
 
 int gs_keyframe_read_level(gs_keyframe* K, int32_t level, double* color, double* depth) {
     return guard([&] {

@@ -147,6 +147,17 @@ class Context:
         _check(lib().gs_context_launch_count(_vp(self.h), C.byref(n)))
         return n.value
 
+    def profile(self, enable: bool = True):
+        """Per-kernel CUDA-event timing on the context stream (resets the table)."""
+        _check(lib().gs_context_profile(_vp(self.h), int(enable)))
+
+    def profile_read(self) -> dict:
+        names = C.create_string_buffer(4096)
+        ms = np.zeros(64); cnt = np.zeros(64, np.int64); n = C.c_int32()
+        _check(lib().gs_context_profile_read(_vp(self.h), names, 4096, _p(ms), _p(cnt), 64, C.byref(n)))
+        keys = names.value.decode().split("\n")[: n.value]
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}
+
 
 _default_ctx = None
 
@@ -456,6 +467,10 @@ class Keyframe:
     @consumed_iters.setter
     def consumed_iters(self, c: int):
         _check(lib().gs_keyframe_set_consumed(_vp(self.h), c))
+
+    def upload_level(self, l: int, color: np.ndarray, depth: np.ndarray):
+        """Overwrite pyramid level ``l`` from host fp64 HWC images (pinned memory recommended)."""
+        _check(lib().gs_keyframe_upload_level(_vp(self.h), l, _p(color), _p(depth)))
 
     def level(self, l: int):
         H, W = self.shape
