@@ -1,0 +1,249 @@
+// K7: reverse replay of the blend (rasterizer.cpp:253-315). Per pixel, walk its contributors
+// back to front, reconstructing T_i = T_{i+1} / (1 - alpha_i) from the forward's T_final. The
+// suffix sums enter dalpha only through B = dC.S_c + dD.S_d, so one running scalar replaces the
+// four suffix sums:
+//   dalpha_i = T_i (dC.c_i + dD.z_i) - B / (1 - alpha_i);   B += w_i (dC.c_i + dD.z_i).
+// Each (tile, Gaussian) pair's 10 cotangent sums are reduced per warp (12 shuffles), across the
+// CTA's warps in shared memory, and written once to the pair's emission slot: deterministic,
+// no global atomics; K8 sums a Gaussian's slots in fp64. Partials 5-6 (mean) and 7-9
+// (covariance) carry the staged conic's exp2 scale k and k^2; K8 divides them out.
+#include "blend_common.cuh"
+#include "kernels.cuh"
+
+namespace gsb {
+
+namespace {
+
+// Transposed butterfly: reduces 10 per-lane values over the warp with 12 shuffles (5+3+2+1+1)
+// instead of 50. Returns the total of value index *idx in this lane (idx = -1: no value).
+__device__ __forceinline__ float warp_reduce10(const float v[kNumPartials], int lane, int* idx) {
+    const bool u4 = lane & 16, u3 = lane & 8, u2 = lane & 4, u1 = lane & 2;
+    float a[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const float send = u4 ? v[k] : v[k + 5];
+        const float keep = u4 ? v[k + 5] : v[k];
+        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float hi = k + 3 < 5 ? a[k + 3] : 0.f;
+        const float send = u3 ? a[k] : hi;
+        const float keep = u3 ? hi : a[k];
+        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float c[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float hi = k + 2 < 3 ? b[k + 2] : 0.f;
+        const float send = u2 ? b[k] : hi;
+        const float keep = u2 ? hi : b[k];
+        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const float send = u1 ? c[0] : c[1];
+    const float keep = u1 ? c[1] : c[0];
+    float r = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    const int ci = u1 ? 1 : 0;
+    const int bi = u2 ? ci + 2 : ci;
+    const int ai = u3 ? bi + 3 : bi;
+    const int vi = u4 ? ai + 5 : ai;
+    *idx = ((lane & 1) == 0 && bi < 3 && ai < 5) ? vi : -1;
+    return r;
+}
+
+constexpr int kBwdBatch = 32;
+
+}  // namespace
+
+template <int PPT>
+__global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
+    const uint32_t* __restrict__ emit_off, ViewParams v, const float* __restrict__ t_final,
+    const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,
+    const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials) {
+    using S = Strip<PPT>;
+    constexpr int NT = S::kThreads, NW = NT / 32, NP = PPT / 2;
+    __shared__ StageBuf<kBwdBatch> sb;
+    __shared__ uint32_t s_slot[kBwdBatch];
+    __shared__ uint32_t s_mask[NW];
+    __shared__ float s_red[NW > 1 ? NW : 1][kBwdBatch][kNumPartials];
+    __shared__ int s_max[NW];
+    const S sc(v.tiles_x);
+    const uint2 range = ranges[blockIdx.x];
+    const double ox = sc.tx * kTile, oy = sc.ty * kTile;
+    const float fx = static_cast<float>(sc.lx);
+    const float dscale = dl_ddepth ? (depth_scale ? *depth_scale : 1.f) : 0.f;
+    const size_t P = static_cast<size_t>(v.width) * v.height;
+
+    float2 T[NP], B[NP], g0[NP], g1[NP], g2[NP], gz[NP];
+    int last[PPT];
+    int my_last = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        float t[2] = {0.f, 0.f}, a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f}, c[2] = {0.f, 0.f}, z[2] = {0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int p = 2 * q + h, y = sc.py0 + p;
+            last[p] = 0;
+            if (sc.px < v.width && y < v.height) {
+                const size_t o = static_cast<size_t>(y) * v.width + sc.px;
+                last[p] = n_proc[o];
+                t[h] = t_final[o];
+                a[h] = dl_dcolor[o];
+                b[h] = dl_dcolor[P + o];
+                c[h] = dl_dcolor[2 * P + o];
+                z[h] = dl_ddepth ? dl_ddepth[o] * dscale : 0.f;
+                // rasterizer.cpp:264: a pixel with an all-zero cotangent contributes nothing
+                if (a[h] == 0.f && b[h] == 0.f && c[h] == 0.f && z[h] == 0.f) last[p] = 0;
+            }
+            my_last = max(my_last, last[p]);
+        }
+        T[q] = make_float2(t[0], t[1]);
+        B[q] = f2(0.f);
+        g0[q] = make_float2(a[0], a[1]);
+        g1[q] = make_float2(b[0], b[1]);
+        g2[q] = make_float2(c[0], c[1]);
+        gz[q] = make_float2(z[0], z[1]);
+    }
+    int max_last = __reduce_max_sync(0xffffffffu, my_last);
+    if (NW > 1) {
+        if (sc.lane == 0) s_max[sc.warp] = max_last;
+        __syncthreads();
+        max_last = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) max_last = max(max_last, s_max[w]);
+    }
+    const int n_list = static_cast<int>(range.y - range.x);
+
+    // entries no pixel reached still own a partial slot: zero it
+    for (int j = max_last + threadIdx.x; j < n_list; j += NT) {
+        const uint32_t r = vals[range.x + j];
+        const uint32_t slot = emission_index(rec[r], emit_off[r], sc.tx, sc.ty);
+        float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(slot) * kNumPartials);
+#pragma unroll
+        for (int k = 0; k < kNumPartials / 2; ++k) dst[k] = make_float2(0.f, 0.f);
+    }
+
+    const int bx0 = sc.tx * kTile, by0 = sc.ty * kTile + sc.warp * S::kRowsPerWarp;
+    for (int hi = max_last; hi > 0; hi -= kBwdBatch) {
+        const int lo = max(0, hi - kBwdBatch);
+        const int cnt = hi - lo;
+        if (NW > 1) __syncthreads();
+        if (threadIdx.x < cnt) {
+            const uint32_t r = vals[range.x + lo + threadIdx.x];
+            const Splat sp = rec[r];
+            sb.put(threadIdx.x, stage_of(sp, ox, oy));
+            s_slot[threadIdx.x] = emission_index(sp, emit_off[r], sc.tx, sc.ty);
+        }
+        if (sc.lane == 0) s_mask[sc.warp] = 0u;
+        if (NW > 1) __syncthreads(); else __syncwarp();
+        for (int k = cnt - 1; k >= 0; --k) {
+            const int4 rc = sb.rect[k];
+            if (rc.x > bx0 + 15 || rc.z < bx0 || rc.y > by0 + S::kRowsPerWarp - 1 || rc.w < by0) continue;
+            const int j = lo + k;
+            const bool colin = sc.px >= rc.x && sc.px <= rc.z;
+            const float2 m = sb.mean[k];
+            const float4 cn = sb.con[k];
+            const float4 col = sb.col[k];
+            float2 acc[kNumPartials];
+#pragma unroll
+            for (int c = 0; c < kNumPartials; ++c) acc[c] = f2(0.f);
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const int p0 = 2 * q, y0 = sc.py0 + p0;
+                const bool a0 = colin && j < last[p0] && y0 >= rc.y && y0 <= rc.w;
+                const bool a1 = colin && j < last[p0 + 1] && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
+                if (!(a0 || a1)) continue;
+                any = true;
+                const float fy = static_cast<float>(sc.ly0 + p0);
+                const AlphaP e = alpha_pair(m, cn, fx, make_float2(fy, fy + 1.f));
+                const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
+                const float2 om = __fadd2_rn(f2(1.f), neg2(al));
+                const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                const float2 ti = __fmul2_rn(T[q], inv);
+                const float2 w = __fmul2_rn(al, ti);
+                const float2 A = __ffma2_rn(g0[q], f2(col.x),
+                                            __ffma2_rn(g1[q], f2(col.y),
+                                                       __ffma2_rn(g2[q], f2(col.z), __fmul2_rn(gz[q], f2(col.w)))));
+                const float2 dalpha = __ffma2_rn(ti, A, __fmul2_rn(neg2(inv), B[q]));
+                B[q] = __ffma2_rn(w, A, B[q]);
+                T[q] = make_float2(a0 ? ti.x : T[q].x, a1 ? ti.y : T[q].y);
+                acc[0] = __ffma2_rn(w, g0[q], acc[0]);
+                acc[1] = __ffma2_rn(w, g1[q], acc[1]);
+                acc[2] = __ffma2_rn(w, g2[q], acc[2]);
+                acc[3] = __ffma2_rn(w, gz[q], acc[3]);
+                // rasterizer.cpp:297: the clamp is flat -> no opacity / mean / covariance terms
+                const float2 gdr = __fmul2_rn(e.g, dalpha);
+                const float2 gd = make_float2(a0 && e.a_raw.x < kAlphaMaxF ? gdr.x : 0.f,
+                                              a1 && e.a_raw.y < kAlphaMaxF ? gdr.y : 0.f);
+                acc[4] = __fadd2_rn(acc[4], gd);
+                const float2 sg = __fmul2_rn(gd, f2(cn.w));
+                acc[5] = __ffma2_rn(sg, e.u0, acc[5]);
+                acc[6] = __ffma2_rn(sg, e.u1, acc[6]);
+                const float2 hs = __fmul2_rn(sg, f2(0.5f));
+                const float2 h0 = __fmul2_rn(hs, e.u0);
+                acc[7] = __ffma2_rn(h0, e.u0, acc[7]);
+                acc[8] = __ffma2_rn(h0, e.u1, acc[8]);
+                acc[9] = __ffma2_rn(__fmul2_rn(hs, e.u1), e.u1, acc[9]);
+            }
+            if (!__any_sync(0xffffffffu, any)) continue;
+            float vsum[kNumPartials];
+#pragma unroll
+            for (int c = 0; c < kNumPartials; ++c) vsum[c] = acc[c].x + acc[c].y;
+            int vi;
+            const float tot = warp_reduce10(vsum, sc.lane, &vi);
+            if (NW == 1) {
+                if (vi >= 0) partials[static_cast<size_t>(s_slot[k]) * kNumPartials + vi] = tot;
+            } else {
+                if (vi >= 0) s_red[sc.warp][k][vi] = tot;
+            }
+            if (sc.lane == 0) s_mask[sc.warp] |= 1u << k;
+        }
+        if (NW == 1) {
+            __syncwarp();
+            // entries of this batch the warp never reduced (no pixel of the tile hit them)
+            for (int k = sc.lane; k < cnt; k += 32)
+                if (!((s_mask[0] >> k) & 1u)) {
+                    float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(s_slot[k]) * kNumPartials);
+#pragma unroll
+                    for (int c = 0; c < kNumPartials / 2; ++c) dst[c] = make_float2(0.f, 0.f);
+                }
+            __syncwarp();
+        } else {
+            __syncthreads();
+            for (int t = threadIdx.x; t < cnt * kNumPartials; t += NT) {
+                const int k = t / kNumPartials, c = t - k * kNumPartials;
+                float a = 0.f;
+#pragma unroll
+                for (int w = 0; w < NW; ++w)
+                    if ((s_mask[w] >> k) & 1u) a += s_red[w][k][c];
+                partials[static_cast<size_t>(s_slot[k]) * kNumPartials + c] = a;
+            }
+        }
+    }
+}
+
+void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
+                      const ViewParams& v, const float* t_final, const int32_t* n_proc,
+                      const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
+                      float* partials, cudaStream_t st) {
+    const int n_tiles = v.tiles_x * v.tiles_y;
+    switch (blend_ppt(v, true)) {
+        case 8:
+            blend_bwd_kernel<8><<<n_tiles, 32, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                        dl_ddepth, depth_scale, partials);
+            break;
+        case 4:
+            blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                        dl_ddepth, depth_scale, partials);
+            break;
+        default:
+            blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                         dl_ddepth, depth_scale, partials);
+    }
+}
+
+}  // namespace gsb

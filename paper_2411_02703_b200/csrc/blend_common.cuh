@@ -1,0 +1,135 @@
+// Shared device helpers of the blend kernels (forward, backward, CSR materialisation).
+//
+// Blend layout: one CTA per 16x16 tile with 256/PPT threads; each thread owns a vertical strip
+// of PPT pixels (warp w: rows w*2*PPT .. +2*PPT-1; lane l: column l&15, rows +PPT*(l>>4)+p).
+// Pixels are processed in vertically adjacent pairs with packed FP32x2 arithmetic (FFMA2 /
+// FMUL2 / FADD2 on sm_100a), which halves the issue slots of the per-contributor math.
+#pragma once
+
+#include "common.cuh"
+
+namespace gsb {
+
+// exp(-q/2) = 2^(k q) with k = -log2(e)/2 folded into the staged conic.
+constexpr float kExpScale = -0.72134752044448170368f;
+
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Staged form of one tile-list entry. The mean is rebased to the tile origin in fp64 and then
+// rounded (keeps ~1e-6 px precision anywhere in the image); the conic carries the exp2 scale.
+struct Staged {
+    float2 mean;
+    float4 con;  // k*a, k*b, k*c, opacity
+    float4 col;  // r, g, b, depth
+    int4 rect;   // x0, y0, x1, y1 (absolute, inclusive)
+};
+
+__device__ __forceinline__ Staged stage_of(const Splat& sp, double ox, double oy) {
+    Staged s;
+    s.mean = make_float2(static_cast<float>(sp.mx - ox), static_cast<float>(sp.my - oy));
+    s.con = make_float4(__fmul_rn(sp.ca, kExpScale), __fmul_rn(sp.cb, kExpScale), __fmul_rn(sp.cc, kExpScale),
+                        sp.opacity);
+    s.col = make_float4(sp.r, sp.g, sp.b, sp.depth);
+    s.rect = make_int4(sp.x0, sp.y0, sp.x1, sp.y1);
+    return s;
+}
+
+template <int N>
+struct StageBuf {
+    float2 mean[N];
+    float4 con[N];
+    float4 col[N];
+    int4 rect[N];
+    __device__ __forceinline__ void put(int t, const Staged& s) {
+        mean[t] = s.mean;
+        con[t] = s.con;
+        col[t] = s.col;
+        rect[t] = s.rect;
+    }
+};
+
+// Per-contributor alpha (eval_gaussian_2d_conic, projection.cpp:80-84, and the 0.99 clamp,
+// rasterizer.cpp:142-143). Every operation is an explicit round-to-nearest intrinsic, and the
+// packed pair version performs the identical sequence lane by lane, so the forward, the
+// backward replay and the CSR materialisation see bit-identical alphas.
+struct AlphaS {
+    float u0, u1, g, a_raw, alpha;
+};
+
+__device__ __forceinline__ AlphaS alpha_scalar(float2 m, float4 cn, float fx, float fy) {
+    const float dx = __fadd_rn(fx, -m.x), dy = __fadd_rn(fy, -m.y);
+    AlphaS a;
+    a.u0 = __fmaf_rn(cn.y, dy, __fmul_rn(cn.x, dx));
+    a.u1 = __fmaf_rn(cn.z, dy, __fmul_rn(cn.y, dx));
+    const float q = __fmaf_rn(dy, a.u1, __fmul_rn(dx, a.u0));
+    a.g = ex2(q);
+    a.a_raw = __fmul_rn(cn.w, a.g);
+    a.alpha = fminf(a.a_raw, kAlphaMaxF);
+    return a;
+}
+
+struct AlphaP {
+    float2 u0, u1, g, a_raw, alpha;
+};
+
+__device__ __forceinline__ AlphaP alpha_pair(float2 m, float4 cn, float fx, float2 fy) {
+    const float dx = __fadd_rn(fx, -m.x);
+    const float2 dy = __fadd2_rn(fy, f2(-m.y));
+    const float adx = __fmul_rn(cn.x, dx), bdx = __fmul_rn(cn.y, dx);
+    AlphaP a;
+    a.u0 = __ffma2_rn(f2(cn.y), dy, f2(adx));
+    a.u1 = __ffma2_rn(f2(cn.z), dy, f2(bdx));
+    const float2 q = __ffma2_rn(dy, a.u1, __fmul2_rn(f2(dx), a.u0));
+    a.g = make_float2(ex2(q.x), ex2(q.y));
+    a.a_raw = __fmul2_rn(f2(cn.w), a.g);
+    a.alpha = make_float2(fminf(a.a_raw.x, kAlphaMaxF), fminf(a.a_raw.y, kAlphaMaxF));
+    return a;
+}
+
+// fp64 transmittance factor (1 - alpha): the clamp substitutes the exact double 0.99, so two
+// stacked clamped splats leave T = (1 - 0.99)^2 = 1.0000000000000018e-4 (no termination),
+// exactly as the fp64 reference (rasterizer.cpp:143-151).
+__device__ __forceinline__ double one_minus_alpha_d(float a_raw, float alpha) {
+    return __dadd_rn(1.0, -(a_raw >= kAlphaMaxF ? kAlphaMaxD : static_cast<double>(alpha)));
+}
+
+__device__ __forceinline__ uint32_t emission_index(const Splat& sp, uint32_t off, int tx, int ty) {
+    const int tx0 = sp.x0 >> 4, ty0 = sp.y0 >> 4;
+    const int ntx = (sp.x1 >> 4) - tx0 + 1;
+    return off + static_cast<uint32_t>((ty - ty0) * ntx + (tx - tx0));
+}
+
+template <int PPT>
+struct Strip {
+    static constexpr int kThreads = kTileThreads / PPT;
+    static constexpr int kRowsPerWarp = 2 * PPT;
+    int tx, ty, warp, lane, lx, ly0, px, py0;
+    __device__ __forceinline__ Strip(int tiles_x) {
+        tx = blockIdx.x % tiles_x;
+        ty = blockIdx.x / tiles_x;
+        warp = threadIdx.x >> 5;
+        lane = threadIdx.x & 31;
+        lx = lane & 15;
+        ly0 = warp * kRowsPerWarp + (lane >> 4) * PPT;
+        px = tx * kTile + lx;
+        py0 = ty * kTile + ly0;
+    }
+};
+
+// pixels-per-thread chosen per level (host override for experiments; 0 = automatic)
+int blend_ppt(const ViewParams& v, bool backward);
+
+}  // namespace gsb

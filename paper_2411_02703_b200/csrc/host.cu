@@ -581,6 +581,7 @@ void keyframe_build(gs_keyframe* K, const float* color0, const float* depth0, in
     if (levels < 0) fail(GS_EINVAL, "build_pyramid: levels must be >= 0");
     if (h < (1 << levels) || w < (1 << levels)) fail(GS_EINVAL, "build_pyramid: image too small for requested levels");
     cudaStream_t st = K->ctx->stream;
+    K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(h) * w);  // host-upload staging, sized once
     K->hs.assign(levels + 1, 0);
     K->ws.assign(levels + 1, 0);
     K->color.resize(levels + 1);
@@ -689,6 +690,21 @@ int gs_context_set_stream(gs_context* C, void* stream) {
 
 int gs_context_launch_count(gs_context* C, int64_t* count) {
     return guard([&] { *count = C->launches; });
+}
+
+int gs_debug_set_blend_ppt(int fwd, int bwd) {
+    return guard([&] { set_blend_ppt(fwd, bwd); });
+}
+
+int gs_debug_counters(gs_context* C, int64_t* out2, int reset) {
+    return guard([&] {
+        C->use();
+        ck(cudaStreamSynchronize(C->stream), "sync");
+        unsigned long long v[2];
+        read_blend_stats(v, reset != 0);
+        out2[0] = static_cast<int64_t>(v[0]);
+        out2[1] = static_cast<int64_t>(v[1]);
+    });
 }
 
 int gs_context_profile(gs_context* C, int enable) {

@@ -28,6 +28,8 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
                       float* partials, cudaStream_t st);
+void read_blend_stats(unsigned long long out[2], bool reset);
+void set_blend_ppt(int fwd, int bwd);
 void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                         const uint32_t* offsets, int32_t* out_gid, double* out_alpha, cudaStream_t st);
 
