@@ -57,3 +57,10 @@ def test_no_cpu_fallback_without_gpu(lib):
     from paper_2411_02703_b200 import gsmap
     with pytest.raises(gsmap.CudaError):
         gsmap.Context(0)
+
+
+def test_cpp_shim_compiles(lib):
+    """The C++ host shim (include/gsmap_b200.hpp) builds against the C-ABI library."""
+    import subprocess
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")])
+    assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "_build", "test_shim"))

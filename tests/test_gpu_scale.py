@@ -91,7 +91,10 @@ def test_c3_properties(c3):
     scene, train = c3
     fx, fy, cx, cy, W, H = scene.camera
     cam = G().Camera(fx, fy, cx, cy, W, H)
-    pose = G().Pose(*scene.poses[0])
+    # frame 3 (non-zero yaw): at frame 0 the rotation is the identity, so camera depth = the
+    # fp32 world z + t_z and many of the 1M Gaussians tie on depth; ties break by map index
+    # (rasterizer.cpp:69-72), which a permutation legitimately changes.
+    pose = G().Pose(*scene.poses[3])
     gm = G().GaussianMap(None, train)
     a = G().render(gm, pose, cam)
     _, t = a.pixel_state()
@@ -103,7 +106,7 @@ def test_c3_properties(c3):
     c = G().render(gm2, pose, cam)
     assert np.array_equal(a.color, c.color) and np.array_equal(a.depth, c.depth)  # order invariance
     # one Adam step moves every scalar by at most ~lr (t = 1: update = -lr * g / (|g| + 1e-15))
-    kf = G().Keyframe(pose, a.color, scene.sparse_depth(0), 3, 2)
+    kf = G().Keyframe(pose, a.color, scene.sparse_depth(3), 3, 2)
     before = gm.gaussians["p"]
     rep = G().train_keyframe_step(gm, kf, G().TrainConfig.make(0.2, 0.5, 2, 1), cam)
     assert rep["level"] == 2 and np.isfinite(rep["loss"])
