@@ -39,7 +39,7 @@ N_GAUSS, W0, H0, N_FRAMES, LEVELS = 1_000_000, 1280, 1024, 8, 2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=24)
+    ap.add_argument("--steps", type=int, default=48)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sh-degree", type=int, default=0)
@@ -82,7 +82,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -221,6 +221,10 @@ def run_ours(args, rank, world):
     for s in range(args.warmup):
         step(s)
     barrier()
+    # GS_PROFILE_RANGE=1: restrict an `ncu --profile-from-start off` capture to the timed steps
+    prof_range = os.environ.get("GS_PROFILE_RANGE") == "1"
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     launches0 = ctx.launches
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
@@ -233,6 +237,8 @@ def run_ours(args, rank, world):
         barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launches - launches0
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     ms_max = ms
     if world > 1:
         import torch.distributed as dist

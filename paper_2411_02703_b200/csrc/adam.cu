@@ -11,41 +11,74 @@ namespace gsb {
 // momentum keeps moving it, as in the reference). The per-Gaussian bias corrections are fp64;
 // the per-scalar update is fp32 on fp32 m/v. Inactive SH coefficients are skipped: their m, v
 // and gradient are exactly zero, so the reference's update there is -lr*0/(0+eps) = -0 (exact).
+namespace {
+struct AdamArgs {
+    float lr[5];        // position (x scene_extent), rotation, log_scale, opacity, sh
+    int32_t t_common;   // the new step of every Gaussian present since the last append
+    float a_common;     // 1 / (1 - 0.9^t_common)
+    float b_common;     // 1 / (1 - 0.999^t_common)
+};
+
+__device__ __forceinline__ void adam_scalar(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                                            float g, float lr, float a, float b) {
+    const float mk = fmaf(0.9f, *m, 0.1f * g);
+    const float vk = fmaf(0.999f, *v, 0.001f * g * g);
+    *m = mk;
+    *v = vk;
+    *p += -lr * (mk * a) / (sqrtf(vk * b) + 1e-15f);
+}
+}  // namespace
+
+// The 11 geometry planes are unrolled so all their loads are in flight at once; SH planes
+// follow per coefficient up to the Gaussian's active degree. The fp64 bias corrections come
+// from the host for the common step count and are computed only for Gaussians appended later.
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, float* __restrict__ m,
                                                    float* __restrict__ v, int32_t* __restrict__ step,
                                                    const int8_t* __restrict__ degree,
                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
-                                                   float lr_pos, float lr_rot, float lr_ls, float lr_op,
-                                                   float lr_sh) {
+                                                   AdamArgs args) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int t = step[i] + 1;
     step[i] = t;
-    const double bc1 = 1.0 - pow(0.9, static_cast<double>(t));
-    const double bc2 = 1.0 - pow(0.999, static_cast<double>(t));
-    const float a = static_cast<float>(1.0 / bc1);
-    const float b = static_cast<float>(1.0 / bc2);
-    const int deg = degree[i];
-    const int nk = kGeomParams + 3 * (deg + 1) * (deg + 1);
-    for (int k = 0; k < nk; ++k) {
-        const float lr = k < 3 ? lr_pos : k < 7 ? lr_rot : k < 10 ? lr_ls : k < 11 ? lr_op : lr_sh;
+    float a = args.a_common, b = args.b_common;
+    if (t != args.t_common) {
+        a = static_cast<float>(1.0 / (1.0 - pow(0.9, static_cast<double>(t))));
+        b = static_cast<float>(1.0 / (1.0 - pow(0.999, static_cast<double>(t))));
+    }
+    float g[kGeomParams];
+#pragma unroll
+    for (int k = 0; k < kGeomParams; ++k) g[k] = __ldg(grads + static_cast<size_t>(k) * gcap + i);
+#pragma unroll
+    for (int k = 0; k < kGeomParams; ++k) {
+        const float lr = k < 3 ? args.lr[0] : k < 7 ? args.lr[1] : k < 10 ? args.lr[2] : args.lr[3];
         const size_t o = static_cast<size_t>(k) * cap + i;
-        const float g = grads[static_cast<size_t>(k) * gcap + i];
-        const float mk = fmaf(0.9f, m[o], 0.1f * g);
-        const float vk = fmaf(0.999f, v[o], 0.001f * g * g);
-        m[o] = mk;
-        v[o] = vk;
-        params[o] += -lr * (mk * a) / (sqrtf(vk * b) + 1e-15f);
+        adam_scalar(params + o, m + o, v + o, g[k], lr, a, b);
+    }
+    const int ncoef = (degree[i] + 1) * (degree[i] + 1);
+    for (int c = 0; c < ncoef; ++c) {
+        float gs[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) gs[ch] = __ldg(grads + static_cast<size_t>(P_SH + 3 * c + ch) * gcap + i);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const size_t o = static_cast<size_t>(P_SH + 3 * c + ch) * cap + i;
+            adam_scalar(params + o, m + o, v + o, gs[ch], args.lr[4], a, b);
+        }
     }
 }
 
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
-                 int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, cudaStream_t st) {
+                 int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
+                 cudaStream_t st) {
     if (n <= 0) return;
-    adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n,
-                                                static_cast<float>(lr[0] * scene_extent), static_cast<float>(lr[1]),
-                                                static_cast<float>(lr[2]), static_cast<float>(lr[3]),
-                                                static_cast<float>(lr[4]));
+    AdamArgs args;
+    args.lr[0] = static_cast<float>(lr[0] * scene_extent);
+    for (int k = 1; k < 5; ++k) args.lr[k] = static_cast<float>(lr[k]);
+    args.t_common = static_cast<int32_t>(t_common);
+    args.a_common = static_cast<float>(1.0 / (1.0 - std::pow(0.9, static_cast<double>(t_common))));
+    args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
+    adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args);
 }
 
 namespace {

@@ -152,6 +152,59 @@ __device__ __forceinline__ double ldp(const float* __restrict__ params, int64_t 
     return static_cast<double>(__ldg(params + plane * cap + i));
 }
 
+// Degree-specialised SH (sh.cpp:82-109): with D a compile-time constant every basis array is
+// fully unrolled into registers (a runtime-bounded loop would spill it to local memory).
+template <int D>
+__device__ __forceinline__ void sh_raw_t(const D3& dir, const float* __restrict__ params, int64_t cap, int i,
+                                         double raw[3]) {
+    double basis[16];
+    sh_basis(dir, D, basis);
+    raw[0] = raw[1] = raw[2] = 0.5;
+#pragma unroll
+    for (int k = 0; k < (D + 1) * (D + 1); ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) raw[c] += basis[k] * ldp(params, cap, P_SH + 3 * k + c, i);
+}
+
+__device__ __forceinline__ void sh_raw(int deg, const D3& dir, const float* __restrict__ params, int64_t cap, int i,
+                                       double raw[3]) {
+    switch (deg) {
+        case 0: sh_raw_t<0>(dir, params, cap, i, raw); break;
+        case 1: sh_raw_t<1>(dir, params, cap, i, raw); break;
+        case 2: sh_raw_t<2>(dir, params, cap, i, raw); break;
+        default: sh_raw_t<3>(dir, params, cap, i, raw); break;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ D3 sh_vjp_t(const D3& dir, const float* __restrict__ params, int64_t cap, int i,
+                                       const double dr[3], float* __restrict__ grads, int64_t gcap) {
+    double basis[16], wk[16];
+    sh_basis(dir, D, basis);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wk[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < (D + 1) * (D + 1); ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s += ldp(params, cap, P_SH + 3 * k + c, i) * dr[c];
+        wk[k] = s;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) grads[(P_SH + 3 * k + c) * gcap + i] += static_cast<float>(basis[k] * dr[c]);
+    }
+    return sh_dir_grad(dir, D, wk);
+}
+
+__device__ __forceinline__ D3 sh_vjp(int deg, const D3& dir, const float* __restrict__ params, int64_t cap, int i,
+                                     const double dr[3], float* __restrict__ grads, int64_t gcap) {
+    switch (deg) {
+        case 0: return sh_vjp_t<0>(dir, params, cap, i, dr, grads, gcap);
+        case 1: return sh_vjp_t<1>(dir, params, cap, i, dr, grads, gcap);
+        case 2: return sh_vjp_t<2>(dir, params, cap, i, dr, grads, gcap);
+        default: return sh_vjp_t<3>(dir, params, cap, i, dr, grads, gcap);
+    }
+}
+
 // covariance.cpp:17-43 rotation_partial(u, k) (without the factor 2, applied by the caller)
 __device__ __forceinline__ void rotation_partial(const double u[4], int k, double d[3][3]) {
     const double w = u[0], x = u[1], y = u[2], z = u[3];
@@ -173,19 +226,75 @@ __device__ __forceinline__ void rotation_partial(const double u[4], int k, doubl
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
-// K1: one thread per Gaussian. Culls (near clip z <= 0.01, off-screen box), writes the 64 B
-// Splat record at the map index, the fp64 depth bit pattern as the sort key, and counts the
-// visible set and the (tile, gaussian) pairs with warp-aggregated atomics.
+// K1 runs in two phases so the expensive exact projection only sees dense warps of likely
+// survivors (about a third of the map in view).
+//
+// K1a: camera transform (exact fp64, as in K1b), near clip, and the off-screen test with a
+// conservative radius bound R >= the exact radius: lambda_max(Sigma_I) <= ||J||_F^2
+// max_k exp(2 ls_k) + 0.3 (W is a rotation). A Gaussian K1a culls is culled by the exact test
+// too, so the candidate list is a superset of the visible set. Candidates are appended with
+// warp-aggregated atomics (their order does not matter: K1b writes by map index).
+__global__ void __launch_bounds__(256) cull_kernel(const float* __restrict__ params, int64_t cap, int n,
+                                                   ViewParams v, int32_t* __restrict__ cand,
+                                                   unsigned long long* __restrict__ counters) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    if (i < n) {
+        const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
+        D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
+        p = {p.x + v.tx, p.y + v.ty, p.z + v.tz};
+        if (!(p.z <= kNearClip)) {
+            const double mx = v.fx * p.x / p.z + v.cx;
+            const double my = v.fy * p.y / p.z + v.cy;
+            const double iz = 1.0 / p.z;
+            const double jf2 = (v.fx * iz) * (v.fx * iz) * (1.0 + (p.x * iz) * (p.x * iz)) +
+                               (v.fy * iz) * (v.fy * iz) * (1.0 + (p.y * iz) * (p.y * iz));
+            const double lsmax = fmax(fmax(ldp(params, cap, P_LS, i), ldp(params, cap, P_LS + 1, i)),
+                                      ldp(params, cap, P_LS + 2, i));
+            const double lam = (jf2 * exp(2.0 * lsmax) + kCovReg) * (1.0 + 1e-6);
+            const double R = ceil(3.0 * sqrt(lam)) + 1.0;
+            keep = !(mx + R < 0.0 || mx - R > static_cast<double>(v.width - 1) || my + R < 0.0 ||
+                     my - R > static_cast<double>(v.height - 1)) ||
+                   !(lam < 1e300);  // non-finite bound: leave the decision to the exact test
+        }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (mask) {
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(counters + 2, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (keep) cand[base + __popc(mask & ((1u << lane) - 1u))] = i;
+    }
+}
+
+void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, int32_t* cand,
+                 unsigned long long* counters, cudaStream_t st) {
+    if (n > 0) cull_kernel<<<div_up(n, 256), 256, 0, st>>>(params, cap, n, v, cand, counters);
+}
+
+// K1b: exact projection of the candidates (grid-stride over the device-side candidate count).
+// Writes the 64 B Splat record at the map index and the fp64 depth bits (map-indexed), and
+// appends visible Gaussians to the sort input: the fp32-rounded depth bits (a monotone
+// non-decreasing key) and the map index. Counts the visible set and the (tile, gaussian) pairs.
 // Reference: rasterizer.cpp:37-68 (project_visible) + projection.cpp:17-40 + sh.cpp:82-92 +
 // rasterizer.cpp:81-88 (pixel rect -> tile rect).
 __global__ void __launch_bounds__(256) preprocess_fwd_kernel(
-    const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, int n,
-    ViewParams v, Splat* __restrict__ rec_by_gid, uint8_t* __restrict__ vis_flag,
-    unsigned long long* __restrict__ depth_key, unsigned long long* __restrict__ counters) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree,
+    const int32_t* __restrict__ cand, ViewParams v, Splat* __restrict__ rec_by_gid,
+    unsigned long long* __restrict__ depth_key, int32_t* __restrict__ vis_gid, uint32_t* __restrict__ key32,
+    unsigned long long* __restrict__ counters) {
+    const int n_cand = static_cast<int>(counters[2]);
+    const int stride = gridDim.x * blockDim.x;
+    const int first = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int base_c = first - (threadIdx.x & 31); base_c < n_cand; base_c += stride) {
+    const int c = base_c + (threadIdx.x & 31);
+    const int i = c < n_cand ? cand[c] : 0;
     bool visible = false;
     uint32_t ntiles = 0;
-    if (i < n) {
+    double depth = 0.0;
+    if (c < n_cand) {
         const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
         D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
         p = {p.x + v.tx, p.y + v.ty, p.z + v.tz};
@@ -236,13 +345,8 @@ __global__ void __launch_bounds__(256) preprocess_fwd_kernel(
                 const D3 vd{pos.x - ctr.x, pos.y - ctr.y, pos.z - ctr.z};
                 const double dist = sqrt((vd.x * vd.x + vd.y * vd.y) + vd.z * vd.z);
                 const D3 dir = dist > 0.0 ? D3{vd.x / dist, vd.y / dist, vd.z / dist} : D3{0.0, 0.0, 1.0};
-                const int deg = degree[i];
-                double basis[16];
-                sh_basis(dir, deg, basis);
-                const int nb = (deg + 1) * (deg + 1);
-                double col[3] = {0.5, 0.5, 0.5};
-                for (int k = 0; k < nb; ++k)
-                    for (int c = 0; c < 3; ++c) col[c] += basis[k] * ldp(params, cap, P_SH + 3 * k + c, i);
+                double col[3];
+                sh_raw(degree[i], dir, params, cap, i, col);
                 s.r = static_cast<float>(fmin(fmax(col[0], 0.0), 1.0));
                 s.g = static_cast<float>(fmin(fmax(col[1], 0.0), 1.0));
                 s.b = static_cast<float>(fmin(fmax(col[2], 0.0), 1.0));
@@ -263,27 +367,37 @@ __global__ void __launch_bounds__(256) preprocess_fwd_kernel(
                 s.ntiles = ntiles;
                 rec_by_gid[i] = s;
                 depth_key[i] = static_cast<unsigned long long>(__double_as_longlong(p.z));
+                depth = p.z;
             }
         }
-        vis_flag[i] = visible ? 1 : 0;
     }
-    // warp-aggregated counters: [0] visible, [1] pairs
-    const unsigned vis_count = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
+    // warp-aggregated: append visible (fp32 depth key, map index); count pairs
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = __ballot_sync(0xffffffffu, visible);
+    if (mask) {
+        const int leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(counters + 0, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (visible) {
+            const size_t slot = base + __popc(mask & ((1u << lane) - 1u));
+            vis_gid[slot] = i;
+            key32[slot] = __float_as_uint(__double2float_rn(depth));
+        }
+    }
     unsigned long long pairs = ntiles;
     for (int o = 16; o > 0; o >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
-    if ((threadIdx.x & 31) == 0) {
-        if (vis_count) atomicAdd(counters + 0, static_cast<unsigned long long>(vis_count));
-        if (pairs) atomicAdd(counters + 1, pairs);
+    if (lane == 0 && pairs) atomicAdd(counters + 1, pairs);
     }
 }
 
-void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, int n,
-                           const ViewParams& v, Splat* rec_by_gid, uint8_t* vis_flag,
-                           unsigned long long* depth_key, unsigned long long* counters,
-                           cudaStream_t st) {
-    if (n <= 0) return;
-    preprocess_fwd_kernel<<<div_up(n, 256), 256, 0, st>>>(params, cap, degree, n, v, rec_by_gid,
-                                                          vis_flag, depth_key, counters);
+void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, const int32_t* cand,
+                           int max_cand, const ViewParams& v, Splat* rec_by_gid, unsigned long long* depth_key,
+                           int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st) {
+    if (max_cand <= 0) return;
+    const int blocks = std::min(div_up(max_cand, 256), 148 * 8);
+    preprocess_fwd_kernel<<<blocks, 256, 0, st>>>(params, cap, degree, cand, v, rec_by_gid, depth_key, vis_gid,
+                                                  key32, counters);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -292,26 +406,40 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 // colour clamp mask -> eval_sh_vjp -> view-direction chain, sigmoid, project_gaussian_vjp
 // (projection.cpp:42-74) -> build_covariance_vjp (covariance.cpp:58-79). Accumulates into the
 // gradient planes (batch semantics = GaussianGrad::add, gaussian.hpp:51-57).
-__global__ void __launch_bounds__(128) preprocess_bwd_kernel(
+// The partial rows of a block's 128 consecutive ranks are one contiguous range of the
+// emission order, so the block streams them through shared memory with coalesced loads and
+// each thread then sums its own rows from shared memory (deterministic order, fp64).
+constexpr int kBwdRanks = 128;
+constexpr int kRowChunk = 640;  // rows staged per pass (640 x 40 B = 25.6 KB)
+
+__global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
     const float* __restrict__ partials, int n_vis, float* __restrict__ grads, int64_t gcap) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_vis) return;
-    const uint32_t e0 = emit_off[r], e1 = emit_off[r + 1];
-    if (e0 == e1) return;  // no tile: never touched (rasterizer.cpp:327)
+    __shared__ float rows[kRowChunk * kNumPartials];
+    const int r0 = blockIdx.x * kBwdRanks;
+    const int r = r0 + threadIdx.x;
+    const int rend = min(r0 + kBwdRanks, n_vis);
+    const uint32_t b0 = emit_off[r0], b1 = emit_off[rend];
+    const uint32_t e0 = r < n_vis ? emit_off[r] : b1, e1 = r < n_vis ? emit_off[r + 1] : b1;
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    for (uint32_t e = e0; e < e1; ++e) {
-        const float2* pp = reinterpret_cast<const float2*>(partials + static_cast<size_t>(e) * kNumPartials);
+    for (uint32_t c0 = b0; c0 < b1; c0 += kRowChunk) {
+        const uint32_t c1 = min(c0 + kRowChunk, b1);
+        const float* src = partials + static_cast<size_t>(c0) * kNumPartials;
+        const int nf = static_cast<int>(c1 - c0) * kNumPartials;
+        __syncthreads();
+        for (int t = threadIdx.x; t < nf; t += kBwdRanks) rows[t] = __ldg(src + t);
+        __syncthreads();
+        const uint32_t s0 = max(e0, c0), s1 = min(e1, c1);
+        for (uint32_t e = s0; e < s1; ++e) {
+            const float* row = rows + (e - c0) * kNumPartials;
 #pragma unroll
-        for (int k = 0; k < kNumPartials / 2; ++k) {
-            const float2 t = __ldg(pp + k);
-            acc[2 * k] += t.x;
-            acc[2 * k + 1] += t.y;
+            for (int k = 0; k < kNumPartials; ++k) acc[k] += row[k];
         }
     }
+    if (r >= n_vis || e0 == e1) return;  // no tile: never touched (rasterizer.cpp:327)
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) any |= (acc[k] != 0.0);
@@ -332,22 +460,11 @@ __global__ void __launch_bounds__(128) preprocess_bwd_kernel(
     const D3 vd{pos.x - ctr.x, pos.y - ctr.y, pos.z - ctr.z};
     const double dist = sqrt((vd.x * vd.x + vd.y * vd.y) + vd.z * vd.z);
     const D3 dir = dist > 0.0 ? D3{vd.x / dist, vd.y / dist, vd.z / dist} : D3{0.0, 0.0, 1.0};
-    double basis[16];
-    sh_basis(dir, deg, basis);
-    const int nb = (deg + 1) * (deg + 1);
-    double raw[3] = {0.5, 0.5, 0.5};
-    for (int k = 0; k < nb; ++k)
-        for (int c = 0; c < 3; ++c) raw[c] += basis[k] * ldp(params, cap, P_SH + 3 * k + c, i);
+    double raw[3];
+    sh_raw(deg, dir, params, cap, i, raw);
     double dr[3];
     for (int c = 0; c < 3; ++c) dr[c] = (raw[c] <= 0.0 || raw[c] >= 1.0) ? 0.0 : acc[c];
-    double wk[16];
-    for (int k = 0; k < nb; ++k) {
-        double s = 0.0;
-        for (int c = 0; c < 3; ++c) s += ldp(params, cap, P_SH + 3 * k + c, i) * dr[c];
-        wk[k] = s;
-        for (int c = 0; c < 3; ++c) grads[(P_SH + 3 * k + c) * gcap + i] += static_cast<float>(basis[k] * dr[c]);
-    }
-    const D3 ddir = sh_dir_grad(dir, deg, wk);
+    const D3 ddir = sh_vjp(deg, dir, params, cap, i, dr, grads, gcap);
     double gpos[3] = {0.0, 0.0, 0.0};
     if (dist > 0.0) {
         const double vdd = (dir.x * ddir.x + dir.y * ddir.y) + dir.z * ddir.z;
@@ -438,7 +555,7 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
                            int n_vis, float* grads, int64_t gcap, cudaStream_t st) {
     if (n_vis <= 0) return;
-    preprocess_bwd_kernel<<<div_up(n_vis, 128), 128, 0, st>>>(params, cap, degree, v, rec, emit_off,
+    preprocess_bwd_kernel<<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off,
                                                              partials, n_vis, grads, gcap);
 }
 

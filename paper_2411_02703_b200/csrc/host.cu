@@ -198,6 +198,7 @@ struct gs_map {
     int max_degree = 0;
     double scene_extent = 1.0;
     int64_t global_step = 0;
+    int64_t step0 = 0;  // host mirror of Gaussian 0's Adam step (hint for the common bias correction)
     DevBuf minmax;
 
     void free_all() {
@@ -222,7 +223,7 @@ struct gs_frame {
     int64_t map_n = 0, n_vis = 0, n_pairs = 0;
     // per-Gaussian / per-rank / per-pair scratch
     DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
-        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials;
+        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, depth_sorted;
     // per-pixel
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
     DevBuf loss;  // LossScalars
@@ -377,17 +378,21 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     F->n_pairs = 0;
     if (n > 0) {
         F->rec_by_gid.ensure(sizeof(Splat) * n);
-        F->vis_flag.ensure(n);
+        F->vis_flag.ensure(sizeof(int32_t) * n);  // K1a candidate list
         F->key_by_gid.ensure(sizeof(unsigned long long) * n);
-        C->counters.ensure(2 * sizeof(unsigned long long));
+        F->vis_gid.ensure(sizeof(int32_t) * n);
+        F->keys_a.ensure(sizeof(uint32_t) * n);
+        C->counters.ensure(3 * sizeof(unsigned long long));
         C->pinned.ensure(64);
-        ck(cudaMemsetAsync(C->counters.p, 0, 2 * sizeof(unsigned long long), st), "memset counters");
+        ck(cudaMemsetAsync(C->counters.p, 0, 3 * sizeof(unsigned long long), st), "memset counters");
         {
             Scope sc(C, "preprocess_fwd");
-            launch_preprocess_fwd(M->params, M->cap, M->degree, n, v, F->rec_by_gid.as<Splat>(),
-                                  F->vis_flag.as<uint8_t>(), F->key_by_gid.as<unsigned long long>(),
+            launch_cull(M->params, M->cap, n, v, F->vis_flag.as<int32_t>(), C->counters.as<unsigned long long>(), st);
+            launch_preprocess_fwd(M->params, M->cap, M->degree, F->vis_flag.as<int32_t>(), n, v,
+                                  F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(),
+                                  F->vis_gid.as<int32_t>(), F->keys_a.as<uint32_t>(),
                                   C->counters.as<unsigned long long>(), st);
-            C->launched();
+            C->launched(2);
         }
         ck(cudaMemcpyAsync(C->pinned.p, C->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
            "d2h counters");
@@ -400,37 +405,26 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     const int nv = static_cast<int>(F->n_vis);
     const uint32_t K = static_cast<uint32_t>(F->n_pairs);
     if (nv > 0) {
-        F->vis_gid.ensure(sizeof(int32_t) * nv);
-        F->keys_a.ensure(sizeof(unsigned long long) * nv);
-        F->keys_b.ensure(sizeof(unsigned long long) * nv);
+        F->keys_b.ensure(sizeof(uint32_t) * nv);
         F->gid_sorted.ensure(sizeof(int32_t) * nv);
         F->rec_sorted.ensure(sizeof(Splat) * nv);
+        F->depth_sorted.ensure(sizeof(unsigned long long) * nv);
         F->ntiles.ensure(sizeof(uint32_t) * (nv + 1));
         F->emit_off.ensure(sizeof(uint32_t) * (nv + 1));
-        F->num_sel.ensure(sizeof(int));
-        // stable compaction of the visible map indices (index order = reference tie-break order)
+        // (depth, index) order (rasterizer.cpp:69-72): stable radix sort on the fp32-rounded
+        // depth, then exact (fp64 depth, index) order inside runs of equal fp32 keys
         Scope sc_sort(C, "depth_sort_pack_scan");
-        cub::CountingInputIterator<int32_t> iota(0);
         size_t tb = 0;
-        cub::DeviceSelect::Flagged(nullptr, tb, iota, F->vis_flag.as<uint8_t>(), F->vis_gid.as<int32_t>(),
-                                   F->num_sel.as<int>(), n, st);
-        ck(cub::DeviceSelect::Flagged(C->cub(tb), tb, iota, F->vis_flag.as<uint8_t>(), F->vis_gid.as<int32_t>(),
-                                      F->num_sel.as<int>(), n, st), "DeviceSelect::Flagged");
-        launch_gather_keys(F->vis_gid.as<int32_t>(), F->key_by_gid.as<unsigned long long>(), nv,
-                           F->keys_a.as<unsigned long long>(), st);
-        C->launched();
-        // (depth, index) order: LSD radix sort on the fp64 depth bits is stable, so equal depths
-        // keep ascending map index (rasterizer.cpp:69-72)
-        tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<unsigned long long>(),
-                                        F->keys_b.as<unsigned long long>(), F->vis_gid.as<int32_t>(),
-                                        F->gid_sorted.as<int32_t>(), nv, 0, 64, st);
-        ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<unsigned long long>(),
-                                           F->keys_b.as<unsigned long long>(), F->vis_gid.as<int32_t>(),
-                                           F->gid_sorted.as<int32_t>(), nv, 0, 64, st), "depth sort");
-        launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), nv, F->rec_sorted.as<Splat>(),
-                    F->ntiles.as<uint32_t>(), st);
-        C->launched();
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
+                                        F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, 32, st);
+        ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
+                                           F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, 32, st),
+           "depth sort");
+        launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(), F->key_by_gid.as<unsigned long long>(),
+                        nv, st);
+        launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(), nv,
+                    F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(), F->depth_sorted.as<unsigned long long>(), st);
+        C->launched(2);
         ck(cudaMemsetAsync(F->ntiles.as<uint32_t>() + nv, 0, sizeof(uint32_t), st), "memset");
         tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), nv + 1, st);
@@ -514,7 +508,8 @@ void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr) {
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
     launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
-                M->scene_extent, M->ctx->stream);
+                M->scene_extent, M->step0 + 1, M->ctx->stream);
+    ++M->step0;
     M->ctx->launched();
     ++M->global_step;
 }
@@ -787,6 +782,7 @@ int gs_map_append(gs_map* M, const gs_gaussian* g, int64_t n) {
             ck(cudaMemset2DAsync(M->v + M->n, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
             ck(cudaMemsetAsync(M->step + M->n, 0, sizeof(int32_t) * n, st), "memset");
         }
+        if (M->n == 0) M->step0 = 0;
         upload_gaussians(M, g, M->n, n);
         M->n += n;
         refresh_extent(M);
@@ -855,6 +851,7 @@ int gs_map_set_adam(gs_map* M, const double* m59, const double* v59, const int64
                 b[static_cast<size_t>(k) * n + i] = static_cast<float>(v59[i * kNumParams + k]);
             }
             s[i] = static_cast<int32_t>(step[i]);
+            if (i == 0) M->step0 = step[0];
         }
         cudaStream_t st = M->ctx->stream;
         ck(cudaMemcpy2DAsync(M->m, sizeof(float) * M->cap, a.data(), sizeof(float) * n, sizeof(float) * n, kNumParams,
@@ -909,7 +906,8 @@ int gs_frame_destroy(gs_frame* F) {
         F->ctx->use();
         cudaStreamSynchronize(F->ctx->stream);
         for (DevBuf* b : {&F->rec_by_gid, &F->vis_flag, &F->key_by_gid, &F->vis_gid, &F->keys_a, &F->keys_b,
-                          &F->gid_sorted, &F->rec_sorted, &F->ntiles, &F->emit_off, &F->num_sel, &F->pair_keys,
+                          &F->gid_sorted, &F->rec_sorted, &F->ntiles, &F->emit_off, &F->num_sel, &F->depth_sorted,
+                          &F->pair_keys,
                           &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->color,
                           &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
                           &F->wbuf, &F->host_stage, &F->loss})
@@ -991,7 +989,8 @@ int gs_frame_read_projected(gs_frame* F, int32_t* index, double* mean2, int32_t*
         std::vector<unsigned long long> keys(nv);
         cudaStream_t st = F->ctx->stream;
         ck(cudaMemcpyAsync(rec.data(), F->rec_sorted.p, sizeof(Splat) * nv, cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaMemcpyAsync(keys.data(), F->keys_b.p, sizeof(unsigned long long) * nv, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(keys.data(), F->depth_sorted.p, sizeof(unsigned long long) * nv, cudaMemcpyDeviceToHost, st),
+           "d2h");
         ck(cudaStreamSynchronize(st), "sync");
         for (int64_t r = 0; r < nv; ++r) {
             const Splat& s = rec[r];

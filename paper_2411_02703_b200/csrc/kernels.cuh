@@ -6,18 +6,22 @@
 namespace gsb {
 
 // geometry.cu (FP64, --fmad=false)
-void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, int n,
-                           const ViewParams& v, Splat* rec_by_gid, uint8_t* vis_flag,
-                           unsigned long long* depth_key, unsigned long long* counters, cudaStream_t st);
+// counters: [0] visible, [1] (tile, gaussian) pairs, [2] K1a candidates
+void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, int32_t* cand,
+                 unsigned long long* counters, cudaStream_t st);
+void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, const int32_t* cand,
+                           int max_cand, const ViewParams& v, Splat* rec_by_gid, unsigned long long* depth_key,
+                           int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st);
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials, int n_vis,
                            float* grads, int64_t gcap, cudaStream_t st);
 
 // raster.cu
-void launch_gather_keys(const int32_t* vis_gid, const unsigned long long* depth_key_by_gid, int n_vis,
-                        unsigned long long* keys_out, cudaStream_t st);
-void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, int n_vis, Splat* rec_sorted,
-                 uint32_t* ntiles_sorted, cudaStream_t st);
+void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
+                     int n_vis, cudaStream_t st);
+void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
+                 int n_vis, Splat* rec_sorted, uint32_t* ntiles_sorted, unsigned long long* depth_sorted,
+                 cudaStream_t st);
 void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, int n_vis, uint32_t n_pairs, int tiles_x,
                        uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_tile_ranges(const uint32_t* keys_sorted, uint32_t n_pairs, uint2* ranges, cudaStream_t st);
@@ -44,7 +48,8 @@ void launch_downsample(const float* in, int h, int w, int channels, bool depth, 
 
 // adam.cu
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
-                 int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, cudaStream_t st);
+                 int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
+                 cudaStream_t st);
 void launch_position_minmax(const float* params, int64_t cap, int n, float* out6, cudaStream_t st);
 void launch_to_hwc_double(const float* planes, int h, int w, int channels, double* out, cudaStream_t st);
 void launch_from_hwc_double(const double* hwc, int h, int w, int channels, float* planes, cudaStream_t st);

@@ -5,62 +5,99 @@
 
 namespace gsb {
 
-__global__ void gather_keys_kernel(const int32_t* __restrict__ vis_gid,
-                                   const unsigned long long* __restrict__ key_by_gid, int n,
-                                   unsigned long long* __restrict__ out) {
+// Depth order = the reference's comparator (depth asc, map index asc), rasterizer.cpp:69-72.
+// The radix sort runs on the fp32-rounded depth (a monotone non-decreasing key, 4 passes
+// instead of 8 for the fp64 bits), so only runs of equal fp32 keys can be out of order; each
+// such run (almost always 2 elements) is insertion-sorted here by (fp64 depth, map index).
+// The result is exactly the fp64 (depth, index) order, independent of the append order.
+__global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __restrict__ gid,
+                                const unsigned long long* __restrict__ depth, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = key_by_gid[vis_gid[i]];
+    if (i >= n) return;
+    const uint32_t k = key[i];
+    if ((i > 0 && key[i - 1] == k) || i + 1 >= n || key[i + 1] != k) return;  // not a run start
+    int end = i + 1;
+    while (end < n && key[end] == k) ++end;
+    for (int a = i + 1; a < end; ++a) {
+        const int g = gid[a];
+        const unsigned long long d = depth[g];
+        int b = a - 1;
+        while (b >= i) {
+            const int gb = gid[b];
+            const unsigned long long db = depth[gb];
+            if (db < d || (db == d && gb < g)) break;
+            gid[b + 1] = gb;
+            --b;
+        }
+        gid[b + 1] = g;
+    }
 }
 
-void launch_gather_keys(const int32_t* vis_gid, const unsigned long long* key_by_gid, int n,
-                        unsigned long long* out, cudaStream_t st) {
-    if (n > 0) gather_keys_kernel<<<div_up(n, 256), 256, 0, st>>>(vis_gid, key_by_gid, n, out);
+void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
+                     int n, cudaStream_t st) {
+    if (n > 1) fix_ties_kernel<<<div_up(n, 256), 256, 0, st>>>(key32_sorted, gid_sorted, depth_by_gid, n);
 }
 
 // rank-ordered copy of the projected records (the reference's sorted `projected` vector)
 __global__ void pack_kernel(const int32_t* __restrict__ gid_sorted, const Splat* __restrict__ rec_by_gid,
-                            int n, Splat* __restrict__ rec_sorted, uint32_t* __restrict__ ntiles) {
+                            const unsigned long long* __restrict__ depth_by_gid, int n,
+                            Splat* __restrict__ rec_sorted, uint32_t* __restrict__ ntiles,
+                            unsigned long long* __restrict__ depth_sorted) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    const Splat s = rec_by_gid[gid_sorted[r]];
+    const int g = gid_sorted[r];
+    const Splat s = rec_by_gid[g];
     rec_sorted[r] = s;
     ntiles[r] = s.ntiles;
+    depth_sorted[r] = depth_by_gid[g];
 }
 
-void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, int n, Splat* rec_sorted,
-                 uint32_t* ntiles, cudaStream_t st) {
-    if (n > 0) pack_kernel<<<div_up(n, 256), 256, 0, st>>>(gid_sorted, rec_by_gid, n, rec_sorted, ntiles);
+void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid, int n,
+                 Splat* rec_sorted, uint32_t* ntiles, unsigned long long* depth_sorted, cudaStream_t st) {
+    if (n > 0)
+        pack_kernel<<<div_up(n, 256), 256, 0, st>>>(gid_sorted, rec_by_gid, depth_by_gid, n, rec_sorted, ntiles,
+                                                    depth_sorted);
 }
 
-// Duplicate-key emission (bin_tiles, rasterizer.cpp:76-91): one thread per (gaussian, tile)
-// pair, owner rank found by binary search over the exclusive scan of tile counts. Keys are
+// Duplicate-key emission (bin_tiles, rasterizer.cpp:76-91). A warp owns 32 consecutive depth
+// ranks; their pairs are contiguous in the exclusive scan, so the warp writes them rank by
+// rank with all lanes (coalesced, load-balanced across large and small footprints). Keys are
 // tile ids; values are depth ranks, so a stable sort by tile yields each tile's list in
-// (depth, index) order, exactly the reference's push_back order.
-__global__ void emit_pairs_kernel(const uint32_t* __restrict__ emit_off, const Splat* __restrict__ rec,
-                                  int n_vis, uint32_t n_pairs, int tiles_x, uint32_t* __restrict__ keys,
-                                  uint32_t* __restrict__ vals) {
-    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n_pairs) return;
-    int lo = 0, hi = n_vis;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(emit_off + mid) <= e) lo = mid; else hi = mid;
+// (depth, index) order, exactly the reference's push_back order (ty outer, tx inner).
+__global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restrict__ emit_off,
+                                                         const Splat* __restrict__ rec, int n_vis, int tiles_x,
+                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x);
+    int off = 0, cnt = 0, tx0 = 0, ty0 = 0, ntx = 1;
+    if (r < n_vis) {
+        off = static_cast<int>(emit_off[r]);
+        cnt = static_cast<int>(emit_off[r + 1]) - off;
+        const Splat& s = rec[r];
+        tx0 = s.x0 >> 4;
+        ty0 = s.y0 >> 4;
+        ntx = (s.x1 >> 4) - tx0 + 1;
     }
-    const int r = lo;
-    const uint32_t l = e - __ldg(emit_off + r);
-    const Splat& s = rec[r];
-    const int tx0 = s.x0 >> 4, ty0 = s.y0 >> 4;
-    const int ntx = (s.x1 >> 4) - tx0 + 1;
-    const int ty = ty0 + static_cast<int>(l) / ntx, tx = tx0 + static_cast<int>(l) % ntx;
-    keys[e] = static_cast<uint32_t>(ty * tiles_x + tx);
-    vals[e] = static_cast<uint32_t>(r);
+    const int rbase = r - lane;
+    for (int i = 0; i < 32; ++i) {
+        const int c = __shfl_sync(0xffffffffu, cnt, i);
+        if (c == 0) continue;
+        const int o = __shfl_sync(0xffffffffu, off, i);
+        const int x0 = __shfl_sync(0xffffffffu, tx0, i);
+        const int y0 = __shfl_sync(0xffffffffu, ty0, i);
+        const int nx = __shfl_sync(0xffffffffu, ntx, i);
+        for (int l = lane; l < c; l += 32) {
+            const int ty = y0 + l / nx, tx = x0 + l % nx;
+            keys[o + l] = static_cast<uint32_t>(ty * tiles_x + tx);
+            vals[o + l] = static_cast<uint32_t>(rbase + i);
+        }
+    }
 }
 
 void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, int n_vis, uint32_t n_pairs, int tiles_x,
                        uint32_t* keys, uint32_t* vals, cudaStream_t st) {
-    if (n_pairs > 0)
-        emit_pairs_kernel<<<div_up(static_cast<int>(n_pairs), 256), 256, 0, st>>>(emit_off, rec, n_vis, n_pairs,
-                                                                                 tiles_x, keys, vals);
+    if (n_pairs > 0 && n_vis > 0)
+        emit_pairs_kernel<<<div_up(n_vis, 256), 256, 0, st>>>(emit_off, rec, n_vis, tiles_x, keys, vals);
 }
 
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t n, uint2* __restrict__ ranges) {
