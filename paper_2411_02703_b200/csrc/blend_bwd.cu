@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,
     const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials) {
     using S = Strip<PPT>;
-    constexpr int NT = S::kThreads, NW = NT / 32, NP = PPT / 2;
+    constexpr int NT = S::kThreads, NW = NT / 32, NP = (PPT + 1) / 2;  // PPT = 1: high half never live
     __shared__ StageBuf<kBwdBatch> sb;
     __shared__ uint32_t s_slot[kBwdBatch];
     __shared__ uint32_t s_mask[NW];
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     const size_t P = static_cast<size_t>(v.width) * v.height;
 
     float2 T[NP], B[NP], g0[NP], g1[NP], g2[NP], gz[NP];
-    int last[PPT];
+    int last[2 * NP];
     int my_last = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
         for (int h = 0; h < 2; ++h) {
             const int p = 2 * q + h, y = sc.py0 + p;
             last[p] = 0;
-            if (sc.px < v.width && y < v.height) {
+            if (p < PPT && sc.px < v.width && y < v.height) {
                 const size_t o = static_cast<size_t>(y) * v.width + sc.px;
                 last[p] = n_proc[o];
                 t[h] = t_final[o];
@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
         for (int k = 0; k < kNumPartials / 2; ++k) dst[k] = make_float2(0.f, 0.f);
     }
 
-    const int bx0 = sc.tx * kTile, by0 = sc.ty * kTile + sc.warp * S::kRowsPerWarp;
     for (int hi = max_last; hi > 0; hi -= kBwdBatch) {
         const int lo = max(0, hi - kBwdBatch);
         const int cnt = hi - lo;
@@ -139,9 +138,12 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
         }
         if (sc.lane == 0) s_mask[sc.warp] = 0u;
         if (NW > 1) __syncthreads(); else __syncwarp();
-        for (int k = cnt - 1; k >= 0; --k) {
+        // ballot the staged entries that touch this warp's block, walk them back to front
+        unsigned todo = __ballot_sync(0xffffffffu, sc.lane < cnt && sc.touches(sb.rect[sc.lane]));
+        while (todo) {
+            const int k = 31 - __clz(todo);
+            todo &= ~(1u << k);
             const int4 rc = sb.rect[k];
-            if (rc.x > bx0 + 15 || rc.z < bx0 || rc.y > by0 + S::kRowsPerWarp - 1 || rc.w < by0) continue;
             const int j = lo + k;
             const bool colin = sc.px >= rc.x && sc.px <= rc.z;
             const float2 m = sb.mean[k];
@@ -239,6 +241,10 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
         case 4:
             blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
                                                         dl_ddepth, depth_scale, partials);
+            break;
+        case 1:
+            blend_bwd_kernel<1><<<n_tiles, 256, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                         dl_ddepth, depth_scale, partials);
             break;
         default:
             blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,

@@ -112,20 +112,32 @@ __device__ __forceinline__ uint32_t emission_index(const Splat& sp, uint32_t off
     return off + static_cast<uint32_t>((ty - ty0) * ntx + (tx - tx0));
 }
 
+// Each warp owns a compact kBW x kBH block of its tile (8x8 quadrants at PPT = 2, 8x16 halves
+// at PPT = 4, 8x4 at PPT = 1, the whole tile at PPT = 8); lane l owns column l % kBW and the
+// PPT rows starting at (l / kBW) * PPT.
 template <int PPT>
 struct Strip {
     static constexpr int kThreads = kTileThreads / PPT;
-    static constexpr int kRowsPerWarp = 2 * PPT;
-    int tx, ty, warp, lane, lx, ly0, px, py0;
+    static constexpr int kBW = PPT == 8 ? 16 : 8;
+    static constexpr int kBH = 32 * PPT / kBW;
+    static constexpr int kWarpsPerRow = kTile / kBW;
+    int tx, ty, warp, lane, lx, ly0, px, py0, bx0, by0;
     __device__ __forceinline__ Strip(int tiles_x) {
         tx = blockIdx.x % tiles_x;
         ty = blockIdx.x / tiles_x;
         warp = threadIdx.x >> 5;
         lane = threadIdx.x & 31;
-        lx = lane & 15;
-        ly0 = warp * kRowsPerWarp + (lane >> 4) * PPT;
+        const int wx = (warp % kWarpsPerRow) * kBW, wy = (warp / kWarpsPerRow) * kBH;
+        lx = wx + lane % kBW;
+        ly0 = wy + (lane / kBW) * PPT;
         px = tx * kTile + lx;
         py0 = ty * kTile + ly0;
+        bx0 = tx * kTile + wx;
+        by0 = ty * kTile + wy;
+    }
+    // the warp's block intersects the integer rect (x0, y0, x1, y1)
+    __device__ __forceinline__ bool touches(const int4& rc) const {
+        return !(rc.x > bx0 + kBW - 1 || rc.z < bx0 || rc.y > by0 + kBH - 1 || rc.w < by0);
     }
 };
 

@@ -54,7 +54,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib) {
     using S = Strip<PPT>;
-    constexpr int NT = S::kThreads, NP = PPT / 2;
+    // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
+    // live, so its packed lane computes nothing that is kept.
+    constexpr int NT = S::kThreads, NP = (PPT + 1) / 2;
     __shared__ StageBuf<NT> sb;
     const S sc(v.tiles_x);
     const uint2 range = ranges[blockIdx.x];
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     const float fx = static_cast<float>(sc.lx);
 
     float2 Th[NP], Tl[NP], c0[NP], c1[NP], c2[NP], dd[NP], vis[NP];
-    int nproc[PPT], ncontrib[PPT];
+    int nproc[2 * NP], ncontrib[2 * NP];
     unsigned live = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
@@ -70,9 +72,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
         Tl[q] = c0[q] = c1[q] = c2[q] = dd[q] = vis[q] = f2(0.f);
     }
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) {
+    for (int p = 0; p < 2 * NP; ++p) {
         nproc[p] = ncontrib[p] = 0;
-        if (sc.px < v.width && sc.py0 + p < v.height) live |= 1u << p;
+        if (p < PPT && sc.px < v.width && sc.py0 + p < v.height) live |= 1u << p;
     }
     for (uint32_t base = range.x; base < range.y; base += NT) {
         if (__syncthreads_count(live != 0) == 0) break;
@@ -80,9 +82,17 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
         if (idx < range.y) sb.put(threadIdx.x, stage_of(rec[vals[idx]], ox, oy));
         __syncthreads();
         const int cnt = min(NT, static_cast<int>(range.y - base));
-        for (int j = 0; j < cnt && live; ++j) {
+        // the warp first ballots which staged entries touch its block, then walks only those
+        // (in list order): no per-entry cull branch for the entries of other blocks
+        for (int b0 = 0; b0 < cnt; b0 += 32) {
+            if (!__any_sync(0xffffffffu, live != 0)) break;
+            const int jj = b0 + sc.lane;
+            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && sc.touches(sb.rect[jj]));
+            while (todo) {
+            const int j = b0 + __ffs(todo) - 1;
+            todo &= todo - 1;
             const int4 rc = sb.rect[j];
-            if (sc.px < rc.x || sc.px > rc.z || sc.py0 + PPT - 1 < rc.y || sc.py0 > rc.w) continue;
+            if (!live || sc.px < rc.x || sc.px > rc.z || sc.py0 + PPT - 1 < rc.y || sc.py0 > rc.w) continue;
             const float2 m = sb.mean[j];
             const float4 cn = sb.con[j];
             const float4 col = sb.col[j];
@@ -141,6 +151,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
                     }
                 }
             }
+            }
         }
     }
     const size_t P = static_cast<size_t>(v.width) * v.height;
@@ -171,12 +182,13 @@ void set_blend_ppt(int fwd, int bwd) {
 
 int blend_ppt(const ViewParams& v, bool backward) {
     const int o = g_ppt_override[backward ? 1 : 0];
-    if (o == 2 || o == 4 || o == 8) return o;
-    // measured on B200 (1M Gaussians, 1280x1024 pyramid): the forward is fastest with 2 pixels
-    // per thread at every level; the backward amortises its per-entry warp reduction over 4
-    // pixels once there are >= 1024 tiles (L0, L1) and needs the extra warps at L2.
-    if (!backward) return 2;
-    return v.tiles_x * v.tiles_y >= 1024 ? 4 : 2;
+    if (o == 1 || o == 2 || o == 4 || o == 8) return o;
+    // measured on B200 (1M Gaussians, 1280x1024 pyramid, tests/diag_fwd.py): the forward wants
+    // 2 pixels per thread, and 1 at the coarsest level where only 320 tiles (long lists) exist;
+    // the backward amortises its per-entry warp reduction over 4 pixels at L0 (5120 tiles).
+    const int tiles = v.tiles_x * v.tiles_y;
+    if (!backward) return tiles >= 1024 ? 2 : 1;
+    return tiles >= 4096 ? 4 : 2;
 }
 
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
@@ -189,6 +201,9 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
             break;
         case 4:
             blend_fwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib);
+            break;
+        case 1:
+            blend_fwd_kernel<1><<<n_tiles, 256, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib);
             break;
         default:
             blend_fwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib);

@@ -176,9 +176,13 @@ __device__ __forceinline__ void sh_raw(int deg, const D3& dir, const float* __re
     }
 }
 
+__device__ __forceinline__ void gput(float* __restrict__ g, int64_t idx, double val, bool acc) {
+    if (acc) g[idx] += static_cast<float>(val); else g[idx] = static_cast<float>(val);
+}
+
 template <int D>
 __device__ __forceinline__ D3 sh_vjp_t(const D3& dir, const float* __restrict__ params, int64_t cap, int i,
-                                       const double dr[3], float* __restrict__ grads, int64_t gcap) {
+                                       const double dr[3], float* __restrict__ grads, int64_t gcap, bool accum) {
     double basis[16], wk[16];
     sh_basis(dir, D, basis);
 #pragma unroll
@@ -190,18 +194,18 @@ __device__ __forceinline__ D3 sh_vjp_t(const D3& dir, const float* __restrict__ 
         for (int c = 0; c < 3; ++c) s += ldp(params, cap, P_SH + 3 * k + c, i) * dr[c];
         wk[k] = s;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) grads[(P_SH + 3 * k + c) * gcap + i] += static_cast<float>(basis[k] * dr[c]);
+        for (int c = 0; c < 3; ++c) gput(grads, (P_SH + 3 * k + c) * gcap + i, basis[k] * dr[c], accum);
     }
     return sh_dir_grad(dir, D, wk);
 }
 
 __device__ __forceinline__ D3 sh_vjp(int deg, const D3& dir, const float* __restrict__ params, int64_t cap, int i,
-                                     const double dr[3], float* __restrict__ grads, int64_t gcap) {
+                                     const double dr[3], float* __restrict__ grads, int64_t gcap, bool accum) {
     switch (deg) {
-        case 0: return sh_vjp_t<0>(dir, params, cap, i, dr, grads, gcap);
-        case 1: return sh_vjp_t<1>(dir, params, cap, i, dr, grads, gcap);
-        case 2: return sh_vjp_t<2>(dir, params, cap, i, dr, grads, gcap);
-        default: return sh_vjp_t<3>(dir, params, cap, i, dr, grads, gcap);
+        case 0: return sh_vjp_t<0>(dir, params, cap, i, dr, grads, gcap, accum);
+        case 1: return sh_vjp_t<1>(dir, params, cap, i, dr, grads, gcap, accum);
+        case 2: return sh_vjp_t<2>(dir, params, cap, i, dr, grads, gcap, accum);
+        default: return sh_vjp_t<3>(dir, params, cap, i, dr, grads, gcap, accum);
     }
 }
 
@@ -412,6 +416,7 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 constexpr int kBwdRanks = 128;
 constexpr int kRowChunk = 640;  // rows staged per pass (640 x 40 B = 25.6 KB)
 
+template <bool ACC>
 __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     sh_raw(deg, dir, params, cap, i, raw);
     double dr[3];
     for (int c = 0; c < 3; ++c) dr[c] = (raw[c] <= 0.0 || raw[c] >= 1.0) ? 0.0 : acc[c];
-    const D3 ddir = sh_vjp(deg, dir, params, cap, i, dr, grads, gcap);
+    const D3 ddir = sh_vjp(deg, dir, params, cap, i, dr, grads, gcap, ACC);
     double gpos[3] = {0.0, 0.0, 0.0};
     if (dist > 0.0) {
         const double vdd = (dir.x * ddir.x + dir.y * ddir.y) + dir.z * ddir.z;
@@ -475,7 +480,7 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
 
     // ---- opacity logit through the sigmoid (rasterizer.cpp:343)
     const double o = 1.0 / (1.0 + exp(-ldp(params, cap, P_OP, i)));
-    grads[P_OP * gcap + i] += static_cast<float>(acc[4] * o * (1.0 - o));
+    gput(grads, P_OP * gcap + i, acc[4] * o * (1.0 - o), ACC);
 
     // ---- geometry (projection.cpp:42-74)
     D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
                 rtg[a][c] = (R[0][a] * dsw[0][c] + R[1][a] * dsw[1][c]) + R[2][a] * dsw[2][c];
         for (int a = 0; a < 3; ++a)
             for (int c = 0; c < 3; ++c) rtgr[a][c] = (rtg[a][0] * R[0][c] + rtg[a][1] * R[1][c]) + rtg[a][2] * R[2][c];
-        for (int k = 0; k < 3; ++k) grads[(P_LS + k) * gcap + i] += static_cast<float>(2.0 * s2[k] * rtgr[k][k]);
+        for (int k = 0; k < 3; ++k) gput(grads, (P_LS + k) * gcap + i, 2.0 * s2[k] * rtgr[k][k], ACC);
         double dR[3][3];
         for (int a = 0; a < 3; ++a)
             for (int c = 0; c < 3; ++c) {
@@ -534,7 +539,7 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
             du[k] = s;
         }
         const double ud = ((u[0] * du[0] + u[1] * du[1]) + u[2] * du[2]) + u[3] * du[3];
-        for (int k = 0; k < 4; ++k) grads[(P_ROT + k) * gcap + i] += static_cast<float>((du[k] - u[k] * ud) / nrm);
+        for (int k = 0; k < 4; ++k) gput(grads, (P_ROT + k) * gcap + i, (du[k] - u[k] * ud) / nrm, ACC);
     }
     // position: J^T d_mean + J(p) terms + depth, then W^T
     double dp[3];
@@ -547,16 +552,22 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     dp[2] += acc[3];
     for (int c = 0; c < 3; ++c) {
         const double dpos = (W[0][c] * dp[0] + W[1][c] * dp[1]) + W[2][c] * dp[2];
-        grads[(P_POS + c) * gcap + i] += static_cast<float>(gpos[c] + dpos);
+        gput(grads, (P_POS + c) * gcap + i, gpos[c] + dpos, ACC);
     }
 }
 
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
-                           int n_vis, float* grads, int64_t gcap, cudaStream_t st) {
+                           int n_vis, float* grads, int64_t gcap, bool accumulate, cudaStream_t st) {
     if (n_vis <= 0) return;
-    preprocess_bwd_kernel<<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off,
-                                                             partials, n_vis, grads, gcap);
+    // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
+    // read-modify-write of randomly addressed (map-indexed) gradient entries
+    if (accumulate)
+        preprocess_bwd_kernel<true><<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(
+            params, cap, degree, v, rec, emit_off, partials, n_vis, grads, gcap);
+    else
+        preprocess_bwd_kernel<false><<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(
+            params, cap, degree, v, rec, emit_off, partials, n_vis, grads, gcap);
 }
 
 }  // namespace gsb

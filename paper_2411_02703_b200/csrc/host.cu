@@ -236,7 +236,8 @@ struct gs_grads {
     gs_context* ctx = nullptr;
     float* planes = nullptr;
     int64_t cap = 0;
-    int64_t n = -1;  // Gaussians the gradient set describes (-1 = unset)
+    int64_t n = -1;      // Gaussians the gradient set describes (-1 = unset)
+    bool clean = false;  // all planes zero since the last gs_grads_zero (no backward yet)
     bool external = false;
     void ensure(int64_t need) {
         if (need <= cap) return;
@@ -476,6 +477,7 @@ void grads_zero(gs_grads* G, gs_map* M) {
            "memset grads");
     }
     G->n = M->n;
+    G->clean = true;
 }
 
 void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* dl_ddepth,
@@ -498,7 +500,9 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     {
         Scope sc(C, "preprocess_bwd");
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
-                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), nv, G->planes, G->cap, st);
+                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), nv, G->planes, G->cap,
+                              !G->clean, st);
+        G->clean = false;
         C->launched();
     }
 }
@@ -1123,6 +1127,7 @@ int gs_grads_write(gs_grads* G, const double* in59, int64_t n) {
                                  kNumParams, cudaMemcpyHostToDevice, G->ctx->stream), "h2d grads");
         ck(cudaStreamSynchronize(G->ctx->stream), "sync");
         G->n = n;
+        G->clean = false;
     });
 }
 
