@@ -36,9 +36,9 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
                                                    float* __restrict__ v, int32_t* __restrict__ step,
                                                    const int8_t* __restrict__ degree,
                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
-                                                   AdamArgs args) {
+                                                   AdamArgs args, const unsigned long long* __restrict__ cnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || overflowed(cnt)) return;
     const int t = step[i] + 1;
     step[i] = t;
     float a = args.a_common, b = args.b_common;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
 
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
-                 cudaStream_t st) {
+                 const unsigned long long* cnt, cudaStream_t st) {
     if (n <= 0) return;
     AdamArgs args;
     args.lr[0] = static_cast<float>(lr[0] * scene_extent);
@@ -78,7 +78,7 @@ void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t*
     args.t_common = static_cast<int32_t>(t_common);
     args.a_common = static_cast<float>(1.0 / (1.0 - std::pow(0.9, static_cast<double>(t_common))));
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
-    adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args);
+    adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
 }
 
 namespace {

@@ -62,7 +62,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     const uint32_t* __restrict__ emit_off, ViewParams v, const float* __restrict__ t_final,
     const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,
-    const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials) {
+    const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials,
+    const unsigned long long* __restrict__ cnt) {
+    if (overflowed(cnt)) return;  // pair capacity exceeded: the host re-runs the step
     using S = Strip<PPT>;
     constexpr int NT = S::kThreads, NW = NT / 32, NP = (PPT + 1) / 2;  // PPT = 1: high half never live
     __shared__ StageBuf<kBwdBatch> sb;
@@ -126,20 +128,41 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
         for (int k = 0; k < kNumPartials / 2; ++k) dst[k] = make_float2(0.f, 0.f);
     }
 
+    // the next batch's records are loaded one batch ahead (their dependent global loads overlap
+    // the current batch's walk)
+    Splat nsp;
+    uint32_t noff = 0;
+    if (max_last > 0 && threadIdx.x < max_last - max(0, max_last - kBwdBatch)) {
+        const uint32_t r = vals[range.x + max(0, max_last - kBwdBatch) + threadIdx.x];
+        nsp = rec[r];
+        noff = emit_off[r];
+    }
     for (int hi = max_last; hi > 0; hi -= kBwdBatch) {
         const int lo = max(0, hi - kBwdBatch);
         const int cnt = hi - lo;
         if (NW > 1) __syncthreads();
         if (threadIdx.x < cnt) {
-            const uint32_t r = vals[range.x + lo + threadIdx.x];
-            const Splat sp = rec[r];
-            sb.put(threadIdx.x, stage_of(sp, ox, oy));
-            s_slot[threadIdx.x] = emission_index(sp, emit_off[r], sc.tx, sc.ty);
+            sb.put(threadIdx.x, stage_of(nsp, ox, oy));
+            s_slot[threadIdx.x] = emission_index(nsp, noff, sc.tx, sc.ty);
+        }
+        {
+            const int nlo = max(0, lo - kBwdBatch);
+            if (threadIdx.x < lo - nlo) {
+                const uint32_t r = vals[range.x + nlo + threadIdx.x];
+                nsp = rec[r];
+                noff = emit_off[r];
+            }
         }
         if (sc.lane == 0) s_mask[sc.warp] = 0u;
+        // bounding box of this warp's pixels whose contributor range reaches into the batch
+        unsigned act = 0u;
+#pragma unroll
+        for (int p = 0; p < 2 * NP; ++p)
+            if (last[p] > lo) act |= 1u << p;
+        const int4 ab = warp_bbox<PPT>(act, sc);
         if (NW > 1) __syncthreads(); else __syncwarp();
-        // ballot the staged entries that touch this warp's block, walk them back to front
-        unsigned todo = __ballot_sync(0xffffffffu, sc.lane < cnt && sc.touches(sb.rect[sc.lane]));
+        // ballot the staged entries that meet the box, walk them back to front
+        unsigned todo = __ballot_sync(0xffffffffu, sc.lane < cnt && rect_meets(sb.rect[sc.lane], ab));
         while (todo) {
             const int k = 31 - __clz(todo);
             todo &= ~(1u << k);
@@ -158,8 +181,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
                 const int p0 = 2 * q, y0 = sc.py0 + p0;
                 const bool a0 = colin && j < last[p0] && y0 >= rc.y && y0 <= rc.w;
                 const bool a1 = colin && j < last[p0 + 1] && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
-                if (!(a0 || a1)) continue;
-                any = true;
+                // no branch on (a0 || a1): inactive halves contribute exact zeros (al = 0 ->
+                // w = 0, gd = 0, T kept), and the pairs of a thread stay independent for ILP
+                any |= a0 || a1;
                 const float fy = static_cast<float>(sc.ly0 + p0);
                 const AlphaP e = alpha_pair(m, cn, fx, make_float2(fy, fy + 1.f));
                 const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
@@ -231,24 +255,24 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
-                      float* partials, cudaStream_t st) {
+                      float* partials, const unsigned long long* cnt, cudaStream_t st) {
     const int n_tiles = v.tiles_x * v.tiles_y;
     switch (blend_ppt(v, true)) {
         case 8:
             blend_bwd_kernel<8><<<n_tiles, 32, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials);
+                                                        dl_ddepth, depth_scale, partials, cnt);
             break;
         case 4:
             blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials);
+                                                        dl_ddepth, depth_scale, partials, cnt);
             break;
         case 1:
             blend_bwd_kernel<1><<<n_tiles, 256, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials);
+                                                         dl_ddepth, depth_scale, partials, cnt);
             break;
         default:
             blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials);
+                                                         dl_ddepth, depth_scale, partials, cnt);
     }
 }
 

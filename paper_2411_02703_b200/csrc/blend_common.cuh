@@ -141,6 +141,23 @@ struct Strip {
     }
 };
 
+// Bounding box (x0, y0, x1, y1) of the warp's pixels flagged in `bits` (bit p = row py0 + p of
+// this lane); empty (x0 > x1) when no lane has one. Entries whose rect misses it cannot touch
+// any of those pixels, so the warp's ballot skips them: as pixels terminate (forward) or before
+// they start (backward), the walk shrinks to the entries that can still matter.
+template <int PPT>
+__device__ __forceinline__ int4 warp_bbox(unsigned bits, const Strip<PPT>& sc) {
+    const bool any = bits != 0u;
+    const int x0 = any ? sc.px : 0x7fffffff, x1 = any ? sc.px : -1;
+    const int y0 = any ? sc.py0 + __ffs(bits) - 1 : 0x7fffffff, y1 = any ? sc.py0 + 31 - __clz(bits) : -1;
+    return make_int4(__reduce_min_sync(0xffffffffu, x0), __reduce_min_sync(0xffffffffu, y0),
+                     __reduce_max_sync(0xffffffffu, x1), __reduce_max_sync(0xffffffffu, y1));
+}
+
+__device__ __forceinline__ bool rect_meets(const int4& rc, const int4& bb) {
+    return !(rc.x > bb.z || rc.z < bb.x || rc.y > bb.w || rc.w < bb.y);
+}
+
 // pixels-per-thread chosen per level (host override for experiments; 0 = automatic)
 int blend_ppt(const ViewParams& v, bool backward);
 

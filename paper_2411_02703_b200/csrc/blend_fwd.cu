@@ -76,18 +76,28 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
         nproc[p] = ncontrib[p] = 0;
         if (p < PPT && sc.px < v.width && sc.py0 + p < v.height) live |= 1u << p;
     }
+    int4 lb = warp_bbox<PPT>(live, sc);
+    unsigned seen = live;
+    // the next batch's record is loaded one batch ahead (its latency overlaps the current walk)
+    Splat nsp;
+    if (range.x + threadIdx.x < range.y) nsp = rec[vals[range.x + threadIdx.x]];
     for (uint32_t base = range.x; base < range.y; base += NT) {
         if (__syncthreads_count(live != 0) == 0) break;
         const uint32_t idx = base + threadIdx.x;
-        if (idx < range.y) sb.put(threadIdx.x, stage_of(rec[vals[idx]], ox, oy));
+        if (idx < range.y) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
+        if (idx + NT < range.y) nsp = rec[vals[idx + NT]];
         __syncthreads();
         const int cnt = min(NT, static_cast<int>(range.y - base));
-        // the warp first ballots which staged entries touch its block, then walks only those
-        // (in list order): no per-entry cull branch for the entries of other blocks
+        // the warp first ballots which staged entries meet the bounding box of its live pixels,
+        // then walks only those (in list order)
         for (int b0 = 0; b0 < cnt; b0 += 32) {
-            if (!__any_sync(0xffffffffu, live != 0)) break;
+            if (__any_sync(0xffffffffu, live != seen)) {
+                seen = live;
+                lb = warp_bbox<PPT>(live, sc);
+            }
+            if (lb.x > lb.z) break;  // no live pixel left in this warp
             const int jj = b0 + sc.lane;
-            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && sc.touches(sb.rect[jj]));
+            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && rect_meets(sb.rect[jj], lb));
             while (todo) {
             const int j = b0 + __ffs(todo) - 1;
             todo &= todo - 1;
@@ -102,7 +112,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
                 const int p0 = 2 * q, y0 = sc.py0 + p0;
                 const bool a0 = ((live >> p0) & 1u) && y0 >= rc.y && y0 <= rc.w;
                 const bool a1 = ((live >> (p0 + 1)) & 1u) && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
-                if (!(a0 || a1)) continue;
+                // no branch on (a0 || a1): an inactive half has al = 0 -> w = 0 and factor 1 + 0,
+                // which leaves Th + Tl exactly unchanged (Fast2Sum renormalisation)
                 const float fy = static_cast<float>(sc.ly0 + p0);
                 const AlphaP e = alpha_pair(m, cn, fx, make_float2(fy, fy + 1.f));
                 const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
@@ -185,10 +196,11 @@ int blend_ppt(const ViewParams& v, bool backward) {
     if (o == 1 || o == 2 || o == 4 || o == 8) return o;
     // measured on B200 (1M Gaussians, 1280x1024 pyramid, tests/diag_fwd.py): the forward wants
     // 2 pixels per thread, and 1 at the coarsest level where only 320 tiles (long lists) exist;
-    // the backward amortises its per-entry warp reduction over 4 pixels at L0 (5120 tiles).
+    // the backward amortises its per-entry warp reduction over 4 pixels once there are >= 1280
+    // tiles (L1, L0) and keeps 2 (more warps per tile) at the 320-tile level.
     const int tiles = v.tiles_x * v.tiles_y;
     if (!backward) return tiles >= 1024 ? 2 : 1;
-    return tiles >= 4096 ? 4 : 2;
+    return tiles >= 1024 ? 4 : 2;
 }
 
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,

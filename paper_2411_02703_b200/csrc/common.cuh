@@ -51,6 +51,16 @@ struct LossScalars {       // device-side loss accumulators (fp64) for one compu
     float pad;
 };
 
+// Per-frame device counters (u64). The step is enqueued without reading them on the host:
+// kernels take their element counts from here, and the pair buffers are sized by a
+// per-resolution capacity; a render whose pair count exceeds it raises kCntOverflow, every
+// consumer (blend_bwd, preprocess_bwd, adam) then does nothing, and the host re-runs the step.
+enum Counter : int { kCntVisible = 0, kCntPairs = 1, kCntCand = 2, kCntOverflow = 3, kNumCounters = 4 };
+
+__device__ __forceinline__ bool overflowed(const unsigned long long* cnt) {
+    return cnt != nullptr && *(volatile const unsigned long long*)(cnt + kCntOverflow) != 0ull;
+}
+
 __host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
 
 }  // namespace gsb

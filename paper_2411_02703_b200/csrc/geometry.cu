@@ -420,9 +420,12 @@ template <bool ACC>
 __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
-    const float* __restrict__ partials, int n_vis, float* __restrict__ grads, int64_t gcap) {
+    const float* __restrict__ partials, const unsigned long long* __restrict__ cnt, float* __restrict__ grads,
+    int64_t gcap) {
     __shared__ float rows[kRowChunk * kNumPartials];
     const int r0 = blockIdx.x * kBwdRanks;
+    const int n_vis = static_cast<int>(cnt[kCntVisible]);
+    if (r0 >= n_vis || overflowed(cnt)) return;  // whole block (before any barrier)
     const int r = r0 + threadIdx.x;
     const int rend = min(r0 + kBwdRanks, n_vis);
     const uint32_t b0 = emit_off[r0], b1 = emit_off[rend];
@@ -558,16 +561,17 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
 
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
-                           int n_vis, float* grads, int64_t gcap, bool accumulate, cudaStream_t st) {
-    if (n_vis <= 0) return;
+                           const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,
+                           bool accumulate, cudaStream_t st) {
+    if (max_ranks <= 0) return;
     // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
     // read-modify-write of randomly addressed (map-indexed) gradient entries
     if (accumulate)
-        preprocess_bwd_kernel<true><<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(
-            params, cap, degree, v, rec, emit_off, partials, n_vis, grads, gcap);
+        preprocess_bwd_kernel<true><<<div_up(max_ranks, kBwdRanks), kBwdRanks, 0, st>>>(
+            params, cap, degree, v, rec, emit_off, partials, cnt, grads, gcap);
     else
-        preprocess_bwd_kernel<false><<<div_up(n_vis, kBwdRanks), kBwdRanks, 0, st>>>(
-            params, cap, degree, v, rec, emit_off, partials, n_vis, grads, gcap);
+        preprocess_bwd_kernel<false><<<div_up(max_ranks, kBwdRanks), kBwdRanks, 0, st>>>(
+            params, cap, degree, v, rec, emit_off, partials, cnt, grads, gcap);
 }
 
 }  // namespace gsb

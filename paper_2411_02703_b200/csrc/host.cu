@@ -130,7 +130,6 @@ struct gs_context {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     DevBuf cub_tmp;
-    DevBuf counters;  // 2 x u64
     PinnedBuf pinned;
     int64_t launches = 0;
     gs_frame* scratch_frame = nullptr;
@@ -221,6 +220,19 @@ struct gs_frame {
     bool rendered = false;
     ViewParams view{};
     int64_t map_n = 0, n_vis = 0, n_pairs = 0;
+    // Device counts (Counter) are read back lazily: n_vis / n_pairs / overflow are valid only
+    // when counts_known. Pair buffers are sized by a capacity remembered per resolution.
+    DevBuf counters;
+    bool counts_known = false, overflow = false;
+    uint32_t pair_cap = 0;
+    std::vector<std::pair<int64_t, uint32_t>> caps;  // (width << 32 | height) -> pair capacity
+    uint32_t& cap_slot(int w, int h) {
+        const int64_t key = (static_cast<int64_t>(w) << 32) | static_cast<uint32_t>(h);
+        for (auto& c : caps)
+            if (c.first == key) return c.second;
+        caps.emplace_back(key, 0u);
+        return caps.back().second;
+    }
     // per-Gaussian / per-rank / per-pair scratch
     DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
         num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, depth_sorted;
@@ -359,9 +371,39 @@ void frame_pixels(gs_frame* F, const ViewParams& v) {
     F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * sizeof(uint2));
 }
 
+unsigned long long* dev_counters(gs_frame* F) { return F->counters.as<unsigned long long>(); }
+
+void take_counts(gs_frame* F, const unsigned long long* cnt) {
+    F->n_vis = static_cast<int64_t>(cnt[kCntVisible]);
+    F->n_pairs = static_cast<int64_t>(cnt[kCntPairs]);
+    F->overflow = cnt[kCntOverflow] != 0;
+    F->counts_known = true;
+    if (F->n_pairs > 0xffffffffLL) fail(GS_ELOGIC, "render: more than 2^32 (tile, gaussian) pairs");
+}
+
+// one host round trip for the frame's device counts (no-op when already read)
+void ensure_counts(gs_frame* F) {
+    if (F->counts_known) return;
+    gs_context* C = F->ctx;
+    C->pinned.ensure(sizeof(LossScalars) + 64);
+    ck(cudaMemcpyAsync(C->pinned.p, F->counters.p, kNumCounters * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       C->stream), "d2h counters");
+    ck(cudaStreamSynchronize(C->stream), "sync counters");
+    take_counts(F, static_cast<const unsigned long long*>(C->pinned.p));
+}
+
+uint32_t grown_cap(int64_t pairs) {
+    const int64_t c = pairs + pairs / 8 + 65536;
+    return static_cast<uint32_t>(std::min<int64_t>(c, 0xffffffffLL));
+}
+
 // render (rasterizer.cpp:100-199) without the CSR: project -> compact -> depth sort -> pack ->
-// scan -> emit (tile, rank) pairs -> stable tile sort -> ranges -> blend.
-void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F) {
+// scan -> emit (tile, rank) pairs -> stable tile sort -> ranges -> blend. Nothing here waits
+// for the device: the sorts and scans run at capacity (the map size for ranks, the
+// resolution's pair capacity for pairs) with sentinel keys past the device counts. With
+// exact_counts (or an unknown capacity) the pair count is read back first and the capacity
+// grown to fit, so the render cannot overflow.
+void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F, bool exact_counts) {
     validate_camera(cam);
     gs_context* C = M->ctx;
     C->use();
@@ -375,89 +417,91 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     const int n = static_cast<int>(M->n);
     const int T = v.tiles_x * v.tiles_y;
     ck(cudaMemsetAsync(F->ranges.p, 0, sizeof(uint2) * T, st), "memset ranges");
+    F->counters.ensure(kNumCounters * sizeof(unsigned long long));
+    ck(cudaMemsetAsync(F->counters.p, 0, kNumCounters * sizeof(unsigned long long), st), "memset counters");
     F->n_vis = 0;
     F->n_pairs = 0;
+    F->overflow = false;
+    F->counts_known = n == 0;
+    F->pair_cap = 0;
+    unsigned long long* cnt = dev_counters(F);
     if (n > 0) {
         F->rec_by_gid.ensure(sizeof(Splat) * n);
         F->vis_flag.ensure(sizeof(int32_t) * n);  // K1a candidate list
         F->key_by_gid.ensure(sizeof(unsigned long long) * n);
         F->vis_gid.ensure(sizeof(int32_t) * n);
         F->keys_a.ensure(sizeof(uint32_t) * n);
-        C->counters.ensure(3 * sizeof(unsigned long long));
-        C->pinned.ensure(64);
-        ck(cudaMemsetAsync(C->counters.p, 0, 3 * sizeof(unsigned long long), st), "memset counters");
+        F->keys_b.ensure(sizeof(uint32_t) * n);
+        F->gid_sorted.ensure(sizeof(int32_t) * n);
+        F->rec_sorted.ensure(sizeof(Splat) * n);
+        F->depth_sorted.ensure(sizeof(unsigned long long) * n);
+        F->ntiles.ensure(sizeof(uint32_t) * (n + 1));
+        F->emit_off.ensure(sizeof(uint32_t) * (n + 1));
+        // sentinel depth keys past the visible count (real keys are positive fp32 bits)
+        ck(cudaMemsetAsync(F->keys_a.p, 0xff, sizeof(uint32_t) * n, st), "memset keys");
         {
             Scope sc(C, "preprocess_fwd");
-            launch_cull(M->params, M->cap, n, v, F->vis_flag.as<int32_t>(), C->counters.as<unsigned long long>(), st);
+            launch_cull(M->params, M->cap, n, v, F->vis_flag.as<int32_t>(), cnt, st);
             launch_preprocess_fwd(M->params, M->cap, M->degree, F->vis_flag.as<int32_t>(), n, v,
                                   F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(),
-                                  F->vis_gid.as<int32_t>(), F->keys_a.as<uint32_t>(),
-                                  C->counters.as<unsigned long long>(), st);
+                                  F->vis_gid.as<int32_t>(), F->keys_a.as<uint32_t>(), cnt, st);
             C->launched(2);
         }
-        ck(cudaMemcpyAsync(C->pinned.p, C->counters.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st),
-           "d2h counters");
-        ck(cudaStreamSynchronize(st), "sync counters");
-        const unsigned long long* cnt = static_cast<unsigned long long*>(C->pinned.p);
-        F->n_vis = static_cast<int64_t>(cnt[0]);
-        F->n_pairs = static_cast<int64_t>(cnt[1]);
-        if (F->n_pairs > 0xffffffffLL) fail(GS_ELOGIC, "render: more than 2^32 (tile, gaussian) pairs");
-    }
-    const int nv = static_cast<int>(F->n_vis);
-    const uint32_t K = static_cast<uint32_t>(F->n_pairs);
-    if (nv > 0) {
-        F->keys_b.ensure(sizeof(uint32_t) * nv);
-        F->gid_sorted.ensure(sizeof(int32_t) * nv);
-        F->rec_sorted.ensure(sizeof(Splat) * nv);
-        F->depth_sorted.ensure(sizeof(unsigned long long) * nv);
-        F->ntiles.ensure(sizeof(uint32_t) * (nv + 1));
-        F->emit_off.ensure(sizeof(uint32_t) * (nv + 1));
-        // (depth, index) order (rasterizer.cpp:69-72): stable radix sort on the fp32-rounded
-        // depth, then exact (fp64 depth, index) order inside runs of equal fp32 keys
-        Scope sc_sort(C, "depth_sort_pack_scan");
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                        F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, 32, st);
-        ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                           F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, 32, st),
-           "depth sort");
-        launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(), F->key_by_gid.as<unsigned long long>(),
-                        nv, st);
-        launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(), nv,
-                    F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(), F->depth_sorted.as<unsigned long long>(), st);
-        C->launched(2);
-        ck(cudaMemsetAsync(F->ntiles.as<uint32_t>() + nv, 0, sizeof(uint32_t), st), "memset");
-        tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), nv + 1, st);
-        ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
-                                         nv + 1, st), "scan");
-        if (K > 0) {
+        uint32_t& cap = F->cap_slot(v.width, v.height);
+        if (cap == 0 || exact_counts) {
+            ensure_counts(F);
+            cap = std::max(cap, grown_cap(F->n_pairs));
+        }
+        F->pair_cap = cap;
+        {
+            // (depth, index) order (rasterizer.cpp:69-72): stable radix sort on the fp32-rounded
+            // depth, then exact (fp64 depth, index) order inside runs of equal fp32 keys
+            Scope sc_sort(C, "depth_sort_pack_scan");
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
+                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, 32, st);
+            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
+                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, 32, st),
+               "depth sort");
+            launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(),
+                            F->key_by_gid.as<unsigned long long>(), cnt, n, st);
+            launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(),
+                        cnt, n, F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(),
+                        F->depth_sorted.as<unsigned long long>(), st);
+            C->launched(2);
+            tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), n + 1, st);
+            ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
+                                             n + 1, st), "scan");
+        }
+        {
             Scope sc_keys(C, "tile_keys_sort_ranges");
-            F->pair_keys.ensure(sizeof(uint32_t) * K);
-            F->pair_keys2.ensure(sizeof(uint32_t) * K);
-            F->pair_vals.ensure(sizeof(uint32_t) * K);
-            F->pair_vals2.ensure(sizeof(uint32_t) * K);
-            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), nv, K, v.tiles_x,
+            F->pair_keys.ensure(sizeof(uint32_t) * cap);
+            F->pair_keys2.ensure(sizeof(uint32_t) * cap);
+            F->pair_vals.ensure(sizeof(uint32_t) * cap);
+            F->pair_vals2.ensure(sizeof(uint32_t) * cap);
+            ck(cudaMemsetAsync(F->pair_keys.p, 0xff, sizeof(uint32_t) * cap, st), "memset pair keys");
+            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, n, cap, v.tiles_x,
                               F->pair_keys.as<uint32_t>(), F->pair_vals.as<uint32_t>(), st);
             C->launched();
-            int bits = 1;
-            while ((1 << bits) < T) ++bits;
-            tb = 0;
+            int bits = 1;  // the sentinel's low bits (2^bits - 1) must sort after every tile id
+            while ((1u << bits) <= static_cast<uint32_t>(T)) ++bits;
+            size_t tb = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tb, F->pair_keys.as<uint32_t>(), F->pair_keys2.as<uint32_t>(),
                                             F->pair_vals.as<uint32_t>(), F->pair_vals2.as<uint32_t>(),
-                                            static_cast<int>(K), 0, bits, st);
+                                            static_cast<int>(cap), 0, bits, st);
             ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->pair_keys.as<uint32_t>(),
                                                F->pair_keys2.as<uint32_t>(), F->pair_vals.as<uint32_t>(),
-                                               F->pair_vals2.as<uint32_t>(), static_cast<int>(K), 0, bits, st),
+                                               F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st),
                "tile sort");
-            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), K, F->ranges.as<uint2>(), st);
+            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), cnt, cap, F->ranges.as<uint2>(), st);
             C->launched();
         }
     }
     {
         Scope sc(C, "blend_fwd");
-        launch_blend_fwd(F->ranges.as<uint2>(), K > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
-                         nv > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
+        launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
+                         n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
                          F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), st);
         C->launched();
@@ -467,6 +511,25 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
 
 void need_rendered(gs_frame* F) {
     if (!F->rendered) fail(GS_ELOGIC, "render_backward: contributor lists missing or inconsistent");
+}
+
+// the public render: synchronous like the reference's, re-rendered at exact capacity if the
+// remembered pair capacity was too small
+void render_checked(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F) {
+    render_impl(M, pose, cam, F, false);
+    ensure_counts(F);
+    if (F->overflow) {
+        render_impl(M, pose, cam, F, true);
+        ensure_counts(F);
+        if (F->overflow) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
+    }
+}
+
+// counts for the read-back entry points (the frame is never left overflowed by the API)
+void need_counts(gs_frame* F) {
+    need_rendered(F);
+    ensure_counts(F);
+    if (F->overflow) fail(GS_ELOGIC, "frame: pair capacity overflow (render again)");
 }
 
 void grads_zero(gs_grads* G, gs_map* M) {
@@ -486,33 +549,33 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     cudaStream_t st = C->stream;
     need_rendered(F);
     if (F->map_n != M->n) fail(GS_ELOGIC, "render_backward: contributor lists missing or inconsistent");
-    const int nv = static_cast<int>(F->n_vis);
-    const uint32_t K = static_cast<uint32_t>(F->n_pairs);
-    if (nv == 0 || K == 0) return;
-    F->partials.ensure(sizeof(float) * kNumPartials * K);
+    if (M->n == 0 || F->pair_cap == 0) return;
+    if (F->counts_known && (F->n_vis == 0 || F->n_pairs == 0)) return;
+    F->partials.ensure(sizeof(float) * kNumPartials * F->pair_cap);
     {
         Scope sc(C, "blend_bwd");
         launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
                          F->emit_off.as<uint32_t>(), F->view, F->t_final.as<float>(), F->n_proc.as<int32_t>(),
-                         dl_dcolor, dl_ddepth, depth_scale, F->partials.as<float>(), st);
+                         dl_dcolor, dl_ddepth, depth_scale, F->partials.as<float>(), dev_counters(F), st);
         C->launched();
     }
     {
         Scope sc(C, "preprocess_bwd");
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
-                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), nv, G->planes, G->cap,
-                              !G->clean, st);
+                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), dev_counters(F),
+                              static_cast<int>(M->n), G->planes, G->cap, !G->clean, st);
         G->clean = false;
         C->launched();
     }
 }
 
-void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr) {
+// counters: the frame whose gradients these are (the update is skipped if it overflowed)
+void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsigned long long* counters = nullptr) {
     if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
     launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
-                M->scene_extent, M->step0 + 1, M->ctx->stream);
+                M->scene_extent, M->step0 + 1, counters, M->ctx->stream);
     ++M->step0;
     M->ctx->launched();
     ++M->global_step;
@@ -548,13 +611,19 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     F->loss_lambda_d = cfg.lambda_d;
 }
 
+// loss scalars and the frame's counts in one round trip
 gs_loss_result read_loss(gs_frame* F) {
     gs_context* C = F->ctx;
     C->pinned.ensure(sizeof(LossScalars) + 64);
-    ck(cudaMemcpyAsync(C->pinned.p, F->loss.p, sizeof(LossScalars), cudaMemcpyDeviceToHost, C->stream), "d2h loss");
+    char* pin = static_cast<char*>(C->pinned.p);
+    ck(cudaMemcpyAsync(pin, F->loss.p, sizeof(LossScalars), cudaMemcpyDeviceToHost, C->stream), "d2h loss");
+    if (!F->counts_known)
+        ck(cudaMemcpyAsync(pin + sizeof(LossScalars), F->counters.p, kNumCounters * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, C->stream), "d2h counters");
     ck(cudaStreamSynchronize(C->stream), "sync loss");
+    if (!F->counts_known) take_counts(F, reinterpret_cast<const unsigned long long*>(pin + sizeof(LossScalars)));
     LossScalars s;
-    std::memcpy(&s, C->pinned.p, sizeof(s));
+    std::memcpy(&s, pin, sizeof(s));
     const int h = F->view.height, w = F->view.width;
     const double inv_n = 1.0 / (static_cast<double>(h) * w * 3);
     gs_loss_result r{};
@@ -622,10 +691,10 @@ gs_grads* scratch_grads(gs_context* C) {
 }
 
 void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_camera& cam, gs_frame* F,
-                gs_grads* G, int* level_out) {
+                gs_grads* G, int* level_out, bool exact_counts) {
     const int level = schedule_level(K, cfg);
     const gs_camera lc = scaled(cam, level);
-    render_impl(M, K->pose, lc, F);
+    render_impl(M, K->pose, lc, F, exact_counts);
     loss_impl(F, K, level, cfg);
     backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(), &F->loss.as<LossScalars>()->depth_scale, G);
     *level_out = level;
@@ -668,7 +737,6 @@ int gs_context_destroy(gs_context* C) {
         if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external) cudaFree(C->scratch_grads->planes);
         delete C->scratch_grads;
         C->cub_tmp.release();
-        C->counters.release();
         if (C->own_stream) cudaStreamDestroy(C->stream);
         delete C;
     });
@@ -921,12 +989,12 @@ int gs_frame_destroy(gs_frame* F) {
 }
 
 int gs_render(gs_map* M, const gs_pose* pose, const gs_camera* cam, gs_frame* F) {
-    return guard([&] { render_impl(M, *pose, *cam, F); });
+    return guard([&] { render_checked(M, *pose, *cam, F); });
 }
 
 int gs_frame_stats_get(gs_frame* F, gs_frame_stats* out) {
     return guard([&] {
-        need_rendered(F);
+        need_counts(F);
         out->n_visible = F->n_vis;
         out->n_pairs = F->n_pairs;
         out->tiles_x = F->view.tiles_x;
@@ -986,7 +1054,7 @@ int gs_frame_read_pixel_state(gs_frame* F, int32_t* n_contrib, float* t_final) {
 int gs_frame_read_projected(gs_frame* F, int32_t* index, double* mean2, int32_t* rect4, float* conic3,
                             float* opacity, float* color3, double* depth) {
     return guard([&] {
-        need_rendered(F);
+        need_counts(F);
         const int64_t nv = F->n_vis;
         if (nv == 0) return;
         std::vector<Splat> rec(nv);
@@ -1017,7 +1085,7 @@ int gs_frame_read_projected(gs_frame* F, int32_t* index, double* mean2, int32_t*
 
 int gs_frame_read_tiles(gs_frame* F, int64_t* tile_offsets, int32_t* entries) {
     return guard([&] {
-        need_rendered(F);
+        need_counts(F);
         const int T = F->view.tiles_x * F->view.tiles_y;
         const int64_t K = F->n_pairs;
         std::vector<uint2> ranges(T);
@@ -1041,7 +1109,7 @@ int gs_frame_read_tiles(gs_frame* F, int64_t* tile_offsets, int32_t* entries) {
 
 int gs_frame_materialize(gs_frame* F, uint32_t* offsets, int32_t* gaussian, double* alpha) {
     return guard([&] {
-        need_rendered(F);
+        need_counts(F);
         const int h = F->view.height, w = F->view.width;
         const size_t P = static_cast<size_t>(h) * w;
         std::vector<int32_t> nc(P);
@@ -1306,12 +1374,21 @@ int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const g
         if (K->consumed >= K->initial_iters) return;  // std::nullopt (mapper.cpp:219)
         gs_frame* F = scratch_frame(M->ctx);
         gs_grads* G = scratch_grads(M->ctx);
-        grads_zero(G, M);
         int level = 0;
-        train_view(M, K, *cfg, *cam, F, G, &level);
-        adam_impl(M, G, cfg->lr);
+        gs_loss_result lr{};
+        // one host round trip per step (the loss read); a step whose render overflowed the
+        // remembered pair capacity changed nothing on the device and is re-run at exact size
+        for (int attempt = 0;; ++attempt) {
+            grads_zero(G, M);
+            train_view(M, K, *cfg, *cam, F, G, &level, attempt > 0);
+            adam_impl(M, G, cfg->lr, dev_counters(F));
+            lr = read_loss(F);
+            if (!F->overflow) break;
+            --M->step0;
+            --M->global_step;
+            if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
+        }
         ++K->consumed;
-        const gs_loss_result lr = read_loss(F);
         report->ran = 1;
         report->level = level;
         report->loss = lr.total;
@@ -1330,15 +1407,20 @@ int gs_train_accumulate(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, c
         G->ensure(std::max<int64_t>(M->n, 1));
         if (G->n != M->n) grads_zero(G, M);
         int level = 0;
-        train_view(M, K, *cfg, *cam, F, G, &level);
-        ++K->consumed;
-        report->ran = 1;
-        report->level = level;
-        if (sync) {
+        // without a loss read-back (sync = 0) the pair count is read before binning instead, so
+        // the accumulation can never be dropped by an overflow
+        for (int attempt = 0;; ++attempt) {
+            train_view(M, K, *cfg, *cam, F, G, &level, attempt > 0 || !sync);
+            if (!sync) break;
             const gs_loss_result lr = read_loss(F);
             report->loss = lr.total;
             report->psnr = lr.psnr;
+            if (!F->overflow) break;
+            if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
         }
+        ++K->consumed;
+        report->ran = 1;
+        report->level = level;
     });
 }
 

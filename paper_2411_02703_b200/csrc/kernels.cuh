@@ -6,32 +6,36 @@
 namespace gsb {
 
 // geometry.cu (FP64, --fmad=false)
-// counters: [0] visible, [1] (tile, gaussian) pairs, [2] K1a candidates
+// counters (Counter in common.cuh): [0] visible, [1] (tile, gaussian) pairs, [2] K1a
+// candidates, [3] overflow. Kernels after K1 read their counts from there; max_* arguments
+// are host-side capacities that size the grids.
 void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, int32_t* cand,
                  unsigned long long* counters, cudaStream_t st);
 void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, const int32_t* cand,
                            int max_cand, const ViewParams& v, Splat* rec_by_gid, unsigned long long* depth_key,
                            int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st);
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
-                           const Splat* rec, const uint32_t* emit_off, const float* partials, int n_vis,
-                           float* grads, int64_t gcap, bool accumulate, cudaStream_t st);
+                           const Splat* rec, const uint32_t* emit_off, const float* partials,
+                           const unsigned long long* counters, int max_ranks, float* grads, int64_t gcap,
+                           bool accumulate, cudaStream_t st);
 
 // raster.cu
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
-                     int n_vis, cudaStream_t st);
+                     const unsigned long long* counters, int max_n, cudaStream_t st);
 void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
-                 int n_vis, Splat* rec_sorted, uint32_t* ntiles_sorted, unsigned long long* depth_sorted,
-                 cudaStream_t st);
-void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, int n_vis, uint32_t n_pairs, int tiles_x,
-                       uint32_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_tile_ranges(const uint32_t* keys_sorted, uint32_t n_pairs, uint2* ranges, cudaStream_t st);
+                 const unsigned long long* counters, int max_n, Splat* rec_sorted, uint32_t* ntiles_sorted,
+                 unsigned long long* depth_sorted, cudaStream_t st);
+void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* counters, int max_n,
+                       uint32_t pair_cap, int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t st);
+void launch_tile_ranges(const uint32_t* keys_sorted, const unsigned long long* counters, uint32_t pair_cap,
+                        uint2* ranges, cudaStream_t st);
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib, cudaStream_t st);
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
-                      float* partials, cudaStream_t st);
+                      float* partials, const unsigned long long* counters, cudaStream_t st);
 void read_blend_stats(unsigned long long out[2], bool reset);
 void set_blend_ppt(int fwd, int bwd);
 void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
@@ -49,7 +53,7 @@ void launch_downsample(const float* in, int h, int w, int channels, bool depth, 
 // adam.cu
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
-                 cudaStream_t st);
+                 const unsigned long long* counters /* nullable: skip on overflow */, cudaStream_t st);
 void launch_position_minmax(const float* params, int64_t cap, int n, float* out6, cudaStream_t st);
 void launch_to_hwc_double(const float* planes, int h, int w, int channels, double* out, cudaStream_t st);
 void launch_from_hwc_double(const double* hwc, int h, int w, int channels, float* planes, cudaStream_t st);

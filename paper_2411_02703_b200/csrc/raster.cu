@@ -11,7 +11,8 @@ namespace gsb {
 // such run (almost always 2 elements) is insertion-sorted here by (fp64 depth, map index).
 // The result is exactly the fp64 (depth, index) order, independent of the append order.
 __global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __restrict__ gid,
-                                const unsigned long long* __restrict__ depth, int n) {
+                                const unsigned long long* __restrict__ depth, const unsigned long long* __restrict__ cnt) {
+    const int n = static_cast<int>(cnt[kCntVisible]);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = key[i];
@@ -34,17 +35,22 @@ __global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __res
 }
 
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
-                     int n, cudaStream_t st) {
-    if (n > 1) fix_ties_kernel<<<div_up(n, 256), 256, 0, st>>>(key32_sorted, gid_sorted, depth_by_gid, n);
+                     const unsigned long long* cnt, int max_n, cudaStream_t st) {
+    if (max_n > 1) fix_ties_kernel<<<div_up(max_n, 256), 256, 0, st>>>(key32_sorted, gid_sorted, depth_by_gid, cnt);
 }
 
-// rank-ordered copy of the projected records (the reference's sorted `projected` vector)
+// rank-ordered copy of the projected records (the reference's sorted `projected` vector);
+// the tile counts past the last visible rank are zeroed so the scan can run at capacity
 __global__ void pack_kernel(const int32_t* __restrict__ gid_sorted, const Splat* __restrict__ rec_by_gid,
-                            const unsigned long long* __restrict__ depth_by_gid, int n,
-                            Splat* __restrict__ rec_sorted, uint32_t* __restrict__ ntiles,
-                            unsigned long long* __restrict__ depth_sorted) {
+                            const unsigned long long* __restrict__ depth_by_gid,
+                            const unsigned long long* __restrict__ cnt, int max_n, Splat* __restrict__ rec_sorted,
+                            uint32_t* __restrict__ ntiles, unsigned long long* __restrict__ depth_sorted) {
+    const int n = static_cast<int>(cnt[kCntVisible]);
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
+    if (r >= n) {
+        if (r <= max_n) ntiles[r] = 0u;
+        return;
+    }
     const int g = gid_sorted[r];
     const Splat s = rec_by_gid[g];
     rec_sorted[r] = s;
@@ -52,11 +58,11 @@ __global__ void pack_kernel(const int32_t* __restrict__ gid_sorted, const Splat*
     depth_sorted[r] = depth_by_gid[g];
 }
 
-void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid, int n,
-                 Splat* rec_sorted, uint32_t* ntiles, unsigned long long* depth_sorted, cudaStream_t st) {
-    if (n > 0)
-        pack_kernel<<<div_up(n, 256), 256, 0, st>>>(gid_sorted, rec_by_gid, depth_by_gid, n, rec_sorted, ntiles,
-                                                    depth_sorted);
+void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
+                 const unsigned long long* cnt, int max_n, Splat* rec_sorted, uint32_t* ntiles,
+                 unsigned long long* depth_sorted, cudaStream_t st) {
+    pack_kernel<<<div_up(max_n + 1, 256), 256, 0, st>>>(gid_sorted, rec_by_gid, depth_by_gid, cnt, max_n, rec_sorted,
+                                                        ntiles, depth_sorted);
 }
 
 // Duplicate-key emission (bin_tiles, rasterizer.cpp:76-91). A warp owns 32 consecutive depth
@@ -64,15 +70,24 @@ void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsig
 // rank with all lanes (coalesced, load-balanced across large and small footprints). Keys are
 // tile ids; values are depth ranks, so a stable sort by tile yields each tile's list in
 // (depth, index) order, exactly the reference's push_back order (ty outer, tx inner).
+// Pairs beyond the capacity raise the overflow flag instead (nothing is written).
 __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restrict__ emit_off,
-                                                         const Splat* __restrict__ rec, int n_vis, int tiles_x,
-                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                                         const Splat* __restrict__ rec,
+                                                         unsigned long long* __restrict__ cnt, uint32_t cap,
+                                                         int tiles_x, uint32_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ vals) {
+    const int n_vis = static_cast<int>(cnt[kCntVisible]);
+    if (cnt[kCntPairs] > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) cnt[kCntOverflow] = 1ull;
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x);
-    int off = 0, cnt = 0, tx0 = 0, ty0 = 0, ntx = 1;
+    if (r - lane >= n_vis) return;  // whole warp past the visible ranks
+    int off = 0, len = 0, tx0 = 0, ty0 = 0, ntx = 1;
     if (r < n_vis) {
         off = static_cast<int>(emit_off[r]);
-        cnt = static_cast<int>(emit_off[r + 1]) - off;
+        len = static_cast<int>(emit_off[r + 1]) - off;
         const Splat& s = rec[r];
         tx0 = s.x0 >> 4;
         ty0 = s.y0 >> 4;
@@ -80,7 +95,7 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
     }
     const int rbase = r - lane;
     for (int i = 0; i < 32; ++i) {
-        const int c = __shfl_sync(0xffffffffu, cnt, i);
+        const int c = __shfl_sync(0xffffffffu, len, i);
         if (c == 0) continue;
         const int o = __shfl_sync(0xffffffffu, off, i);
         const int x0 = __shfl_sync(0xffffffffu, tx0, i);
@@ -94,13 +109,18 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
     }
 }
 
-void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, int n_vis, uint32_t n_pairs, int tiles_x,
-                       uint32_t* keys, uint32_t* vals, cudaStream_t st) {
-    if (n_pairs > 0 && n_vis > 0)
-        emit_pairs_kernel<<<div_up(n_vis, 256), 256, 0, st>>>(emit_off, rec, n_vis, tiles_x, keys, vals);
+void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* cnt, int max_n, uint32_t cap,
+                       int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+    if (max_n > 0)
+        emit_pairs_kernel<<<div_up(max_n, 256), 256, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, keys, vals);
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t n, uint2* __restrict__ ranges) {
+// keys are sorted at capacity: the pairs past the device count carry the sentinel key
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ cnt,
+                                   uint32_t cap, uint2* __restrict__ ranges) {
+    const unsigned long long n64 = cnt[kCntPairs];
+    if (n64 > cap) return;
+    const uint32_t n = static_cast<uint32_t>(n64);
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
@@ -108,8 +128,9 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, uint32_t n
     if (i == n - 1 || keys[i + 1] != k) ranges[k].y = i + 1;
 }
 
-void launch_tile_ranges(const uint32_t* keys, uint32_t n, uint2* ranges, cudaStream_t st) {
-    if (n > 0) tile_ranges_kernel<<<div_up(static_cast<int>(n), 256), 256, 0, st>>>(keys, n, ranges);
+void launch_tile_ranges(const uint32_t* keys, const unsigned long long* cnt, uint32_t cap, uint2* ranges,
+                        cudaStream_t st) {
+    if (cap > 0) tile_ranges_kernel<<<div_up(static_cast<int>(cap), 256), 256, 0, st>>>(keys, cnt, cap, ranges);
 }
 
 // RenderOutput::contribs materialised on request (tests, gradcheck): one thread per pixel

@@ -28,7 +28,7 @@ L = G.lib()
 for stage in range(3):
     for lvl in (2, 1, 0):
         line = []
-        for ppt in (1, 2, 4):
+        for ppt in (1, 2, 4, 8):
             L.gs_debug_set_blend_ppt(ppt, ppt)
             kf = kfs[0]
             kf.consumed_iters = 2 - lvl

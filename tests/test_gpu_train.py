@@ -146,3 +146,43 @@ def test_train_step_requires_pyramid_semantics():
     _, gm = pair(O.make_blob([0, 0, 2], 0.5, [1, 0, 0]))
     kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), np.zeros((64, 64, 3)), np.zeros((64, 64)), 0, 0)
     assert G().train_keyframe_step(gm, kf, G().TrainConfig.make(), G().Camera(100, 100, 32, 32, 64, 64)) is None
+
+
+def test_pair_capacity_overflow_reruns_step():
+    """The step is enqueued without reading the (tile, gaussian) pair count back; the pair
+    buffers use a capacity remembered per resolution. A render that outgrows it must leave the
+    map untouched (no Adam update, no step count) and be re-run at exact size."""
+    cam = O.camera(400, 400, 319.5, 239.5, 640, 480)
+    g = random_scene(31, 6000, cam, O.pose(), 0.0, 2.0)
+    small, big = g.copy(), g.copy()
+    small["p"][:, 7:10] = np.log(0.002)  # ~1 tile each: a small remembered capacity
+    big["p"][:, 7:10] = np.log(0.2)      # tens of tiles each: far beyond it
+    gen = np.random.default_rng(2)
+    color = f32(gen.uniform(0, 1, (480, 640, 3)))
+    sparse = f32(np.where(gen.uniform(size=(480, 640)) < 0.1, gen.uniform(1, 8, (480, 640)), 0.0))
+    cfg = G().TrainConfig.make(0.2, 0.5, 0)
+
+    def step(ctx, gmap):
+        kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), color, sparse, 5, 0, ctx=ctx)
+        return G().train_keyframe_step(gmap, kf, cfg, gpu_cam(cam))
+
+    ctx1 = G().Context(0)
+    step(ctx1, G().GaussianMap(ctx1, round32(small)))
+    mb1 = G().GaussianMap(ctx1, round32(big))
+    r1 = step(ctx1, mb1)
+    ctx2 = G().Context(0)
+    mb2 = G().GaussianMap(ctx2, round32(big))
+    r2 = step(ctx2, mb2)
+    assert r1["loss"] == pytest.approx(r2["loss"], rel=1e-9)
+    assert mb1.global_step == mb2.global_step == 1
+    assert np.all(mb1.adam_state()[2] == 1)
+    d = np.abs(mb1.gaussians["p"] - mb2.gaussians["p"])
+    assert np.mean(d <= 1e-6) > 0.999 and d.max() < 0.2
+
+    # the public render re-renders too: same frame object, small then big
+    fr = G().RenderOutput(ctx1)
+    G().render(G().GaussianMap(ctx1, round32(small)), gpu_pose(O.pose()), gpu_cam(cam), fr)
+    G().render(G().GaussianMap(ctx1, round32(big)), gpu_pose(O.pose()), gpu_cam(cam), fr)
+    fresh = G().render(G().GaussianMap(ctx2, round32(big)), gpu_pose(O.pose()), gpu_cam(cam))
+    assert fr.stats().n_pairs == fresh.stats().n_pairs > 100_000
+    np.testing.assert_array_equal(fr.color, fresh.color)
