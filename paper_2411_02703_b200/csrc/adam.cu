@@ -68,6 +68,84 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
     }
 }
 
+// Four consecutive Gaussians per thread with 16-byte loads and stores (every plane base is
+// 16-byte aligned when both capacities are multiples of 4). Same per-scalar arithmetic as
+// adam_kernel; SH coefficients past a Gaussian's degree are left untouched exactly as there.
+__device__ __forceinline__ void adam_vec(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
+                                         float4 g, float lr, const float (&a)[4], const float (&b)[4], int live) {
+    float4 P = *p, Mv = *m, V = *v;
+    float* pp = &P.x;
+    float* mm = &Mv.x;
+    float* vv = &V.x;
+    const float* gg = &g.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (!((live >> e) & 1)) continue;
+        adam_scalar(pp + e, mm + e, vv + e, gg[e], lr, a[e], b[e]);
+    }
+    *p = P;
+    *m = Mv;
+    *v = V;
+}
+
+__global__ void __launch_bounds__(256) adam4_kernel(float* __restrict__ params, float* __restrict__ m,
+                                                    float* __restrict__ v, int32_t* __restrict__ step,
+                                                    const int8_t* __restrict__ degree,
+                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
+                                                    AdamArgs args, const unsigned long long* __restrict__ cnt) {
+    const int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n || overflowed(cnt)) return;
+    const int ne = min(4, n - i);
+    const int all = (1 << ne) - 1;
+    int4 t4 = *reinterpret_cast<const int4*>(step + i);
+    int* tt = &t4.x;
+    float a[4], b[4];
+    int deg[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        a[e] = args.a_common;
+        b[e] = args.b_common;
+        deg[e] = -1;
+        if (e < ne) {
+            const int t = tt[e] + 1;
+            tt[e] = t;
+            deg[e] = degree[i + e];
+            if (t != args.t_common) {
+                a[e] = static_cast<float>(1.0 / (1.0 - pow(0.9, static_cast<double>(t))));
+                b[e] = static_cast<float>(1.0 / (1.0 - pow(0.999, static_cast<double>(t))));
+            }
+        }
+    }
+    *reinterpret_cast<int4*>(step + i) = t4;  // step entries past n are never read
+    float4 g[kGeomParams];
+#pragma unroll
+    for (int k = 0; k < kGeomParams; ++k) g[k] = __ldg(reinterpret_cast<const float4*>(grads + k * gcap + i));
+#pragma unroll
+    for (int k = 0; k < kGeomParams; ++k) {
+        const float lr = k < 3 ? args.lr[0] : k < 7 ? args.lr[1] : k < 10 ? args.lr[2] : args.lr[3];
+        const int64_t o = k * cap + i;
+        adam_vec(reinterpret_cast<float4*>(params + o), reinterpret_cast<float4*>(m + o),
+                 reinterpret_cast<float4*>(v + o), g[k], lr, a, b, all);
+    }
+    const int dmax = max(max(deg[0], deg[1]), max(deg[2], deg[3]));
+    const int ncoef = (dmax + 1) * (dmax + 1);
+    for (int c = 0; c < ncoef; ++c) {
+        int live = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) live |= ((deg[e] + 1) * (deg[e] + 1) > c) << e;
+        float4 gs[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+            gs[ch] = __ldg(reinterpret_cast<const float4*>(grads + (P_SH + 3 * c + ch) * gcap + i));
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const int64_t o = (P_SH + 3 * c + ch) * cap + i;
+            adam_vec(reinterpret_cast<float4*>(params + o), reinterpret_cast<float4*>(m + o),
+                     reinterpret_cast<float4*>(v + o), gs[ch], args.lr[4], a, b, live);
+        }
+    }
+}
+
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
                  const unsigned long long* cnt, cudaStream_t st) {
@@ -78,7 +156,11 @@ void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t*
     args.t_common = static_cast<int32_t>(t_common);
     args.a_common = static_cast<float>(1.0 / (1.0 - std::pow(0.9, static_cast<double>(t_common))));
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
-    adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
+    if (cap % 4 == 0 && gcap % 4 == 0)
+        adam4_kernel<<<div_up(div_up(n, 4), 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args,
+                                                                 cnt);
+    else
+        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
 }
 
 namespace {

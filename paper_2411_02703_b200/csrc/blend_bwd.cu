@@ -6,7 +6,8 @@
 // Each (tile, Gaussian) pair's 10 cotangent sums are reduced per warp (12 shuffles), across the
 // CTA's warps in shared memory, and written once to the pair's emission slot: deterministic,
 // no global atomics; K8 sums a Gaussian's slots in fp64. Partials 5-6 (mean) and 7-9
-// (covariance) carry the staged conic's exp2 scale k and k^2; K8 divides them out.
+// (covariance) carry the staged conic's exp2 scale k and k^2 and omit the opacity factor (op,
+// op / 2); K8 applies both in fp64.
 #include "blend_common.cuh"
 #include "kernels.cuh"
 
@@ -206,14 +207,14 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
                 const float2 gd = make_float2(a0 && e.a_raw.x < kAlphaMaxF ? gdr.x : 0.f,
                                               a1 && e.a_raw.y < kAlphaMaxF ? gdr.y : 0.f);
                 acc[4] = __fadd2_rn(acc[4], gd);
-                const float2 sg = __fmul2_rn(gd, f2(cn.w));
-                acc[5] = __ffma2_rn(sg, e.u0, acc[5]);
-                acc[6] = __ffma2_rn(sg, e.u1, acc[6]);
-                const float2 hs = __fmul2_rn(sg, f2(0.5f));
-                const float2 h0 = __fmul2_rn(hs, e.u0);
+                // mean / covariance terms without the opacity (K8 applies op and op / 2)
+                const float2 h0 = __fmul2_rn(gd, e.u0);
+                const float2 h1 = __fmul2_rn(gd, e.u1);
+                acc[5] = __fadd2_rn(acc[5], h0);
+                acc[6] = __fadd2_rn(acc[6], h1);
                 acc[7] = __ffma2_rn(h0, e.u0, acc[7]);
                 acc[8] = __ffma2_rn(h0, e.u1, acc[8]);
-                acc[9] = __ffma2_rn(__fmul2_rn(hs, e.u1), e.u1, acc[9]);
+                acc[9] = __ffma2_rn(h1, e.u1, acc[9]);
             }
             if (!__any_sync(0xffffffffu, any)) continue;
             float vsum[kNumPartials];

@@ -453,12 +453,14 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     for (int k = 0; k < kNumPartials; ++k) any |= (acc[k] != 0.0);
     if (!any) return;  // untouched (or all-zero cotangent): exact zero gradient
     // the blend evaluates u = Sigma^-1 d with the conic pre-scaled by k = -log2(e)/2 (exp2 form)
+    // and accumulates the mean / covariance terms without the opacity factor (op and op / 2)
     const double inv_k = 1.0 / static_cast<double>(-0.72134752044448170368f);
-    acc[5] *= inv_k;
-    acc[6] *= inv_k;
-    acc[7] *= inv_k * inv_k;
-    acc[8] *= inv_k * inv_k;
-    acc[9] *= inv_k * inv_k;
+    const double op = static_cast<double>(rec[r].opacity);
+    acc[5] *= op * inv_k;
+    acc[6] *= op * inv_k;
+    acc[7] *= 0.5 * op * inv_k * inv_k;
+    acc[8] *= 0.5 * op * inv_k * inv_k;
+    acc[9] *= 0.5 * op * inv_k * inv_k;
     const int i = rec[r].gid;
     const int deg = degree[i];
     const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};

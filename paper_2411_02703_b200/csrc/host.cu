@@ -240,6 +240,7 @@ struct gs_frame {
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
     DevBuf loss;  // LossScalars
     bool has_cotangent = false;
+    bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)
     int loss_level = -1;
     double loss_lambda = 0.0, loss_lambda_d = 0.0;
 };
@@ -256,7 +257,7 @@ struct gs_grads {
         if (external) fail(GS_EINVAL, "gs_grads: external buffer too small for the map");
         if (planes) cudaFree(planes);
         planes = nullptr;
-        const int64_t c = std::max<int64_t>(need + need / 4, 1024);
+        const int64_t c = (std::max<int64_t>(need + need / 4, 1024) + 63) / 64 * 64;
         ck(cudaMalloc(&planes, sizeof(float) * kNumParams * c), "cudaMalloc grads");
         ck(cudaMemsetAsync(planes, 0, sizeof(float) * kNumParams * c, ctx->stream), "memset grads");
         cap = c;
@@ -282,7 +283,8 @@ namespace {
 
 void map_reserve(gs_map* M, int64_t need) {
     if (need <= M->cap) return;
-    const int64_t nc = std::max<int64_t>(need, M->cap + M->cap / 2);
+    // multiples of 64: every plane base stays 16-byte aligned (vectorised Adam)
+    const int64_t nc = (std::max<int64_t>(need, M->cap + M->cap / 2) + 63) / 64 * 64;
     cudaStream_t st = M->ctx->stream;
     float *p = nullptr, *m = nullptr, *v = nullptr;
     int32_t* s = nullptr;
@@ -403,7 +405,8 @@ uint32_t grown_cap(int64_t pairs) {
 // resolution's pair capacity for pairs) with sentinel keys past the device counts. With
 // exact_counts (or an unknown capacity) the pair count is read back first and the capacity
 // grown to fit, so the render cannot overflow.
-void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F, bool exact_counts) {
+void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F, bool exact_counts,
+                 bool stats = true) {
     validate_camera(cam);
     gs_context* C = M->ctx;
     C->use();
@@ -503,10 +506,11 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
         launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
                          n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
-                         F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), st);
+                         F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, st);
         C->launched();
     }
     F->rendered = true;
+    F->has_contrib = stats;
 }
 
 void need_rendered(gs_frame* F) {
@@ -530,6 +534,7 @@ void need_counts(gs_frame* F) {
     need_rendered(F);
     ensure_counts(F);
     if (F->overflow) fail(GS_ELOGIC, "frame: pair capacity overflow (render again)");
+    if (!F->has_contrib) fail(GS_ELOGIC, "frame: contributor counts not recorded for this render");
 }
 
 void grads_zero(gs_grads* G, gs_map* M) {
@@ -694,7 +699,7 @@ void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_
                 gs_grads* G, int* level_out, bool exact_counts) {
     const int level = schedule_level(K, cfg);
     const gs_camera lc = scaled(cam, level);
-    render_impl(M, K->pose, lc, F, exact_counts);
+    render_impl(M, K->pose, lc, F, exact_counts, F != M->ctx->scratch_frame);
     loss_impl(F, K, level, cfg);
     backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(), &F->loss.as<LossScalars>()->depth_scale, G);
     *level_out = level;

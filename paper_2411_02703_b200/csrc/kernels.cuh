@@ -31,7 +31,7 @@ void launch_tile_ranges(const uint32_t* keys_sorted, const unsigned long long* c
                         uint2* ranges, cudaStream_t st);
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
-                      int32_t* n_contrib, cudaStream_t st);
+                      int32_t* n_contrib /* written only when stats */, bool stats, cudaStream_t st);
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
