@@ -68,87 +68,67 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
     }
 }
 
-// Four consecutive Gaussians per thread with 16-byte loads and stores (every plane base is
-// 16-byte aligned when both capacities are multiples of 4). Same per-scalar arithmetic as
-// adam_kernel; SH coefficients past a Gaussian's degree are left untouched exactly as there.
-__device__ __forceinline__ void adam_vec(float4* __restrict__ p, float4* __restrict__ m, float4* __restrict__ v,
-                                         float4 g, float lr, const float (&a)[4], const float (&b)[4], int live) {
-    float4 P = *p, Mv = *m, V = *v;
-    float* pp = &P.x;
-    float* mm = &Mv.x;
-    float* vv = &V.x;
-    const float* gg = &g.x;
+// One thread per (parameter plane, 4 consecutive Gaussians): four independent 16-byte loads
+// (gradient, value, m, v), the per-scalar update of adam_kernel, three 16-byte stores. Many
+// small independent threads keep enough loads in flight to stream HBM (the per-Gaussian form
+// serialises its planes). Every plane base is 16-byte aligned when both capacities are
+// multiples of 4. The step counters are advanced afterwards by adam_step_kernel; here every
+// plane reads the pre-step value. SH planes past a Gaussian's degree are left untouched.
+__global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ params, float* __restrict__ m,
+                                                         float* __restrict__ v, const int32_t* __restrict__ step,
+                                                         const int8_t* __restrict__ degree,
+                                                         const float* __restrict__ grads, int64_t gcap, int64_t cap,
+                                                         int n, AdamArgs args,
+                                                         const unsigned long long* __restrict__ cnt) {
+    const int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    const int k = blockIdx.y;  // plane
+    if (i >= n || overflowed(cnt)) return;
+    const float4 g = __ldg(reinterpret_cast<const float4*>(grads + k * gcap + i));
+    float4* pp = reinterpret_cast<float4*>(params + k * cap + i);
+    float4* mp = reinterpret_cast<float4*>(m + k * cap + i);
+    float4* vp = reinterpret_cast<float4*>(v + k * cap + i);
+    float4 P = *pp, M = *mp, V = *vp;
+    const int4 t4 = __ldg(reinterpret_cast<const int4*>(step + i));
+    const float lr = k < 3 ? args.lr[0] : k < 7 ? args.lr[1] : k < 10 ? args.lr[2] : k < 11 ? args.lr[3] : args.lr[4];
+    const int ne = min(4, n - i);
+    int live = (1 << ne) - 1;
+    if (k >= P_SH) {  // coefficient c = (k - 11) / 3 exists up to the Gaussian's degree
+        const int c = (k - P_SH) / 3;
+        const char4 d4 = *reinterpret_cast<const char4*>(degree + i);
+        const int d[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if ((d[e] + 1) * (d[e] + 1) <= c) live &= ~(1 << e);
+        if (!live) return;
+    }
+    const int t[4] = {t4.x + 1, t4.y + 1, t4.z + 1, t4.w + 1};
+    float* ps = &P.x;
+    float* ms = &M.x;
+    float* vs = &V.x;
+    const float* gs = &g.x;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if (!((live >> e) & 1)) continue;
-        adam_scalar(pp + e, mm + e, vv + e, gg[e], lr, a[e], b[e]);
+        float a = args.a_common, b = args.b_common;
+        if (t[e] != args.t_common) {
+            a = static_cast<float>(1.0 / (1.0 - pow(0.9, static_cast<double>(t[e]))));
+            b = static_cast<float>(1.0 / (1.0 - pow(0.999, static_cast<double>(t[e]))));
+        }
+        adam_scalar(ps + e, ms + e, vs + e, gs[e], lr, a, b);
     }
-    *p = P;
-    *m = Mv;
-    *v = V;
+    *pp = P;
+    *mp = M;
+    *vp = V;
 }
 
-__global__ void __launch_bounds__(256) adam4_kernel(float* __restrict__ params, float* __restrict__ m,
-                                                    float* __restrict__ v, int32_t* __restrict__ step,
-                                                    const int8_t* __restrict__ degree,
-                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
-                                                    AdamArgs args, const unsigned long long* __restrict__ cnt) {
-    const int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i >= n || overflowed(cnt)) return;
-    const int ne = min(4, n - i);
-    const int all = (1 << ne) - 1;
-    int4 t4 = *reinterpret_cast<const int4*>(step + i);
-    int* tt = &t4.x;
-    float a[4], b[4];
-    int deg[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        a[e] = args.a_common;
-        b[e] = args.b_common;
-        deg[e] = -1;
-        if (e < ne) {
-            const int t = tt[e] + 1;
-            tt[e] = t;
-            deg[e] = degree[i + e];
-            if (t != args.t_common) {
-                a[e] = static_cast<float>(1.0 / (1.0 - pow(0.9, static_cast<double>(t))));
-                b[e] = static_cast<float>(1.0 / (1.0 - pow(0.999, static_cast<double>(t))));
-            }
-        }
-    }
-    *reinterpret_cast<int4*>(step + i) = t4;  // step entries past n are never read
-    float4 g[kGeomParams];
-#pragma unroll
-    for (int k = 0; k < kGeomParams; ++k) g[k] = __ldg(reinterpret_cast<const float4*>(grads + k * gcap + i));
-#pragma unroll
-    for (int k = 0; k < kGeomParams; ++k) {
-        const float lr = k < 3 ? args.lr[0] : k < 7 ? args.lr[1] : k < 10 ? args.lr[2] : args.lr[3];
-        const int64_t o = k * cap + i;
-        adam_vec(reinterpret_cast<float4*>(params + o), reinterpret_cast<float4*>(m + o),
-                 reinterpret_cast<float4*>(v + o), g[k], lr, a, b, all);
-    }
-    const int dmax = max(max(deg[0], deg[1]), max(deg[2], deg[3]));
-    const int ncoef = (dmax + 1) * (dmax + 1);
-    for (int c = 0; c < ncoef; ++c) {
-        int live = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) live |= ((deg[e] + 1) * (deg[e] + 1) > c) << e;
-        float4 gs[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-            gs[ch] = __ldg(reinterpret_cast<const float4*>(grads + (P_SH + 3 * c + ch) * gcap + i));
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            const int64_t o = (P_SH + 3 * c + ch) * cap + i;
-            adam_vec(reinterpret_cast<float4*>(params + o), reinterpret_cast<float4*>(m + o),
-                     reinterpret_cast<float4*>(v + o), gs[ch], args.lr[4], a, b, live);
-        }
-    }
+__global__ void adam_step_kernel(int32_t* __restrict__ step, int n, const unsigned long long* __restrict__ cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && !overflowed(cnt)) step[i] += 1;
 }
 
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
-                 const unsigned long long* cnt, cudaStream_t st) {
+                 const unsigned long long* cnt, int max_degree, cudaStream_t st) {
     if (n <= 0) return;
     AdamArgs args;
     args.lr[0] = static_cast<float>(lr[0] * scene_extent);
@@ -156,10 +136,11 @@ void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t*
     args.t_common = static_cast<int32_t>(t_common);
     args.a_common = static_cast<float>(1.0 / (1.0 - std::pow(0.9, static_cast<double>(t_common))));
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
-    if (cap % 4 == 0 && gcap % 4 == 0)
-        adam4_kernel<<<div_up(div_up(n, 4), 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args,
-                                                                 cnt);
-    else
+    if (cap % 4 == 0 && gcap % 4 == 0) {
+        const dim3 grid(div_up(div_up(n, 4), 256), kGeomParams + 3 * (max_degree + 1) * (max_degree + 1));
+        adam_plane_kernel<<<grid, 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
+        adam_step_kernel<<<div_up(n, 256), 256, 0, st>>>(step, n, cnt);
+    } else
         adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
 }
 

@@ -580,9 +580,9 @@ void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsign
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
     launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
-                M->scene_extent, M->step0 + 1, counters, M->ctx->stream);
+                M->scene_extent, M->step0 + 1, counters, M->max_degree, M->ctx->stream);
     ++M->step0;
-    M->ctx->launched();
+    M->ctx->launched(2);
     ++M->global_step;
 }
 

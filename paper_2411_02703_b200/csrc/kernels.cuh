@@ -53,7 +53,8 @@ void launch_downsample(const float* in, int h, int w, int channels, bool depth, 
 // adam.cu
 void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
-                 const unsigned long long* counters /* nullable: skip on overflow */, cudaStream_t st);
+                 const unsigned long long* counters /* nullable: skip on overflow */, int max_degree,
+                 cudaStream_t st);
 void launch_position_minmax(const float* params, int64_t cap, int n, float* out6, cudaStream_t st);
 void launch_to_hwc_double(const float* planes, int h, int w, int channels, double* out, cudaStream_t st);
 void launch_from_hwc_double(const double* hwc, int h, int w, int channels, float* planes, cudaStream_t st);

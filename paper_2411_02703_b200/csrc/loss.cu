@@ -93,17 +93,20 @@ void launch_loss_pixel(const float* color, const float* depth, const float* vis,
 }
 
 // ---------------------------------------------------------------------------------- SSIM
-// Tiles of 32x16 valid-window outputs. Moments use values shifted by 0.5 (variance and
-// covariance are shift invariant) to cut fp32 cancellation in E[a^2] - mu^2; the gradient
-// weights are re-expressed for the shifted moments (same function, same derivative).
-constexpr int kSx = 32, kSy = 16, kHalo = 10;
+// Tiles of 32x32 valid-window outputs, separable 11-tap passes through shared memory with
+// register blocking (a thread slides its window over 4 consecutive outputs, so each staged
+// value is read once per 4 outputs instead of once per tap). Moments use values shifted by
+// 0.5 (variance and covariance are shift invariant) to cut fp32 cancellation in
+// E[a^2] - mu^2; the gradient weights are re-expressed for the shifted moments.
+constexpr int kSx = 32, kSy = 32, kHalo = 10, kRB = 4;  // kRB outputs per thread and pass
+constexpr int kInX = kSx + kHalo, kInY = kSy + kHalo;   // 42 x 42 staged inputs
 constexpr float kShift = 0.5f;
 
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, float inv_n, float* __restrict__ wbuf,
                                                        LossScalars* __restrict__ acc) {
-    __shared__ float sa[kSy + kHalo][kSx + kHalo + 1], sb[kSy + kHalo][kSx + kHalo + 1];
-    __shared__ float hs[5][kSy + kHalo][kSx];
+    __shared__ float sa[kInY][kInX + 2], sb[kInY][kInX + 2];
+    __shared__ float hs[5][kInY][kSx + 1];
     __shared__ double scratch[8];
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * kSx, y0 = blockIdx.y * kSy;
@@ -111,60 +114,89 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
     const size_t P = static_cast<size_t>(h) * w;
     const float* Ac = A + c * P;
     const float* Bc = B + c * P;
-    for (int i = threadIdx.x; i < (kSy + kHalo) * (kSx + kHalo); i += blockDim.x) {
-        const int r = i / (kSx + kHalo), q = i % (kSx + kHalo);
+    for (int i = threadIdx.x; i < kInY * kInX; i += blockDim.x) {
+        const int r = i / kInX, q = i % kInX;
         const int gy = y0 + r, gx = x0 + q;
         const bool ok = gy < h && gx < w;
         sa[r][q] = ok ? Ac[static_cast<size_t>(gy) * w + gx] - kShift : 0.f;
         sb[r][q] = ok ? Bc[static_cast<size_t>(gy) * w + gx] - kShift : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (kSy + kHalo) * kSx; i += blockDim.x) {
-        const int r = i / kSx, q = i % kSx;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+    // horizontal: item = (row r, 4 consecutive output columns)
+    for (int it = threadIdx.x; it < kInY * (kSx / kRB); it += blockDim.x) {
+        const int r = it / (kSx / kRB), q0 = (it % (kSx / kRB)) * kRB;
+        float va[kRB + 10], vb[kRB + 10];
 #pragma unroll
-        for (int l = 0; l < 11; ++l) {
-            const float g = c_taps[l], a = sa[r][q + l], b = sb[r][q + l];
-            m0 = fmaf(g, a, m0);
-            m1 = fmaf(g, b, m1);
-            m2 = fmaf(g * a, a, m2);
-            m3 = fmaf(g * b, b, m3);
-            m4 = fmaf(g * a, b, m4);
+        for (int l = 0; l < kRB + 10; ++l) {
+            va[l] = sa[r][q0 + l];
+            vb[l] = sb[r][q0 + l];
         }
-        hs[0][r][q] = m0; hs[1][r][q] = m1; hs[2][r][q] = m2; hs[3][r][q] = m3; hs[4][r][q] = m4;
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+            float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+#pragma unroll
+            for (int l = 0; l < 11; ++l) {
+                const float g = c_taps[l], a = va[o + l], b = vb[o + l];
+                const float ga = g * a;
+                m0 = fmaf(g, a, m0);
+                m1 = fmaf(g, b, m1);
+                m2 = fmaf(ga, a, m2);
+                m3 = fmaf(g * b, b, m3);
+                m4 = fmaf(ga, b, m4);
+            }
+            hs[0][r][q0 + o] = m0; hs[1][r][q0 + o] = m1; hs[2][r][q0 + o] = m2;
+            hs[3][r][q0 + o] = m3; hs[4][r][q0 + o] = m4;
+        }
     }
     __syncthreads();
+    // vertical: item = (column q, 4 consecutive output rows) -> 256 items
     double ssum = 0.0;
-    const int q = threadIdx.x % kSx;
-    for (int r = threadIdx.x / kSx; r < kSy; r += blockDim.x / kSx) {
-        const int oy = y0 + r, ox = x0 + q;
-        if (oy >= vh || ox >= vw) continue;
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    {
+        const int q = threadIdx.x % kSx, r0 = (threadIdx.x / kSx) * kRB;
+        float m[kRB][5];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float g = c_taps[k];
+        for (int o = 0; o < kRB; ++o)
 #pragma unroll
-            for (int t = 0; t < 5; ++t) m[t] = fmaf(g, hs[t][r + k][q], m[t]);
+            for (int t = 0; t < 5; ++t) m[o][t] = 0.f;
+#pragma unroll
+        for (int l = 0; l < kRB + 10; ++l) {
+            float hv[5];
+#pragma unroll
+            for (int t = 0; t < 5; ++t) hv[t] = hs[t][r0 + l][q];
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+                const int k = l - o;
+                if (k < 0 || k > 10) continue;
+                const float g = c_taps[k];
+#pragma unroll
+                for (int t = 0; t < 5; ++t) m[o][t] = fmaf(g, hv[t], m[o][t]);
+            }
         }
-        const float mas = m[0], mbs = m[1];  // shifted means
-        const float ma = mas + kShift, mb = mbs + kShift;
-        const float va = m[2] - mas * mas, vb = m[3] - mbs * mbs, cab = m[4] - mas * mbs;
-        const float C1 = 1e-4f, C2 = 9e-4f;
-        const float num1 = 2.f * ma * mb + C1, num2 = 2.f * cab + C2;
-        const float den1 = ma * ma + mb * mb + C1, den2 = va + vb + C2;
-        const float inv_dd = 1.f / (den1 * den2);
-        const float s = num1 * num2 * inv_dd;
-        ssum += s;
-        const float ds_dsab = 2.f * num1 * inv_dd;
-        const float ds_dsa = -s / den2;
-        const float ds_dmu_direct = 2.f * mb * num2 * inv_dd - s * 2.f * ma / den1;
-        const float ds_dmu = ds_dmu_direct + ds_dsa * (-2.f * mas) + ds_dsab * (-mbs);
         const size_t VP = static_cast<size_t>(vh) * vw;
-        const size_t o = static_cast<size_t>(oy) * vw + ox;
         float* wc = wbuf + static_cast<size_t>(c) * 3 * VP;
-        wc[o] = ds_dmu * inv_n;
-        wc[VP + o] = ds_dsa * inv_n;
-        wc[2 * VP + o] = ds_dsab * inv_n;
+        const int ox = x0 + q;
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+            const int oy = y0 + r0 + o;
+            if (oy >= vh || ox >= vw) continue;
+            const float mas = m[o][0], mbs = m[o][1];  // shifted means
+            const float ma = mas + kShift, mb = mbs + kShift;
+            const float va = m[o][2] - mas * mas, vb = m[o][3] - mbs * mbs, cab = m[o][4] - mas * mbs;
+            const float C1 = 1e-4f, C2 = 9e-4f;
+            const float num1 = 2.f * ma * mb + C1, num2 = 2.f * cab + C2;
+            const float den1 = ma * ma + mb * mb + C1, den2 = va + vb + C2;
+            const float inv_dd = 1.f / (den1 * den2);
+            const float s = num1 * num2 * inv_dd;
+            ssum += s;
+            const float ds_dsab = 2.f * num1 * inv_dd;
+            const float ds_dsa = -s / den2;
+            const float ds_dmu_direct = 2.f * mb * num2 * inv_dd - s * 2.f * ma / den1;
+            const float ds_dmu = ds_dmu_direct + ds_dsa * (-2.f * mas) + ds_dsab * (-mbs);
+            const size_t oo = static_cast<size_t>(oy) * vw + ox;
+            wc[oo] = ds_dmu * inv_n;
+            wc[VP + oo] = ds_dsa * inv_n;
+            wc[2 * VP + oo] = ds_dsab * inv_n;
+        }
     }
     block_add(ssum, &acc->ssim_sum, scratch);
 }
@@ -174,15 +206,15 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, const float* __restrict__ wbuf,
                                                        float neg_lambda, float* __restrict__ dl) {
-    __shared__ float sw[3][kSy + kHalo][kSx + kHalo + 1];
-    __shared__ float hx[3][kSy + kHalo][kSx];
+    __shared__ float sw[3][kInY][kInX + 2];
+    __shared__ float hx[3][kInY][kSx + 1];
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * kSx, y0 = blockIdx.y * kSy;
     const int vh = h - kHalo, vw = w - kHalo;
     const size_t VP = static_cast<size_t>(vh) * vw;
     const float* wc = wbuf + static_cast<size_t>(c) * 3 * VP;
-    for (int i = threadIdx.x; i < (kSy + kHalo) * (kSx + kHalo); i += blockDim.x) {
-        const int r = i / (kSx + kHalo), q = i % (kSx + kHalo);
+    for (int i = threadIdx.x; i < kInY * kInX; i += blockDim.x) {
+        const int r = i / kInX, q = i % kInX;
         const int gy = y0 - kHalo + r, gx = x0 - kHalo + q;
         const bool ok = gy >= 0 && gx >= 0 && gy < vh && gx < vw;
         const size_t o = static_cast<size_t>(gy) * vw + gx;
@@ -191,35 +223,53 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
         sw[2][r][q] = ok ? wc[2 * VP + o] : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (kSy + kHalo) * kSx; i += blockDim.x) {
-        const int r = i / kSx, q = i % kSx;
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    // horizontal adjoint: out[q] = sum_l g[l] w[q + 10 - l]
+    for (int it = threadIdx.x; it < kInY * (kSx / kRB); it += blockDim.x) {
+        const int r = it / (kSx / kRB), q0 = (it % (kSx / kRB)) * kRB;
 #pragma unroll
-        for (int l = 0; l < 11; ++l) {
-            const float g = c_taps[l];
-            t0 = fmaf(g, sw[0][r][q + kHalo - l], t0);
-            t1 = fmaf(g, sw[1][r][q + kHalo - l], t1);
-            t2 = fmaf(g, sw[2][r][q + kHalo - l], t2);
+        for (int t = 0; t < 3; ++t) {
+            float vw_[kRB + 10];
+#pragma unroll
+            for (int l = 0; l < kRB + 10; ++l) vw_[l] = sw[t][r][q0 + l];
+#pragma unroll
+            for (int o = 0; o < kRB; ++o) {
+                float a = 0.f;
+#pragma unroll
+                for (int l = 0; l < 11; ++l) a = fmaf(c_taps[l], vw_[o + kHalo - l], a);
+                hx[t][r][q0 + o] = a;
+            }
         }
-        hx[0][r][q] = t0; hx[1][r][q] = t1; hx[2][r][q] = t2;
     }
     __syncthreads();
-    const int q = threadIdx.x % kSx;
-    const size_t P = static_cast<size_t>(h) * w;
-    for (int r = threadIdx.x / kSx; r < kSy; r += blockDim.x / kSx) {
-        const int y = y0 + r, x = x0 + q;
-        if (y >= h || x >= w) continue;
-        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+    const int q = threadIdx.x % kSx, r0 = (threadIdx.x / kSx) * kRB;
+    float bsum[kRB][3];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
+    for (int o = 0; o < kRB; ++o)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) bsum[o][t] = 0.f;
+#pragma unroll
+    for (int l = 0; l < kRB + 10; ++l) {  // staged row r0 + l feeds output row r0 + o with tap 10 - (l - o)
+        float hv[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) hv[t] = hx[t][r0 + l][q];
+#pragma unroll
+        for (int o = 0; o < kRB; ++o) {
+            const int k = kHalo - (l - o);
+            if (k < 0 || k > 10) continue;
             const float g = c_taps[k];
-            b0 = fmaf(g, hx[0][r + kHalo - k][q], b0);
-            b1 = fmaf(g, hx[1][r + kHalo - k][q], b1);
-            b2 = fmaf(g, hx[2][r + kHalo - k][q], b2);
+#pragma unroll
+            for (int t = 0; t < 3; ++t) bsum[o][t] = fmaf(g, hv[t], bsum[o][t]);
         }
+    }
+    const size_t P = static_cast<size_t>(h) * w;
+    const int x = x0 + q;
+#pragma unroll
+    for (int o = 0; o < kRB; ++o) {
+        const int y = y0 + r0 + o;
+        if (y >= h || x >= w) continue;
         const size_t p = c * P + static_cast<size_t>(y) * w + x;
         const float as = A[p] - kShift, bs = B[p] - kShift;
-        const float d = b0 + 2.f * as * b1 + bs * b2;
+        const float d = bsum[o][0] + 2.f * as * bsum[o][1] + bs * bsum[o][2];
         dl[p] = fmaf(neg_lambda, d, dl[p]);
     }
 }
