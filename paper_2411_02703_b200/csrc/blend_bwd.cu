@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
                                                        __ffma2_rn(g2[q], f2(col.z), __fmul2_rn(gz[q], f2(col.w)))));
                 const float2 dalpha = __ffma2_rn(ti, A, __fmul2_rn(neg2(inv), B[q]));
                 B[q] = __ffma2_rn(w, A, B[q]);
-                T[q] = make_float2(a0 ? ti.x : T[q].x, a1 ? ti.y : T[q].y);
+                // an inactive half has al = 0 -> om = 1 -> rcp.approx(1) = 1 exactly -> ti = T
+                T[q] = ti;
                 acc[0] = __ffma2_rn(w, g0[q], acc[0]);
                 acc[1] = __ffma2_rn(w, g1[q], acc[1]);
                 acc[2] = __ffma2_rn(w, g2[q], acc[2]);

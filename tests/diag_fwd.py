@@ -1,6 +1,7 @@
 """Diagnostic (not a test): per-level blend kernel times for each pixels-per-thread variant and
 forward slow-path counts as training proceeds."""
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -25,10 +26,11 @@ m = G.GaussianMap(ctx, train)
 cfg = G.TrainConfig.make(0.2, 0.5, 2, 1)
 cnt = np.zeros(2, np.int64)
 L = G.lib()
-for stage in range(3):
+PPTS = tuple(int(x) for x in os.environ.get("DIAG_PPTS", "1,2,4,8").split(","))
+for stage in range(int(os.environ.get("DIAG_STAGES", "3"))):
     for lvl in (2, 1, 0):
         line = []
-        for ppt in (1, 2, 4, 8):
+        for ppt in PPTS:
             L.gs_debug_set_blend_ppt(ppt, ppt)
             kf = kfs[0]
             kf.consumed_iters = 2 - lvl
