@@ -305,7 +305,18 @@ def run_ours(args, rank, world):
                 "unit": "TFLOP/s" if t_fp >= t_ex else "Tex2/s"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["kernel"] = dom
-    roof["traffic"] = None
+    # measured DRAM bytes per launch of the same kernel (ncu dram__bytes_read + _write, one
+    # capture per pyramid level, averaged like `achieved`), committed under profiles/
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if os.path.exists(tpath):
+        tk = json.load(open(tpath)).get("kernels", {}).get(dom)
+        traffic = tk.get("dram_bytes_per_launch") if tk else None
+    roof["traffic"] = traffic
+    roof["algorithmic_bytes_per_launch"] = int(b)
+    # the same kernel seen against HBM (it is not bandwidth-bound: this is the minor roof)
+    roof["hbm_view"] = {"achieved": round(b / avg / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(b / avg / 1e9 / hbm, 4)}
     roof["peak_source"] = ("MEASURED_PEAKS.json hbm_gbs" if roof["bound"] == "hbm"
                            else "gs_microbench on this device (FP32 FMA / MUFU.EX2 issue rate)")
     roof["model"] = "SURVEY §8d algorithmic bytes/flops per launch, averaged over the 3 pyramid levels"

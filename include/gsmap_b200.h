@@ -75,10 +75,13 @@ int gs_context_set_stream(gs_context* ctx, void* cuda_stream);
 int gs_context_launch_count(gs_context* ctx, int64_t* count);
 /* per-kernel CUDA-event timing on the context stream (enable != 0 resets the table) */
 int gs_context_profile(gs_context* ctx, int enable);
-/* forward-blend slow-path statistics: [0] guard-band checks, [1] exact fp64 replays */
+/* forward-blend slow-path statistics: [0] near-threshold checks, [1] exact fp64 replays */
 int gs_debug_counters(gs_context* ctx, int64_t* out2, int reset);
 /* override the blend kernels' pixels-per-thread (2, 4 or 8; 0 = automatic per level) */
 int gs_debug_set_blend_ppt(int fwd, int bwd);
+/* forward blend: tiles with more list entries than this carry the transmittance as df32
+   instead of fp32 + error band (tuning knob; negative = default) */
+int gs_debug_set_blend_df_list(int entries);
 /* reads the table: names as one '\n'-separated string, per-name total ms and launch counts */
 int gs_context_profile_read(gs_context* ctx, char* names, int32_t names_len, double* total_ms,
                             int64_t* launches, int32_t max_entries, int32_t* n_entries);

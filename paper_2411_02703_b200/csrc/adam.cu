@@ -7,14 +7,16 @@
 
 namespace gsb {
 
-// One thread per Gaussian; every Gaussian steps (its counter increments even when unseen, so
+// Step counts are stored as births: Gaussian i's Adam step after this update is
+// t = t_common - birth[i] (birth = the map's update count when its state was reset), so the
+// update only reads them. One thread per Gaussian; every Gaussian steps (even when unseen, so
 // momentum keeps moving it, as in the reference). The per-Gaussian bias corrections are fp64;
 // the per-scalar update is fp32 on fp32 m/v. Inactive SH coefficients are skipped: their m, v
 // and gradient are exactly zero, so the reference's update there is -lr*0/(0+eps) = -0 (exact).
 namespace {
 struct AdamArgs {
     float lr[5];        // position (x scene_extent), rotation, log_scale, opacity, sh
-    int32_t t_common;   // the new step of every Gaussian present since the last append
+    int32_t t_common;   // count + 1: the new step of every Gaussian with birth 0
     float a_common;     // 1 / (1 - 0.9^t_common)
     float b_common;     // 1 / (1 - 0.999^t_common)
 };
@@ -33,14 +35,13 @@ __device__ __forceinline__ void adam_scalar(float* __restrict__ p, float* __rest
 // follow per coefficient up to the Gaussian's active degree. The fp64 bias corrections come
 // from the host for the common step count and are computed only for Gaussians appended later.
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, float* __restrict__ m,
-                                                   float* __restrict__ v, int32_t* __restrict__ step,
+                                                   float* __restrict__ v, const int32_t* __restrict__ birth,
                                                    const int8_t* __restrict__ degree,
                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
                                                    AdamArgs args, const unsigned long long* __restrict__ cnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || overflowed(cnt)) return;
-    const int t = step[i] + 1;
-    step[i] = t;
+    const int t = args.t_common - birth[i];
     float a = args.a_common, b = args.b_common;
     if (t != args.t_common) {
         a = static_cast<float>(1.0 / (1.0 - pow(0.9, static_cast<double>(t))));
@@ -72,10 +73,9 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
 // (gradient, value, m, v), the per-scalar update of adam_kernel, three 16-byte stores. Many
 // small independent threads keep enough loads in flight to stream HBM (the per-Gaussian form
 // serialises its planes). Every plane base is 16-byte aligned when both capacities are
-// multiples of 4. The step counters are advanced afterwards by adam_step_kernel; here every
-// plane reads the pre-step value. SH planes past a Gaussian's degree are left untouched.
+// multiples of 4. SH planes past a Gaussian's degree are left untouched.
 __global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ params, float* __restrict__ m,
-                                                         float* __restrict__ v, const int32_t* __restrict__ step,
+                                                         float* __restrict__ v, const int32_t* __restrict__ birth,
                                                          const int8_t* __restrict__ degree,
                                                          const float* __restrict__ grads, int64_t gcap, int64_t cap,
                                                          int n, AdamArgs args,
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ par
     float4* mp = reinterpret_cast<float4*>(m + k * cap + i);
     float4* vp = reinterpret_cast<float4*>(v + k * cap + i);
     float4 P = *pp, M = *mp, V = *vp;
-    const int4 t4 = __ldg(reinterpret_cast<const int4*>(step + i));
+    const int4 b4 = __ldg(reinterpret_cast<const int4*>(birth + i));
     const float lr = k < 3 ? args.lr[0] : k < 7 ? args.lr[1] : k < 10 ? args.lr[2] : k < 11 ? args.lr[3] : args.lr[4];
     const int ne = min(4, n - i);
     int live = (1 << ne) - 1;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ par
             if ((d[e] + 1) * (d[e] + 1) <= c) live &= ~(1 << e);
         if (!live) return;
     }
-    const int t[4] = {t4.x + 1, t4.y + 1, t4.z + 1, t4.w + 1};
+    const int t[4] = {args.t_common - b4.x, args.t_common - b4.y, args.t_common - b4.z, args.t_common - b4.w};
     float* ps = &P.x;
     float* ms = &M.x;
     float* vs = &V.x;
@@ -121,12 +121,7 @@ __global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ par
     *vp = V;
 }
 
-__global__ void adam_step_kernel(int32_t* __restrict__ step, int n, const unsigned long long* __restrict__ cnt) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && !overflowed(cnt)) step[i] += 1;
-}
-
-void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
+void launch_adam(float* params, float* m, float* v, const int32_t* birth, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
                  const unsigned long long* cnt, int max_degree, cudaStream_t st) {
     if (n <= 0) return;
@@ -138,10 +133,9 @@ void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t*
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
     if (cap % 4 == 0 && gcap % 4 == 0) {
         const dim3 grid(div_up(div_up(n, 4), 256), kGeomParams + 3 * (max_degree + 1) * (max_degree + 1));
-        adam_plane_kernel<<<grid, 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
-        adam_step_kernel<<<div_up(n, 256), 256, 0, st>>>(step, n, cnt);
+        adam_plane_kernel<<<grid, 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
     } else
-        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, step, degree, grads, gcap, cap, n, args, cnt);
+        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
 }
 
 namespace {

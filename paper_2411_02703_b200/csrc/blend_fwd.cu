@@ -3,12 +3,14 @@
 // pixel it keeps n_proc (list position + 1 of the last contributor) and T_final for the
 // backward instead of the reference's CSR table (rasterizer.cpp:164-197).
 //
-// Exact termination without fp64 arithmetic: the transmittance is carried as an unevaluated
-// pair of floats (Th + Tl, "df32"). Each factor (1 - alpha) is split exactly (Fast2Sum) and the
-// product uses the FMA-exact product error, so Th + Tl tracks the real product to ~2^-46 per
-// step. The fp64 reference rounds by <= 2^-52 per step, so both decide T < 1e-4 identically
-// unless T lies within ~k 2^-44 of the threshold; only then is the pixel replayed in fp64 with
-// the reference's own operation order (never observed in practice; counted in g_blend_stats).
+// Exact termination with fp32 arithmetic: the transmittance is carried in fp32 together with a
+// rigorous bound on its distance from the reference's fp64 product. Each fp32 factor
+// fl(1 - alpha) (0.01f for a clamp) is within 2^-24 of the reference's fp64 factor and each
+// product rounds by <= 2^-24, so after k factors |T32 / T64 - 1| <= beta(k) = 2k 2^-24 (+5%).
+// Only when T32 lies inside [1e-4 (1 - beta), 1e-4 (1 + beta)] is the decision ambiguous; the
+// warp then replays that pixel cooperatively in fp64 (32 entries per step, product tree), and
+// only if even that lands within its own rounding bound of 1e-4 does one lane replay it
+// sequentially in the reference's operation order. (Counted in g_blend_stats.)
 #include "blend_common.cuh"
 #include "kernels.cuh"
 
@@ -26,12 +28,14 @@ void read_blend_stats(unsigned long long out[2], bool reset) {
 
 namespace {
 
-// 1 - 0.99 (fp64) = 0.010000000000000009 and 1e-4 (fp64) as exact float pairs
+constexpr float kClampFac = 0.01f;              // within 2^-24 of 1 - 0.99 (fp64) = 0.010000000000000009
+// df32 mode: 1 - 0.99 (fp64) and 1e-4 (fp64) as exact float pairs
 constexpr float kClampFacHi = 0.009999999776482582f, kClampFacLo = 2.2351742678949904e-10f;
 constexpr float kTMinHi = 9.999999747378752e-05f, kTMinLo = 2.5262125290942405e-12f;
-constexpr float kTNear = 1.0001e-4f;
+constexpr double kBetaPerFactor = 1.2517e-7;     // 2 * 2^-24 * 1.05
 
-// Exact fp64 transmittance of pixel (px, py) after the contributor at list position `upto`.
+// Exact fp64 transmittance of pixel (px, py) after the contributor at list position `upto`, in
+// the reference's sequential operation order (rasterizer.cpp:143-151).
 __device__ __noinline__ double replay_transmittance(const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
                                                      uint2 range, int upto, int px, int py, double ox, double oy,
                                                      float fx, float fy) {
@@ -46,26 +50,117 @@ __device__ __noinline__ double replay_transmittance(const uint32_t* __restrict__
     return T;
 }
 
+// The same product computed by the whole warp (uniform arguments): lane l evaluates entry
+// base + l, each chunk of 32 factors is multiplied as a butterfly tree. Differs from the
+// sequential product by at most ~2 (upto + 1) 2^-53 relative.
+__device__ __noinline__ double warp_replay(const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
+                                           uint2 range, int upto, int px, int py, double ox, double oy, float fx,
+                                           float fy) {
+    const int lane = threadIdx.x & 31;
+    double T = 1.0;
+    for (int base = 0; base <= upto; base += 32) {
+        const int j = base + lane;
+        double f = 1.0;
+        if (j <= upto) {
+            const Splat sp = rec[vals[range.x + j]];
+            if (!(px < sp.x0 || px > sp.x1 || py < sp.y0 || py > sp.y1)) {
+                const Staged s = stage_of(sp, ox, oy);
+                const AlphaS e = alpha_scalar(s.mean, s.con, fx, fy);
+                f = one_minus_alpha_d(e.a_raw, e.alpha);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) f = __dmul_rn(f, __shfl_xor_sync(0xffffffffu, f, o));
+        T = __dmul_rn(T, f);
+    }
+    return T;
+}
+
 }  // namespace
 
 // Per-pixel blend state of one thread (NP packed pairs of vertically adjacent pixels).
 template <int NP>
 struct FwdState {
-    float2 Th[NP], Tl[NP], c0[NP], c1[NP], c2[NP], dd[NP], vis[NP];
+    float2 T[NP], Tl[NP], c0[NP], c1[NP], c2[NP], dd[NP], vis[NP];  // Tl: df32 low part (DF mode)
     int nproc[2 * NP], ncontrib[2 * NP];
     unsigned live;
 };
 
+// Pixels whose fp32 transmittance fell below t_near after the entry at `pos` (bits in `near`):
+// decide T64 < 1e-4 exactly. Called by the whole warp; kw = entries this warp has walked so far
+// (every pixel of the warp has taken at most kw factors).
+template <int PPT>
+__device__ __forceinline__ void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
+                                          int kw, float fx, const uint32_t* __restrict__ vals,
+                                          const Splat* __restrict__ rec, uint2 range, double ox, double oy) {
+    const double beta = kBetaPerFactor * kw;
+    unsigned amb = 0;
+#pragma unroll
+    for (int p = 0; p < 2 * ((PPT + 1) / 2); ++p) {
+        if (!((near >> p) & 1u)) continue;
+        atomicAdd(&g_blend_stats[0], 1ull);
+        const double t = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x;
+        if (t / (1.0 - beta) < kTMin) s.live &= ~(1u << p);  // T64 <= T32 / (1 - beta) < 1e-4
+        else if (!(t / (1.0 + beta) >= kTMin)) amb |= 1u << p;  // else T64 >= T32 / (1 + beta) >= 1e-4
+    }
+    unsigned need = __ballot_sync(0xffffffffu, amb != 0u);
+    while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1;
+        const unsigned bits = __shfl_sync(0xffffffffu, amb, src);
+        const int px = __shfl_sync(0xffffffffu, sc.px, src);
+        const int py0 = __shfl_sync(0xffffffffu, sc.py0, src);
+        const int ly0 = __shfl_sync(0xffffffffu, sc.ly0, src);
+        const float sfx = __shfl_sync(0xffffffffu, fx, src);
+        for (int p = 0; p < PPT; ++p) {
+            if (!((bits >> p) & 1u)) continue;
+            atomicAdd(&g_blend_stats[1], 1ull);
+            const float fy = static_cast<float>(ly0 + p);
+            double T = warp_replay(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
+            if (fabs(T / kTMin - 1.0) <= 2.5 * (pos + 1) * 1.1102230246251565e-16 && (threadIdx.x & 31) == src)
+                T = replay_transmittance(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
+            if ((threadIdx.x & 31) == src && T < kTMin) s.live &= ~(1u << p);
+        }
+    }
+}
+
+// DF mode: sign of (Th + Tl) - 1e-4 per near pixel; the sequential fp64 replay only if even the
+// df32 value is within its rounding bound of the threshold (not observed in practice).
+template <int PPT>
+__device__ __forceinline__ void df_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
+                                        float fx, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
+                                        uint2 range, double ox, double oy) {
+#pragma unroll
+    for (int p = 0; p < 2 * ((PPT + 1) / 2); ++p) {
+        if (!((near >> p) & 1u)) continue;
+        atomicAdd(&g_blend_stats[0], 1ull);
+        const float th = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x, tl = (p & 1) ? s.Tl[p >> 1].y : s.Tl[p >> 1].x;
+        // Th - kTMinHi is exact (Sterbenz)
+        const float d = __fadd_rn(th, -kTMinHi) + __fadd_rn(tl, -kTMinLo);
+        const float tol = 1e-4f * 5.7e-14f * static_cast<float>(pos + 16);
+        bool term = d < -tol;
+        if (!(d < -tol) && !(d > tol)) {
+            atomicAdd(&g_blend_stats[1], 1ull);
+            term = replay_transmittance(vals, rec, range, pos, sc.px, sc.py0 + p, ox, oy, fx,
+                                        static_cast<float>(sc.ly0 + p)) < kTMin;
+        }
+        if (term) s.live &= ~(1u << p);
+    }
+}
+
 // One tile-list entry over the thread's pixels. COVER: the entry's rect contains every live
 // pixel of the warp (warp-uniform), so the per-pixel box test reduces to the live bits.
 // STATS: maintain n_contrib (only the public render reports it).
-template <int PPT, bool COVER, bool STATS>
+// DF: carry the transmittance as df32 (Th + Tl, exact to ~2^-46 per step: never ambiguous in
+// practice) instead of fp32 + band; chosen per tile for long lists, where the band is wide.
+template <int PPT, bool COVER, bool STATS, bool DF>
 __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, const int4& rc,
-                                          float2 m, float4 cn, float4 col, int pos, float fx,
+                                          float2 m, float4 cn, float4 col, int pos, int kw, float fx, float t_near,
                                           const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
                                           uint2 range, double ox, double oy) {
     constexpr int NP = (PPT + 1) / 2;
     const bool colin = COVER || (sc.px >= rc.x && sc.px <= rc.z);
+    unsigned near = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const int p0 = 2 * q, y0 = sc.py0 + p0;
@@ -74,51 +169,95 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             a0 = a0 && colin && y0 >= rc.y && y0 <= rc.w;
             a1 = a1 && colin && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
         }
-        // no branch on (a0 || a1): an inactive half has al = 0 -> w = 0 and factor 1 + 0,
-        // which leaves Th + Tl exactly unchanged (Fast2Sum renormalisation)
+        // no branch on (a0 || a1): an inactive half has al = 0 -> w = 0 and factor exactly 1
         const float fy = static_cast<float>(sc.ly0 + p0);
         const AlphaP e = alpha_pair(m, cn, fx, make_float2(fy, fy + 1.f));
         const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
-        const float2 w = __fmul2_rn(al, s.Th[q]);
+        const float2 w = __fmul2_rn(al, s.T[q]);
         s.c0[q] = __ffma2_rn(w, f2(col.x), s.c0[q]);
         s.c1[q] = __ffma2_rn(w, f2(col.y), s.c1[q]);
         s.c2[q] = __ffma2_rn(w, f2(col.z), s.c2[q]);
         s.dd[q] = __ffma2_rn(w, f2(col.w), s.dd[q]);
         s.vis[q] = __fadd2_rn(s.vis[q], w);
-        // exact factor 1 - alpha = fh + fl (Fast2Sum(1, -alpha)); clamp -> 1 - 0.99 (fp64)
-        float2 fh = __fadd2_rn(f2(1.f), neg2(al));
-        float2 fl = __fadd2_rn(neg2(al), neg2(__fadd2_rn(fh, f2(-1.f))));
-        if (a0 && e.a_raw.x >= kAlphaMaxF) { fh.x = kClampFacHi; fl.x = kClampFacLo; }
-        if (a1 && e.a_raw.y >= kAlphaMaxF) { fh.y = kClampFacHi; fl.y = kClampFacLo; }
-        // (Th + Tl) * (fh + fl) with the exact product error of Th * fh
-        const float2 pr = __fmul2_rn(s.Th[q], fh);
-        const float2 er = __ffma2_rn(s.Th[q], fh, neg2(pr));
-        const float2 t = __ffma2_rn(s.Th[q], fl, __ffma2_rn(s.Tl[q], fh, er));
-        s.Th[q] = __fadd2_rn(pr, t);
-        s.Tl[q] = __fadd2_rn(t, neg2(__fadd2_rn(s.Th[q], neg2(pr))));
+        if (DF) {
+            // exact factor 1 - alpha = fh + fl (Fast2Sum(1, -alpha)); clamp -> 1 - 0.99 (fp64)
+            float2 fh = __fadd2_rn(f2(1.f), neg2(al));
+            float2 fl = __fadd2_rn(neg2(al), neg2(__fadd2_rn(fh, f2(-1.f))));
+            if (a0 && e.a_raw.x >= kAlphaMaxF) { fh.x = kClampFacHi; fl.x = kClampFacLo; }
+            if (a1 && e.a_raw.y >= kAlphaMaxF) { fh.y = kClampFacHi; fl.y = kClampFacLo; }
+            // (Th + Tl) * (fh + fl) with the exact product error of Th * fh
+            const float2 pr = __fmul2_rn(s.T[q], fh);
+            const float2 er = __ffma2_rn(s.T[q], fh, neg2(pr));
+            const float2 t = __ffma2_rn(s.T[q], fl, __ffma2_rn(s.Tl[q], fh, er));
+            s.T[q] = __fadd2_rn(pr, t);
+            s.Tl[q] = __fadd2_rn(t, neg2(__fadd2_rn(s.T[q], neg2(pr))));
+        } else {
+            float2 f = __fadd2_rn(f2(1.f), neg2(al));
+            if (a0 && e.a_raw.x >= kAlphaMaxF) f.x = kClampFac;
+            if (a1 && e.a_raw.y >= kAlphaMaxF) f.y = kClampFac;
+            s.T[q] = __fmul2_rn(s.T[q], f);
+        }
         if (a0) s.nproc[p0] = pos + 1;
         if (a1) s.nproc[p0 + 1] = pos + 1;
         if (STATS) {
             s.ncontrib[p0] += a0;
             s.ncontrib[p0 + 1] += a1;
         }
-        if ((a0 && s.Th[q].x < kTNear) || (a1 && s.Th[q].y < kTNear)) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int p = p0 + h;
-                const float th = h ? s.Th[q].y : s.Th[q].x, tl = h ? s.Tl[q].y : s.Tl[q].x;
-                if (!(h ? a1 : a0) || !(th < kTNear)) continue;
-                atomicAdd(&g_blend_stats[0], 1ull);
-                // sign of (Th + Tl) - 1e-4, with Th - kTMinHi exact (Sterbenz)
-                const float d = __fadd_rn(th, -kTMinHi) + __fadd_rn(tl, -kTMinLo);
-                const float tol = 1e-4f * 5.7e-14f * static_cast<float>(pos + 16);
-                bool term = d < -tol;
-                if (!(d < -tol) && !(d > tol)) {
-                    atomicAdd(&g_blend_stats[1], 1ull);
-                    term = replay_transmittance(vals, rec, range, pos, sc.px, sc.py0 + p, ox, oy, fx,
-                                                static_cast<float>(sc.ly0 + p)) < kTMin;
-                }
-                if (term) s.live &= ~(1u << p);
+        near |= (static_cast<unsigned>(a0 && s.T[q].x < t_near) << p0) |
+                (static_cast<unsigned>(a1 && s.T[q].y < t_near) << (p0 + 1));
+    }
+    if (DF) {
+        if (near) df_near<PPT>(s, near, sc, pos, fx, vals, rec, range, ox, oy);
+    } else if (__any_sync(0xffffffffu, near != 0u)) {
+        resolve_near<PPT>(s, near, sc, pos, kw, fx, vals, rec, range, ox, oy);
+    }
+}
+
+// The walk over one tile's list (staging batches of NT entries, per-warp ballot against the
+// live-pixel box, list order within the warp).
+template <int PPT, bool STATS, bool DF>
+__device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<kTileThreads / PPT>& sb,
+                                           const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
+                                           const Splat* __restrict__ rec, uint2 range, double ox, double oy,
+                                           float fx) {
+    constexpr int NT = Strip<PPT>::kThreads;
+    // below t_near the termination needs the exact check: fp32 mode 1e-4 (1 + beta(list length)),
+    // rounded up; df32 mode a fixed guard
+    const float t_near = DF ? 1.0001e-4f
+                            : __double2float_ru(kTMin * (1.0 + kBetaPerFactor * (range.y - range.x + 1)));
+    int4 lb = warp_bbox<PPT>(s.live, sc);
+    unsigned seen = s.live;
+    int kw = 0;  // entries this warp has walked (uniform)
+    // the next batch's record is loaded one batch ahead (its latency overlaps the current walk)
+    Splat nsp;
+    if (range.x + threadIdx.x < range.y) nsp = rec[vals[range.x + threadIdx.x]];
+    for (uint32_t base = range.x; base < range.y; base += NT) {
+        if (__syncthreads_count(s.live != 0) == 0) break;
+        const uint32_t idx = base + threadIdx.x;
+        if (idx < range.y) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
+        if (idx + NT < range.y) nsp = rec[vals[idx + NT]];
+        __syncthreads();
+        const int cnt = min(NT, static_cast<int>(range.y - base));
+        for (int b0 = 0; b0 < cnt; b0 += 32) {
+            if (__any_sync(0xffffffffu, s.live != seen)) {
+                seen = s.live;
+                lb = warp_bbox<PPT>(s.live, sc);
+            }
+            if (lb.x > lb.z) break;  // no live pixel left in this warp
+            const int jj = b0 + sc.lane;
+            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && rect_meets(sb.rect[jj], lb));
+            while (todo) {
+                const int j = b0 + __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int4 rc = sb.rect[j];
+                const int pos = static_cast<int>(base - range.x) + j;
+                ++kw;
+                if (rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w)
+                    fwd_entry<PPT, true, STATS, DF>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx, t_near,
+                                                    vals, rec, range, ox, oy);
+                else
+                    fwd_entry<PPT, false, STATS, DF>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx, t_near,
+                                                     vals, rec, range, ox, oy);
             }
         }
     }
@@ -128,7 +267,7 @@ template <int PPT, bool STATS>
 __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
-    float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib) {
+    float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list) {
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
     // live, so its packed lane computes nothing that is kept.
@@ -143,7 +282,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     s.live = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-        s.Th[q] = f2(1.f);
+        s.T[q] = f2(1.f);
         s.Tl[q] = s.c0[q] = s.c1[q] = s.c2[q] = s.dd[q] = s.vis[q] = f2(0.f);
     }
 #pragma unroll
@@ -151,42 +290,11 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
         s.nproc[p] = s.ncontrib[p] = 0;
         if (p < PPT && sc.px < v.width && sc.py0 + p < v.height) s.live |= 1u << p;
     }
-    int4 lb = warp_bbox<PPT>(s.live, sc);
-    unsigned seen = s.live;
-    // the next batch's record is loaded one batch ahead (its latency overlaps the current walk)
-    Splat nsp;
-    if (range.x + threadIdx.x < range.y) nsp = rec[vals[range.x + threadIdx.x]];
-    for (uint32_t base = range.x; base < range.y; base += NT) {
-        if (__syncthreads_count(s.live != 0) == 0) break;
-        const uint32_t idx = base + threadIdx.x;
-        if (idx < range.y) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
-        if (idx + NT < range.y) nsp = rec[vals[idx + NT]];
-        __syncthreads();
-        const int cnt = min(NT, static_cast<int>(range.y - base));
-        // the warp first ballots which staged entries meet the bounding box of its live pixels,
-        // then walks only those (in list order)
-        for (int b0 = 0; b0 < cnt; b0 += 32) {
-            if (__any_sync(0xffffffffu, s.live != seen)) {
-                seen = s.live;
-                lb = warp_bbox<PPT>(s.live, sc);
-            }
-            if (lb.x > lb.z) break;  // no live pixel left in this warp
-            const int jj = b0 + sc.lane;
-            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && rect_meets(sb.rect[jj], lb));
-            while (todo) {
-                const int j = b0 + __ffs(todo) - 1;
-                todo &= todo - 1;
-                const int4 rc = sb.rect[j];
-                const int pos = static_cast<int>(base - range.x) + j;
-                if (rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w)
-                    fwd_entry<PPT, true, STATS>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, fx, vals, rec,
-                                                range, ox, oy);
-                else
-                    fwd_entry<PPT, false, STATS>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, fx, vals, rec,
-                                                 range, ox, oy);
-            }
-        }
-    }
+    // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
+    if (static_cast<int>(range.y - range.x) > df_list)
+        blend_walk<PPT, STATS, true>(s, sb, sc, vals, rec, range, ox, oy, fx);
+    else
+        blend_walk<PPT, STATS, false>(s, sb, sc, vals, rec, range, ox, oy, fx);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
@@ -200,13 +308,17 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
         out_color[2 * P + o] = hi ? s.c2[q].y : s.c2[q].x;
         out_depth[o] = hi ? s.dd[q].y : s.dd[q].x;
         out_vis[o] = hi ? s.vis[q].y : s.vis[q].x;
-        out_t[o] = hi ? s.Th[q].y + s.Tl[q].y : s.Th[q].x + s.Tl[q].x;
+        out_t[o] = hi ? s.T[q].y + s.Tl[q].y : s.T[q].x + s.Tl[q].x;
         out_nproc[o] = s.nproc[p];
         if (STATS) out_ncontrib[o] = s.ncontrib[p];
     }
 }
 
 static int g_ppt_override[2] = {0, 0};  // [forward, backward]; 0 = automatic
+// tiles with longer lists use the df32 transmittance (measured crossover, tests/diag_fwd.py)
+static int g_df_list = 1100;
+
+void set_blend_df_list(int n) { g_df_list = n < 0 ? 1100 : n; }
 
 void set_blend_ppt(int fwd, int bwd) {
     g_ppt_override[0] = fwd;
@@ -231,7 +343,7 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
     const int n_tiles = v.tiles_x * v.tiles_y;
 #define GSB_FWD(P, S) \
     blend_fwd_kernel<P, S><<<n_tiles, kTileThreads / P, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, \
-                                                               n_proc, n_contrib)
+                                                               n_proc, n_contrib, g_df_list)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);

@@ -191,21 +191,21 @@ struct gs_map {
     float* params = nullptr;
     float* m = nullptr;
     float* v = nullptr;
-    int32_t* step = nullptr;
+    int32_t* birth = nullptr;  // per Gaussian: adam_count when its optimizer state was reset
     int8_t* degree = nullptr;
     std::vector<int8_t> deg_host;
     int max_degree = 0;
     double scene_extent = 1.0;
     int64_t global_step = 0;
-    int64_t step0 = 0;  // host mirror of Gaussian 0's Adam step (hint for the common bias correction)
+    int64_t adam_count = 0;  // updates applied to this map; Gaussian i's Adam step = adam_count - birth[i]
     DevBuf minmax;
 
     void free_all() {
         for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
-                        static_cast<void*>(step), static_cast<void*>(degree)})
+                        static_cast<void*>(birth), static_cast<void*>(degree)})
             if (p) cudaFree(p);
         params = m = v = nullptr;
-        step = nullptr;
+        birth = nullptr;
         degree = nullptr;
     }
     void recompute_max_degree() {
@@ -304,12 +304,12 @@ void map_reserve(gs_map* M, int64_t need) {
                              kNumParams, cudaMemcpyDeviceToDevice, st), "copy m");
         ck(cudaMemcpy2DAsync(v, sizeof(float) * nc, M->v, sizeof(float) * M->cap, sizeof(float) * M->n,
                              kNumParams, cudaMemcpyDeviceToDevice, st), "copy v");
-        ck(cudaMemcpyAsync(s, M->step, sizeof(int32_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy step");
+        ck(cudaMemcpyAsync(s, M->birth, sizeof(int32_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy birth");
         ck(cudaMemcpyAsync(d, M->degree, sizeof(int8_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy degree");
     }
     ck(cudaStreamSynchronize(st), "sync");
     M->free_all();
-    M->params = p; M->m = m; M->v = v; M->step = s; M->degree = d;
+    M->params = p; M->m = m; M->v = v; M->birth = s; M->degree = d;
     M->cap = nc;
 }
 
@@ -579,10 +579,10 @@ void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsign
     if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
-    launch_adam(M->params, M->m, M->v, M->step, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
-                M->scene_extent, M->step0 + 1, counters, M->max_degree, M->ctx->stream);
-    ++M->step0;
-    M->ctx->launched(2);
+    launch_adam(M->params, M->m, M->v, M->birth, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
+                M->scene_extent, M->adam_count + 1, counters, M->max_degree, M->ctx->stream);
+    ++M->adam_count;
+    M->ctx->launched();
     ++M->global_step;
 }
 
@@ -768,6 +768,10 @@ int gs_debug_set_blend_ppt(int fwd, int bwd) {
     return guard([&] { set_blend_ppt(fwd, bwd); });
 }
 
+int gs_debug_set_blend_df_list(int entries) {
+    return guard([&] { set_blend_df_list(entries); });
+}
+
 int gs_debug_counters(gs_context* C, int64_t* out2, int reset) {
     return guard([&] {
         C->use();
@@ -857,9 +861,10 @@ int gs_map_append(gs_map* M, const gs_gaussian* g, int64_t n) {
         if (n > 0) {
             ck(cudaMemset2DAsync(M->m + M->n, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
             ck(cudaMemset2DAsync(M->v + M->n, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
-            ck(cudaMemsetAsync(M->step + M->n, 0, sizeof(int32_t) * n, st), "memset");
+            const std::vector<int32_t> b(n, static_cast<int32_t>(M->adam_count));  // fresh state: step 0
+            ck(cudaMemcpyAsync(M->birth + M->n, b.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d birth");
+            ck(cudaStreamSynchronize(st), "sync");
         }
-        if (M->n == 0) M->step0 = 0;
         upload_gaussians(M, g, M->n, n);
         M->n += n;
         refresh_extent(M);
@@ -903,14 +908,14 @@ int gs_map_get_adam(gs_map* M, double* m59, double* v59, int64_t* step, int64_t 
                              cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaMemcpy2DAsync(b.data(), sizeof(float) * n, M->v, sizeof(float) * M->cap, sizeof(float) * n, kNumParams,
                              cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaMemcpyAsync(s.data(), M->step, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(s.data(), M->birth, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
         for (int64_t i = 0; i < n; ++i) {
             for (int k = 0; k < kNumParams; ++k) {
                 if (m59) m59[i * kNumParams + k] = a[static_cast<size_t>(k) * n + i];
                 if (v59) v59[i * kNumParams + k] = b[static_cast<size_t>(k) * n + i];
             }
-            if (step) step[i] = s[i];
+            if (step) step[i] = M->adam_count - s[i];
         }
     });
 }
@@ -927,15 +932,14 @@ int gs_map_set_adam(gs_map* M, const double* m59, const double* v59, const int64
                 a[static_cast<size_t>(k) * n + i] = static_cast<float>(m59[i * kNumParams + k]);
                 b[static_cast<size_t>(k) * n + i] = static_cast<float>(v59[i * kNumParams + k]);
             }
-            s[i] = static_cast<int32_t>(step[i]);
-            if (i == 0) M->step0 = step[0];
+            s[i] = static_cast<int32_t>(M->adam_count - step[i]);
         }
         cudaStream_t st = M->ctx->stream;
         ck(cudaMemcpy2DAsync(M->m, sizeof(float) * M->cap, a.data(), sizeof(float) * n, sizeof(float) * n, kNumParams,
                              cudaMemcpyHostToDevice, st), "h2d");
         ck(cudaMemcpy2DAsync(M->v, sizeof(float) * M->cap, b.data(), sizeof(float) * n, sizeof(float) * n, kNumParams,
                              cudaMemcpyHostToDevice, st), "h2d");
-        ck(cudaMemcpyAsync(M->step, s.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(M->birth, s.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
         ck(cudaStreamSynchronize(st), "sync");
     });
 }
@@ -1389,7 +1393,7 @@ int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const g
             adam_impl(M, G, cfg->lr, dev_counters(F));
             lr = read_loss(F);
             if (!F->overflow) break;
-            --M->step0;
+            --M->adam_count;
             --M->global_step;
             if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
         }

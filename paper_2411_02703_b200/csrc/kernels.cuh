@@ -38,6 +38,7 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
                       float* partials, const unsigned long long* counters, cudaStream_t st);
 void read_blend_stats(unsigned long long out[2], bool reset);
 void set_blend_ppt(int fwd, int bwd);
+void set_blend_df_list(int entries);
 void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                         const uint32_t* offsets, int32_t* out_gid, double* out_alpha, cudaStream_t st);
 
@@ -51,7 +52,7 @@ void launch_loss_finalize(LossScalars* acc, double lambda_d, cudaStream_t st);
 void launch_downsample(const float* in, int h, int w, int channels, bool depth, float* out, cudaStream_t st);
 
 // adam.cu
-void launch_adam(float* params, float* m, float* v, int32_t* step, const int8_t* degree, const float* grads,
+void launch_adam(float* params, float* m, float* v, const int32_t* birth, const int8_t* degree, const float* grads,
                  int64_t gcap, int64_t cap, int n, const double lr[5], double scene_extent, int64_t t_common,
                  const unsigned long long* counters /* nullable: skip on overflow */, int max_degree,
                  cudaStream_t st);

@@ -34,12 +34,17 @@ def full(path):
             "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
     units = r[1]
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
     for row in r[2:]:
         print("---")
         for w in want:
             if w in h:
                 i = h.index(w)
                 print(f"  {w:58s} {row[i][:70]} {units[i]}")
+        stalls = [(k[len(pre):-len(suf)], float(row[i])) for i, k in enumerate(h)
+                  if k.startswith(pre) and k.endswith(suf) and row[i]]
+        stalls.sort(key=lambda t: -t[1])
+        print("  stalls per issued instruction: " + ", ".join(f"{k}={v:.2f}" for k, v in stalls[:8]))
 
 
 if __name__ == "__main__":
