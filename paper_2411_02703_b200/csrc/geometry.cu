@@ -410,44 +410,115 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 // colour clamp mask -> eval_sh_vjp -> view-direction chain, sigmoid, project_gaussian_vjp
 // (projection.cpp:42-74) -> build_covariance_vjp (covariance.cpp:58-79). Accumulates into the
 // gradient planes (batch semantics = GaussianGrad::add, gaussian.hpp:51-57).
-// The partial rows of a block's 128 consecutive ranks are one contiguous range of the
-// emission order, so the block streams them through shared memory with coalesced loads and
-// each thread then sums its own rows from shared memory (deterministic order, fp64).
+// Two kernels: K8a reduces each rank's (tile, gaussian) partial rows to fp64 sums in a
+// rank-ordered buffer; K8b runs the fp64 VJP per rank with its map-indexed parameter loads
+// issued up front. Splitting keeps the streaming kernel at low register count (occupancy).
 constexpr int kBwdRanks = 128;
-constexpr int kRowChunk = 640;  // rows staged per pass (640 x 40 B = 25.6 KB)
+
+// K8a: a warp owns 32 consecutive ranks, whose partial rows are one contiguous range. It
+// streams them 32 rows at a time (lane l reads row base + l: 1280 B coalesced), finds each
+// row's rank with a 5-step shuffle search over the 33 segment offsets, sums runs of equal rank
+// with a segmented shuffle reduction (fixed tree: deterministic), and the owning lane adds the
+// run total into its fp64 accumulator. No block barriers; load balance is per row, not per rank.
+__global__ void __launch_bounds__(kBwdRanks) reduce_partials_kernel(const uint32_t* __restrict__ emit_off,
+                                                                    const float* __restrict__ partials,
+                                                                    const unsigned long long* __restrict__ cnt,
+                                                                    double* __restrict__ sums) {
+    __shared__ float seg[kBwdRanks / 32][32][kNumPartials + 1];
+    __shared__ int stamp[kBwdRanks / 32][32];  // pass in which rank l's run total was written
+    const int n_vis = static_cast<int>(cnt[kCntVisible]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = blockIdx.x * kBwdRanks + warp * 32;
+    if (q0 >= n_vis || overflowed(cnt)) return;  // warp-uniform; no block barrier below
+    const int nr = min(32, n_vis - q0);
+    const uint32_t off = emit_off[q0 + min(lane, nr)];  // lane l: first row of rank q0 + l
+    const uint32_t end = __shfl_sync(0xffffffffu, emit_off[q0 + nr], 0);
+    const uint32_t beg = __shfl_sync(0xffffffffu, off, 0);
+    double acc[kNumPartials];
+#pragma unroll
+    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
+    stamp[warp][lane] = -1;
+    __syncwarp();
+    int pass = 0;
+    for (uint32_t base = beg; base < end; base += 32, ++pass) {
+        const uint32_t e = base + lane;
+        const bool valid = e < end;
+        // rank (0..nr-1) of row e: largest l with off_l <= e (offsets are non-decreasing)
+        int rl = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int c = rl + step;
+            const uint32_t oc = __shfl_sync(0xffffffffu, off, c < nr ? c : 0);
+            if (c < nr && oc <= e) rl = c;
+        }
+        float v[kNumPartials];
+        if (valid) {
+            const float2* row = reinterpret_cast<const float2*>(partials + static_cast<size_t>(e) * kNumPartials);
+#pragma unroll
+            for (int k = 0; k < kNumPartials / 2; ++k) {
+                const float2 t = __ldg(row + k);
+                v[2 * k] = t.x;
+                v[2 * k + 1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) v[k] = 0.f;
+            rl = -1;  // never matches a real run
+        }
+        // segmented suffix sums: lane ends up with the sum over [lane, end of its run]
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int ro = __shfl_down_sync(0xffffffffu, rl, d);
+            const bool same = lane + d < 32 && ro == rl;
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) {
+                const float o = __shfl_down_sync(0xffffffffu, v[k], d);
+                if (same) v[k] += o;
+            }
+        }
+        const int rprev = __shfl_up_sync(0xffffffffu, rl, 1);
+        const bool head = valid && (lane == 0 || rprev != rl);
+        if (head) {
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) seg[warp][rl][k] = v[k];
+            stamp[warp][rl] = pass;
+        }
+        __syncwarp();
+        if (stamp[warp][lane] == pass) {
+#pragma unroll
+            for (int k = 0; k < kNumPartials; ++k) acc[k] += static_cast<double>(seg[warp][lane][k]);
+        }
+        __syncwarp();
+    }
+    if (lane >= nr) return;
+    double2* out = reinterpret_cast<double2*>(sums + static_cast<size_t>(q0 + lane) * kNumPartials);
+#pragma unroll
+    for (int k = 0; k < kNumPartials / 2; ++k) out[k] = make_double2(acc[2 * k], acc[2 * k + 1]);
+}
 
 template <bool ACC>
 __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
-    const float* __restrict__ partials, const unsigned long long* __restrict__ cnt, float* __restrict__ grads,
+    const double* __restrict__ sums, const unsigned long long* __restrict__ cnt, float* __restrict__ grads,
     int64_t gcap) {
-    __shared__ float rows[kRowChunk * kNumPartials];
-    const int r0 = blockIdx.x * kBwdRanks;
-    const int n_vis = static_cast<int>(cnt[kCntVisible]);
-    if (r0 >= n_vis || overflowed(cnt)) return;  // whole block (before any barrier)
-    const int r = r0 + threadIdx.x;
-    const int rend = min(r0 + kBwdRanks, n_vis);
-    const uint32_t b0 = emit_off[r0], b1 = emit_off[rend];
-    const uint32_t e0 = r < n_vis ? emit_off[r] : b1, e1 = r < n_vis ? emit_off[r + 1] : b1;
+    const int r = blockIdx.x * kBwdRanks + threadIdx.x;
+    if (r >= static_cast<int>(cnt[kCntVisible]) || overflowed(cnt)) return;
+    if (emit_off[r] == emit_off[r + 1]) return;  // no tile: never touched (rasterizer.cpp:327)
+    const int i = rec[r].gid;
+    const float opf = rec[r].opacity;
+    float gp[kGeomParams];  // map-indexed: all loads in flight at once
+#pragma unroll
+    for (int k = 0; k < kGeomParams; ++k) gp[k] = __ldg(params + static_cast<int64_t>(k) * cap + i);
+    const int deg = degree[i];
     double acc[kNumPartials];
+    const double2* in = reinterpret_cast<const double2*>(sums + static_cast<size_t>(r) * kNumPartials);
 #pragma unroll
-    for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
-    for (uint32_t c0 = b0; c0 < b1; c0 += kRowChunk) {
-        const uint32_t c1 = min(c0 + kRowChunk, b1);
-        const float* src = partials + static_cast<size_t>(c0) * kNumPartials;
-        const int nf = static_cast<int>(c1 - c0) * kNumPartials;
-        __syncthreads();
-        for (int t = threadIdx.x; t < nf; t += kBwdRanks) rows[t] = __ldg(src + t);
-        __syncthreads();
-        const uint32_t s0 = max(e0, c0), s1 = min(e1, c1);
-        for (uint32_t e = s0; e < s1; ++e) {
-            const float* row = rows + (e - c0) * kNumPartials;
-#pragma unroll
-            for (int k = 0; k < kNumPartials; ++k) acc[k] += row[k];
-        }
+    for (int k = 0; k < kNumPartials / 2; ++k) {
+        const double2 t = in[k];
+        acc[2 * k] = t.x;
+        acc[2 * k + 1] = t.y;
     }
-    if (r >= n_vis || e0 == e1) return;  // no tile: never touched (rasterizer.cpp:327)
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) any |= (acc[k] != 0.0);
@@ -455,15 +526,13 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     // the blend evaluates u = Sigma^-1 d with the conic pre-scaled by k = -log2(e)/2 (exp2 form)
     // and accumulates the mean / covariance terms without the opacity factor (op and op / 2)
     const double inv_k = 1.0 / static_cast<double>(-0.72134752044448170368f);
-    const double op = static_cast<double>(rec[r].opacity);
+    const double op = static_cast<double>(opf);
     acc[5] *= op * inv_k;
     acc[6] *= op * inv_k;
     acc[7] *= 0.5 * op * inv_k * inv_k;
     acc[8] *= 0.5 * op * inv_k * inv_k;
     acc[9] *= 0.5 * op * inv_k * inv_k;
-    const int i = rec[r].gid;
-    const int deg = degree[i];
-    const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
+    const D3 pos{gp[P_POS], gp[P_POS + 1], gp[P_POS + 2]};
 
     // ---- colour: clamp mask, SH, view direction (rasterizer.cpp:330-340)
     const D3 ctr = quat_rotate(v.qw, -v.qx, -v.qy, -v.qz, D3{-v.tx, -v.ty, -v.tz});
@@ -484,7 +553,7 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     }
 
     // ---- opacity logit through the sigmoid (rasterizer.cpp:343)
-    const double o = 1.0 / (1.0 + exp(-ldp(params, cap, P_OP, i)));
+    const double o = 1.0 / (1.0 + exp(-static_cast<double>(gp[P_OP])));
     gput(grads, P_OP * gcap + i, acc[4] * o * (1.0 - o), ACC);
 
     // ---- geometry (projection.cpp:42-74)
@@ -494,9 +563,8 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     pose_matrix(v, W);
     perspective_jacobian(p, v, J);
     mul23_33(J, W, M);
-    const double q[4] = {ldp(params, cap, P_ROT, i), ldp(params, cap, P_ROT + 1, i),
-                         ldp(params, cap, P_ROT + 2, i), ldp(params, cap, P_ROT + 3, i)};
-    const double ls[3] = {ldp(params, cap, P_LS, i), ldp(params, cap, P_LS + 1, i), ldp(params, cap, P_LS + 2, i)};
+    const double q[4] = {gp[P_ROT], gp[P_ROT + 1], gp[P_ROT + 2], gp[P_ROT + 3]};
+    const double ls[3] = {gp[P_LS], gp[P_LS + 1], gp[P_LS + 2]};
     build_covariance(q, ls, S);
     const double dcov[2][2] = {{acc[7], acc[8]}, {acc[8], acc[9]}};
     // d_sigma_w = M^T dcov M
@@ -562,18 +630,20 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
 }
 
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
-                           const Splat* rec, const uint32_t* emit_off, const float* partials,
+                           const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
                            const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,
                            bool accumulate, cudaStream_t st) {
     if (max_ranks <= 0) return;
+    const int blocks = div_up(max_ranks, kBwdRanks);
+    reduce_partials_kernel<<<blocks, kBwdRanks, 0, st>>>(emit_off, partials, cnt, sums);
     // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
     // read-modify-write of randomly addressed (map-indexed) gradient entries
     if (accumulate)
-        preprocess_bwd_kernel<true><<<div_up(max_ranks, kBwdRanks), kBwdRanks, 0, st>>>(
-            params, cap, degree, v, rec, emit_off, partials, cnt, grads, gcap);
+        preprocess_bwd_kernel<true><<<blocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, sums, cnt,
+                                                                  grads, gcap);
     else
-        preprocess_bwd_kernel<false><<<div_up(max_ranks, kBwdRanks), kBwdRanks, 0, st>>>(
-            params, cap, degree, v, rec, emit_off, partials, cnt, grads, gcap);
+        preprocess_bwd_kernel<false><<<blocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, sums,
+                                                                   cnt, grads, gcap);
 }
 
 }  // namespace gsb

@@ -235,7 +235,7 @@ struct gs_frame {
     }
     // per-Gaussian / per-rank / per-pair scratch
     DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
-        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, depth_sorted;
+        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, rank_sums, depth_sorted;
     // per-pixel
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
     DevBuf loss;  // LossScalars
@@ -557,6 +557,7 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     if (M->n == 0 || F->pair_cap == 0) return;
     if (F->counts_known && (F->n_vis == 0 || F->n_pairs == 0)) return;
     F->partials.ensure(sizeof(float) * kNumPartials * F->pair_cap);
+    F->rank_sums.ensure(sizeof(double) * kNumPartials * M->n);
     {
         Scope sc(C, "blend_bwd");
         launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
@@ -567,8 +568,8 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     {
         Scope sc(C, "preprocess_bwd");
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
-                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), dev_counters(F),
-                              static_cast<int>(M->n), G->planes, G->cap, !G->clean, st);
+                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
+                              dev_counters(F), static_cast<int>(M->n), G->planes, G->cap, !G->clean, st);
         G->clean = false;
         C->launched();
     }
@@ -989,7 +990,7 @@ int gs_frame_destroy(gs_frame* F) {
         for (DevBuf* b : {&F->rec_by_gid, &F->vis_flag, &F->key_by_gid, &F->vis_gid, &F->keys_a, &F->keys_b,
                           &F->gid_sorted, &F->rec_sorted, &F->ntiles, &F->emit_off, &F->num_sel, &F->depth_sorted,
                           &F->pair_keys,
-                          &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->color,
+                          &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->rank_sums, &F->color,
                           &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
                           &F->wbuf, &F->host_stage, &F->loss})
             b->release();

@@ -16,8 +16,8 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
                            int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st);
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
-                           const unsigned long long* counters, int max_ranks, float* grads, int64_t gcap,
-                           bool accumulate, cudaStream_t st);
+                           double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
+                           int max_ranks, float* grads, int64_t gcap, bool accumulate, cudaStream_t st);
 
 // raster.cu
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
