@@ -16,6 +16,8 @@ constexpr double kTMin = 1e-4;            // rasterizer.hpp:19
 constexpr int kNumParams = 59;            // gaussian.hpp:16-26 flattened
 constexpr int kGeomParams = 11;           // position 3, rotation 4, log_scale 3, opacity 1
 constexpr int kNumPartials = 10;          // per (tile, gaussian) backward partial sums
+constexpr uint32_t kDepthKeyBase = 0x3C23D70Au;  // fp32 bits of 0.01f (visible depths are >= it)
+constexpr int kDepthKeyBits = 24;
 
 // Parameter planes ([59][capacity], fp32): same order as the reference's Gaussian3D.
 enum Plane : int { P_POS = 0, P_ROT = 3, P_LS = 7, P_OP = 10, P_SH = 11 };

@@ -280,8 +280,8 @@ void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, i
 
 // K1b: exact projection of the candidates (grid-stride over the device-side candidate count).
 // Writes the 64 B Splat record at the map index and the fp64 depth bits (map-indexed), and
-// appends visible Gaussians to the sort input: the fp32-rounded depth bits (a monotone
-// non-decreasing key) and the map index. Counts the visible set and the (tile, gaussian) pairs.
+// appends visible Gaussians to the sort input: a 24-bit key from the fp32-rounded depth bits (a
+// monotone non-decreasing function of the depth) and the map index. Counts the visible set and the (tile, gaussian) pairs.
 // Reference: rasterizer.cpp:37-68 (project_visible) + projection.cpp:17-40 + sh.cpp:82-92 +
 // rasterizer.cpp:81-88 (pixel rect -> tile rect).
 __global__ void __launch_bounds__(256) preprocess_fwd_kernel(
@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(256) preprocess_fwd_kernel(
         if (visible) {
             const size_t slot = base + __popc(mask & ((1u << lane) - 1u));
             vis_gid[slot] = i;
-            key32[slot] = __float_as_uint(__double2float_rn(depth));
+            // 24-bit monotone depth key: fp32 bits above the near plane, 16 ulps per step,
+            // clamped (ties, including the clamp, are ordered exactly by fix_ties)
+            const uint32_t bits = __float_as_uint(__double2float_rn(depth)) - kDepthKeyBase;
+            key32[slot] = min(bits >> 4, 0xffffffu);
         }
     }
     unsigned long long pairs = ntiles;

@@ -395,8 +395,8 @@ void ensure_counts(gs_frame* F) {
 }
 
 uint32_t grown_cap(int64_t pairs) {
-    const int64_t c = pairs + pairs / 8 + 65536;
-    return static_cast<uint32_t>(std::min<int64_t>(c, 0xffffffffLL));
+    const int64_t c = (pairs + pairs / 8 + 65536 + 63) / 64 * 64;  // multiple of 64 (vector loads)
+    return static_cast<uint32_t>(std::min<int64_t>(c, 0xffffffc0LL));
 }
 
 // render (rasterizer.cpp:100-199) without the CSR: project -> compact -> depth sort -> pack ->
@@ -462,9 +462,9 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
             Scope sc_sort(C, "depth_sort_pack_scan");
             size_t tb = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, 32, st);
+                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, kDepthKeyBits, st);
             ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, 32, st),
+                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, kDepthKeyBits, st),
                "depth sort");
             launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(),
                             F->key_by_gid.as<unsigned long long>(), cnt, n, st);

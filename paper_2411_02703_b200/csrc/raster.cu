@@ -6,9 +6,10 @@
 namespace gsb {
 
 // Depth order = the reference's comparator (depth asc, map index asc), rasterizer.cpp:69-72.
-// The radix sort runs on the fp32-rounded depth (a monotone non-decreasing key, 4 passes
-// instead of 8 for the fp64 bits), so only runs of equal fp32 keys can be out of order; each
-// such run (almost always 2 elements) is insertion-sorted here by (fp64 depth, map index).
+// The radix sort runs on a 24-bit key derived from the fp32-rounded depth (a monotone
+// non-decreasing function of the fp64 depth: 3 passes instead of 8 for the fp64 bits), so only
+// runs of equal keys can be out of order; each such run (almost always 2 elements) is
+// insertion-sorted here by (fp64 depth, map index).
 // The result is exactly the fp64 (depth, index) order, independent of the append order.
 __global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __restrict__ gid,
                                 const unsigned long long* __restrict__ depth, const unsigned long long* __restrict__ cnt) {
@@ -84,7 +85,10 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x);
     if (r - lane >= n_vis) return;  // whole warp past the visible ranks
+    // per rank: offset, count, rect origin and width, and the magic multiplier of the width
+    // (l / nx = umulhi(l, ceil(2^32 / nx)), exact for l, nx < 2^16) so no pair divides
     int off = 0, len = 0, tx0 = 0, ty0 = 0, ntx = 1;
+    uint32_t magic = 0;
     if (r < n_vis) {
         off = static_cast<int>(emit_off[r]);
         len = static_cast<int>(emit_off[r + 1]) - off;
@@ -92,19 +96,20 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
         tx0 = s.x0 >> 4;
         ty0 = s.y0 >> 4;
         ntx = (s.x1 >> 4) - tx0 + 1;
+        magic = 0xffffffffu / static_cast<uint32_t>(ntx) + 1u;  // (wraps to 0 for ntx = 1: not used)
     }
-    const int rbase = r - lane;
+    const uint32_t rbase = static_cast<uint32_t>(r - lane);
     for (int i = 0; i < 32; ++i) {
         const int c = __shfl_sync(0xffffffffu, len, i);
         if (c == 0) continue;
         const int o = __shfl_sync(0xffffffffu, off, i);
-        const int x0 = __shfl_sync(0xffffffffu, tx0, i);
-        const int y0 = __shfl_sync(0xffffffffu, ty0, i);
+        const int base_key = __shfl_sync(0xffffffffu, ty0 * tiles_x + tx0, i);
         const int nx = __shfl_sync(0xffffffffu, ntx, i);
+        const uint32_t mg = __shfl_sync(0xffffffffu, magic, i);
         for (int l = lane; l < c; l += 32) {
-            const int ty = y0 + l / nx, tx = x0 + l % nx;
-            keys[o + l] = static_cast<uint32_t>(ty * tiles_x + tx);
-            vals[o + l] = static_cast<uint32_t>(rbase + i);
+            const int row = nx == 1 ? l : static_cast<int>(__umulhi(static_cast<uint32_t>(l), mg));
+            keys[o + l] = static_cast<uint32_t>(base_key + row * tiles_x + (l - row * nx));
+            vals[o + l] = rbase + i;
         }
     }
 }
@@ -115,22 +120,34 @@ void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long
         emit_pairs_kernel<<<div_up(max_n, 256), 256, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, keys, vals);
 }
 
-// keys are sorted at capacity: the pairs past the device count carry the sentinel key
+// keys are sorted at capacity: the pairs past the device count carry the sentinel key. A
+// thread covers 4 consecutive keys (one 16-byte load plus the two neighbours).
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ cnt,
                                    uint32_t cap, uint2* __restrict__ ranges) {
     const unsigned long long n64 = cnt[kCntPairs];
     if (n64 > cap) return;
     const uint32_t n = static_cast<uint32_t>(n64);
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = i;
-    if (i == n - 1 || keys[i + 1] != k) ranges[k].y = i + 1;
+    const uint32_t i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= n) return;
+    const uint4 k4 = *reinterpret_cast<const uint4*>(keys + i0);  // cap is a multiple of 4
+    const uint32_t k[4] = {k4.x, k4.y, k4.z, k4.w};
+    uint32_t prev = i0 > 0 ? keys[i0 - 1] : 0xffffffffu;
+    const uint32_t next = i0 + 4 < n ? keys[i0 + 4] : 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t i = i0 + j;
+        if (i >= n) break;
+        const uint32_t nk = (j < 3 && i + 1 < n) ? k[j + 1] : (j == 3 ? next : 0xffffffffu);
+        if (i == 0 || prev != k[j]) ranges[k[j]].x = i;
+        if (i == n - 1 || nk != k[j]) ranges[k[j]].y = i + 1;
+        prev = k[j];
+    }
 }
 
 void launch_tile_ranges(const uint32_t* keys, const unsigned long long* cnt, uint32_t cap, uint2* ranges,
                         cudaStream_t st) {
-    if (cap > 0) tile_ranges_kernel<<<div_up(static_cast<int>(cap), 256), 256, 0, st>>>(keys, cnt, cap, ranges);
+    if (cap > 0)
+        tile_ranges_kernel<<<div_up(div_up(static_cast<int>(cap), 4), 256), 256, 0, st>>>(keys, cnt, cap, ranges);
 }
 
 // RenderOutput::contribs materialised on request (tests, gradcheck): one thread per pixel
