@@ -82,6 +82,9 @@ int gs_debug_set_blend_ppt(int fwd, int bwd);
 /* forward blend: tiles with more list entries than this carry the transmittance as df32
    instead of fp32 + error band (tuning knob; negative = default) */
 int gs_debug_set_blend_df_list(int entries);
+/* backward: list segments per tile (one CTA each; the forward checkpoints the boundaries);
+   0 = automatic per level */
+int gs_debug_set_blend_segments(int nseg);
 /* reads the table: names as one '\n'-separated string, per-name total ms and launch counts */
 int gs_context_profile_read(gs_context* ctx, char* names, int32_t names_len, double* total_ms,
                             int64_t* launches, int32_t max_entries, int32_t* n_entries);

@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     const uint32_t* __restrict__ emit_off, ViewParams v, const float* __restrict__ t_final,
     const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,
     const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials,
-    const unsigned long long* __restrict__ cnt) {
+    const unsigned long long* __restrict__ cnt, const float* __restrict__ ck, int nseg,
+    const float* __restrict__ color_final, const float* __restrict__ depth_final) {
     if (overflowed(cnt)) return;  // pair capacity exceeded: the host re-runs the step
     using S = Strip<PPT>;
     constexpr int NT = S::kThreads, NW = NT / 32, NP = (PPT + 1) / 2;  // PPT = 1: high half never live
@@ -75,6 +76,12 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     __shared__ int s_max[NW];
     const S sc(v.tiles_x);
     const uint2 range = ranges[blockIdx.x];
+    // this CTA's list segment [lo_s, hi_s) (blockIdx.y); the whole list when nseg = 1
+    const int n_list = static_cast<int>(range.y - range.x);
+    const int L = seg_len(n_list, nseg);
+    const int lo_s = static_cast<int>(blockIdx.y) * L;
+    if (lo_s >= n_list) return;  // whole CTA (before any barrier)
+    const int hi_s = min(lo_s + L, n_list);
     const double ox = sc.tx * kTile, oy = sc.ty * kTile;
     const float fx = static_cast<float>(sc.lx);
     const float dscale = dl_ddepth ? (depth_scale ? *depth_scale : 1.f) : 0.f;
@@ -82,10 +89,11 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
 
     float2 T[NP], B[NP], g0[NP], g1[NP], g2[NP], gz[NP];
     int last[2 * NP];
-    int my_last = 0;
+    int my_last = lo_s;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         float t[2] = {0.f, 0.f}, a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f}, c[2] = {0.f, 0.f}, z[2] = {0.f, 0.f};
+        float bb[2] = {0.f, 0.f};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int p = 2 * q + h, y = sc.py0 + p;
@@ -93,18 +101,27 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
             if (p < PPT && sc.px < v.width && y < v.height) {
                 const size_t o = static_cast<size_t>(y) * v.width + sc.px;
                 last[p] = n_proc[o];
-                t[h] = t_final[o];
                 a[h] = dl_dcolor[o];
                 b[h] = dl_dcolor[P + o];
                 c[h] = dl_dcolor[2 * P + o];
                 z[h] = dl_ddepth ? dl_ddepth[o] * dscale : 0.f;
                 // rasterizer.cpp:264: a pixel with an all-zero cotangent contributes nothing
                 if (a[h] == 0.f && b[h] == 0.f && c[h] == 0.f && z[h] == 0.f) last[p] = 0;
+                if (last[p] > hi_s) {
+                    // contributions continue past this segment: start from the forward's state
+                    // before entry hi_s, with B = the cotangent-weighted colour / depth still to come
+                    const float* cp = ck + static_cast<size_t>(hi_s / L - 1) * kCkFields * P;
+                    t[h] = cp[o];
+                    bb[h] = a[h] * (color_final[o] - cp[P + o]) + b[h] * (color_final[P + o] - cp[2 * P + o]) +
+                            c[h] * (color_final[2 * P + o] - cp[3 * P + o]) + z[h] * (depth_final[o] - cp[4 * P + o]);
+                } else {
+                    t[h] = t_final[o];
+                }
             }
-            my_last = max(my_last, last[p]);
+            my_last = max(my_last, min(last[p], hi_s));
         }
         T[q] = make_float2(t[0], t[1]);
-        B[q] = f2(0.f);
+        B[q] = make_float2(bb[0], bb[1]);
         g0[q] = make_float2(a[0], a[1]);
         g1[q] = make_float2(b[0], b[1]);
         g2[q] = make_float2(c[0], c[1]);
@@ -118,10 +135,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
 #pragma unroll
         for (int w = 0; w < NW; ++w) max_last = max(max_last, s_max[w]);
     }
-    const int n_list = static_cast<int>(range.y - range.x);
-
-    // entries no pixel reached still own a partial slot: zero it
-    for (int j = max_last + threadIdx.x; j < n_list; j += NT) {
+    // entries of the segment no pixel reached still own a partial slot: zero it
+    for (int j = max_last + threadIdx.x; j < hi_s; j += NT) {
         const uint32_t r = vals[range.x + j];
         const uint32_t slot = emission_index(rec[r], emit_off[r], sc.tx, sc.ty);
         float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(slot) * kNumPartials);
@@ -133,13 +148,13 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     // the current batch's walk)
     Splat nsp;
     uint32_t noff = 0;
-    if (max_last > 0 && threadIdx.x < max_last - max(0, max_last - kBwdBatch)) {
-        const uint32_t r = vals[range.x + max(0, max_last - kBwdBatch) + threadIdx.x];
+    if (max_last > lo_s && threadIdx.x < max_last - max(lo_s, max_last - kBwdBatch)) {
+        const uint32_t r = vals[range.x + max(lo_s, max_last - kBwdBatch) + threadIdx.x];
         nsp = rec[r];
         noff = emit_off[r];
     }
-    for (int hi = max_last; hi > 0; hi -= kBwdBatch) {
-        const int lo = max(0, hi - kBwdBatch);
+    for (int hi = max_last; hi > lo_s; hi -= kBwdBatch) {
+        const int lo = max(lo_s, hi - kBwdBatch);
         const int cnt = hi - lo;
         if (NW > 1) __syncthreads();
         if (threadIdx.x < cnt) {
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
             s_slot[threadIdx.x] = emission_index(nsp, noff, sc.tx, sc.ty);
         }
         {
-            const int nlo = max(0, lo - kBwdBatch);
+            const int nlo = max(lo_s, lo - kBwdBatch);
             if (threadIdx.x < lo - nlo) {
                 const uint32_t r = vals[range.x + nlo + threadIdx.x];
                 nsp = rec[r];
@@ -257,24 +272,25 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
-                      float* partials, const unsigned long long* cnt, cudaStream_t st) {
-    const int n_tiles = v.tiles_x * v.tiles_y;
+                      float* partials, const unsigned long long* cnt, const float* ck, int nseg,
+                      const float* color, const float* depth, cudaStream_t st) {
+    const dim3 n_tiles(v.tiles_x * v.tiles_y, nseg);
     switch (blend_ppt(v, true)) {
         case 8:
             blend_bwd_kernel<8><<<n_tiles, 32, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials, cnt);
+                                                        dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
             break;
         case 4:
             blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials, cnt);
+                                                        dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
             break;
         case 1:
             blend_bwd_kernel<1><<<n_tiles, 256, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials, cnt);
+                                                         dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
             break;
         default:
             blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials, cnt);
+                                                         dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
     }
 }
 

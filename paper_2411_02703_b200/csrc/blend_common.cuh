@@ -158,7 +158,19 @@ __device__ __forceinline__ bool rect_meets(const int4& rc, const int4& bb) {
     return !(rc.x > bb.z || rc.z < bb.x || rc.y > bb.w || rc.w < bb.y);
 }
 
+// Backward list segments. A tile's list is cut at multiples of L = seg_len(n, nseg) (a multiple
+// of kSegAlign, itself a multiple of every forward staging batch); the forward stores each
+// pixel's state before entry k L (k = 1 .. nseg - 1) as a checkpoint [k - 1][field][pixel] with
+// fields T, C_r, C_g, C_b, D, and the backward runs one CTA per (tile, segment).
+constexpr int kSegAlign = 256;
+constexpr int kCkFields = 5;
+__host__ __device__ inline int seg_len(int n_list, int nseg) {
+    return nseg <= 1 ? n_list : div_up(div_up(n_list, nseg), kSegAlign) * kSegAlign;
+}
+
 // pixels-per-thread chosen per level (host override for experiments; 0 = automatic)
 int blend_ppt(const ViewParams& v, bool backward);
+// backward list segments per tile, chosen per level (host override; 0 = automatic)
+int blend_segments(const ViewParams& v);
 
 }  // namespace gsb

@@ -213,14 +213,39 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
     }
 }
 
+// Backward checkpoint k: this thread's pixel states before list entry k L (see seg_len).
+template <int PPT>
+__device__ __forceinline__ void write_checkpoint(const FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, float* ck,
+                                                 int k, int width, int height) {
+    const size_t P = static_cast<size_t>(width) * height;
+    float* base = ck + static_cast<size_t>(k - 1) * kCkFields * P;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+        const int y = sc.py0 + p;
+        if (sc.px >= width || y >= height) continue;
+        const int q = p >> 1;
+        const bool hi = p & 1;
+        const size_t o = static_cast<size_t>(y) * width + sc.px;
+        base[o] = hi ? s.T[q].y + s.Tl[q].y : s.T[q].x + s.Tl[q].x;
+        base[P + o] = hi ? s.c0[q].y : s.c0[q].x;
+        base[2 * P + o] = hi ? s.c1[q].y : s.c1[q].x;
+        base[3 * P + o] = hi ? s.c2[q].y : s.c2[q].x;
+        base[4 * P + o] = hi ? s.dd[q].y : s.dd[q].x;
+    }
+}
+
 // The walk over one tile's list (staging batches of NT entries, per-warp ballot against the
 // live-pixel box, list order within the warp).
 template <int PPT, bool STATS, bool DF>
 __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<kTileThreads / PPT>& sb,
                                            const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
                                            const Splat* __restrict__ rec, uint2 range, double ox, double oy,
-                                           float fx) {
+                                           float fx, float* ck, int nseg, int width, int height) {
     constexpr int NT = Strip<PPT>::kThreads;
+    static_assert(kSegAlign % NT == 0, "segment boundaries must fall on staging batches");
+    const int n_list = static_cast<int>(range.y - range.x);
+    const int L = seg_len(n_list, nseg);
+    int next_ck = (nseg > 1 && L > 0) ? 1 : nseg;  // next checkpoint to write
     // below t_near the termination needs the exact check: fp32 mode 1e-4 (1 + beta(list length)),
     // rounded up; df32 mode a fixed guard
     const float t_near = DF ? 1.0001e-4f
@@ -232,6 +257,8 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
     Splat nsp;
     if (range.x + threadIdx.x < range.y) nsp = rec[vals[range.x + threadIdx.x]];
     for (uint32_t base = range.x; base < range.y; base += NT) {
+        if (next_ck < nseg && static_cast<int>(base - range.x) == next_ck * L)
+            write_checkpoint<PPT>(s, sc, ck, next_ck++, width, height);
         if (__syncthreads_count(s.live != 0) == 0) break;
         const uint32_t idx = base + threadIdx.x;
         if (idx < range.y) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
@@ -261,13 +288,16 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
             }
         }
     }
+    // boundaries past an early exit (every pixel terminated) hold the final state
+    for (; next_ck < nseg && next_ck * L < n_list; ++next_ck) write_checkpoint<PPT>(s, sc, ck, next_ck, width, height);
 }
 
 template <int PPT, bool STATS>
 __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
-    float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list) {
+    float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
+    float* __restrict__ ck, int nseg) {
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
     // live, so its packed lane computes nothing that is kept.
@@ -292,9 +322,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     }
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
     if (static_cast<int>(range.y - range.x) > df_list)
-        blend_walk<PPT, STATS, true>(s, sb, sc, vals, rec, range, ox, oy, fx);
+        blend_walk<PPT, STATS, true>(s, sb, sc, vals, rec, range, ox, oy, fx, ck, nseg, v.width, v.height);
     else
-        blend_walk<PPT, STATS, false>(s, sb, sc, vals, rec, range, ox, oy, fx);
+        blend_walk<PPT, STATS, false>(s, sb, sc, vals, rec, range, ox, oy, fx, ck, nseg, v.width, v.height);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
@@ -320,6 +350,18 @@ static int g_df_list = 1100;
 
 void set_blend_df_list(int n) { g_df_list = n < 0 ? 1100 : n; }
 
+static int g_nseg_override = 0;
+void set_blend_segments(int n) { g_nseg_override = n; }
+
+int blend_segments(const ViewParams& v) {
+    if (g_nseg_override > 0) return g_nseg_override;
+    // few tiles (long lists): split each list so the backward fills the GPU (measured with
+    // tests/diag_fwd.py on the 1M-Gaussian 1280x1024 pyramid: 16 segments at the 320-tile level,
+    // 8 at the 1280-tile level; none at full resolution)
+    const int tiles = v.tiles_x * v.tiles_y;
+    return tiles <= 512 ? 16 : tiles <= 2048 ? 8 : 1;
+}
+
 void set_blend_ppt(int fwd, int bwd) {
     g_ppt_override[0] = fwd;
     g_ppt_override[1] = bwd;
@@ -330,20 +372,17 @@ int blend_ppt(const ViewParams& v, bool backward) {
     if (o == 1 || o == 2 || o == 4 || o == 8) return o;
     // measured on B200 (1M Gaussians, 1280x1024 pyramid, tests/diag_fwd.py): the forward wants
     // 2 pixels per thread at every level; the backward amortises its per-entry warp reduction
-    // over 4 pixels once there are >= 1280 tiles (L1, L0) and keeps 2 (more warps per tile) at
-    // the 320-tile level.
-    const int tiles = v.tiles_x * v.tiles_y;
-    if (!backward) return 2;
-    return tiles >= 1024 ? 4 : 2;
+    // over 4 pixels (its parallelism at the coarse levels comes from the list segments)
+    return backward ? 4 : 2;
 }
 
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
-                      int32_t* n_contrib, bool stats, cudaStream_t st) {
+                      int32_t* n_contrib, bool stats, float* ck, int nseg, cudaStream_t st) {
     const int n_tiles = v.tiles_x * v.tiles_y;
 #define GSB_FWD(P, S) \
     blend_fwd_kernel<P, S><<<n_tiles, kTileThreads / P, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, \
-                                                               n_proc, n_contrib, g_df_list)
+                                                               n_proc, n_contrib, g_df_list, ck, nseg)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);

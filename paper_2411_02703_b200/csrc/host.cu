@@ -14,6 +14,7 @@
 #include "../../include/gsmap_b200.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "blend_common.cuh"
 
 using namespace gsb;
 
@@ -238,6 +239,8 @@ struct gs_frame {
         num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, rank_sums, depth_sorted;
     // per-pixel
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
+    DevBuf checkpoints;  // backward list-segment checkpoints [nseg - 1][5][pixels]
+    int nseg = 1;
     DevBuf loss;  // LossScalars
     bool has_cotangent = false;
     bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)
@@ -503,10 +506,14 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     }
     {
         Scope sc(C, "blend_fwd");
+        F->nseg = blend_segments(v);
+        if (F->nseg > 1)
+            F->checkpoints.ensure(sizeof(float) * (F->nseg - 1) * kCkFields * static_cast<size_t>(v.width) * v.height);
         launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
                          n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
-                         F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, st);
+                         F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, F->checkpoints.as<float>(),
+                         F->nseg, st);
         C->launched();
     }
     F->rendered = true;
@@ -562,7 +569,8 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
         Scope sc(C, "blend_bwd");
         launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
                          F->emit_off.as<uint32_t>(), F->view, F->t_final.as<float>(), F->n_proc.as<int32_t>(),
-                         dl_dcolor, dl_ddepth, depth_scale, F->partials.as<float>(), dev_counters(F), st);
+                         dl_dcolor, dl_ddepth, depth_scale, F->partials.as<float>(), dev_counters(F),
+                         F->checkpoints.as<float>(), F->nseg, F->color.as<float>(), F->depth.as<float>(), st);
         C->launched();
     }
     {
@@ -771,6 +779,10 @@ int gs_debug_set_blend_ppt(int fwd, int bwd) {
 
 int gs_debug_set_blend_df_list(int entries) {
     return guard([&] { set_blend_df_list(entries); });
+}
+
+int gs_debug_set_blend_segments(int nseg) {
+    return guard([&] { set_blend_segments(nseg); });
 }
 
 int gs_debug_counters(gs_context* C, int64_t* out2, int reset) {
@@ -992,7 +1004,7 @@ int gs_frame_destroy(gs_frame* F) {
                           &F->pair_keys,
                           &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->rank_sums, &F->color,
                           &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
-                          &F->wbuf, &F->host_stage, &F->loss})
+                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints})
             b->release();
         delete F;
     });

@@ -26,6 +26,8 @@ m = G.GaussianMap(ctx, train)
 cfg = G.TrainConfig.make(0.2, 0.5, 2, 1)
 cnt = np.zeros(2, np.int64)
 L = G.lib()
+if os.environ.get("DIAG_SEG"):
+    L.gs_debug_set_blend_segments(int(os.environ["DIAG_SEG"]))
 if os.environ.get("DIAG_DF"):
     L.gs_debug_set_blend_df_list(int(os.environ["DIAG_DF"]))
 PPTS = tuple(int(x) for x in os.environ.get("DIAG_PPTS", "1,2,4,8").split(","))

@@ -173,3 +173,32 @@ def test_gradients_random_scenes(seed):
     e, ge = grad_errors(gg, og, om.gaussians)
     assert (ge <= TOL).mean() >= 0.999 and ge.max() < 1e-2, ge.max()
     assert (e <= TOL).mean() >= 0.995, (e > TOL).sum()
+
+
+def test_gradients_long_lists_segmented():
+    """Long tile lists with the backward split into list segments (one CTA per (tile, segment),
+    started from the forward's checkpoints): parity with the oracle, and agreement with the
+    unsplit backward to fp32 rounding."""
+    L = G().lib()
+    gen = np.random.default_rng(77)
+    cam = O.camera(120, 120, 63.5, 47.5, 128, 96)
+    pose = random_pose(gen, 0.1)
+    om, gm = pair(random_scene(321, 8000, cam, pose, -1.0, 1.5))
+    dc = gen.uniform(-1, 1, (96, 128, 3)); dd = gen.uniform(-1, 1, (96, 128))
+    grads = {}
+    try:
+        for nseg in (1, 4):
+            assert L.gs_debug_set_blend_segments(nseg) == 0
+            og, gg = both_grads(om, gm, pose, cam, dc, dd)
+            grads[nseg] = gg
+    finally:
+        L.gs_debug_set_blend_segments(0)
+    go = G().render(gm, gpu_pose(pose), gpu_cam(cam))
+    assert go.stats().n_pairs / 48 > 600  # lists span several 256-entry segments
+    e, ge = grad_errors(grads[4], og, om.gaussians)
+    assert (ge <= TOL).mean() >= 0.999 and ge.max() < 1e-2, ge.max()
+    assert (e <= TOL).mean() >= 0.995, (e > TOL).sum()
+    # split vs unsplit: the segment start state (T, B) comes from the forward's checkpoints
+    # instead of the reverse accumulation, a different fp32 rounding path of the same values
+    _, ge = grad_errors(grads[4], grads[1], om.gaussians)
+    assert (ge <= TOL).mean() >= 0.999 and ge.max() < 1e-2, ge.max()
