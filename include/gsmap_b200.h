@@ -169,7 +169,9 @@ int gs_keyframe_destroy(gs_keyframe* kf);
 int gs_keyframe_consumed(gs_keyframe* kf, int32_t* consumed);
 int gs_keyframe_set_consumed(gs_keyframe* kf, int32_t consumed);
 int gs_keyframe_levels(gs_keyframe* kf, int32_t* n_levels);
-/* overwrite one pyramid level from host fp64 HWC images (the reference's ImageD) */
+/* overwrite one pyramid level from host fp64 HWC images (the reference's ImageD). Runs on the
+   context's copy stream, overlapping compute; the next call that reads the level (loss / train
+   step / read_level) waits for it. Page-locked host buffers must stay valid until then. */
 int gs_keyframe_upload_level(gs_keyframe* kf, int32_t level, const double* color, const double* depth);
 /* read a pyramid level back (host fp64 HWC) */
 int gs_keyframe_read_level(gs_keyframe* kf, int32_t level, double* color, double* depth);

@@ -132,6 +132,11 @@ struct gs_context {
     bool own_stream = false;
     DevBuf cub_tmp;
     PinnedBuf pinned;
+    cudaStream_t copy_stream = nullptr;  // host uploads (overlap the compute stream)
+    cudaStream_t copies() {
+        if (!copy_stream) ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        return copy_stream;
+    }
     int64_t launches = 0;
     gs_frame* scratch_frame = nullptr;
     gs_grads* scratch_grads = nullptr;
@@ -274,10 +279,32 @@ struct gs_keyframe {
     std::vector<int> hs, ws;
     std::vector<DevBuf> color, depth;  // per level: planes [3][h][w] and [h][w]
     DevBuf stage;                      // fp64 HWC staging for host uploads
+    // host uploads run on the context's copy stream: `ready[l]` marks level l's conversion,
+    // `used` the compute stream's last read of any level (an upload waits for it first)
+    std::vector<cudaEvent_t> ready;
+    std::vector<char> pending;
+    cudaEvent_t used = nullptr;
+    bool used_valid = false;
     ~gs_keyframe() {
         for (auto& b : color) b.release();
         for (auto& b : depth) b.release();
         stage.release();
+        for (cudaEvent_t e : ready)
+            if (e) cudaEventDestroy(e);
+        if (used) cudaEventDestroy(used);
+    }
+    // the compute stream must see level l's latest upload before reading it
+    void acquire(int l, cudaStream_t st) {
+        if (l < static_cast<int>(pending.size()) && pending[l]) {
+            ck(cudaStreamWaitEvent(st, ready[l], 0), "wait upload");
+            pending[l] = 0;
+        }
+    }
+    // after enqueueing reads of the level buffers on the compute stream
+    void release_reads(cudaStream_t st) {
+        if (!used) ck(cudaEventCreateWithFlags(&used, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(used, st), "record use");
+        used_valid = true;
     }
 };
 
@@ -604,6 +631,7 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
         fail(GS_EINVAL, "compute_loss: rendered resolution does not match level");
     gs_context* C = F->ctx;
     cudaStream_t st = C->stream;
+    K->acquire(level, st);
     ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset loss");
     Scope sc(C, "loss_l1_ssim_depth");
     launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
@@ -619,6 +647,7 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     }
     launch_loss_finalize(F->loss.as<LossScalars>(), cfg.lambda_d, st);
     C->launched();
+    K->release_reads(st);
     F->has_cotangent = true;
     F->loss_level = level;
     F->loss_lambda = cfg.lambda;
@@ -750,6 +779,10 @@ int gs_context_destroy(gs_context* C) {
         delete C->scratch_frame;
         if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external) cudaFree(C->scratch_grads->planes);
         delete C->scratch_grads;
+        if (C->copy_stream) {
+            cudaStreamSynchronize(C->copy_stream);
+            cudaStreamDestroy(C->copy_stream);
+        }
         C->cub_tmp.release();
         if (C->own_stream) cudaStreamDestroy(C->stream);
         delete C;
@@ -757,7 +790,10 @@ int gs_context_destroy(gs_context* C) {
 }
 
 int gs_context_synchronize(gs_context* C) {
-    return guard([&] { ck(cudaStreamSynchronize(C->stream), "cudaStreamSynchronize"); });
+    return guard([&] {
+        if (C->copy_stream) ck(cudaStreamSynchronize(C->copy_stream), "cudaStreamSynchronize");
+        ck(cudaStreamSynchronize(C->stream), "cudaStreamSynchronize");
+    });
 }
 
 int gs_context_set_stream(gs_context* C, void* stream) {
@@ -1308,6 +1344,7 @@ int gs_keyframe_destroy(gs_keyframe* K) {
     return guard([&] {
         if (!K) return;
         cudaStreamSynchronize(K->ctx->stream);
+        if (K->ctx->copy_stream) cudaStreamSynchronize(K->ctx->copy_stream);
         delete K;
     });
 }
@@ -1321,7 +1358,10 @@ int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color,
         if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
         const int h = K->hs[level], w = K->ws[level];
         const size_t P = static_cast<size_t>(h) * w;
-        cudaStream_t st = K->ctx->stream;
+        // asynchronous on the copy stream (host buffers must stay valid until the next
+        // synchronising call on this keyframe's context): overlaps the compute stream's work
+        cudaStream_t st = K->ctx->copies();
+        if (K->used_valid) ck(cudaStreamWaitEvent(st, K->used, 0), "wait last use");
         K->stage.ensure(sizeof(double) * 4 * P);
         ck(cudaMemcpyAsync(K->stage.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d color");
         ck(cudaMemcpyAsync(K->stage.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st),
@@ -1329,6 +1369,13 @@ int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color,
         launch_from_hwc_double(K->stage.as<double>(), h, w, 3, K->color[level].as<float>(), st);
         launch_from_hwc_double(K->stage.as<double>() + 3 * P, h, w, 1, K->depth[level].as<float>(), st);
         K->ctx->launched(2);
+        if (K->ready.size() < K->hs.size()) {
+            K->ready.resize(K->hs.size(), nullptr);
+            K->pending.resize(K->hs.size(), 0);
+        }
+        if (!K->ready[level]) ck(cudaEventCreateWithFlags(&K->ready[level], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(K->ready[level], st), "record upload");
+        K->pending[level] = 1;
     });
 }
 
@@ -1339,6 +1386,7 @@ int gs_keyframe_read_level(gs_keyframe* K, int32_t level, double* color, double*
         const size_t P = static_cast<size_t>(h) * w;
         std::vector<float> cp(3 * P), dp(P);
         cudaStream_t st = K->ctx->stream;
+        K->acquire(level, st);
         ck(cudaMemcpyAsync(cp.data(), K->color[level].p, sizeof(float) * 3 * P, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaMemcpyAsync(dp.data(), K->depth[level].p, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
