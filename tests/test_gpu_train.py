@@ -186,3 +186,28 @@ def test_pair_capacity_overflow_reruns_step():
     fresh = G().render(G().GaussianMap(ctx2, round32(big)), gpu_pose(O.pose()), gpu_cam(cam))
     assert fr.stats().n_pairs == fresh.stats().n_pairs > 100_000
     np.testing.assert_array_equal(fr.color, fresh.color)
+
+
+def test_upload_level_is_seen_by_next_reader():
+    """gs_keyframe_upload_level runs on the copy stream; the loss / read-back that follows must
+    see the new level (same loss as a keyframe built from that image)."""
+    cam = O.camera(120, 120, 63.5, 47.5, 128, 96)
+    om, gm = pair(random_scene(8, 300, cam, O.pose(), 0.0, 2.5))
+    gen = np.random.default_rng(5)
+    c0 = f32(gen.uniform(0, 1, (96, 128, 3))); d0 = np.zeros((96, 128))
+    c1 = f32(gen.uniform(0, 1, (96, 128, 3)))
+    d1 = f32(np.where(gen.uniform(size=(96, 128)) < 0.3, gen.uniform(1, 8, (96, 128)), 0.0))
+    ka = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), c0, d0, 10, 1)
+    kb = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), c1, d1, 10, 1)
+    go = G().render(gm, gpu_pose(O.pose()), gpu_cam(cam))
+    cfg = G().TrainConfig.make(0.2, 0.5, 1)
+    before = G().compute_loss(go, ka, 0, cfg)["total"]
+    for _ in range(3):  # repeated uploads, each read right after
+        ka.upload_level(0, c1, d1)
+        c, d = ka.level(0)
+        np.testing.assert_array_equal(c, c1)
+        np.testing.assert_array_equal(d, d1)
+        assert G().compute_loss(go, ka, 0, cfg)["total"] == pytest.approx(
+            G().compute_loss(go, kb, 0, cfg)["total"], rel=1e-12)
+        ka.upload_level(0, c0, d0)
+        assert G().compute_loss(go, ka, 0, cfg)["total"] == pytest.approx(before, rel=1e-12)
