@@ -231,12 +231,17 @@ struct gs_frame {
     DevBuf counters;
     bool counts_known = false, overflow = false;
     uint32_t pair_cap = 0;
-    std::vector<std::pair<int64_t, uint32_t>> caps;  // (width << 32 | height) -> pair capacity
-    uint32_t& cap_slot(int w, int h) {
+    int vis_cap = 0;  // ranks the depth sort and the rank-indexed kernels cover
+    struct Caps {
+        uint32_t pairs = 0;  // (tile, gaussian) pairs
+        int vis = 0;         // visible Gaussians
+    };
+    std::vector<std::pair<int64_t, Caps>> caps;  // (width << 32 | height) -> capacities
+    Caps& cap_slot(int w, int h) {
         const int64_t key = (static_cast<int64_t>(w) << 32) | static_cast<uint32_t>(h);
         for (auto& c : caps)
             if (c.first == key) return c.second;
-        caps.emplace_back(key, 0u);
+        caps.emplace_back(key, Caps{});
         return caps.back().second;
     }
     // per-Gaussian / per-rank / per-pair scratch
@@ -457,6 +462,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     F->overflow = false;
     F->counts_known = n == 0;
     F->pair_cap = 0;
+    F->vis_cap = 0;
     unsigned long long* cnt = dev_counters(F);
     if (n > 0) {
         F->rec_by_gid.ensure(sizeof(Splat) * n);
@@ -480,32 +486,36 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
                                   F->vis_gid.as<int32_t>(), F->keys_a.as<uint32_t>(), cnt, st);
             C->launched(2);
         }
-        uint32_t& cap = F->cap_slot(v.width, v.height);
-        if (cap == 0 || exact_counts) {
+        gs_frame::Caps& cs = F->cap_slot(v.width, v.height);
+        if (cs.pairs == 0 || exact_counts) {
             ensure_counts(F);
-            cap = std::max(cap, grown_cap(F->n_pairs));
+            cs.pairs = std::max(cs.pairs, grown_cap(F->n_pairs));
+            cs.vis = std::max(cs.vis, static_cast<int>((F->n_vis + F->n_vis / 8 + 4096 + 63) / 64 * 64));
         }
+        const uint32_t cap = cs.pairs;
+        const int nv = std::min(n, cs.vis);  // a larger visible count raises the overflow flag
         F->pair_cap = cap;
+        F->vis_cap = nv;
         {
             // (depth, index) order (rasterizer.cpp:69-72): stable radix sort on the fp32-rounded
             // depth, then exact (fp64 depth, index) order inside runs of equal fp32 keys
             Scope sc_sort(C, "depth_sort_pack_scan");
             size_t tb = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, kDepthKeyBits, st);
+                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, kDepthKeyBits, st);
             ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), n, 0, kDepthKeyBits, st),
+                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, kDepthKeyBits, st),
                "depth sort");
             launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(),
-                            F->key_by_gid.as<unsigned long long>(), cnt, n, st);
+                            F->key_by_gid.as<unsigned long long>(), cnt, nv, st);
             launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(),
-                        cnt, n, F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(),
+                        cnt, nv, F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(),
                         F->depth_sorted.as<unsigned long long>(), st);
             C->launched(2);
             tb = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), n + 1, st);
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), nv + 1, st);
             ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
-                                             n + 1, st), "scan");
+                                             nv + 1, st), "scan");
         }
         {
             Scope sc_keys(C, "tile_keys_sort_ranges");
@@ -514,7 +524,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
             F->pair_vals.ensure(sizeof(uint32_t) * cap);
             F->pair_vals2.ensure(sizeof(uint32_t) * cap);
             ck(cudaMemsetAsync(F->pair_keys.p, 0xff, sizeof(uint32_t) * cap, st), "memset pair keys");
-            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, n, cap, v.tiles_x,
+            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, nv, cap, v.tiles_x,
                               F->pair_keys.as<uint32_t>(), F->pair_vals.as<uint32_t>(), st);
             C->launched();
             int bits = 1;  // the sentinel's low bits (2^bits - 1) must sort after every tile id
@@ -527,7 +537,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
                                                F->pair_keys2.as<uint32_t>(), F->pair_vals.as<uint32_t>(),
                                                F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st),
                "tile sort");
-            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), cnt, cap, F->ranges.as<uint2>(), st);
+            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), cnt, cap, T, F->ranges.as<uint2>(), st);
             C->launched();
         }
     }
@@ -591,7 +601,7 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     if (M->n == 0 || F->pair_cap == 0) return;
     if (F->counts_known && (F->n_vis == 0 || F->n_pairs == 0)) return;
     F->partials.ensure(sizeof(float) * kNumPartials * F->pair_cap);
-    F->rank_sums.ensure(sizeof(double) * kNumPartials * M->n);
+    F->rank_sums.ensure(sizeof(double) * kNumPartials * F->vis_cap);
     {
         Scope sc(C, "blend_bwd");
         launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
@@ -604,7 +614,7 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
         Scope sc(C, "preprocess_bwd");
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
                               F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
-                              dev_counters(F), static_cast<int>(M->n), G->planes, G->cap, !G->clean, st);
+                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, st);
         G->clean = false;
         C->launched();
     }

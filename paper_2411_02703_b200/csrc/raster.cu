@@ -12,9 +12,17 @@ namespace gsb {
 // insertion-sorted here by (fp64 depth, map index).
 // The result is exactly the fp64 (depth, index) order, independent of the append order.
 __global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __restrict__ gid,
-                                const unsigned long long* __restrict__ depth, const unsigned long long* __restrict__ cnt) {
-    const int n = static_cast<int>(cnt[kCntVisible]);
+                                const unsigned long long* __restrict__ depth, unsigned long long* __restrict__ cnt,
+                                int max_n) {
+    // the sort covered max_n ranks: a larger visible count is clamped and flagged (the step is
+    // re-run at exact size), so every later kernel sees a consistent truncated set
+    const unsigned long long nv = cnt[kCntVisible];
+    const int n = static_cast<int>(min(nv, static_cast<unsigned long long>(max_n)));
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && nv > static_cast<unsigned long long>(max_n)) {
+        cnt[kCntVisible] = static_cast<unsigned long long>(max_n);
+        cnt[kCntOverflow] = 1ull;
+    }
     if (i >= n) return;
     const uint32_t k = key[i];
     if ((i > 0 && key[i - 1] == k) || i + 1 >= n || key[i + 1] != k) return;  // not a run start
@@ -36,8 +44,9 @@ __global__ void fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __res
 }
 
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
-                     const unsigned long long* cnt, int max_n, cudaStream_t st) {
-    if (max_n > 1) fix_ties_kernel<<<div_up(max_n, 256), 256, 0, st>>>(key32_sorted, gid_sorted, depth_by_gid, cnt);
+                     unsigned long long* cnt, int max_n, cudaStream_t st) {
+    if (max_n > 0)
+        fix_ties_kernel<<<div_up(max_n, 256), 256, 0, st>>>(key32_sorted, gid_sorted, depth_by_gid, cnt, max_n);
 }
 
 // rank-ordered copy of the projected records (the reference's sorted `projected` vector);
@@ -123,7 +132,7 @@ void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long
 // keys are sorted at capacity: the pairs past the device count carry the sentinel key. A
 // thread covers 4 consecutive keys (one 16-byte load plus the two neighbours).
 __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ cnt,
-                                   uint32_t cap, uint2* __restrict__ ranges) {
+                                   uint32_t cap, uint32_t tiles, uint2* __restrict__ ranges) {
     const unsigned long long n64 = cnt[kCntPairs];
     if (n64 > cap) return;
     const uint32_t n = static_cast<uint32_t>(n64);
@@ -136,7 +145,7 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsi
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const uint32_t i = i0 + j;
-        if (i >= n) break;
+        if (i >= n || k[j] >= tiles) break;  // sentinels (a truncated, flagged render) end the list
         const uint32_t nk = (j < 3 && i + 1 < n) ? k[j + 1] : (j == 3 ? next : 0xffffffffu);
         if (i == 0 || prev != k[j]) ranges[k[j]].x = i;
         if (i == n - 1 || nk != k[j]) ranges[k[j]].y = i + 1;
@@ -144,10 +153,11 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsi
     }
 }
 
-void launch_tile_ranges(const uint32_t* keys, const unsigned long long* cnt, uint32_t cap, uint2* ranges,
-                        cudaStream_t st) {
+void launch_tile_ranges(const uint32_t* keys, const unsigned long long* cnt, uint32_t cap, int tiles,
+                        uint2* ranges, cudaStream_t st) {
     if (cap > 0)
-        tile_ranges_kernel<<<div_up(div_up(static_cast<int>(cap), 4), 256), 256, 0, st>>>(keys, cnt, cap, ranges);
+        tile_ranges_kernel<<<div_up(div_up(static_cast<int>(cap), 4), 256), 256, 0, st>>>(
+            keys, cnt, cap, static_cast<uint32_t>(tiles), ranges);
 }
 
 // RenderOutput::contribs materialised on request (tests, gradcheck): one thread per pixel

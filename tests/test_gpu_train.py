@@ -211,3 +211,39 @@ def test_upload_level_is_seen_by_next_reader():
             G().compute_loss(go, kb, 0, cfg)["total"], rel=1e-12)
         ka.upload_level(0, c0, d0)
         assert G().compute_loss(go, ka, 0, cfg)["total"] == pytest.approx(before, rel=1e-12)
+
+
+def test_visible_capacity_overflow_reruns_step():
+    """Same as above for the visible-count capacity (depth sort / rank-indexed kernels): a view
+    that sees far more Gaussians than the remembered capacity is flagged and re-run exactly."""
+    cam = O.camera(400, 400, 319.5, 239.5, 640, 480)
+    g = random_scene(32, 20000, cam, O.pose(), 0.0, 2.0)
+    g["p"][:, 7:10] = np.log(0.003)
+    few = g.copy()
+    few["p"][1000:, 2] = -5.0  # behind the camera: 1000 visible
+    gen = np.random.default_rng(3)
+    color = f32(gen.uniform(0, 1, (480, 640, 3)))
+    sparse = np.zeros((480, 640))
+    cfg = G().TrainConfig.make(0.2, 0.5, 0)
+
+    def step(ctx, gmap):
+        kf = G().Keyframe(G().Pose(1, 0, 0, 0, 0, 0, 0), color, sparse, 5, 0, ctx=ctx)
+        return G().train_keyframe_step(gmap, kf, cfg, gpu_cam(cam))
+
+    ctx1 = G().Context(0)
+    step(ctx1, G().GaussianMap(ctx1, round32(few)))
+    m1 = G().GaussianMap(ctx1, round32(g))
+    r1 = step(ctx1, m1)
+    ctx2 = G().Context(0)
+    m2 = G().GaussianMap(ctx2, round32(g))
+    r2 = step(ctx2, m2)
+    assert r1["loss"] == pytest.approx(r2["loss"], rel=1e-9)
+    assert np.all(m1.adam_state()[2] == 1)
+    d = np.abs(m1.gaussians["p"] - m2.gaussians["p"])
+    assert np.mean(d <= 1e-6) > 0.999
+    fr = G().RenderOutput(ctx1)
+    G().render(G().GaussianMap(ctx1, round32(few)), gpu_pose(O.pose()), gpu_cam(cam), fr)
+    G().render(G().GaussianMap(ctx1, round32(g)), gpu_pose(O.pose()), gpu_cam(cam), fr)
+    fresh = G().render(G().GaussianMap(ctx2, round32(g)), gpu_pose(O.pose()), gpu_cam(cam))
+    assert fr.stats().n_visible == fresh.stats().n_visible > 15000
+    np.testing.assert_array_equal(fr.color, fresh.color)
