@@ -144,7 +144,11 @@ def run_ours(args, rank, world):
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream()
+    # one explicit stream for everything: the C-ABI context launches on it and the timing
+    # events are recorded on it (torch's default stream handle is 0, for which the context
+    # would create a stream of its own)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     ctx = G.Context(dev, stream.cuda_stream)
     scene, train, t_fix = build_fixture(args.n_gaussians)
     fx, fy, cx, cy, W, H = scene.camera

@@ -85,6 +85,16 @@ int gs_debug_set_blend_df_list(int entries);
 /* backward: list segments per tile (one CTA each; the forward checkpoints the boundaries);
    0 = automatic per level */
 int gs_debug_set_blend_segments(int nseg);
+/* forward: walk the list segments in parallel (local pass, chain, exact finish) on levels with
+   list segments and at most this many tiles (default 512; 0 = always the sequential walk;
+   negative = default) */
+int gs_debug_set_seg_forward(int max_tiles);
+/* diagnostics: gs_train_step skips its loss read-back (report.loss = NaN, no overflow re-run),
+   so the host can enqueue ahead of the device */
+int gs_debug_defer_step_sync(gs_context* ctx, int defer);
+/* host-side enqueue time per profiling scope (same table as gs_context_profile_read) */
+int gs_debug_profile_host(gs_context* ctx, char* names, int32_t names_len, double* host_ms, int32_t max_entries,
+                          int32_t* n_entries);
 /* reads the table: names as one '\n'-separated string, per-name total ms and launch counts */
 int gs_context_profile_read(gs_context* ctx, char* names, int32_t names_len, double* total_ms,
                             int64_t* launches, int32_t max_entries, int32_t* n_entries);

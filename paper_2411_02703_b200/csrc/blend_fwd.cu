@@ -148,12 +148,18 @@ __device__ __forceinline__ void df_near(FwdState<(PPT + 1) / 2>& s, unsigned nea
     }
 }
 
+// Transmittance modes of the forward walk.
+//   kBand:  fp32 T + rigorous error band, warp-cooperative fp64 replay when ambiguous.
+//   kDf:    df32 T (Th + Tl, exact to ~2^-46 per step), sequential replay only if even that is
+//           ambiguous (not observed in practice).
+//   kLocal: df32 T of one list segment started at T = 1 (segmented forward, pass 1): a pixel
+//           stops only once its local T is certainly below 1e-4 (the global T is then too).
+enum FwdMode : int { kBand = 0, kDf = 1, kLocal = 2 };
+
 // One tile-list entry over the thread's pixels. COVER: the entry's rect contains every live
 // pixel of the warp (warp-uniform), so the per-pixel box test reduces to the live bits.
 // STATS: maintain n_contrib (only the public render reports it).
-// DF: carry the transmittance as df32 (Th + Tl, exact to ~2^-46 per step: never ambiguous in
-// practice) instead of fp32 + band; chosen per tile for long lists, where the band is wide.
-template <int PPT, bool COVER, bool STATS, bool DF>
+template <int PPT, bool COVER, bool STATS, int MODE>
 __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, const int4& rc,
                                           float2 m, float4 cn, float4 col, int pos, int kw, float fx, float t_near,
                                           const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
@@ -179,7 +185,7 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
         s.c2[q] = __ffma2_rn(w, f2(col.z), s.c2[q]);
         s.dd[q] = __ffma2_rn(w, f2(col.w), s.dd[q]);
         s.vis[q] = __fadd2_rn(s.vis[q], w);
-        if (DF) {
+        if (MODE != kBand) {
             // exact factor 1 - alpha = fh + fl (Fast2Sum(1, -alpha)); clamp -> 1 - 0.99 (fp64)
             float2 fh = __fadd2_rn(f2(1.f), neg2(al));
             float2 fl = __fadd2_rn(neg2(al), neg2(__fadd2_rn(fh, f2(-1.f))));
@@ -206,8 +212,16 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
         near |= (static_cast<unsigned>(a0 && s.T[q].x < t_near) << p0) |
                 (static_cast<unsigned>(a1 && s.T[q].y < t_near) << (p0 + 1));
     }
-    if (DF) {
+    if (MODE == kDf) {
         if (near) df_near<PPT>(s, near, sc, pos, fx, vals, rec, range, ox, oy);
+    } else if (MODE == kLocal) {
+#pragma unroll
+        for (int p = 0; p < 2 * NP; ++p) {
+            if (!((near >> p) & 1u)) continue;
+            const float th = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x, tl = (p & 1) ? s.Tl[p >> 1].y : s.Tl[p >> 1].x;
+            const float d = __fadd_rn(th, -kTMinHi) + __fadd_rn(tl, -kTMinLo);
+            if (d < -1e-4f * 5.7e-14f * static_cast<float>(pos + 16)) s.live &= ~(1u << p);  // certainly below
+        }
     } else if (__any_sync(0xffffffffu, near != 0u)) {
         resolve_near<PPT>(s, near, sc, pos, kw, fx, vals, rec, range, ox, oy);
     }
@@ -234,37 +248,39 @@ __device__ __forceinline__ void write_checkpoint(const FwdState<(PPT + 1) / 2>& 
     }
 }
 
-// The walk over one tile's list (staging batches of NT entries, per-warp ballot against the
-// live-pixel box, list order within the warp).
-template <int PPT, bool STATS, bool DF>
+// The walk over entries [start, end) of one tile's list `full` (staging batches of NT entries,
+// per-warp ballot against the live-pixel box, list order within the warp). Positions are
+// relative to the list start; checkpoints are written only by a whole-list walk (start = 0).
+template <int PPT, bool STATS, int MODE>
 __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<kTileThreads / PPT>& sb,
                                            const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
-                                           const Splat* __restrict__ rec, uint2 range, double ox, double oy,
-                                           float fx, float* ck, int nseg, int width, int height) {
+                                           const Splat* __restrict__ rec, uint2 full, int start, int end, double ox,
+                                           double oy, float fx, float* ck, int nseg, int width, int height) {
     constexpr int NT = Strip<PPT>::kThreads;
     static_assert(kSegAlign % NT == 0, "segment boundaries must fall on staging batches");
-    const int n_list = static_cast<int>(range.y - range.x);
+    const int n_list = static_cast<int>(full.y - full.x);
     const int L = seg_len(n_list, nseg);
-    int next_ck = (nseg > 1 && L > 0) ? 1 : nseg;  // next checkpoint to write
-    // below t_near the termination needs the exact check: fp32 mode 1e-4 (1 + beta(list length)),
-    // rounded up; df32 mode a fixed guard
-    const float t_near = DF ? 1.0001e-4f
-                            : __double2float_ru(kTMin * (1.0 + kBetaPerFactor * (range.y - range.x + 1)));
+    int next_ck = (start == 0 && nseg > 1 && L > 0) ? 1 : nseg;  // next checkpoint to write
+    // below t_near the termination needs a closer look: fp32 mode 1e-4 (1 + beta(list length)),
+    // rounded up; df32 modes a fixed guard
+    const float t_near = MODE != kBand ? 1.0001e-4f
+                                       : __double2float_ru(kTMin * (1.0 + kBetaPerFactor * (n_list + 1)));
     int4 lb = warp_bbox<PPT>(s.live, sc);
     unsigned seen = s.live;
     int kw = 0;  // entries this warp has walked (uniform)
+    const uint32_t b_end = full.x + end;
     // the next batch's record is loaded one batch ahead (its latency overlaps the current walk)
     Splat nsp;
-    if (range.x + threadIdx.x < range.y) nsp = rec[vals[range.x + threadIdx.x]];
-    for (uint32_t base = range.x; base < range.y; base += NT) {
-        if (next_ck < nseg && static_cast<int>(base - range.x) == next_ck * L)
+    if (full.x + start + threadIdx.x < b_end) nsp = rec[vals[full.x + start + threadIdx.x]];
+    for (uint32_t base = full.x + start; base < b_end; base += NT) {
+        if (next_ck < nseg && static_cast<int>(base - full.x) == next_ck * L)
             write_checkpoint<PPT>(s, sc, ck, next_ck++, width, height);
         if (__syncthreads_count(s.live != 0) == 0) break;
         const uint32_t idx = base + threadIdx.x;
-        if (idx < range.y) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
-        if (idx + NT < range.y) nsp = rec[vals[idx + NT]];
+        if (idx < b_end) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
+        if (idx + NT < b_end) nsp = rec[vals[idx + NT]];
         __syncthreads();
-        const int cnt = min(NT, static_cast<int>(range.y - base));
+        const int cnt = min(NT, static_cast<int>(b_end - base));
         for (int b0 = 0; b0 < cnt; b0 += 32) {
             if (__any_sync(0xffffffffu, s.live != seen)) {
                 seen = s.live;
@@ -277,14 +293,14 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
                 const int j = b0 + __ffs(todo) - 1;
                 todo &= todo - 1;
                 const int4 rc = sb.rect[j];
-                const int pos = static_cast<int>(base - range.x) + j;
+                const int pos = static_cast<int>(base - full.x) + j;
                 ++kw;
                 if (rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w)
-                    fwd_entry<PPT, true, STATS, DF>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx, t_near,
-                                                    vals, rec, range, ox, oy);
+                    fwd_entry<PPT, true, STATS, MODE>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx,
+                                                      t_near, vals, rec, full, ox, oy);
                 else
-                    fwd_entry<PPT, false, STATS, DF>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx, t_near,
-                                                     vals, rec, range, ox, oy);
+                    fwd_entry<PPT, false, STATS, MODE>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx,
+                                                       t_near, vals, rec, full, ox, oy);
             }
         }
     }
@@ -322,14 +338,217 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
     }
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
     if (static_cast<int>(range.y - range.x) > df_list)
-        blend_walk<PPT, STATS, true>(s, sb, sc, vals, rec, range, ox, oy, fx, ck, nseg, v.width, v.height);
+        blend_walk<PPT, STATS, kDf>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
+                                    fx, ck, nseg, v.width, v.height);
     else
-        blend_walk<PPT, STATS, false>(s, sb, sc, vals, rec, range, ox, oy, fx, ck, nseg, v.width, v.height);
+        blend_walk<PPT, STATS, kBand>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
+                                      oy, fx, ck, nseg, v.width, v.height);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
         const int y = sc.py0 + p;
         if (sc.px >= v.width || y >= v.height) continue;
+        const int q = p >> 1;
+        const bool hi = p & 1;
+        const size_t o = static_cast<size_t>(y) * v.width + sc.px;
+        out_color[o] = hi ? s.c0[q].y : s.c0[q].x;
+        out_color[P + o] = hi ? s.c1[q].y : s.c1[q].x;
+        out_color[2 * P + o] = hi ? s.c2[q].y : s.c2[q].x;
+        out_depth[o] = hi ? s.dd[q].y : s.dd[q].x;
+        out_vis[o] = hi ? s.vis[q].y : s.vis[q].x;
+        out_t[o] = hi ? s.T[q].y + s.Tl[q].y : s.T[q].x + s.Tl[q].x;
+        out_nproc[o] = s.nproc[p];
+        if (STATS) out_ncontrib[o] = s.ncontrib[p];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Segmented forward (few tiles, long lists): the tile lists are cut at the backward's segment
+// boundaries and walked in three passes, so the latency-bound sequential walk is spread over
+// (tile, segment) CTAs. Exactness: every termination decision is taken either on a df32 product
+// certainly above 1e-4 or by the exact df32 walk of pass 3.
+constexpr int kSegFields = 9;  // Th, Tl, C_r, C_g, C_b, D, V, last contributor + 1, contributions
+
+template <int PPT>
+__device__ __forceinline__ void init_state(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, int width, int height) {
+    constexpr int NP = (PPT + 1) / 2;
+    s.live = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        s.T[q] = f2(1.f);
+        s.Tl[q] = s.c0[q] = s.c1[q] = s.c2[q] = s.dd[q] = s.vis[q] = f2(0.f);
+    }
+#pragma unroll
+    for (int p = 0; p < 2 * NP; ++p) {
+        s.nproc[p] = s.ncontrib[p] = 0;
+        if (p < PPT && sc.px < width && sc.py0 + p < height) s.live |= 1u << p;
+    }
+}
+
+// pass 1: CTA (tile, segment) walks the segment from T = 1 (df32) and stores the local state
+template <int PPT, bool STATS>
+__global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
+    ViewParams v, float* __restrict__ seg, int nseg) {
+    using S = Strip<PPT>;
+    __shared__ StageBuf<S::kThreads> sb;
+    const S sc(v.tiles_x);
+    const uint2 range = ranges[blockIdx.x];
+    const int n_list = static_cast<int>(range.y - range.x);
+    const int L = seg_len(n_list, nseg);
+    const int lo = static_cast<int>(blockIdx.y) * L;
+    if (lo >= n_list) return;
+    const double ox = sc.tx * kTile, oy = sc.ty * kTile;
+    const float fx = static_cast<float>(sc.lx);
+    FwdState<(PPT + 1) / 2> s;
+    init_state<PPT>(s, sc, v.width, v.height);
+    blend_walk<PPT, STATS, kLocal>(s, sb, sc, vals, rec, range, lo, min(lo + L, n_list), ox, oy, fx, nullptr, 1,
+                                   v.width, v.height);
+    const size_t P = static_cast<size_t>(v.width) * v.height;
+    float* base = seg + static_cast<size_t>(blockIdx.y) * kSegFields * P;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+        const int y = sc.py0 + p;
+        if (sc.px >= v.width || y >= v.height) continue;
+        const int q = p >> 1;
+        const bool hi = p & 1;
+        const size_t o = static_cast<size_t>(y) * v.width + sc.px;
+        base[o] = hi ? s.T[q].y : s.T[q].x;
+        base[P + o] = hi ? s.Tl[q].y : s.Tl[q].x;
+        base[2 * P + o] = hi ? s.c0[q].y : s.c0[q].x;
+        base[3 * P + o] = hi ? s.c1[q].y : s.c1[q].x;
+        base[4 * P + o] = hi ? s.c2[q].y : s.c2[q].x;
+        base[5 * P + o] = hi ? s.dd[q].y : s.dd[q].x;
+        base[6 * P + o] = hi ? s.vis[q].y : s.vis[q].x;
+        base[7 * P + o] = __int_as_float(s.nproc[p]);
+        base[8 * P + o] = __int_as_float(s.ncontrib[p]);
+    }
+}
+
+// pass 2: per pixel, chain the segments front to back; a segment is taken whole only if the
+// df32 product after it is certainly >= 1e-4, else the pixel stops there (star) for pass 3.
+// Writes the backward checkpoints at the segment boundaries it passes.
+__global__ void fwd_seg_chain_kernel(const uint2* __restrict__ ranges, ViewParams v, const float* __restrict__ seg,
+                                     int nseg, float* __restrict__ out_color, float* __restrict__ out_depth,
+                                     float* __restrict__ out_vis, float* __restrict__ out_t,
+                                     int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib,
+                                     float* __restrict__ tl_plane, int32_t* __restrict__ star_plane,
+                                     float* __restrict__ ck) {
+    const int P = v.width * v.height;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= P) return;
+    const int x = o % v.width, y = o / v.width;
+    const uint2 range = ranges[(y / kTile) * v.tiles_x + x / kTile];
+    const int n_list = static_cast<int>(range.y - range.x);
+    const int L = seg_len(n_list, nseg);
+    float th = 1.f, tl = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dd = 0.f, vis = 0.f;
+    int nproc = 0, ncontrib = 0, star = -1;
+    for (int s = 0; s < nseg && s * L < n_list; ++s) {
+        if (s >= 1) {
+            float* cp = ck + static_cast<size_t>(s - 1) * kCkFields * P;
+            cp[o] = th + tl;
+            cp[P + o] = c0;
+            cp[2 * P + o] = c1;
+            cp[3 * P + o] = c2;
+            cp[4 * P + o] = dd;
+        }
+        const float* sg = seg + static_cast<size_t>(s) * kSegFields * P;
+        const float lh = sg[o], ll = sg[P + o];
+        // (th + tl) * (lh + ll) with the exact product error of th * lh
+        const float pr = __fmul_rn(th, lh);
+        const float er = __fmaf_rn(th, lh, -pr);
+        const float t = __fmaf_rn(th, ll, __fmaf_rn(tl, lh, er));
+        const float nh = __fadd_rn(pr, t);
+        const float nl = __fadd_rn(t, -__fadd_rn(nh, -pr));
+        const float d = __fadd_rn(nh, -kTMinHi) + __fadd_rn(nl, -kTMinLo);
+        const float tol = 1e-4f * 1.2e-13f * static_cast<float>(min(n_list, (s + 1) * L) + 16);
+        if (!(d > tol)) {
+            star = s;
+            break;
+        }
+        c0 = __fmaf_rn(th, sg[2 * P + o], c0);
+        c1 = __fmaf_rn(th, sg[3 * P + o], c1);
+        c2 = __fmaf_rn(th, sg[4 * P + o], c2);
+        dd = __fmaf_rn(th, sg[5 * P + o], dd);
+        vis = __fmaf_rn(th, sg[6 * P + o], vis);
+        const int last = __float_as_int(sg[7 * P + o]);
+        if (last) nproc = last;
+        ncontrib += __float_as_int(sg[8 * P + o]);
+        th = nh;
+        tl = nl;
+    }
+    out_color[o] = c0;
+    out_color[P + o] = c1;
+    out_color[2 * P + o] = c2;
+    out_depth[o] = dd;
+    out_vis[o] = vis;
+    out_t[o] = star < 0 ? th + tl : th;  // pass 3 continues from (th, tl)
+    out_nproc[o] = nproc;
+    if (out_ncontrib) out_ncontrib[o] = ncontrib;
+    tl_plane[o] = tl;
+    star_plane[o] = star;
+}
+
+// pass 3: CTA (tile, segment s) finishes the pixels that stopped at s with the exact df32 walk
+template <int PPT, bool STATS>
+__global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
+    const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
+    ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
+    float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib,
+    const float* __restrict__ tl_plane, const int32_t* __restrict__ star_plane, int nseg) {
+    using S = Strip<PPT>;
+    constexpr int NP = (PPT + 1) / 2;
+    __shared__ StageBuf<S::kThreads> sb;
+    const S sc(v.tiles_x);
+    const uint2 range = ranges[blockIdx.x];
+    const int n_list = static_cast<int>(range.y - range.x);
+    const int L = seg_len(n_list, nseg);
+    const int lo = static_cast<int>(blockIdx.y) * L;
+    if (lo >= n_list) return;
+    const size_t P = static_cast<size_t>(v.width) * v.height;
+    FwdState<NP> s;
+    s.live = 0;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        float th[2] = {1.f, 1.f}, tl[2] = {0.f, 0.f}, a[2] = {0.f, 0.f}, b[2] = {0.f, 0.f}, c[2] = {0.f, 0.f};
+        float d[2] = {0.f, 0.f}, w[2] = {0.f, 0.f};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int p = 2 * q + h, y = sc.py0 + p;
+            s.nproc[p] = s.ncontrib[p] = 0;
+            if (p < PPT && sc.px < v.width && y < v.height) {
+                const size_t o = static_cast<size_t>(y) * v.width + sc.px;
+                if (star_plane[o] == static_cast<int>(blockIdx.y)) {
+                    s.live |= 1u << p;
+                    th[h] = out_t[o];
+                    tl[h] = tl_plane[o];
+                    a[h] = out_color[o];
+                    b[h] = out_color[P + o];
+                    c[h] = out_color[2 * P + o];
+                    d[h] = out_depth[o];
+                    w[h] = out_vis[o];
+                    s.nproc[p] = out_nproc[o];
+                    if (STATS) s.ncontrib[p] = out_ncontrib[o];
+                }
+            }
+        }
+        s.T[q] = make_float2(th[0], th[1]);
+        s.Tl[q] = make_float2(tl[0], tl[1]);
+        s.c0[q] = make_float2(a[0], a[1]);
+        s.c1[q] = make_float2(b[0], b[1]);
+        s.c2[q] = make_float2(c[0], c[1]);
+        s.dd[q] = make_float2(d[0], d[1]);
+        s.vis[q] = make_float2(w[0], w[1]);
+    }
+    const unsigned mine = s.live;
+    if (__syncthreads_count(mine != 0u) == 0) return;
+    const double ox = sc.tx * kTile, oy = sc.ty * kTile;
+    const float fx = static_cast<float>(sc.lx);
+    blend_walk<PPT, STATS, kDf>(s, sb, sc, vals, rec, range, lo, n_list, ox, oy, fx, nullptr, 1, v.width, v.height);
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+        if (!((mine >> p) & 1u)) continue;
+        const int y = sc.py0 + p;
         const int q = p >> 1;
         const bool hi = p & 1;
         const size_t o = static_cast<size_t>(y) * v.width + sc.px;
@@ -352,6 +571,10 @@ void set_blend_df_list(int n) { g_df_list = n < 0 ? 1100 : n; }
 
 static int g_nseg_override = 0;
 void set_blend_segments(int n) { g_nseg_override = n; }
+// segmented forward up to this many tiles (measured: it pays at the 320-tile level, where the
+// sequential walk is latency-bound, and loses at 1280 tiles); 0 = never
+static int g_seg_forward_tiles = 512;
+void set_blend_seg_forward(int max_tiles) { g_seg_forward_tiles = max_tiles < 0 ? 512 : max_tiles; }
 
 int blend_segments(const ViewParams& v) {
     if (g_nseg_override > 0) return g_nseg_override;
@@ -378,8 +601,26 @@ int blend_ppt(const ViewParams& v, bool backward) {
 
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
-                      int32_t* n_contrib, bool stats, float* ck, int nseg, cudaStream_t st) {
+                      int32_t* n_contrib, bool stats, float* ck, int nseg, float* seg_scratch, cudaStream_t st) {
     const int n_tiles = v.tiles_x * v.tiles_y;
+    if (nseg > 1 && n_tiles <= g_seg_forward_tiles && seg_scratch) {
+        const size_t P = static_cast<size_t>(v.width) * v.height;
+        float* seg = seg_scratch;
+        float* tl_plane = seg_scratch + static_cast<size_t>(nseg) * kSegFields * P;
+        int32_t* star = reinterpret_cast<int32_t*>(tl_plane + P);
+        const dim3 grid(n_tiles, nseg);
+        if (stats) fwd_seg_local_kernel<2, true><<<grid, kTileThreads / 2, 0, st>>>(ranges, vals, rec, v, seg, nseg);
+        else fwd_seg_local_kernel<2, false><<<grid, kTileThreads / 2, 0, st>>>(ranges, vals, rec, v, seg, nseg);
+        fwd_seg_chain_kernel<<<div_up(static_cast<int>(P), 256), 256, 0, st>>>(
+            ranges, v, seg, nseg, color, depth, vis, t_final, n_proc, stats ? n_contrib : nullptr, tl_plane, star, ck);
+        if (stats)
+            fwd_seg_finish_kernel<2, true><<<grid, kTileThreads / 2, 0, st>>>(
+                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
+        else
+            fwd_seg_finish_kernel<2, false><<<grid, kTileThreads / 2, 0, st>>>(
+                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
+        return;
+    }
 #define GSB_FWD(P, S) \
     blend_fwd_kernel<P, S><<<n_tiles, kTileThreads / P, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, \
                                                                n_proc, n_contrib, g_df_list, ck, nseg)

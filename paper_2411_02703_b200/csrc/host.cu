@@ -5,6 +5,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -133,6 +134,7 @@ struct gs_context {
     DevBuf cub_tmp;
     PinnedBuf pinned;
     cudaStream_t copy_stream = nullptr;  // host uploads (overlap the compute stream)
+    bool defer_sync = false;             // diagnostics: train steps skip the loss read-back
     cudaStream_t copies() {
         if (!copy_stream) ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
         return copy_stream;
@@ -145,6 +147,7 @@ struct gs_context {
     struct ProfRec {
         const char* name;
         cudaEvent_t a, b;
+        double host_us;  // host time spent enqueueing the scope
     };
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
@@ -175,8 +178,10 @@ struct Scope {
     gs_context* C;
     const char* name;
     cudaEvent_t a = nullptr;
+    std::chrono::steady_clock::time_point h0;
     Scope(gs_context* c, const char* n) : C(c), name(n) {
         if (C->profile) {
+            h0 = std::chrono::steady_clock::now();
             a = C->ev();
             cudaEventRecord(a, C->stream);
         }
@@ -185,7 +190,8 @@ struct Scope {
         if (C->profile && a) {
             cudaEvent_t b = C->ev();
             cudaEventRecord(b, C->stream);
-            C->prof.push_back({name, a, b});
+            const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+            C->prof.push_back({name, a, b, us});
         }
     }
 };
@@ -250,6 +256,7 @@ struct gs_frame {
     // per-pixel
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
     DevBuf checkpoints;  // backward list-segment checkpoints [nseg - 1][5][pixels]
+    DevBuf seg_scratch;  // segmented forward: per-segment local states, Tl and stop segment
     int nseg = 1;
     DevBuf loss;  // LossScalars
     bool has_cotangent = false;
@@ -544,13 +551,16 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     {
         Scope sc(C, "blend_fwd");
         F->nseg = blend_segments(v);
-        if (F->nseg > 1)
-            F->checkpoints.ensure(sizeof(float) * (F->nseg - 1) * kCkFields * static_cast<size_t>(v.width) * v.height);
+        const size_t P = static_cast<size_t>(v.width) * v.height;
+        if (F->nseg > 1) {
+            F->checkpoints.ensure(sizeof(float) * (F->nseg - 1) * kCkFields * P);
+            F->seg_scratch.ensure(sizeof(float) * (9 * F->nseg + 2) * P);
+        }
         launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
                          n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
                          F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, F->checkpoints.as<float>(),
-                         F->nseg, st);
+                         F->nseg, n > 0 && F->nseg > 1 ? F->seg_scratch.as<float>() : nullptr, st);
         C->launched();
     }
     F->rendered = true;
@@ -827,8 +837,43 @@ int gs_debug_set_blend_df_list(int entries) {
     return guard([&] { set_blend_df_list(entries); });
 }
 
+int gs_debug_profile_host(gs_context* C, char* names, int32_t names_len, double* host_ms, int32_t max_entries,
+                          int32_t* n_entries) {
+    return guard([&] {
+        std::vector<std::string> keys;
+        std::vector<double> ms;
+        for (const auto& r : C->prof) {
+            size_t k = 0;
+            while (k < keys.size() && keys[k] != r.name) ++k;
+            if (k == keys.size()) {
+                keys.emplace_back(r.name);
+                ms.push_back(0.0);
+            }
+            ms[k] += r.host_us * 1e-3;
+        }
+        std::string joined;
+        const int n = std::min<int>(static_cast<int>(keys.size()), max_entries);
+        for (int i = 0; i < n; ++i) {
+            joined += keys[i];
+            joined += '\n';
+            host_ms[i] = ms[i];
+        }
+        if (static_cast<int>(joined.size()) + 1 > names_len) fail(GS_EINVAL, "profile_host: names buffer too small");
+        std::memcpy(names, joined.c_str(), joined.size() + 1);
+        *n_entries = n;
+    });
+}
+
+int gs_debug_defer_step_sync(gs_context* C, int defer) {
+    return guard([&] { C->defer_sync = defer != 0; });
+}
+
 int gs_debug_set_blend_segments(int nseg) {
     return guard([&] { set_blend_segments(nseg); });
+}
+
+int gs_debug_set_seg_forward(int max_tiles) {
+    return guard([&] { set_blend_seg_forward(max_tiles); });
 }
 
 int gs_debug_counters(gs_context* C, int64_t* out2, int reset) {
@@ -1050,7 +1095,7 @@ int gs_frame_destroy(gs_frame* F) {
                           &F->pair_keys,
                           &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->rank_sums, &F->color,
                           &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
-                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints})
+                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints, &F->seg_scratch})
             b->release();
         delete F;
     });
@@ -1462,6 +1507,10 @@ int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const g
             grads_zero(G, M);
             train_view(M, K, *cfg, *cam, F, G, &level, attempt > 0);
             adam_impl(M, G, cfg->lr, dev_counters(F));
+            if (M->ctx->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
+                lr.total = lr.psnr = std::nan("");
+                break;
+            }
             lr = read_loss(F);
             if (!F->overflow) break;
             --M->adam_count;

@@ -32,7 +32,8 @@ void launch_tile_ranges(const uint32_t* keys_sorted, const unsigned long long* c
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib /* written only when stats */, bool stats,
-                      float* checkpoints /* [nseg - 1][5][pixels] */, int nseg, cudaStream_t st);
+                      float* checkpoints /* [nseg - 1][5][pixels] */, int nseg,
+                      float* seg_scratch /* [(9 nseg + 2) pixels]: segmented forward, nullable */, cudaStream_t st);
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,
@@ -42,6 +43,7 @@ void read_blend_stats(unsigned long long out[2], bool reset);
 void set_blend_ppt(int fwd, int bwd);
 void set_blend_df_list(int entries);
 void set_blend_segments(int nseg);
+void set_blend_seg_forward(int on);
 void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                         const uint32_t* offsets, int32_t* out_gid, double* out_alpha, cudaStream_t st);
 

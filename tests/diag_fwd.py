@@ -26,6 +26,8 @@ m = G.GaussianMap(ctx, train)
 cfg = G.TrainConfig.make(0.2, 0.5, 2, 1)
 cnt = np.zeros(2, np.int64)
 L = G.lib()
+if os.environ.get("DIAG_SEGFWD"):
+    L.gs_debug_set_seg_forward(int(os.environ["DIAG_SEGFWD"]))
 if os.environ.get("DIAG_SEG"):
     L.gs_debug_set_blend_segments(int(os.environ["DIAG_SEG"]))
 if os.environ.get("DIAG_DF"):
