@@ -3,8 +3,9 @@
 // suffix sums enter dalpha only through B = dC.S_c + dD.S_d, so one running scalar replaces the
 // four suffix sums:
 //   dalpha_i = T_i (dC.c_i + dD.z_i) - B / (1 - alpha_i);   B += w_i (dC.c_i + dD.z_i).
-// Each (tile, Gaussian) pair's 10 cotangent sums are reduced per warp (12 shuffles), across the
-// CTA's warps in shared memory, and written once to the pair's emission slot: deterministic,
+// Each (tile, Gaussian) pair's 10 cotangent sums are reduced per warp (staged rows summed over
+// the lanes), across the CTA's warps in shared memory, and written once to the pair's emission
+// slot: deterministic,
 // no global atomics; K8 sums a Gaussian's slots in fp64. Partials 5-6 (mean) and 7-9
 // (covariance) carry the staged conic's exp2 scale k and k^2 and omit the opacity factor (op,
 // op / 2); K8 applies both in fp64.
@@ -15,46 +16,12 @@ namespace gsb {
 
 namespace {
 
-// Transposed butterfly: reduces 10 per-lane values over the warp with 12 shuffles (5+3+2+1+1)
-// instead of 50. Returns the total of value index *idx in this lane (idx = -1: no value).
-__device__ __forceinline__ float warp_reduce10(const float v[kNumPartials], int lane, int* idx) {
-    const bool u4 = lane & 16, u3 = lane & 8, u2 = lane & 4, u1 = lane & 2;
-    float a[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-        const float send = u4 ? v[k] : v[k + 5];
-        const float keep = u4 ? v[k + 5] : v[k];
-        a[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    float b[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const float hi = k + 3 < 5 ? a[k + 3] : 0.f;
-        const float send = u3 ? a[k] : hi;
-        const float keep = u3 ? hi : a[k];
-        b[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    float c[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const float hi = k + 2 < 3 ? b[k + 2] : 0.f;
-        const float send = u2 ? b[k] : hi;
-        const float keep = u2 ? hi : b[k];
-        c[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    const float send = u1 ? c[0] : c[1];
-    const float keep = u1 ? c[1] : c[0];
-    float r = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    r += __shfl_xor_sync(0xffffffffu, r, 1);
-    const int ci = u1 ? 1 : 0;
-    const int bi = u2 ? ci + 2 : ci;
-    const int ai = u3 ? bi + 3 : bi;
-    const int vi = u4 ? ai + 5 : ai;
-    *idx = ((lane & 1) == 0 && bi < 3 && ai < 5) ? vi : -1;
-    return r;
-}
-
 constexpr int kBwdBatch = 32;
+// Per-warp reduction buffer: a processed entry's 10 per-lane sums are staged as rows of 32 lanes
+// (stride 36 floats: 16-byte aligned, conflict-free float4 reads), and every kFlush entries the
+// warp sums each row over its lanes (lane i takes rows i, i + 32, ...). No shuffles or selects.
+constexpr int kFlush = 4;
+constexpr int kRowStride = 36;
 
 }  // namespace
 
@@ -74,7 +41,30 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
     __shared__ uint32_t s_mask[NW];
     __shared__ float s_red[NW > 1 ? NW : 1][kBwdBatch][kNumPartials];
     __shared__ int s_max[NW];
+    __shared__ __align__(16) float s_pv[NW][kFlush][kNumPartials][kRowStride];
+    __shared__ int s_pk[NW][kFlush];
     const S sc(v.tiles_x);
+    // sums the warp's staged rows over its lanes and stores them per (entry, partial)
+    auto flush = [&](int nb) {
+        __syncwarp();
+        for (int idx = sc.lane; idx < nb * kNumPartials; idx += 32) {
+            const int e = idx / kNumPartials, c = idx - e * kNumPartials;
+            const float4* row = reinterpret_cast<const float4*>(&s_pv[sc.warp][e][c][0]);
+            float4 a = row[0];
+#pragma unroll
+            for (int i = 1; i < 8; ++i) {
+                const float4 b = row[i];
+                const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+                const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+                a = make_float4(lo.x, lo.y, hi.x, hi.y);
+            }
+            const float tot = (a.x + a.y) + (a.z + a.w);
+            const int k = s_pk[sc.warp][e];
+            if (NW == 1) partials[static_cast<size_t>(s_slot[k]) * kNumPartials + c] = tot;
+            else s_red[sc.warp][k][c] = tot;
+        }
+        __syncwarp();
+    };
     const uint2 range = ranges[blockIdx.x];
     // this CTA's list segment [lo_s, hi_s) (blockIdx.y); the whole list when nseg = 1
     const int n_list = static_cast<int>(range.y - range.x);
@@ -179,6 +169,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
         if (NW > 1) __syncthreads(); else __syncwarp();
         // ballot the staged entries that meet the box, walk them back to front
         unsigned todo = __ballot_sync(0xffffffffu, sc.lane < cnt && rect_meets(sb.rect[sc.lane], ab));
+        int nb = 0;  // entries staged in s_pv (warp-uniform)
         while (todo) {
             const int k = 31 - __clz(todo);
             todo &= ~(1u << k);
@@ -233,18 +224,19 @@ __global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
                 acc[9] = __ffma2_rn(h1, e.u1, acc[9]);
             }
             if (!__any_sync(0xffffffffu, any)) continue;
-            float vsum[kNumPartials];
 #pragma unroll
-            for (int c = 0; c < kNumPartials; ++c) vsum[c] = acc[c].x + acc[c].y;
-            int vi;
-            const float tot = warp_reduce10(vsum, sc.lane, &vi);
-            if (NW == 1) {
-                if (vi >= 0) partials[static_cast<size_t>(s_slot[k]) * kNumPartials + vi] = tot;
-            } else {
-                if (vi >= 0) s_red[sc.warp][k][vi] = tot;
+            for (int c = 0; c < kNumPartials; ++c) s_pv[sc.warp][nb][c][sc.lane] = acc[c].x + acc[c].y;
+            if (sc.lane == 0) {
+                s_pk[sc.warp][nb] = k;
+                s_mask[sc.warp] |= 1u << k;
             }
-            if (sc.lane == 0) s_mask[sc.warp] |= 1u << k;
+            if (++nb == kFlush) {
+                flush(nb);
+                nb = 0;
+            }
         }
+        if (nb) flush(nb);
+        nb = 0;
         if (NW == 1) {
             __syncwarp();
             // entries of this batch the warp never reduced (no pixel of the tile hit them)
@@ -275,23 +267,13 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
                       float* partials, const unsigned long long* cnt, const float* ck, int nseg,
                       const float* color, const float* depth, cudaStream_t st) {
     const dim3 n_tiles(v.tiles_x * v.tiles_y, nseg);
-    switch (blend_ppt(v, true)) {
-        case 8:
-            blend_bwd_kernel<8><<<n_tiles, 32, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
-            break;
-        case 4:
-            blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                        dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
-            break;
-        case 1:
-            blend_bwd_kernel<1><<<n_tiles, 256, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
-            break;
-        default:
-            blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                         dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
-    }
+    // 4 pixels per thread (2 warps per tile) unless overridden to 2 (4 warps per tile)
+    if (blend_ppt(v, true) == 2)
+        blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                     dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
+    else
+        blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+                                                    dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
 }
 
 }  // namespace gsb
