@@ -628,9 +628,6 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);
             break;
-        case 1:
-            if (stats) GSB_FWD(1, true); else GSB_FWD(1, false);
-            break;
         default:
             if (stats) GSB_FWD(2, true); else GSB_FWD(2, false);
     }
