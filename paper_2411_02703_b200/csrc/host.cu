@@ -654,16 +654,19 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     K->acquire(level, st);
     ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset loss");
     Scope sc(C, "loss_l1_ssim_depth");
-    launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
-                      K->depth[level].as<float>(), h, w, cfg.lambda, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
-                      F->loss.as<LossScalars>(), st);
-    C->launched();
     if (cfg.lambda != 0.0) {
         if (h < 11 || w < 11) fail(GS_EINVAL, "ssim: image smaller than the 11x11 window");
         F->wbuf.ensure(sizeof(float) * 9 * static_cast<size_t>(h - 10) * (w - 10));
+        // SSIM forward, then its adjoint fused with the per-pixel L1 / psnr / depth terms
         launch_ssim(F->color.as<float>(), K->color[level].as<float>(), h, w, cfg.lambda, F->wbuf.as<float>(),
-                    F->dl_dcolor.as<float>(), F->loss.as<LossScalars>(), st);
+                    F->dl_dcolor.as<float>(), F->loss.as<LossScalars>(), F->depth.as<float>(), F->vis.as<float>(),
+                    K->depth[level].as<float>(), F->depth_cot.as<float>(), st);
         C->launched(2);
+    } else {
+        launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
+                          K->depth[level].as<float>(), h, w, cfg.lambda, F->dl_dcolor.as<float>(),
+                          F->depth_cot.as<float>(), F->loss.as<LossScalars>(), st);
+        C->launched();
     }
     launch_loss_finalize(F->loss.as<LossScalars>(), cfg.lambda_d, st);
     C->launched();

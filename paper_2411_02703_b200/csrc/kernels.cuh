@@ -51,8 +51,10 @@ void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* 
 void launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
                        const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
                        float* depth_cot, LossScalars* acc, cudaStream_t st);
+// depth != nullptr: also computes loss_pixel's terms (L1 / psnr / masked depth) in the adjoint pass
 void launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
-                 float* dl_dcolor, LossScalars* acc, cudaStream_t st);
+                 float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis, const float* gt_depth,
+                 float* depth_cot, cudaStream_t st);
 void launch_loss_finalize(LossScalars* acc, double lambda_d, cudaStream_t st);
 void launch_downsample(const float* in, int h, int w, int channels, bool depth, float* out, cudaStream_t st);
 

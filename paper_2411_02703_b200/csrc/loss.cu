@@ -203,9 +203,22 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
 
 // Adjoint of the valid correlation (metrics.cpp:55-73) for the three weight maps, combined as
 // d/da = adj(w_mu) + 2 a' adj(w_a2) + b' adj(w_ab), then dL/dC += -lambda * d.
+// PixelLoss: the per-pixel L1 / psnr / masked-depth terms of loss_pixel_kernel, fused here when
+// SSIM runs (this kernel visits every pixel of every channel once with colour and target in
+// hand): dL/dC = sign(C - I) l1_grad - lambda dSSIM is written without a read-modify-write.
+struct PixelLoss {
+    const float* depth;
+    const float* vis;
+    const float* gt_depth;
+    float* depth_cot;
+    float l1_grad;
+    LossScalars* acc;
+};
+
+template <bool FUSED>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, const float* __restrict__ wbuf,
-                                                       float neg_lambda, float* __restrict__ dl) {
+                                                       float neg_lambda, float* __restrict__ dl, PixelLoss pl) {
     __shared__ float sw[3][kInY][kInX + 2];
     __shared__ float hx[3][kInY][kSx + 1];
     const int c = blockIdx.z;
@@ -263,26 +276,68 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
     }
     const size_t P = static_cast<size_t>(h) * w;
     const int x = x0 + q;
+    double l1 = 0.0, sq = 0.0, dabs = 0.0;
+    unsigned long long nv = 0;
 #pragma unroll
     for (int o = 0; o < kRB; ++o) {
         const int y = y0 + r0 + o;
         if (y >= h || x >= w) continue;
         const size_t p = c * P + static_cast<size_t>(y) * w + x;
-        const float as = A[p] - kShift, bs = B[p] - kShift;
+        const float av = A[p], bv = B[p];
+        const float as = av - kShift, bs = bv - kShift;
         const float d = bsum[o][0] + 2.f * as * bsum[o][1] + bs * bsum[o][2];
-        dl[p] = fmaf(neg_lambda, d, dl[p]);
+        if (FUSED) {  // loss_pixel_kernel's terms for this pixel and channel
+            const double e = static_cast<double>(av) - static_cast<double>(bv);
+            l1 += fabs(e);
+            sq += e * e;
+            dl[p] = fmaf(neg_lambda, d, sgnf(e) * pl.l1_grad);
+            if (c == 0) {
+                const size_t o2 = static_cast<size_t>(y) * w + x;
+                const double gd = pl.gt_depth[o2];
+                const double vv = pl.vis[o2];
+                float cot = 0.f;
+                if (gd > 0.0 && vv > 0.98) {  // kDepthLossMinVisibility (mapper.hpp:15)
+                    const double r = static_cast<double>(pl.depth[o2]) / vv - gd;
+                    dabs += fabs(r);
+                    ++nv;
+                    cot = static_cast<float>(sgnf(r) / vv);
+                }
+                pl.depth_cot[o2] = cot;
+            }
+        } else {
+            dl[p] = fmaf(neg_lambda, d, dl[p]);
+        }
+    }
+    if (FUSED) {
+        __shared__ double scratch[8];
+        block_add(l1, &pl.acc->l1_sum, scratch);
+        block_add(sq, &pl.acc->sq_sum, scratch);
+        if (c == 0) {
+            block_add(dabs, &pl.acc->depth_abs_sum, scratch);
+            nv = warp_sum(nv);
+            if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&pl.acc->n_valid, nv);
+        }
     }
 }
 
 void launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
-                 float* dl_dcolor, LossScalars* acc, cudaStream_t st) {
+                 float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis, const float* gt_depth,
+                 float* depth_cot, cudaStream_t st) {
     ensure_taps();
     const int vh = h - kHalo, vw = w - kHalo;
     const float inv_n = static_cast<float>(1.0 / (static_cast<double>(vh) * vw * 3));
     dim3 gf(div_up(vw, kSx), div_up(vh, kSy), 3);
     ssim_fwd_kernel<<<gf, 256, 0, st>>>(color, gt_color, h, w, inv_n, wbuf, acc);
     dim3 gb(div_up(w, kSx), div_up(h, kSy), 3);
-    ssim_bwd_kernel<<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda), dl_dcolor);
+    if (depth) {  // fused pixel loss (loss_pixel_kernel is not launched)
+        PixelLoss pl{depth, vis, gt_depth, depth_cot,
+                     static_cast<float>((1.0 / (static_cast<double>(h) * w * 3)) * (1.0 - lambda)), acc};
+        ssim_bwd_kernel<true><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda), dl_dcolor,
+                                                   pl);
+    } else {
+        ssim_bwd_kernel<false><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda),
+                                                    dl_dcolor, PixelLoss{});
+    }
 }
 
 __global__ void loss_finalize_kernel(LossScalars* acc, double lambda_d) {
