@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import pyoracle as O
-from tests._common import gpu_cam, gpu_pose, pair, random_pose, random_scene, rel_err
+from tests._common import active_columns, gpu_cam, gpu_pose, grad_errors, pair, random_pose, random_scene
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-3
@@ -33,16 +33,6 @@ def both_grads(om, gm, pose, cam, dc, dd):
     go = G().render(gm, gpu_pose(pose), gpu_cam(cam))
     gg = G().render_backward(gm, gpu_pose(pose), gpu_cam(cam), go, dc, dd).read()
     return og, gg
-
-
-def active_columns(gaussians):
-    """Mask of meaningful scalars per Gaussian: geometry + the active SH coefficients."""
-    n = len(gaussians)
-    mask = np.zeros((n, 59), bool)
-    mask[:, :11] = True
-    for i, d in enumerate(gaussians["degree"]):
-        mask[i, 11:11 + 3 * (d + 1) ** 2] = True
-    return mask
 
 
 def test_zero_cotangent_gives_zero():  # test_rasterizer.cpp:178-193
@@ -124,33 +114,6 @@ def _rotmat(p):
 
 # Parameter groups of a Gaussian's gradient (gaussian.hpp:40-58): position, rotation,
 # log_scale, opacity, and each SH coefficient's RGB triplet.
-GROUPS = [(0, 3), (3, 7), (7, 10), (10, 11)] + [(11 + 3 * k, 14 + 3 * k) for k in range(16)]
-
-
-def grad_errors(gg, og, gaussians):
-    """Returns (gradcheck rel_err over the active scalars, normwise rel error per active
-    (Gaussian, parameter group)).
-
-    The per-pixel blend runs in fp32, so a gradient that is the sum of N per-pixel terms carries
-    an absolute error ~eps32*sqrt(N)*|term| whatever the accumulation precision. When such a sum
-    cancels to <1e-4 of its terms (about 1e-4 of the independent sums do) the scalar gradcheck
-    metric exceeds 1e-3 although the error is ~1e-7 of the Gaussian's gradient scale. The
-    "within 1e-3 relative" bar is therefore applied (a) to every parameter group as a vector,
-    ||g_gpu - g_ref|| / max(||g_gpu||, ||g_ref||, 1e-3 ||g_ref||_inf(Gaussian), 1e-6), and
-    (b) as the reference's scalar gradcheck metric on >= 99.5% of the active scalars."""
-    mask = active_columns(gaussians)
-    e = rel_err(gg, og)[mask]
-    rowmax = np.abs(og).max(axis=1)
-    ge = []
-    for s, t in GROUPS:
-        active = mask[:, s]
-        d = np.linalg.norm(gg[:, s:t] - og[:, s:t], axis=1)
-        n = np.maximum.reduce([np.linalg.norm(gg[:, s:t], axis=1), np.linalg.norm(og[:, s:t], axis=1),
-                               1e-3 * rowmax, np.full(len(og), 1e-6)])
-        ge.append((d / n)[active])
-    return e, np.concatenate(ge)
-
-
 def test_gradients_smooth_configs():
     es, ges = [], []
     for om, gm, pose, cam, wc, wd in gradcheck_configs(3, 40):
