@@ -15,7 +15,7 @@ import pytest
 from fixtures import pyfixture as F
 from oracle import pyoracle as O
 from tests._common import gpu_cam, gpu_pose, pair, rect_of
-from tests.test_gpu_backward import GROUPS, active_columns
+from tests._common import GROUPS, active_columns
 
 pytestmark = pytest.mark.gpu
 THREADS = os.cpu_count() or 8
