@@ -122,6 +122,10 @@ int gs_map_set_scene_extent(gs_map* map, double extent);
 int gs_map_global_step(const gs_map* map, int64_t* step);
 int gs_map_set_global_step(gs_map* map, int64_t step);
 int gs_map_raise_sh_degree(gs_map* map, int degree);   /* gaussian_map.cpp:75-79 */
+/* GaussianMap::prune (gaussian_map.hpp:79, gaussian_map.cpp:56-73): drop every Gaussian with
+   sigmoid(opacity_logit) < threshold, compacting parameters and optimizer state in order;
+   threshold outside (0, 1) -> GS_EINVAL. *removed = the number dropped. */
+int gs_map_prune(gs_map* map, double opacity_threshold, int64_t* removed);
 int gs_map_max_active_degree(gs_map* map, int* degree);
 /* device SoA access: params/m/v planes [59][capacity] fp32 */
 int gs_map_device_planes(gs_map* map, float** params, float** adam_m, float** adam_v, int64_t* capacity);

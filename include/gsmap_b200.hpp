@@ -197,6 +197,11 @@ public:
         return e;
     }
     void raise_sh_degree(int d) { check(gs_map_raise_sh_degree(h_, d)); }
+    std::size_t prune(double opacity_threshold) {  // gaussian_map.hpp:79
+        int64_t removed = 0;
+        check(gs_map_prune(h_, opacity_threshold, &removed));
+        return static_cast<std::size_t>(removed);
+    }
     gs_map* get() const { return h_; }
     Context& context() const { return *ctx_; }
 

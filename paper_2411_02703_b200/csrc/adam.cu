@@ -138,6 +138,43 @@ void launch_adam(float* params, float* m, float* v, const int32_t* birth, const 
         adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
 }
 
+// GaussianMap::prune (gaussian_map.cpp:56-73): keep sigmoid(opacity_logit) >= threshold (fp64,
+// types.hpp:10), then a stable compaction of every per-Gaussian array (parameters, Adam m / v,
+// births, degrees) so the optimizer state stays aligned.
+__global__ void prune_flags_kernel(const float* __restrict__ params, int64_t cap, int n, double thr,
+                                   int32_t* __restrict__ keep) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double o = 1.0 / (1.0 + exp(-static_cast<double>(params[P_OP * cap + i])));
+    keep[i] = o >= thr ? 1 : 0;
+}
+
+template <class T>
+__global__ void compact_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t scap, int64_t dcap, int n,
+                               const int32_t* __restrict__ keep, const int32_t* __restrict__ pos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int plane = blockIdx.y;
+    if (i >= n || !keep[i]) return;
+    dst[plane * dcap + pos[i]] = src[plane * scap + i];
+}
+
+void launch_prune_flags(const float* params, int64_t cap, int n, double thr, int32_t* keep, cudaStream_t st) {
+    if (n > 0) prune_flags_kernel<<<div_up(n, 256), 256, 0, st>>>(params, cap, n, thr, keep);
+}
+
+void launch_compact(const float* src, float* dst, int64_t scap, int64_t dcap, int planes, int n, const int32_t* keep,
+                    const int32_t* pos, cudaStream_t st) {
+    if (n > 0) compact_kernel<float><<<dim3(div_up(n, 256), planes), 256, 0, st>>>(src, dst, scap, dcap, n, keep, pos);
+}
+
+void launch_compact(const int32_t* src, int32_t* dst, int n, const int32_t* keep, const int32_t* pos, cudaStream_t st) {
+    if (n > 0) compact_kernel<int32_t><<<div_up(n, 256), 256, 0, st>>>(src, dst, 0, 0, n, keep, pos);
+}
+
+void launch_compact(const int8_t* src, int8_t* dst, int n, const int32_t* keep, const int32_t* pos, cudaStream_t st) {
+    if (n > 0) compact_kernel<int8_t><<<div_up(n, 256), 256, 0, st>>>(src, dst, 0, 0, n, keep, pos);
+}
+
 namespace {
 __device__ __forceinline__ unsigned int ord(float f) {
     const unsigned int u = __float_as_uint(f);

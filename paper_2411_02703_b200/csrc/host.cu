@@ -1070,6 +1070,64 @@ int gs_map_raise_sh_degree(gs_map* M, int degree) {  // gaussian_map.cpp:75-79
 
 int gs_map_max_active_degree(gs_map* M, int* degree) { return guard([&] { *degree = M->max_degree; }); }
 
+int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // gaussian_map.cpp:56-73
+    return guard([&] {
+        if (opacity_threshold <= 0.0 || opacity_threshold >= 1.0)
+            fail(GS_EINVAL, "prune: threshold must be in (0, 1)");
+        M->ctx->use();
+        *removed = 0;
+        const int n = static_cast<int>(M->n);
+        if (n == 0) return;
+        gs_context* C = M->ctx;
+        cudaStream_t st = C->stream;
+        DevBuf keep, pos;
+        keep.ensure(sizeof(int32_t) * (n + 1));
+        pos.ensure(sizeof(int32_t) * (n + 1));
+        ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
+        launch_prune_flags(M->params, M->cap, n, opacity_threshold, keep.as<int32_t>(), st);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st);
+        ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st), "scan");
+        int32_t kept = 0;
+        std::vector<int32_t> flags(n);
+        ck(cudaMemcpyAsync(&kept, pos.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(flags.data(), keep.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        C->launched(2);
+        if (kept == n) return;
+        // stable compaction into fresh arrays of the same capacity
+        const int64_t cap = M->cap;
+        float *p = nullptr, *m = nullptr, *v = nullptr;
+        int32_t* b = nullptr;
+        int8_t* d = nullptr;
+        ck(cudaMalloc(&p, sizeof(float) * kNumParams * cap), "cudaMalloc params");
+        ck(cudaMalloc(&m, sizeof(float) * kNumParams * cap), "cudaMalloc adam m");
+        ck(cudaMalloc(&v, sizeof(float) * kNumParams * cap), "cudaMalloc adam v");
+        ck(cudaMalloc(&b, sizeof(int32_t) * cap), "cudaMalloc birth");
+        ck(cudaMalloc(&d, sizeof(int8_t) * cap), "cudaMalloc degree");
+        ck(cudaMemsetAsync(p, 0, sizeof(float) * kNumParams * cap, st), "memset");
+        ck(cudaMemsetAsync(m, 0, sizeof(float) * kNumParams * cap, st), "memset");
+        ck(cudaMemsetAsync(v, 0, sizeof(float) * kNumParams * cap, st), "memset");
+        launch_compact(M->params, p, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        launch_compact(M->m, m, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        launch_compact(M->v, v, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        launch_compact(M->birth, b, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        launch_compact(M->degree, d, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        C->launched(5);
+        ck(cudaStreamSynchronize(st), "sync");
+        M->free_all();
+        M->params = p; M->m = m; M->v = v; M->birth = b; M->degree = d;
+        std::vector<int8_t> deg;
+        deg.reserve(kept);
+        for (int i = 0; i < n; ++i)
+            if (flags[i]) deg.push_back(M->deg_host[i]);
+        M->deg_host = std::move(deg);
+        M->recompute_max_degree();
+        M->n = kept;
+        *removed = n - kept;
+    });
+}
+
 int gs_map_device_planes(gs_map* M, float** params, float** m, float** v, int64_t* cap) {
     return guard([&] {
         if (params) *params = M->params;

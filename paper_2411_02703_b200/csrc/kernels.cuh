@@ -64,6 +64,11 @@ void launch_adam(float* params, float* m, float* v, const int32_t* birth, const 
                  const unsigned long long* counters /* nullable: skip on overflow */, int max_degree,
                  cudaStream_t st);
 void launch_position_minmax(const float* params, int64_t cap, int n, float* out6, cudaStream_t st);
+void launch_prune_flags(const float* params, int64_t cap, int n, double thr, int32_t* keep, cudaStream_t st);
+void launch_compact(const float* src, float* dst, int64_t scap, int64_t dcap, int planes, int n, const int32_t* keep,
+                    const int32_t* pos, cudaStream_t st);
+void launch_compact(const int32_t* src, int32_t* dst, int n, const int32_t* keep, const int32_t* pos, cudaStream_t st);
+void launch_compact(const int8_t* src, int8_t* dst, int n, const int32_t* keep, const int32_t* pos, cudaStream_t st);
 void launch_to_hwc_double(const float* planes, int h, int w, int channels, double* out, cudaStream_t st);
 void launch_from_hwc_double(const double* hwc, int h, int w, int channels, float* planes, cudaStream_t st);
 

@@ -254,6 +254,12 @@ class GaussianMap:
     def raise_sh_degree(self, d: int):
         _check(lib().gs_map_raise_sh_degree(_vp(self.h), d))
 
+    def prune(self, opacity_threshold: float) -> int:
+        """GaussianMap::prune (gaussian_map.cpp:56-73): removed count; state stays aligned."""
+        removed = C.c_int64()
+        _check(lib().gs_map_prune(_vp(self.h), C.c_double(opacity_threshold), C.byref(removed)))
+        return removed.value
+
     def max_active_degree(self) -> int:
         d = C.c_int()
         _check(lib().gs_map_max_active_degree(_vp(self.h), C.byref(d)))

@@ -247,3 +247,60 @@ def test_visible_capacity_overflow_reruns_step():
     fresh = G().render(G().GaussianMap(ctx2, round32(g)), gpu_pose(O.pose()), gpu_cam(cam))
     assert fr.stats().n_visible == fresh.stats().n_visible > 15000
     np.testing.assert_array_equal(fr.color, fresh.color)
+
+
+def test_prune_keeps_state_aligned():  # test_mapper.cpp:298-311
+    from oracle import pyoracle as O
+    g = O.empty_gaussians(10)
+    g["p"][:, 0] = np.arange(10.0)
+    g["p"][:, 2] = 3.0
+    g["p"][:, 3] = 1.0
+    g["p"][:, 7:10] = np.log(0.3)
+    g["p"][:, 10] = 0.0  # logit(0.5)
+    m = G().GaussianMap(None, g)
+    assert m.prune(0.005) == 0
+    g["p"][4, 10] = np.log(0.001 / 0.999)
+    m = G().GaussianMap(None, round32(g))
+    assert m.prune(0.005) == 1
+    assert len(m) == 9
+    p = m.gaussians["p"]
+    assert p[4, 0] == 5.0  # compacted over the hole
+    mm, vv, steps = m.adam_state()
+    assert mm.shape[0] == vv.shape[0] == steps.shape[0] == 9
+    with pytest.raises(ValueError):
+        m.prune(0.0)
+    with pytest.raises(ValueError):
+        m.prune(1.0)
+
+
+def test_prune_matches_oracle_after_training():
+    """Train a few steps (non-trivial Adam state), prune a third of the map on both, then the
+    parameters, optimizer state and a render agree; training continues in lockstep."""
+    from oracle import pyoracle as O
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    g = random_scene(31, 60, cam, O.pose(), 1.0, 2.0)
+    g["p"][::3, 10] = np.log(0.001 / 0.999)  # a third below the threshold
+    om, gm = pair(g)
+    gt = O.render(O.OracleMap(round32(random_scene(5, 40, cam, O.pose()))), O.pose(), cam)
+    color = f32(gt.color)
+    okf = O.Keyframe(O.pose(), color, np.zeros((48, 64)), 20, 0)
+    gkf = G().Keyframe(gpu_pose(O.pose()), color, np.zeros((48, 64)), 20, 0)
+    ocfg = O.make_cfg(0.2, 0.0, 0)
+    gcfg = G().TrainConfig.make(0.2, 0.0, 0)
+    for _ in range(3):
+        O.train_keyframe_step(om, okf, ocfg, cam)
+        G().train_keyframe_step(gm, gkf, gcfg, gpu_cam(cam))
+    ro, rg = om.prune(0.005), gm.prune(0.005)
+    assert ro == rg == 20
+    assert len(om) == len(gm) == 40
+    lr = np.array([1.6e-4 * om.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+    assert np.all(np.abs(gm.gaussians["p"] - om.gaussians["p"]) <= 3 * 2 * lr + 1e-6)
+    om_m, om_v, om_s = om.adam_state()
+    gm_m, gm_v, gm_s = gm.adam_state()
+    np.testing.assert_array_equal(om_s, gm_s)
+    o_out = O.render(om, O.pose(), cam)
+    g_out = G().render(gm, gpu_pose(O.pose()), gpu_cam(cam))
+    assert np.abs(g_out.color - o_out.color).max() < 2e-2  # params differ by a few Adam steps
+    r_o = O.train_keyframe_step(om, okf, ocfg, cam)
+    r_g = G().train_keyframe_step(gm, gkf, gcfg, gpu_cam(cam))
+    assert r_g["loss"] == pytest.approx(r_o["loss"], rel=5e-3)
