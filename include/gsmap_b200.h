@@ -122,6 +122,11 @@ int gs_map_set_scene_extent(gs_map* map, double extent);
 int gs_map_global_step(const gs_map* map, int64_t* step);
 int gs_map_set_global_step(gs_map* map, int64_t step);
 int gs_map_raise_sh_degree(gs_map* map, int degree);   /* gaussian_map.cpp:75-79 */
+/* project_sparse_depth (io/sequence.hpp:70, sequence.cpp:246-259): host points [n][stride]
+   (x, y, z world first, fp64; stride 6 = the reference's ColoredPoint xyz+rgb) -> host depth
+   [h][w] fp64, the minimum camera z per pixel, 0 where no point lands. */
+int gs_project_sparse_depth(gs_context* ctx, const double* points, int64_t n, int32_t stride, const gs_pose* pose,
+                            const gs_camera* cam, double* depth);
 /* GaussianMap::prune (gaussian_map.hpp:79, gaussian_map.cpp:56-73): drop every Gaussian with
    sigmoid(opacity_logit) < threshold, compacting parameters and optimizer state in order;
    threshold outside (0, 1) -> GS_EINVAL. *removed = the number dropped. */

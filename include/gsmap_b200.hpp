@@ -258,6 +258,27 @@ inline std::shared_ptr<gs_grads> make_grads(Context& ctx) {
     return std::shared_ptr<gs_grads>(g, [](gs_grads* p) { gs_grads_destroy(p); });
 }
 
+// io/sequence.hpp:70 (sequence.cpp:246-259): ColoredPoint = position xyz + colour rgb (6 doubles)
+struct ColoredPoint {
+    Vec3 position{0, 0, 0};
+    Vec3 color{0, 0, 0};
+};
+
+inline ImageD project_sparse_depth(Context& ctx, const std::vector<ColoredPoint>& points, const Pose& pose,
+                                   const CameraModel& cam) {
+    std::vector<double> flat(points.size() * 6);
+    for (size_t i = 0; i < points.size(); ++i) {
+        for (int k = 0; k < 3; ++k) flat[6 * i + k] = points[i].position[k];
+        for (int k = 0; k < 3; ++k) flat[6 * i + 3 + k] = points[i].color[k];
+    }
+    ImageD depth(cam.height, cam.width, 1, 0.0);
+    const gs_pose p = pose.p();
+    const gs_camera c = cam.c();
+    check(gs_project_sparse_depth(ctx.get(), flat.data(), static_cast<int64_t>(points.size()), 6, &p, &c,
+                                  depth.data.data()));
+    return depth;
+}
+
 // rasterizer.hpp:69-70
 inline RenderOutput render(const GaussianMap& map, const Pose& pose, const CameraModel& cam, ThreadPool* = nullptr) {
     RenderOutput out{make_frame(map.context()), cam};

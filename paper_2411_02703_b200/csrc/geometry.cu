@@ -632,6 +632,43 @@ __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     }
 }
 
+// project_sparse_depth (sequence.cpp:246-259): LiDAR points -> per-pixel minimum camera z. The
+// camera transform is K1's exact fp64 sequence; the pixel is lround(f x / z + c); the min rule is
+// an atomicMin on the bits of the (positive) fp64 depths, so the result is order independent.
+__global__ void sparse_depth_kernel(const double* __restrict__ pts, int stride, int64_t n, ViewParams v,
+                                    unsigned long long* __restrict__ depth_bits) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* q = pts + k * stride;
+    D3 pc = quat_rotate(v.qw, v.qx, v.qy, v.qz, D3{q[0], q[1], q[2]});
+    pc = {pc.x + v.tx, pc.y + v.ty, pc.z + v.tz};
+    if (pc.z <= kNearClip) return;
+    const long long px = llround(v.fx * pc.x / pc.z + v.cx);
+    const long long py = llround(v.fy * pc.y / pc.z + v.cy);
+    if (px < 0 || px >= v.width || py < 0 || py >= v.height) return;
+    atomicMin(depth_bits + py * v.width + px, static_cast<unsigned long long>(__double_as_longlong(pc.z)));
+}
+
+__global__ void sparse_depth_finish_kernel(unsigned long long* __restrict__ bits, int P) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P && bits[i] == 0x7ff0000000000000ull) bits[i] = 0ull;  // no point: 0.0 (the reference's empty)
+}
+
+__global__ void fill_u64_kernel(unsigned long long* __restrict__ out, int P, unsigned long long val) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) out[i] = val;
+}
+
+void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,
+                         cudaStream_t st) {
+    const int P = v.width * v.height;
+    auto* bits = reinterpret_cast<unsigned long long*>(depth);
+    fill_u64_kernel<<<div_up(P, 256), 256, 0, st>>>(bits, P, 0x7ff0000000000000ull);  // +inf
+    if (n > 0)
+        sparse_depth_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pts, stride, n, v, bits);
+    sparse_depth_finish_kernel<<<div_up(P, 256), 256, 0, st>>>(bits, P);
+}
+
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
                            const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,

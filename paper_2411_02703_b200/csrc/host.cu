@@ -1070,6 +1070,30 @@ int gs_map_raise_sh_degree(gs_map* M, int degree) {  // gaussian_map.cpp:75-79
 
 int gs_map_max_active_degree(gs_map* M, int* degree) { return guard([&] { *degree = M->max_degree; }); }
 
+int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int32_t stride, const gs_pose* pose,
+                            const gs_camera* cam, double* depth) {  // sequence.cpp:246-259
+    return guard([&] {
+        validate_camera(*cam);
+        if (n < 0 || stride < 3) fail(GS_EINVAL, "project_sparse_depth: bad point array");
+        C->use();
+        cudaStream_t st = C->stream;
+        const ViewParams v = make_view(*pose, *cam);
+        const size_t P = static_cast<size_t>(cam->width) * cam->height;
+        DevBuf pts, out;
+        pts.ensure(sizeof(double) * static_cast<size_t>(std::max<int64_t>(n, 1)) * stride);
+        out.ensure(sizeof(double) * P);
+        if (n > 0)
+            ck(cudaMemcpyAsync(pts.p, points, sizeof(double) * static_cast<size_t>(n) * stride, cudaMemcpyHostToDevice,
+                               st), "h2d points");
+        launch_sparse_depth(pts.as<double>(), stride, n, v, out.as<double>(), st);
+        C->launched(3);
+        ck(cudaMemcpyAsync(depth, out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "d2h depth");
+        ck(cudaStreamSynchronize(st), "sync");
+        pts.release();
+        out.release();
+    });
+}
+
 int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // gaussian_map.cpp:56-73
     return guard([&] {
         if (opacity_threshold <= 0.0 || opacity_threshold >= 1.0)

@@ -19,6 +19,10 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
                            double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
                            int max_ranks, float* grads, int64_t gcap, bool accumulate, cudaStream_t st);
 
+// project_sparse_depth: points [n][stride] (x, y, z first, fp64, device) -> depth [h][w] fp64
+void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,
+                         cudaStream_t st);
+
 // raster.cu
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
                      unsigned long long* counters, int max_n, cudaStream_t st);

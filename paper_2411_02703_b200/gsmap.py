@@ -408,6 +408,18 @@ class RenderOutput:
         return c.value, d.value, v.value
 
 
+def project_sparse_depth(points: np.ndarray, pose: Pose, cam: Camera, ctx: Context | None = None) -> np.ndarray:
+    """sequence.cpp:246-259 on the device: points [n][>=3] (world xyz first) -> [h][w] min camera z."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, np.float64)
+    if pts.ndim != 2 or pts.shape[1] < 3:
+        raise ValueError("project_sparse_depth: points must be [n][>=3]")
+    out = np.zeros((cam.height, cam.width))
+    _check(lib().gs_project_sparse_depth(_vp(ctx.h), _p(pts), C.c_int64(len(pts)), C.c_int32(pts.shape[1]),
+                                         C.byref(pose), C.byref(cam), _p(out)))
+    return out
+
+
 def render(m: GaussianMap, pose: Pose, cam: Camera, out: RenderOutput | None = None, pool=None) -> RenderOutput:
     """rasterizer.hpp:69-70. ``pool`` (the reference's ThreadPool*) is accepted and ignored."""
     out = out or RenderOutput(m.ctx)

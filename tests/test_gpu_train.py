@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import pyoracle as O
-from tests._common import gpu_cam, gpu_pose, pair, random_scene, rel_err, round32
+from tests._common import gpu_cam, gpu_pose, pair, random_pose, random_scene, rel_err, round32
 
 pytestmark = pytest.mark.gpu
 
@@ -304,3 +304,38 @@ def test_prune_matches_oracle_after_training():
     r_o = O.train_keyframe_step(om, okf, ocfg, cam)
     r_g = G().train_keyframe_step(gm, gkf, gcfg, gpu_cam(cam))
     assert r_g["loss"] == pytest.approx(r_o["loss"], rel=5e-3)
+
+
+def test_project_sparse_depth_kats_and_oracle():  # test_io.cpp:106-147
+    from oracle import pyoracle as O
+    cam = O.camera(100, 100, 32, 32, 64, 64)
+    p = np.array([[0.0, 0.0, 2.0, 0.5, 0.5, 0.5]])
+    d1 = G().project_sparse_depth(p, gpu_pose(O.pose()), gpu_cam(cam))
+    assert d1[32, 32] == 2.0 and (d1 > 0).sum() == 1
+    far = p.copy(); far[0, 2] = 3.0
+    d2 = G().project_sparse_depth(np.concatenate([far, p]), gpu_pose(O.pose()), gpu_cam(cam))
+    assert d2[32, 32] == 2.0  # min depth wins
+    gen = np.random.default_rng(8)
+    cloud = np.zeros((500, 6))
+    cloud[:, :3] = gen.uniform(-1.5, 1.5, (500, 3)); cloud[:, 2] += 2.0
+    pose = random_pose(gen, 0.3)
+    dg = G().project_sparse_depth(cloud, gpu_pose(pose), gpu_cam(cam))
+    do = O.project_sparse_depth(cloud, pose, cam)
+    np.testing.assert_array_equal(dg, do)  # bit-exact (fp64 transform in the oracle's order)
+    assert (dg > 0).sum() <= len(cloud)
+    gen.shuffle(cloud)
+    np.testing.assert_array_equal(G().project_sparse_depth(cloud, gpu_pose(pose), gpu_cam(cam)), dg)
+
+
+def test_project_sparse_depth_matches_oracle_on_scene_clouds():
+    from fixtures import pyfixture as F
+    from oracle import pyoracle as O
+    scene = F.Scene(n_gaussians=20000, width=320, height=256, n_frames=3, seed=1)
+    cam = O.camera(*scene.camera)
+    for f in range(3):
+        q = scene.poses[f]
+        pose = O.pose(q[0], q[1], q[2], q[3], t=q[4:7])
+        cloud = scene.cloud(f)
+        dg = G().project_sparse_depth(cloud, gpu_pose(pose), gpu_cam(cam))
+        np.testing.assert_array_equal(dg, O.project_sparse_depth(cloud, pose, cam))
+        np.testing.assert_array_equal(dg, scene.sparse_depth(f))
