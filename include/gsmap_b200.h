@@ -127,6 +127,11 @@ int gs_map_raise_sh_degree(gs_map* map, int degree);   /* gaussian_map.cpp:75-79
    [h][w] fp64, the minimum camera z per pixel, 0 where no point lands. */
 int gs_project_sparse_depth(gs_context* ctx, const double* points, int64_t n, int32_t stride, const gs_pose* pose,
                             const gs_camera* cam, double* depth);
+/* init_gaussians_from_points (map/mapper.hpp, mapper.cpp:43-61) on the device: host points
+   [n][6] (x y z world, r g b) -> n new Gaussians appended to the map (isotropic scale = mean
+   distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;
+   degree 0; fresh optimizer state). *added = n. */
+int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64_t* added);
 /* GaussianMap::prune (gaussian_map.hpp:79, gaussian_map.cpp:56-73): drop every Gaussian with
    sigmoid(opacity_logit) < threshold, compacting parameters and optimizer state in order;
    threshold outside (0, 1) -> GS_EINVAL. *removed = the number dropped. */

@@ -279,6 +279,18 @@ inline ImageD project_sparse_depth(Context& ctx, const std::vector<ColoredPoint>
     return depth;
 }
 
+// mapper.cpp:43-61 (device grid 3-NN); returns the number of Gaussians appended
+inline std::size_t init_gaussians_from_points(GaussianMap& map, const std::vector<ColoredPoint>& points) {
+    std::vector<double> flat(points.size() * 6);
+    for (size_t i = 0; i < points.size(); ++i) {
+        for (int k = 0; k < 3; ++k) flat[6 * i + k] = points[i].position[k];
+        for (int k = 0; k < 3; ++k) flat[6 * i + 3 + k] = points[i].color[k];
+    }
+    int64_t added = 0;
+    check(gs_map_init_from_points(map.get(), flat.data(), static_cast<int64_t>(points.size()), &added));
+    return static_cast<std::size_t>(added);
+}
+
 // rasterizer.hpp:69-70
 inline RenderOutput render(const GaussianMap& map, const Pose& pose, const CameraModel& cam, ThreadPool* = nullptr) {
     RenderOutput out{make_frame(map.context()), cam};

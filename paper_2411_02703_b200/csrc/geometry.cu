@@ -669,6 +669,176 @@ void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewPar
     sparse_depth_finish_kernel<<<div_up(P, 256), 256, 0, st>>>(bits, P);
 }
 
+// ------------------------------------------------------------------------------------------
+// init_gaussians_from_points (mapper.cpp:19-61) on the device. The isotropic scale is the mean
+// distance to the k = min(3, n - 1) nearest other points (floored at 1e-4 m; 0.1 m with no
+// neighbour), found exactly by expanding Chebyshev shells over a uniform grid whose occupied
+// cells sit in an open-addressing hash table. Distances use the oracle's fp64 order
+// ((dx^2 + dy^2) + dz^2, this file is --fmad=false); the k distances are summed in ascending
+// order (the reference sums its heap's array order: at most 1 fp64 ulp apart).
+namespace {
+__device__ __forceinline__ uint64_t knn_pack(int64_t x, int64_t y, int64_t z) {
+    return (static_cast<uint64_t>(x & 0x1fffff) << 42) | (static_cast<uint64_t>(y & 0x1fffff) << 21) |
+           static_cast<uint64_t>(z & 0x1fffff);
+}
+__device__ __forceinline__ uint32_t knn_hash(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return static_cast<uint32_t>(k);
+}
+constexpr uint64_t kKnnEmpty = ~0ull;
+}  // namespace
+
+__global__ void knn_keys_kernel(const double* __restrict__ pts, int64_t n, KnnGrid g, uint64_t* __restrict__ keys,
+                                int32_t* __restrict__ idx) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* q = pts + 6 * i;
+    const int64_t x = static_cast<int64_t>(floor((q[0] - g.lo[0]) / g.cell));
+    const int64_t y = static_cast<int64_t>(floor((q[1] - g.lo[1]) / g.cell));
+    const int64_t z = static_cast<int64_t>(floor((q[2] - g.lo[2]) / g.cell));
+    keys[i] = knn_pack(x, y, z);
+    idx[i] = static_cast<int32_t>(i);
+}
+
+// one thread per run of equal keys in the sorted order: insert (key -> [start, end))
+__global__ void knn_table_kernel(const uint64_t* __restrict__ skeys, int64_t n, uint64_t* __restrict__ hkeys,
+                                 int2* __restrict__ hvals, uint32_t hmask) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n || (i > 0 && skeys[i - 1] == skeys[i])) return;
+    const uint64_t k = skeys[i];
+    int64_t e = i + 1;
+    while (e < n && skeys[e] == k) ++e;
+    uint32_t h = knn_hash(k) & hmask;
+    while (true) {
+        const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(hkeys + h), kKnnEmpty, k);
+        if (prev == kKnnEmpty || prev == k) break;
+        h = (h + 1) & hmask;
+    }
+    hvals[h] = make_int2(static_cast<int>(i), static_cast<int>(e));
+}
+
+__device__ __forceinline__ int2 knn_lookup(const uint64_t* __restrict__ hkeys, const int2* __restrict__ hvals,
+                                           uint32_t hmask, uint64_t k) {
+    uint32_t h = knn_hash(k) & hmask;
+    while (true) {
+        const uint64_t c = hkeys[h];
+        if (c == k) return hvals[h];
+        if (c == kKnnEmpty) return make_int2(0, 0);
+        h = (h + 1) & hmask;
+    }
+}
+
+// writes the new Gaussians (fp32 SoA) at map index first + i (gaussian_from_point, mapper.cpp:47-58)
+__global__ void knn_init_kernel(const double* __restrict__ pts, int64_t n, int k, KnnGrid g,
+                                const uint64_t* __restrict__ hkeys, const int2* __restrict__ hvals, uint32_t hmask,
+                                const int32_t* __restrict__ sidx, float* __restrict__ params, int64_t cap,
+                                int64_t first) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* q = pts + 6 * i;
+    const double px = q[0], py = q[1], pz = q[2];
+    const int64_t cx = static_cast<int64_t>(floor((px - g.lo[0]) / g.cell));
+    const int64_t cy = static_cast<int64_t>(floor((py - g.lo[1]) / g.cell));
+    const int64_t cz = static_cast<int64_t>(floor((pz - g.lo[2]) / g.cell));
+    double best[3] = {1e300, 1e300, 1e300};  // ascending
+    int found = 0;
+    for (int64_t r = 0; k > 0 && r <= g.max_ring; ++r) {
+        for (int64_t dx = -r; dx <= r; ++dx)
+            for (int64_t dy = -r; dy <= r; ++dy)
+                for (int64_t dz = -r; dz <= r; ++dz) {
+                    if (max(max(llabs(dx), llabs(dy)), llabs(dz)) != r) continue;
+                    const int2 range = knn_lookup(hkeys, hvals, hmask, knn_pack(cx + dx, cy + dy, cz + dz));
+                    for (int qq = range.x; qq < range.y; ++qq) {
+                        const int64_t j = sidx[qq];
+                        if (j == i) continue;
+                        const double* o = pts + 6 * j;
+                        const double ddx = o[0] - px, ddy = o[1] - py, ddz = o[2] - pz;
+                        const double d2 = (ddx * ddx + ddy * ddy) + ddz * ddz;
+                        int slot;
+                        if (found < k) slot = found++;
+                        else if (d2 < best[k - 1]) slot = k - 1;
+                        else continue;
+                        while (slot > 0 && best[slot - 1] > d2) {
+                            best[slot] = best[slot - 1];
+                            --slot;
+                        }
+                        best[slot] = d2;
+                    }
+                }
+        if (found == k && sqrt(best[k - 1]) <= static_cast<double>(r) * g.cell) break;
+    }
+    double sc = 0.1;  // kDefaultInitScale
+    if (k > 0 && found > 0) {
+        double sum = 0.0;
+        for (int j = 0; j < found; ++j) sum += sqrt(best[j]);
+        sc = fmax(sum / found, 1e-4);  // kMinInitScale
+    }
+    const int64_t o = first + i;
+    for (int pl = 0; pl < kNumParams; ++pl) params[pl * cap + o] = 0.f;
+    params[P_POS * cap + o] = static_cast<float>(px);
+    params[(P_POS + 1) * cap + o] = static_cast<float>(py);
+    params[(P_POS + 2) * cap + o] = static_cast<float>(pz);
+    params[P_ROT * cap + o] = 1.f;
+    const float ls = static_cast<float>(log(sc));
+    for (int a = 0; a < 3; ++a) params[(P_LS + a) * cap + o] = ls;
+    params[P_OP * cap + o] = static_cast<float>(log(0.1 / (1.0 - 0.1)));  // logit(kInitOpacity)
+    const double kShC0 = 0.28209479177387814;
+    for (int c = 0; c < 3; ++c) params[(P_SH + c) * cap + o] = static_cast<float>((q[3 + c] - 0.5) / kShC0);
+}
+
+__global__ void knn_bbox_kernel(const double* __restrict__ pts, int64_t n, unsigned long long* __restrict__ out6) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int a = 0; a < 3; ++a) {
+        const long long b = __double_as_longlong(pts[6 * i + a]);
+        // order-preserving map of doubles onto unsigned integers
+        const unsigned long long u = b < 0 ? ~static_cast<unsigned long long>(b)
+                                           : static_cast<unsigned long long>(b) | 0x8000000000000000ull;
+        atomicMin(out6 + a, u);
+        atomicMax(out6 + 3 + a, u);
+    }
+}
+
+__global__ void knn_count_runs_kernel(const uint64_t* __restrict__ skeys, int64_t n,
+                                      unsigned long long* __restrict__ runs) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool start = i < n && (i == 0 || skeys[i - 1] != skeys[i]);
+    const unsigned m = __ballot_sync(0xffffffffu, start);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(runs, static_cast<unsigned long long>(__popc(m)));
+}
+
+void launch_knn_count_runs(const uint64_t* skeys, int64_t n, unsigned long long* runs, cudaStream_t st) {
+    cudaMemsetAsync(runs, 0, sizeof(unsigned long long), st);
+    if (n > 0) knn_count_runs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(skeys, n, runs);
+}
+
+void launch_knn_bbox(const double* pts, int64_t n, unsigned long long* out6, cudaStream_t st) {
+    cudaMemsetAsync(out6, 0xff, 3 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(out6 + 3, 0, 3 * sizeof(unsigned long long), st);
+    if (n > 0) knn_bbox_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pts, n, out6);
+}
+
+void launch_knn_keys(const double* pts, int64_t n, const KnnGrid& g, uint64_t* keys, int32_t* idx, cudaStream_t st) {
+    if (n > 0) knn_keys_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pts, n, g, keys, idx);
+}
+
+void launch_knn_table(const uint64_t* skeys, int64_t n, uint64_t* hkeys, int2* hvals, uint32_t hmask,
+                      cudaStream_t st) {
+    cudaMemsetAsync(hkeys, 0xff, sizeof(uint64_t) * (static_cast<size_t>(hmask) + 1), st);
+    if (n > 0) knn_table_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(skeys, n, hkeys, hvals, hmask);
+}
+
+void launch_knn_init(const double* pts, int64_t n, int k, const KnnGrid& g, const uint64_t* hkeys, const int2* hvals,
+                     uint32_t hmask, const int32_t* sidx, float* params, int64_t cap, int64_t first, cudaStream_t st) {
+    if (n > 0)
+        knn_init_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(pts, n, k, g, hkeys, hvals, hmask,
+                                                                                 sidx, params, cap, first);
+}
+
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
                            const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,

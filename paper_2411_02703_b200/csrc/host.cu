@@ -1094,6 +1094,90 @@ int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int3
     });
 }
 
+int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
+    return guard([&] {
+        *added = 0;
+        if (n <= 0) return;  // points.empty() -> 0
+        if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
+        M->ctx->use();
+        gs_context* C = M->ctx;
+        cudaStream_t st = C->stream;
+        DevBuf pts, keys, keys2, idx, idx2, bb, hk, hv;
+        pts.ensure(sizeof(double) * 6 * n);
+        keys.ensure(sizeof(uint64_t) * n);
+        keys2.ensure(sizeof(uint64_t) * n);
+        idx.ensure(sizeof(int32_t) * n);
+        idx2.ensure(sizeof(int32_t) * n);
+        bb.ensure(sizeof(unsigned long long) * 8);
+        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st), "h2d points");
+        launch_knn_bbox(pts.as<double>(), n, bb.as<unsigned long long>(), st);
+        unsigned long long enc[6];
+        ck(cudaMemcpyAsync(enc, bb.p, sizeof(enc), cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        double lo[3], hi[3];
+        auto dec = [](unsigned long long u) {
+            const unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+            double d;
+            std::memcpy(&d, &b, sizeof d);
+            return d;
+        };
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = dec(enc[a]);
+            hi[a] = dec(enc[3 + a]);
+        }
+        const double ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+        const double vol = std::max(ext[0], 1e-9) * std::max(ext[1], 1e-9) * std::max(ext[2], 1e-9);
+        KnnGrid g{};
+        for (int a = 0; a < 3; ++a) g.lo[a] = lo[a];
+        g.cell = std::cbrt(vol / static_cast<double>(n)) * 1.5;
+        size_t tb = 0;
+        auto sort_keys = [&]() {
+            launch_knn_keys(pts.as<double>(), n, g, keys.as<uint64_t>(), idx.as<int32_t>(), st);
+            tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(), idx.as<int32_t>(),
+                                            idx2.as<int32_t>(), static_cast<int>(n), 0, 64, st);
+            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                               idx.as<int32_t>(), idx2.as<int32_t>(), static_cast<int>(n), 0, 64, st),
+               "knn sort");
+        };
+        // adapt the cell so occupied cells hold ~4 points (fixtures/synthetic.cpp init_from_points)
+        for (int it = 0; it < 2; ++it) {
+            sort_keys();
+            launch_knn_count_runs(keys2.as<uint64_t>(), n, bb.as<unsigned long long>() + 6, st);
+            unsigned long long runs = 1;
+            ck(cudaMemcpyAsync(&runs, bb.as<unsigned long long>() + 6, sizeof(runs), cudaMemcpyDeviceToHost, st), "d2h");
+            ck(cudaStreamSynchronize(st), "sync");
+            g.cell *= std::cbrt(4.0 / (static_cast<double>(n) / static_cast<double>(std::max(runs, 1ull))));
+        }
+        sort_keys();
+        g.max_ring = std::max({static_cast<int64_t>(ext[0] / g.cell) + 1, static_cast<int64_t>(ext[1] / g.cell) + 1,
+                               static_cast<int64_t>(ext[2] / g.cell) + 1});
+        uint32_t hsize = 1024;
+        while (hsize < 2 * static_cast<uint64_t>(n)) hsize <<= 1;
+        hk.ensure(sizeof(uint64_t) * hsize);
+        hv.ensure(sizeof(int2) * hsize);
+        launch_knn_table(keys2.as<uint64_t>(), n, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, st);
+        // new Gaussians at [first, first + n): fresh optimizer state, degree 0 (gaussian_map.cpp:33)
+        const int64_t first = M->n;
+        map_reserve(M, first + n);
+        ck(cudaMemset2DAsync(M->m + first, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
+        ck(cudaMemset2DAsync(M->v + first, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
+        ck(cudaMemsetAsync(M->degree + first, 0, n, st), "memset");
+        const std::vector<int32_t> birth(n, static_cast<int32_t>(M->adam_count));
+        ck(cudaMemcpyAsync(M->birth + first, birth.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
+        const int k = static_cast<int>(std::min<int64_t>(3, n - 1));
+        launch_knn_init(pts.as<double>(), n, k, g, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, idx2.as<int32_t>(),
+                        M->params, M->cap, first, st);
+        C->launched(8);
+        ck(cudaStreamSynchronize(st), "sync");
+        M->deg_host.resize(first + n, 0);
+        M->n = first + n;
+        M->recompute_max_degree();
+        refresh_extent(M);
+        *added = n;
+    });
+}
+
 int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // gaussian_map.cpp:56-73
     return guard([&] {
         if (opacity_threshold <= 0.0 || opacity_threshold >= 1.0)

@@ -23,6 +23,22 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
 void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,
                          cudaStream_t st);
 
+// init_gaussians_from_points: uniform grid (lo, cell), occupied cells in a hash table
+struct KnnGrid {
+    double lo[3];
+    double cell;
+    int64_t max_ring;
+};
+void launch_knn_bbox(const double* pts6, int64_t n, unsigned long long* out6 /* ordered min xyz, max xyz */,
+                     cudaStream_t st);
+void launch_knn_count_runs(const uint64_t* sorted_keys, int64_t n, unsigned long long* runs, cudaStream_t st);
+void launch_knn_keys(const double* pts6, int64_t n, const KnnGrid& g, uint64_t* keys, int32_t* idx, cudaStream_t st);
+void launch_knn_table(const uint64_t* sorted_keys, int64_t n, uint64_t* hkeys, int2* hvals, uint32_t hmask,
+                      cudaStream_t st);
+void launch_knn_init(const double* pts6, int64_t n, int k, const KnnGrid& g, const uint64_t* hkeys, const int2* hvals,
+                     uint32_t hmask, const int32_t* sorted_idx, float* params, int64_t cap, int64_t first,
+                     cudaStream_t st);
+
 // raster.cu
 void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
                      unsigned long long* counters, int max_n, cudaStream_t st);

@@ -254,6 +254,15 @@ class GaussianMap:
     def raise_sh_degree(self, d: int):
         _check(lib().gs_map_raise_sh_degree(_vp(self.h), d))
 
+    def init_from_points(self, points6: np.ndarray) -> int:
+        """init_gaussians_from_points (mapper.cpp:43-61) on the device; returns the number added."""
+        pts = np.ascontiguousarray(points6, np.float64)
+        if pts.ndim != 2 or pts.shape[1] != 6:
+            raise ValueError("init_from_points: points must be [n][6]")
+        added = C.c_int64()
+        _check(lib().gs_map_init_from_points(_vp(self.h), _p(pts), C.c_int64(len(pts)), C.byref(added)))
+        return added.value
+
     def prune(self, opacity_threshold: float) -> int:
         """GaussianMap::prune (gaussian_map.cpp:56-73): removed count; state stays aligned."""
         removed = C.c_int64()

@@ -339,3 +339,50 @@ def test_project_sparse_depth_matches_oracle_on_scene_clouds():
         dg = G().project_sparse_depth(cloud, gpu_pose(pose), gpu_cam(cam))
         np.testing.assert_array_equal(dg, O.project_sparse_depth(cloud, pose, cam))
         np.testing.assert_array_equal(dg, scene.sparse_depth(f))
+
+
+def _init_close(gp, op):
+    """fp32 parameters equal; the log-scale may differ by 1 fp32 ulp in rare cases (the reference
+    sums its 3 distances in heap order, the device in ascending order: <= 1 fp64 ulp apart)."""
+    a, b = gp.astype(np.float32), op.astype(np.float32)
+    other = np.r_[0:7, 10:59]
+    np.testing.assert_array_equal(a[:, other], b[:, other])
+    ulp = np.abs(a[:, 7:10].view(np.int32).astype(np.int64) - b[:, 7:10].view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1 and (ulp == 0).mean() >= 0.999
+
+
+@pytest.mark.parametrize("n,spread", [(1, 1.0), (2, 1.0), (7, 0.01), (3000, 3.0)])
+def test_init_from_points_matches_oracle(n, spread):  # mapper.cpp:19-61, test_mapper.cpp init KATs
+    from oracle import pyoracle as O
+    gen = np.random.default_rng(n)
+    pts = np.zeros((n, 6))
+    pts[:, :3] = gen.uniform(-spread, spread, (n, 3)) + np.array([0.0, 0.0, 4.0])
+    pts[:, 3:] = gen.uniform(0, 1, (n, 3))
+    if n >= 7:
+        pts[1, :3] = pts[0, :3]  # a duplicate point: distance 0 -> floored scale
+    om = O.OracleMap()
+    assert om.init_from_points(pts) == n
+    gm = G().GaussianMap(None)
+    assert gm.init_from_points(pts) == n
+    assert len(gm) == n
+    _init_close(gm.gaussians["p"], om.gaussians["p"])
+    assert np.all(gm.gaussians["degree"] == 0)
+    # the device keeps fp32 positions: its extent is the oracle's on the fp32-rounded map
+    assert gm.scene_extent == pytest.approx(O.OracleMap(round32(om.gaussians)).scene_extent, rel=1e-12)
+    m, v, steps = gm.adam_state()
+    assert np.all(m == 0) and np.all(v == 0) and np.all(steps == 0)
+
+
+def test_init_from_points_appends_and_matches_fixture_grid():
+    """On a scene's LiDAR cloud: the fixture's CPU grid 3-NN (same ascending sum) agrees exactly,
+    and appending to a non-empty map keeps the existing Gaussians and optimizer state."""
+    from fixtures import pyfixture as F
+    scene = F.Scene(n_gaussians=20000, width=320, height=256, n_frames=2, seed=1)
+    cloud = scene.cloud(0)
+    ref = F.init_from_points(cloud, threads=1)
+    gm = G().GaussianMap(None, round32(ref[:10]))
+    before = gm.gaussians["p"].copy()
+    assert gm.init_from_points(cloud) == len(cloud)
+    p = gm.gaussians["p"]
+    np.testing.assert_array_equal(p[:10], before)
+    np.testing.assert_array_equal(p[10:].astype(np.float32), ref["p"].astype(np.float32))
