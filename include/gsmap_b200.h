@@ -127,6 +127,9 @@ int gs_map_raise_sh_degree(gs_map* map, int degree);   /* gaussian_map.cpp:75-79
    [h][w] fp64, the minimum camera z per pixel, 0 where no point lands. */
 int gs_project_sparse_depth(gs_context* ctx, const double* points, int64_t n, int32_t stride, const gs_pose* pose,
                             const gs_camera* cam, double* depth);
+/* maybe_upgrade_sh (mapper.hpp:78-80, mapper.cpp:240-246): raise every Gaussian's SH degree to
+   min(3, global_step / sh_interval) (sh_interval <= 0: unchanged); *degree = the result */
+int gs_maybe_upgrade_sh(gs_map* map, int32_t sh_interval, int32_t* degree);
 /* init_gaussians_from_points (map/mapper.hpp, mapper.cpp:43-61) on the device: host points
    [n][6] (x y z world, r g b) -> n new Gaussians appended to the map (isotropic scale = mean
    distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;

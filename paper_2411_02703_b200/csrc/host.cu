@@ -1094,6 +1094,30 @@ int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int3
     });
 }
 
+int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // mapper.cpp:240-246
+    return guard([&] {
+        if (sh_interval <= 0) {
+            *degree = M->max_degree;
+            return;
+        }
+        const int target = static_cast<int>(std::min<int64_t>(3, M->global_step / sh_interval));
+        const int d = std::clamp(target, 0, 3);
+        bool change = false;
+        for (auto& x : M->deg_host)
+            if (x < d) {
+                x = static_cast<int8_t>(d);
+                change = true;
+            }
+        if (change && M->n > 0) {
+            M->ctx->use();
+            ck(cudaMemcpyAsync(M->degree, M->deg_host.data(), M->n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
+            ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+        }
+        M->recompute_max_degree();
+        *degree = target;
+    });
+}
+
 int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
     return guard([&] {
         *added = 0;

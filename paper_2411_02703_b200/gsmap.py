@@ -254,6 +254,12 @@ class GaussianMap:
     def raise_sh_degree(self, d: int):
         _check(lib().gs_map_raise_sh_degree(_vp(self.h), d))
 
+    def maybe_upgrade_sh(self, sh_interval: int) -> int:
+        """maybe_upgrade_sh (mapper.cpp:240-246): degree = min(3, global_step / sh_interval)."""
+        d = C.c_int32()
+        _check(lib().gs_maybe_upgrade_sh(_vp(self.h), C.c_int32(sh_interval), C.byref(d)))
+        return d.value
+
     def init_from_points(self, points6: np.ndarray) -> int:
         """init_gaussians_from_points (mapper.cpp:43-61) on the device; returns the number added."""
         pts = np.ascontiguousarray(points6, np.float64)

@@ -386,3 +386,18 @@ def test_init_from_points_appends_and_matches_fixture_grid():
     p = gm.gaussians["p"]
     np.testing.assert_array_equal(p[:10], before)
     np.testing.assert_array_equal(p[10:].astype(np.float32), ref["p"].astype(np.float32))
+
+
+def test_sh_schedule():  # test_mapper.cpp:278-296 on the device map
+    m = G().GaussianMap(None)
+    m.init_from_points(np.array([[0, 0, 2, 0.5, 0.5, 0.5]], dtype=float))
+    m.global_step = 99
+    assert m.maybe_upgrade_sh(100) == 0
+    m.global_step = 100
+    assert m.maybe_upgrade_sh(100) == 1
+    m.global_step = 300
+    assert m.maybe_upgrade_sh(100) == 3
+    assert m.gaussians["degree"][0] == 3
+    m.global_step = 1000
+    assert m.maybe_upgrade_sh(100) == 3
+    assert m.maybe_upgrade_sh(0) == 3  # disabled: the current maximum
