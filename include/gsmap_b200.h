@@ -135,6 +135,16 @@ int gs_maybe_upgrade_sh(gs_map* map, int32_t sh_interval, int32_t* degree);
    distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;
    degree 0; fresh optimizer state). *added = n. */
 int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64_t* added);
+/* filter_points_by_visibility (map/keyframe.hpp, keyframe.cpp:49-74): render the map at the pose
+   and keep the points (in order) that are behind the near plane, project outside the image or
+   land on a pixel with visibility <= tau_alpha; tau_alpha outside [0, 1] -> GS_EINVAL.
+   kept6 must hold n points. */
+int gs_filter_points_by_visibility(gs_map* map, const double* points6, int64_t n, const gs_pose* pose,
+                                   const gs_camera* cam, double tau_alpha, double* kept6, int64_t* n_kept);
+/* keyframe integration (pipeline.cpp:151-155) without a host round trip of the kept set:
+   filter_points_by_visibility then init_gaussians_from_points; *added = the kept count */
+int gs_map_integrate_points(gs_map* map, const double* points6, int64_t n, const gs_pose* pose,
+                            const gs_camera* cam, double tau_alpha, int64_t* added);
 /* GaussianMap::prune (gaussian_map.hpp:79, gaussian_map.cpp:56-73): drop every Gaussian with
    sigmoid(opacity_logit) < threshold, compacting parameters and optimizer state in order;
    threshold outside (0, 1) -> GS_EINVAL. *removed = the number dropped. */

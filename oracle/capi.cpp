@@ -425,6 +425,19 @@ int orc_project_sparse_depth(const double* pts6, int64_t n, const orc_pose_t* po
     });
 }
 
+// kept: indices of the kept points (n capacity)
+int orc_filter_points_by_visibility(void* mp, const double* pts6, int64_t n, const orc_pose_t* pose,
+                                    const orc_camera_t* cam, double tau_alpha, int64_t* kept, int64_t* n_kept) {
+    return guard([&] {
+        std::vector<ColoredPoint> pts(n);
+        for (int64_t i = 0; i < n; ++i) pts[i].position = {pts6[6 * i], pts6[6 * i + 1], pts6[6 * i + 2]};
+        const auto k = filter_points_by_visibility(pts, to_pose(pose), *static_cast<GaussianMap*>(mp), to_cam(cam),
+                                                   tau_alpha);
+        for (size_t i = 0; i < k.size(); ++i) kept[i] = static_cast<int64_t>(k[i]);
+        *n_kept = static_cast<int64_t>(k.size());
+    });
+}
+
 // ---------------------------------------------------------------- fixtures
 void* orc_rng_create(uint32_t seed) { return new std::mt19937(seed); }
 void orc_rng_free(void* r) { delete static_cast<std::mt19937*>(r); }

@@ -300,6 +300,9 @@ int maybe_upgrade_sh(GaussianMap& map, const TrainConfig& cfg);
 size_t init_gaussians_from_points(GaussianMap& map, const std::vector<ColoredPoint>& points);
 ImageD project_sparse_depth(const std::vector<ColoredPoint>& points, const Pose& pose,
                             const CameraModel& cam);  // io/sequence.cpp:246-259
+std::vector<size_t> filter_points_by_visibility(const std::vector<ColoredPoint>& points, const Pose& pose,
+                                                const GaussianMap& map, const CameraModel& cam,
+                                                double tau_alpha);  // keyframe.cpp:49-74
 
 // ---------------------------------------------------------------- fixtures
 GaussianMap random_scene(std::mt19937& rng, int n, const CameraModel& cam, const Pose& pose,

@@ -461,6 +461,17 @@ def project_sparse_depth(pts6, p: Pose, cam: Camera):
     return out
 
 
+def filter_points_by_visibility(pts6, m: OracleMap, p: Pose, cam: Camera, tau_alpha: float) -> np.ndarray:
+    """keyframe.cpp:49-74: indices of the kept points."""
+    pts6 = np.ascontiguousarray(pts6, np.float64)
+    kept = np.zeros(max(len(pts6), 1), np.int64)
+    nk = C.c_int64()
+    _check(lib().orc_filter_points_by_visibility(C.c_void_p(m.h), _ptr(pts6), C.c_int64(len(pts6)), C.byref(p),
+                                                 C.byref(cam), C.c_double(tau_alpha),
+                                                 kept.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(nk)))
+    return kept[: nk.value]
+
+
 class Rng:
     """std::mt19937 with std::uniform_real_distribution<double> draws (libstdc++)."""
 

@@ -482,6 +482,27 @@ ImageD project_sparse_depth(const std::vector<ColoredPoint>& points, const Pose&
     return depth;
 }
 
+std::vector<size_t> filter_points_by_visibility(const std::vector<ColoredPoint>& points, const Pose& pose,
+                                                const GaussianMap& map, const CameraModel& cam,
+                                                double tau_alpha) {  // keyframe.cpp:49-74 (kept indices)
+    if (tau_alpha < 0.0 || tau_alpha > 1.0)
+        throw std::invalid_argument("filter_points_by_visibility: tau_alpha must be in [0,1]");
+    const RenderOutput out = render(map, pose, cam);
+    std::vector<size_t> kept;
+    for (size_t i = 0; i < points.size(); ++i) {
+        const Vec3 pc = pose.world_to_camera(points[i].position);
+        bool keep = true;
+        if (pc.z > kNearClip) {
+            const long px = std::lround(cam.fx * pc.x / pc.z + cam.cx);
+            const long py = std::lround(cam.fy * pc.y / pc.z + cam.cy);
+            if (px >= 0 && px < cam.width && py >= 0 && py < cam.height)
+                keep = out.visibility.at(static_cast<int>(py), static_cast<int>(px)) <= tau_alpha;
+        }
+        if (keep) kept.push_back(i);
+    }
+    return kept;
+}
+
 // ------------------------------------------------------------------ tests/support/brute_force.hpp
 GaussianMap random_scene(std::mt19937& rng, int n, const CameraModel& cam, const Pose& pose,
                          double lo, double hi) {  // brute_force.hpp:92-117

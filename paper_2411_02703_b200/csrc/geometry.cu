@@ -816,6 +816,43 @@ void launch_knn_count_runs(const uint64_t* skeys, int64_t n, unsigned long long*
     if (n > 0) knn_count_runs_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(skeys, n, runs);
 }
 
+// filter_points_by_visibility (keyframe.cpp:49-74): keep a point when it is behind the near
+// plane, projects outside the image, or lands on a pixel whose rendered visibility is <= tau.
+__global__ void vis_filter_kernel(const double* __restrict__ pts, int64_t n, ViewParams v,
+                                  const float* __restrict__ vis, double tau, int32_t* __restrict__ keep) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* q = pts + 6 * k;
+    D3 pc = quat_rotate(v.qw, v.qx, v.qy, v.qz, D3{q[0], q[1], q[2]});
+    pc = {pc.x + v.tx, pc.y + v.ty, pc.z + v.tz};
+    int32_t kp = 1;
+    if (pc.z > kNearClip) {
+        const long long px = llround(v.fx * pc.x / pc.z + v.cx);
+        const long long py = llround(v.fy * pc.y / pc.z + v.cy);
+        if (px >= 0 && px < v.width && py >= 0 && py < v.height)
+            kp = static_cast<double>(vis[py * v.width + px]) <= tau ? 1 : 0;
+    }
+    keep[k] = kp;
+}
+
+__global__ void compact_points_kernel(const double* __restrict__ src, int64_t n, const int32_t* __restrict__ keep,
+                                      const int32_t* __restrict__ pos, double* __restrict__ dst) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n || !keep[k]) return;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) dst[6 * static_cast<int64_t>(pos[k]) + c] = src[6 * k + c];
+}
+
+void launch_vis_filter(const double* pts6, int64_t n, const ViewParams& v, const float* vis, double tau,
+                       int32_t* keep, cudaStream_t st) {
+    if (n > 0) vis_filter_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(pts6, n, v, vis, tau, keep);
+}
+
+void launch_compact_points(const double* src6, int64_t n, const int32_t* keep, const int32_t* pos, double* dst6,
+                           cudaStream_t st) {
+    if (n > 0) compact_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(src6, n, keep, pos, dst6);
+}
+
 void launch_knn_bbox(const double* pts, int64_t n, unsigned long long* out6, cudaStream_t st) {
     cudaMemsetAsync(out6, 0xff, 3 * sizeof(unsigned long long), st);
     cudaMemsetAsync(out6 + 3, 0, 3 * sizeof(unsigned long long), st);

@@ -1118,23 +1118,17 @@ int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // m
     });
 }
 
-int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
-    return guard([&] {
-        *added = 0;
-        if (n <= 0) return;  // points.empty() -> 0
-        if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
-        M->ctx->use();
+// init_gaussians_from_points on device-resident points [n][6] (n > 0); appends to the map
+void init_points_device(gs_map* M, const double* dpts, int64_t n) {
         gs_context* C = M->ctx;
         cudaStream_t st = C->stream;
-        DevBuf pts, keys, keys2, idx, idx2, bb, hk, hv;
-        pts.ensure(sizeof(double) * 6 * n);
+        DevBuf keys, keys2, idx, idx2, bb, hk, hv;
         keys.ensure(sizeof(uint64_t) * n);
         keys2.ensure(sizeof(uint64_t) * n);
         idx.ensure(sizeof(int32_t) * n);
         idx2.ensure(sizeof(int32_t) * n);
         bb.ensure(sizeof(unsigned long long) * 8);
-        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st), "h2d points");
-        launch_knn_bbox(pts.as<double>(), n, bb.as<unsigned long long>(), st);
+        launch_knn_bbox(dpts, n, bb.as<unsigned long long>(), st);
         unsigned long long enc[6];
         ck(cudaMemcpyAsync(enc, bb.p, sizeof(enc), cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
@@ -1156,7 +1150,7 @@ int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* a
         g.cell = std::cbrt(vol / static_cast<double>(n)) * 1.5;
         size_t tb = 0;
         auto sort_keys = [&]() {
-            launch_knn_keys(pts.as<double>(), n, g, keys.as<uint64_t>(), idx.as<int32_t>(), st);
+            launch_knn_keys(dpts, n, g, keys.as<uint64_t>(), idx.as<int32_t>(), st);
             tb = 0;
             cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(), idx.as<int32_t>(),
                                             idx2.as<int32_t>(), static_cast<int>(n), 0, 64, st);
@@ -1190,7 +1184,7 @@ int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* a
         const std::vector<int32_t> birth(n, static_cast<int32_t>(M->adam_count));
         ck(cudaMemcpyAsync(M->birth + first, birth.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
         const int k = static_cast<int>(std::min<int64_t>(3, n - 1));
-        launch_knn_init(pts.as<double>(), n, k, g, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, idx2.as<int32_t>(),
+        launch_knn_init(dpts, n, k, g, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, idx2.as<int32_t>(),
                         M->params, M->cap, first, st);
         C->launched(8);
         ck(cudaStreamSynchronize(st), "sync");
@@ -1198,7 +1192,85 @@ int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* a
         M->n = first + n;
         M->recompute_max_degree();
         refresh_extent(M);
+}
+
+int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
+    return guard([&] {
+        *added = 0;
+        if (n <= 0) return;  // points.empty() -> 0
+        if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
+        M->ctx->use();
+        DevBuf pts;
+        pts.ensure(sizeof(double) * 6 * n);
+        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d points");
+        init_points_device(M, pts.as<double>(), n);
         *added = n;
+    });
+}
+
+// filter_points_by_visibility on the device: render the map at the pose, flag, compact (stable);
+// returns the kept count, kept points in `out` (device, [kept][6])
+int64_t filter_points_device(gs_map* M, const double* dpts, int64_t n, const gs_pose& pose, const gs_camera& cam,
+                             double tau_alpha, DevBuf& out) {
+    if (tau_alpha < 0.0 || tau_alpha > 1.0)
+        fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
+    gs_context* C = M->ctx;
+    cudaStream_t st = C->stream;
+    gs_frame* F = scratch_frame(C);
+    render_impl(M, pose, cam, F, true, false);
+    DevBuf keep, pos;
+    keep.ensure(sizeof(int32_t) * (n + 1));
+    pos.ensure(sizeof(int32_t) * (n + 1));
+    ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
+    launch_vis_filter(dpts, n, F->view, F->vis.as<float>(), tau_alpha, keep.as<int32_t>(), st);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st);
+    ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st), "scan");
+    int32_t kept = 0;
+    ck(cudaMemcpyAsync(&kept, pos.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
+    out.ensure(sizeof(double) * 6 * std::max<int64_t>(kept, 1));
+    launch_compact_points(dpts, n, keep.as<int32_t>(), pos.as<int32_t>(), out.as<double>(), st);
+    C->launched(3);
+    return kept;
+}
+
+int gs_filter_points_by_visibility(gs_map* M, const double* pts6, int64_t n, const gs_pose* pose,
+                                   const gs_camera* cam, double tau_alpha, double* kept6, int64_t* n_kept) {
+    return guard([&] {  // keyframe.cpp:49-74
+        validate_camera(*cam);
+        M->ctx->use();
+        *n_kept = 0;
+        if (tau_alpha < 0.0 || tau_alpha > 1.0)
+            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
+        if (n <= 0) return;
+        DevBuf pts, out;
+        pts.ensure(sizeof(double) * 6 * n);
+        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
+        const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
+        if (kept > 0)
+            ck(cudaMemcpyAsync(kept6, out.p, sizeof(double) * 6 * kept, cudaMemcpyDeviceToHost, M->ctx->stream), "d2h");
+        ck(cudaStreamSynchronize(M->ctx->stream), "sync");
+        *n_kept = kept;
+    });
+}
+
+int gs_map_integrate_points(gs_map* M, const double* pts6, int64_t n, const gs_pose* pose, const gs_camera* cam,
+                            double tau_alpha, int64_t* added) {
+    return guard([&] {  // pipeline.cpp:151-155: filter_points_by_visibility -> init_gaussians_from_points
+        validate_camera(*cam);
+        M->ctx->use();
+        *added = 0;
+        if (tau_alpha < 0.0 || tau_alpha > 1.0)
+            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
+        if (n <= 0) return;
+        if (n > 0x7fffffff) fail(GS_EINVAL, "integrate_points: too many points");
+        DevBuf pts, out;
+        pts.ensure(sizeof(double) * 6 * n);
+        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
+        const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
+        if (kept > 0) init_points_device(M, out.as<double>(), kept);
+        *added = kept;
     });
 }
 

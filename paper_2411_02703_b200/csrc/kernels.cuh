@@ -31,6 +31,10 @@ struct KnnGrid {
 };
 void launch_knn_bbox(const double* pts6, int64_t n, unsigned long long* out6 /* ordered min xyz, max xyz */,
                      cudaStream_t st);
+void launch_vis_filter(const double* pts6, int64_t n, const ViewParams& v, const float* vis, double tau,
+                       int32_t* keep, cudaStream_t st);
+void launch_compact_points(const double* src6, int64_t n, const int32_t* keep, const int32_t* pos, double* dst6,
+                           cudaStream_t st);
 void launch_knn_count_runs(const uint64_t* sorted_keys, int64_t n, unsigned long long* runs, cudaStream_t st);
 void launch_knn_keys(const double* pts6, int64_t n, const KnnGrid& g, uint64_t* keys, int32_t* idx, cudaStream_t st);
 void launch_knn_table(const uint64_t* sorted_keys, int64_t n, uint64_t* hkeys, int2* hvals, uint32_t hmask,

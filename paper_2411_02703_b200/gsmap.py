@@ -269,6 +269,14 @@ class GaussianMap:
         _check(lib().gs_map_init_from_points(_vp(self.h), _p(pts), C.c_int64(len(pts)), C.byref(added)))
         return added.value
 
+    def integrate_points(self, points6: np.ndarray, pose: Pose, cam: Camera, tau_alpha: float) -> int:
+        """filter_points_by_visibility + init_gaussians_from_points on the device (pipeline.cpp:151-155)."""
+        pts = np.ascontiguousarray(points6, np.float64)
+        added = C.c_int64()
+        _check(lib().gs_map_integrate_points(_vp(self.h), _p(pts), C.c_int64(len(pts)), C.byref(pose), C.byref(cam),
+                                             C.c_double(tau_alpha), C.byref(added)))
+        return added.value
+
     def prune(self, opacity_threshold: float) -> int:
         """GaussianMap::prune (gaussian_map.cpp:56-73): removed count; state stays aligned."""
         removed = C.c_int64()
@@ -421,6 +429,17 @@ class RenderOutput:
         c, d, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _check(lib().gs_frame_device_images(_vp(self.h), C.byref(c), C.byref(d), C.byref(v)))
         return c.value, d.value, v.value
+
+
+def filter_points_by_visibility(points6: np.ndarray, m: GaussianMap, pose: Pose, cam: Camera,
+                                tau_alpha: float) -> np.ndarray:
+    """keyframe.cpp:49-74 on the device: the kept points, in order."""
+    pts = np.ascontiguousarray(points6, np.float64)
+    out = np.zeros_like(pts)
+    kept = C.c_int64()
+    _check(lib().gs_filter_points_by_visibility(_vp(m.h), _p(pts), C.c_int64(len(pts)), C.byref(pose), C.byref(cam),
+                                                C.c_double(tau_alpha), _p(out), C.byref(kept)))
+    return out[: kept.value]
 
 
 def project_sparse_depth(points: np.ndarray, pose: Pose, cam: Camera, ctx: Context | None = None) -> np.ndarray:

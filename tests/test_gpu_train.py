@@ -401,3 +401,88 @@ def test_sh_schedule():  # test_mapper.cpp:278-296 on the device map
     m.global_step = 1000
     assert m.maybe_upgrade_sh(100) == 3
     assert m.maybe_upgrade_sh(0) == 3  # disabled: the current maximum
+
+
+def _kf_cam():
+    return O.camera(100, 100, 31.5, 23.5, 64, 48)
+
+
+def _opaque(pos, opacity):  # test_keyframe.cpp:22-30
+    return O.make_blob(pos, opacity, (0.8, 0.2, 0.2), log_scale=np.log(0.5))
+
+
+def test_filter_points_by_visibility_kats():  # test_keyframe.cpp:98-136 on the device
+    cam, pose = _kf_cam(), O.pose()
+    gen = np.random.default_rng(1)
+    pts = np.zeros((20, 6))
+    pts[:, :3] = gen.uniform(-1, 1, (20, 3)) + [0, 0, 3.0]
+    empty = G().GaussianMap(None)
+    np.testing.assert_array_equal(G().filter_points_by_visibility(pts, empty, gpu_pose(pose), gpu_cam(cam), 0.5), pts)
+    wall = np.concatenate([_opaque((x, y, 4.0), 0.95) for x in np.arange(-2.0, 2.0 + 1e-9, 0.25)
+                           for y in np.arange(-1.5, 1.5 + 1e-9, 0.25)])
+    _, gm = pair(wall)
+    pts = np.array([[0, 0, 3.0, 0, 0, 0], [50, 0, 3.0, 0.1, 0.2, 0.3], [0, 0, -3.0, 0, 0, 0]])
+    kept = G().filter_points_by_visibility(pts, gm, gpu_pose(pose), gpu_cam(cam), 0.5)
+    np.testing.assert_array_equal(kept, pts[1:])
+    for tau in (-0.1, 1.5):
+        with pytest.raises(ValueError, match="tau_alpha"):
+            G().filter_points_by_visibility(pts, gm, gpu_pose(pose), gpu_cam(cam), tau)
+
+
+def _filter_case(seed, n_pts):
+    cam = O.camera(300, 300, 159.5, 119.5, 320, 240)
+    pose = O.pose(1, 0.02, -0.03, 0.01, t=(0.05, -0.02, 0.1))
+    g = random_scene(seed, 3000, cam, pose)
+    om, gm = pair(g)
+    gen = np.random.default_rng(seed)
+    pts = np.zeros((n_pts, 6))
+    pts[:, 2] = gen.uniform(-1.0, 9.0, n_pts)
+    pts[:, 0] = gen.uniform(-0.7, 0.7, n_pts) * np.abs(pts[:, 2])
+    pts[:, 1] = gen.uniform(-0.6, 0.6, n_pts) * np.abs(pts[:, 2])
+    pts[:, 3:] = gen.uniform(0, 1, (n_pts, 3))
+    return cam, pose, om, gm, pts
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.3, 0.5, 0.9, 1.0])
+def test_filter_points_by_visibility_matches_oracle(tau):  # keyframe.cpp:49-74
+    """Kept sets equal; a point may differ only where the oracle's fp64 visibility at its pixel
+    is within the render tolerance (1e-5) of tau (the device's visibility is fp32)."""
+    cam, pose, om, gm, pts = _filter_case(7, 20000)
+    ref = O.filter_points_by_visibility(pts, om, pose, cam, tau)
+    kept = G().filter_points_by_visibility(pts, gm, gpu_pose(pose), gpu_cam(cam), tau)
+    ok = np.zeros(len(pts), bool); ok[ref] = True
+    row = {r.tobytes(): i for i, r in enumerate(pts)}
+    dev = np.zeros(len(pts), bool)
+    order = [row[r.tobytes()] for r in kept]
+    assert order == sorted(order)  # stable: the input order
+    dev[order] = True
+    diff = np.nonzero(dev != ok)[0]
+    if len(diff):
+        vis = O.render(om, pose, cam).visibility
+        w, x, y, z = pose.qw, pose.qx, pose.qy, pose.qz
+        R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                      [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                      [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+        for i in diff:
+            pc = R @ pts[i, :3] + [pose.tx, pose.ty, pose.tz]
+            px = int(np.floor(cam.fx * pc[0] / pc[2] + cam.cx + 0.5))
+            py = int(np.floor(cam.fy * pc[1] / pc[2] + cam.cy + 0.5))
+            assert abs(vis[py, px] - tau) < 1e-5, (i, vis[py, px])
+    assert (dev != ok).sum() <= 3
+    assert 0 < ok.sum() <= len(pts)
+
+
+def test_integrate_points_matches_filter_then_init():  # pipeline.cpp:151-155
+    cam, pose, om, gm, pts = _filter_case(11, 5000)
+    ref = O.filter_points_by_visibility(pts, om, pose, cam, 0.5)
+    n0 = len(gm)
+    before = gm.gaussians["p"].copy()
+    assert gm.integrate_points(pts, gpu_pose(pose), gpu_cam(cam), 0.5) == len(ref)
+    assert len(gm) == n0 + len(ref)
+    p = gm.gaussians["p"]
+    np.testing.assert_array_equal(p[:n0], before)
+    fresh = O.OracleMap()
+    fresh.init_from_points(pts[ref])
+    _init_close(p[n0:], fresh.gaussians["p"])
+    m, v, steps = gm.adam_state()
+    assert np.all(m[n0:] == 0) and np.all(v[n0:] == 0)

@@ -239,6 +239,54 @@ def test_init_from_points_kats():  # test_mapper.cpp:32-83
     assert s == pytest.approx([0.3, 0.2, 0.3], rel=1e-12)
 
 
+def kf_cam():
+    return O.camera(100, 100, 31.5, 23.5, 64, 48)
+
+
+def opaque_blob(pos, opacity):  # test_keyframe.cpp:22-30
+    return O.make_blob(pos, opacity, (0.8, 0.2, 0.2), log_scale=math.log(0.5))
+
+
+def wall_map():
+    return O.OracleMap(np.concatenate([opaque_blob((x, y, 4.0), 0.95) for x in np.arange(-2.0, 2.0 + 1e-9, 0.25)
+                                       for y in np.arange(-1.5, 1.5 + 1e-9, 0.25)]))
+
+
+def test_filter_points_by_visibility_kats():  # test_keyframe.cpp:98-136
+    cam, pose = kf_cam(), O.pose()
+    gen = np.random.default_rng(1)
+    pts = np.zeros((20, 6))
+    pts[:, :3] = gen.uniform(-1, 1, (20, 3)) + [0, 0, 3.0]
+    assert len(O.filter_points_by_visibility(pts, O.OracleMap(), pose, cam, 0.5)) == 20
+    pts = np.array([[0, 0, 3.0, 0, 0, 0], [50, 0, 3.0, 0, 0, 0], [0, 0, -3.0, 0, 0, 0]])
+    assert list(O.filter_points_by_visibility(pts, wall_map(), pose, cam, 0.5)) == [1, 2]
+    for tau in (-0.1, 1.5):
+        with pytest.raises(ValueError, match="tau_alpha"):
+            O.filter_points_by_visibility(pts, wall_map(), pose, cam, tau)
+
+
+def test_filter_points_by_visibility_per_pixel_lookup():  # test_keyframe.cpp:138-181
+    cam, pose = kf_cam(), O.pose()
+    m = O.OracleMap(np.concatenate([opaque_blob((x, y, 4.0), 0.9) for x in np.arange(-1.6, -0.2 + 1e-9, 0.15)
+                                    for y in np.arange(-1.0, 1.0 + 1e-9, 0.15)]))
+    gen = np.random.default_rng(2)
+    pts = np.zeros((200, 6))
+    pts[:, 0] = gen.uniform(-1.5, 1.5, 200)
+    pts[:, 1] = gen.uniform(-1.5, 1.5, 200) * 0.8
+    pts[:, 2] = 3.5
+    vis = O.render(m, pose, cam).visibility
+    px = np.floor(100 * pts[:, 0] / 3.5 + 31.5 + 0.5).astype(int)
+    py = np.floor(100 * pts[:, 1] / 3.5 + 23.5 + 0.5).astype(int)
+    inside = (px >= 0) & (px < 64) & (py >= 0) & (py < 48)
+    v = np.where(inside, vis[np.clip(py, 0, 47), np.clip(px, 0, 63)], 0.0)
+    kept = O.filter_points_by_visibility(pts, m, pose, cam, 0.5)
+    np.testing.assert_array_equal(kept, np.nonzero(~inside | (v <= 0.5))[0])
+    assert 0 < len(kept) < 200
+    assert len(O.filter_points_by_visibility(pts, m, pose, cam, 1.0)) == 200
+    strict = O.filter_points_by_visibility(pts, m, pose, cam, 0.0)
+    assert np.all(v[strict] == 0.0)
+
+
 def test_adam_known_answer_numpy():
     """Adam has no KAT in the reference; pin the restatement of
     gaussian_map.cpp:15-54 against an independent numpy formula over two steps, including the
