@@ -182,13 +182,11 @@ def run_ours(args, rank, world):
 
     batch = world > 1 or args.batch
     views_per_rank = 1
-    if batch:  # C4: 8-view batch sharded over ranks, NCCL all-reduce of the gradient SoA
-        import torch.distributed as dist
-        cap = len(m) + 1024
-        gbuf = torch.zeros(59 * cap, dtype=torch.float32, device=f"cuda:{dev}")
-        grads = G.RenderGradients(ctx, external_ptr=gbuf.data_ptr(), capacity=cap)
-        views_per_rank = N_FRAMES // world
-        frame = G.RenderOutput(ctx)
+    if batch:  # C4: 8-view batch sharded over ranks, NCCL all-reduce of the active gradient planes
+        from paper_2411_02703_b200.batch import BatchTrainer, rank_views
+        trainer = BatchTrainer(m, ctx, torch.device(f"cuda:{dev}"))
+        my_views = rank_views(N_FRAMES, rank, world)
+        views_per_rank = len(my_views)
 
     def step(s, e2e=False):
         if not batch:
@@ -202,18 +200,14 @@ def run_ours(args, rank, world):
             assert rep is not None and rep["level"] == lvl
             return 1, shapes[lvl][0] * shapes[lvl][1]
         lvl = LEVELS - (s % 3)
-        grads.zero(m)
         px = 0
-        for v in range(views_per_rank):
-            k = rank * views_per_rank + v
+        for k in my_views:
             kf = kfs[k]
             kf.consumed_iters = (LEVELS - lvl)
             if e2e:
                 kf.upload_level(lvl, *host_levels[k][lvl])
-            G.train_accumulate(m, kf, cfg, cam, grads, frame, sync=False)
             px += shapes[lvl][0] * shapes[lvl][1]
-        dist.all_reduce(gbuf[: 59 * cap])
-        m.apply_gradients(grads, cfg.lr)
+        trainer.step(kfs, my_views, cfg, cam)
         torch.cuda.current_stream().synchronize()
         return views_per_rank, px
 

@@ -16,6 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import pyoracle as O
+from paper_2411_02703_b200.batch import active_planes, rank_views, reduce_gradient_planes
 
 N_VIEWS, N_G = 4, 60
 
@@ -23,6 +24,7 @@ N_VIEWS, N_G = 4, 60
 def scene():
     cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
     g = O.random_scene(O.Rng(17), N_G, cam, O.pose(), -1.0, 1.0).gaussians
+    g["degree"] = np.minimum(g["degree"], 1)  # d <= 1: the collective covers planes [0, 23)
     gen = np.random.default_rng(17)
     poses = [O.pose(1.0, *(gen.normal(size=3) * 0.02), t=tuple(gen.normal(size=3) * 0.05)) for _ in range(N_VIEWS)]
     cots = [(gen.uniform(-1, 1, (48, 64, 3)), gen.uniform(-1, 1, (48, 64))) for _ in range(N_VIEWS)]
@@ -39,12 +41,15 @@ def worker(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cam, g, poses, cots = scene()
     m = O.OracleMap(g)
-    per = N_VIEWS // world
-    acc = np.zeros((N_G, 59))
-    for v in range(rank * per, (rank + 1) * per):
-        acc += view_grads(m, cam, poses[v], cots[v])
-    t = torch.from_numpy(acc)
-    dist.all_reduce(t)  # the NCCL all-reduce of the gradient planes on GPU
+    cap = N_G + 5  # the device buffer's plane stride (capacity > map size)
+    buf = torch.zeros(59 * cap, dtype=torch.float64)
+    planes = buf.view(59, cap)
+    for v in rank_views(N_VIEWS, rank, world):
+        planes[:, :N_G] += torch.from_numpy(view_grads(m, cam, poses[v], cots[v]).T)
+    s_p = active_planes(int(g["degree"].max()))
+    assert s_p == 23 and torch.all(planes[s_p:] == 0)
+    reduce_gradient_planes(buf, s_p, cap)  # the NCCL all-reduce of the active planes on GPU
+    t = planes[:, :N_G].T.contiguous()
     m.apply_gradients(t.numpy())
     np.save(os.path.join(outdir, f"rank{rank}.npy"), m.gaussians["p"])
     dist.destroy_process_group()
@@ -73,3 +78,12 @@ def test_sharded_batch_step_matches_single_process():
     # sum order differs (per-rank partial sums); Adam's step is ~lr*sign(g), so the maps agree
     # to within rounding of the summed gradients
     np.testing.assert_allclose(r0, m.gaussians["p"], rtol=0, atol=1e-9)
+
+
+def test_batch_helpers():
+    assert [active_planes(d) for d in range(4)] == [14, 23, 38, 59]
+    assert list(rank_views(8, 3, 4)) == [6, 7]
+    with pytest.raises(ValueError):
+        rank_views(8, 0, 3)
+    with pytest.raises(ValueError):
+        active_planes(4)

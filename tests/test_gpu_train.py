@@ -486,3 +486,43 @@ def test_integrate_points_matches_filter_then_init():  # pipeline.cpp:151-155
     _init_close(p[n0:], fresh.gaussians["p"])
     m, v, steps = gm.adam_state()
     assert np.all(m[n0:] == 0) and np.all(v[n0:] == 0)
+
+
+def test_batch_trainer_matches_summed_oracle_views():  # sum of per-view grads, one Adam step
+    """BatchTrainer at world size 1 (the collective is skipped): the accumulated gradient planes
+    equal the oracle's per-view RenderGradients summed (GaussianGrad::add), and the replica
+    after the single Adam step tracks the oracle's apply_gradients of that sum."""
+    from paper_2411_02703_b200.batch import BatchTrainer
+    import torch
+    from tests._common import grad_errors
+    cam = O.camera(120, 120, 47.5, 39.5, 96, 80)
+    gt_map = O.random_scene(O.Rng(31), 60, cam, O.pose(), 1.0, 2.0)
+    g = gt_map.gaussians
+    g["p"][:, 10] = np.log(0.3 / 0.7)
+    g["p"][:, 7:10] += 0.3
+    om, gm = pair(g)
+    gen = np.random.default_rng(5)
+    poses = [O.pose(1.0, *(gen.normal(size=3) * 0.02), t=tuple(gen.normal(size=3) * 0.05)) for _ in range(4)]
+    ocfg = O.make_cfg(0.2, 0.5, 0)
+    gcfg = G().TrainConfig.make(0.2, 0.5, 0)
+    kfs, acc = [], np.zeros((len(g), 59))
+    for p in poses:
+        gt = O.render(gt_map, p, cam)
+        color = f32(gt.color)
+        sparse = f32(np.where(gen.uniform(size=(80, 96)) < 0.2, gt.depth, 0.0))
+        kfs.append(G().Keyframe(gpu_pose(p), color, sparse, 6, 0))
+        out = O.render(om, p, cam)
+        loss = O.compute_loss(out.color, out.depth, out.visibility, color, sparse, ocfg)
+        acc += O.render_backward(om, p, cam, out, loss["dl_dcolor"], loss["dl_ddepth"])
+    tr = BatchTrainer(gm, gm.ctx, torch.device("cuda:0"))
+    assert tr.step(kfs, range(4), gcfg, gpu_cam(cam)) == 4
+    torch.cuda.synchronize()
+    gg = tr.buf.view(59, tr.cap)[:, : len(g)].T.double().cpu().numpy()
+    e, ge = grad_errors(gg, acc, round32(g))
+    assert ge.max() < 1e-3 and np.mean(e < 1e-3) >= 0.995
+    om.apply_gradients(acc)
+    lr = np.array([1.6e-4 * om.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+    d = np.abs(gm.gaussians["p"] - om.gaussians["p"])
+    assert np.all(d <= 2 * lr + 1e-6)
+    assert np.mean(d <= 0.05 * lr + 1e-6) > 0.95
+    assert gm.global_step == 1
