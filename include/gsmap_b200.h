@@ -36,7 +36,8 @@ enum {
     GS_ELOGIC = 2, /* std::logic_error (rasterizer.cpp:236-237) */
     GS_ECUDA = 3,
     GS_ENCCL = 4,
-    GS_ENOMEM = 5
+    GS_ENOMEM = 5,
+    GS_ERUNTIME = 6 /* std::runtime_error (io/checkpoint.cpp: open / format / truncation) */
 };
 
 typedef struct gs_camera { double fx, fy, cx, cy; int32_t width, height; } gs_camera;
@@ -135,6 +136,22 @@ int gs_maybe_upgrade_sh(gs_map* map, int32_t sh_interval, int32_t* degree);
    distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;
    degree 0; fresh optimizer state). *added = n. */
 int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64_t* added);
+/* checkpoint format v1 (io/checkpoint.cpp:17-73): text header + 476-byte fp64 AoS records.
+   save_checkpoint writes the device map's parameters (exact fp64 widening of the fp32 store);
+   load_checkpoint returns a NEW map (fresh Adam state, GaussianMap::append) or GS_ERUNTIME for
+   a missing / foreign / wrong-version / truncated file, with the reference's messages. */
+int gs_save_checkpoint(gs_map* map, const char* path);
+int gs_load_checkpoint(gs_context* ctx, const char* path, gs_map** out);
+/* evaluate_sequence (pipeline.cpp:41-64) for one frame: render at the pose, quantize_8bit the
+   colour (pipeline.cpp:34-39), psnr / ssim against gt_color (H x W x 3, HWC) and depth_rmse of
+   the raw depth against gt_depth (H x W; NULL -> depth_rmse = NaN, as with no valid pixel). */
+typedef struct gs_eval_metrics {
+    double psnr;
+    double ssim;
+    double depth_rmse;
+} gs_eval_metrics;
+int gs_evaluate_view(gs_map* map, const gs_pose* pose, const gs_camera* cam, const double* gt_color,
+                     const double* gt_depth, gs_eval_metrics* out);
 /* filter_points_by_visibility (map/keyframe.hpp, keyframe.cpp:49-74): render the map at the pose
    and keep the points (in order) that are behind the near plane, project outside the image or
    land on a pixel with visibility <= tau_alpha; tau_alpha outside [0, 1] -> GS_EINVAL.

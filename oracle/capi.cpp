@@ -438,6 +438,26 @@ int orc_filter_points_by_visibility(void* mp, const double* pts6, int64_t n, con
     });
 }
 
+int orc_save_checkpoint(void* mp, const char* path) {
+    return guard([&] { save_checkpoint(path, *static_cast<GaussianMap*>(mp)); });
+}
+int orc_load_checkpoint(const char* path, void** out) {
+    return guard([&] { *out = new GaussianMap(load_checkpoint(path)); });
+}
+// res3 = psnr, ssim, depth_rmse (gt_depth may be NULL)
+int orc_evaluate_view(void* mp, const orc_pose_t* pose, const orc_camera_t* cam, const double* gt_color,
+                      const double* gt_depth, double* res3) {
+    return guard([&] {
+        const ImageD gc = to_image(gt_color, cam->height, cam->width, 3);
+        const ImageD gd = gt_depth ? to_image(gt_depth, cam->height, cam->width, 1) : ImageD();
+        const EvalMetrics m = evaluate_view(*static_cast<GaussianMap*>(mp), to_pose(pose), to_cam(cam), gc,
+                                            gt_depth ? &gd : nullptr);
+        res3[0] = m.psnr;
+        res3[1] = m.ssim;
+        res3[2] = m.depth_rmse;
+    });
+}
+
 // ---------------------------------------------------------------- fixtures
 void* orc_rng_create(uint32_t seed) { return new std::mt19937(seed); }
 void orc_rng_free(void* r) { delete static_cast<std::mt19937*>(r); }

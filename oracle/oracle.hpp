@@ -300,6 +300,14 @@ int maybe_upgrade_sh(GaussianMap& map, const TrainConfig& cfg);
 size_t init_gaussians_from_points(GaussianMap& map, const std::vector<ColoredPoint>& points);
 ImageD project_sparse_depth(const std::vector<ColoredPoint>& points, const Pose& pose,
                             const CameraModel& cam);  // io/sequence.cpp:246-259
+void save_checkpoint(const std::string& path, const GaussianMap& map);  // io/checkpoint.cpp:17-35
+GaussianMap load_checkpoint(const std::string& path);                   // io/checkpoint.cpp:37-71
+ImageD quantize_8bit(const ImageD& image);                              // pipeline.cpp:34-39
+struct EvalMetrics {
+    double psnr = 0.0, ssim = 0.0, depth_rmse = 0.0;
+};
+EvalMetrics evaluate_view(const GaussianMap& map, const Pose& pose, const CameraModel& cam, const ImageD& gt_color,
+                          const ImageD* gt_depth);  // pipeline.cpp:46-60, one frame
 std::vector<size_t> filter_points_by_visibility(const std::vector<ColoredPoint>& points, const Pose& pose,
                                                 const GaussianMap& map, const CameraModel& cam,
                                                 double tau_alpha);  // keyframe.cpp:49-74

@@ -472,6 +472,28 @@ def filter_points_by_visibility(pts6, m: OracleMap, p: Pose, cam: Camera, tau_al
     return kept[: nk.value]
 
 
+def save_checkpoint(path: str, m: OracleMap):
+    """io/checkpoint.cpp:17-35 (format v1)."""
+    _check(lib().orc_save_checkpoint(C.c_void_p(m.h), os.fsencode(path)))
+
+
+def load_checkpoint(path: str) -> OracleMap:
+    """io/checkpoint.cpp:37-71: a fresh map (fresh Adam state) holding the file's Gaussians."""
+    h = C.c_void_p()
+    _check(lib().orc_load_checkpoint(os.fsencode(path), C.byref(h)))
+    return OracleMap(handle=h.value)
+
+
+def evaluate_view(m: OracleMap, p: Pose, cam: Camera, gt_color, gt_depth=None) -> dict:
+    """evaluate_sequence (pipeline.cpp:41-64) for one frame: psnr / ssim of the quantized render, depth_rmse."""
+    gc = np.ascontiguousarray(gt_color, np.float64)
+    gd = None if gt_depth is None else np.ascontiguousarray(gt_depth, np.float64)
+    r = np.zeros(3)
+    _check(lib().orc_evaluate_view(C.c_void_p(m.h), C.byref(p), C.byref(cam), _ptr(gc),
+                                   None if gd is None else _ptr(gd), _ptr(r)))
+    return dict(psnr=r[0], ssim=r[1], depth_rmse=r[2])
+
+
 class Rng:
     """std::mt19937 with std::uniform_real_distribution<double> draws (libstdc++)."""
 

@@ -1,8 +1,11 @@
 // TEST INFRASTRUCTURE ONLY — oracle restatement of proj/src/map/gaussian_map.cpp (Adam),
 // proj/src/metrics/metrics.cpp (SSIM/PSNR), proj/src/map/mapper.cpp (loss, pyramid, schedule,
 // init), proj/src/io/sequence.cpp:246-259, proj/tests/support/brute_force.hpp:92-117 and
-// proj/src/pipeline/gradcheck.cpp.
+// proj/src/pipeline/gradcheck.cpp, io/checkpoint.cpp (format v1) and pipeline.cpp:34-64 (eval).
 #include <algorithm>
+#include <fstream>
+#include <limits>
+#include <sstream>
 #include <unordered_map>
 
 #include "oracle.hpp"
@@ -501,6 +504,73 @@ std::vector<size_t> filter_points_by_visibility(const std::vector<ColoredPoint>&
         if (keep) kept.push_back(i);
     }
     return kept;
+}
+
+// ------------------------------------------------------------------ io/checkpoint.cpp:17-73 (format v1)
+void save_checkpoint(const std::string& path, const GaussianMap& map) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("save_checkpoint: cannot open " + path);
+    out << "gsmap-checkpoint" << ' ' << 1 << '\n' << "count " << map.size() << '\n'
+        << "sh_degree " << map.max_active_degree() << '\n' << "end_header\n";
+    double rec[59];
+    for (const Gaussian3D& g : map.gaussians()) {
+        gaussian_to_flat(g, rec);  // position, rotation (w,x,y,z), log_scale, opacity, sh: the v1 order
+        out.write(reinterpret_cast<const char*>(rec), sizeof(rec));
+        const int32_t deg = g.active_degree;
+        out.write(reinterpret_cast<const char*>(&deg), sizeof(deg));
+    }
+    if (!out) throw std::runtime_error("save_checkpoint: write failed for " + path);
+}
+
+GaussianMap load_checkpoint(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("load_checkpoint: cannot open " + path);
+    std::string line, magic;
+    std::getline(in, line);
+    std::istringstream head(line);
+    int version = 0;
+    head >> magic >> version;
+    if (magic != "gsmap-checkpoint") throw std::runtime_error("load_checkpoint: not a checkpoint file: " + path);
+    if (version != 1) throw std::runtime_error("load_checkpoint: unsupported version in " + path);
+    size_t count = 0;
+    while (std::getline(in, line) && line != "end_header") {
+        std::istringstream is(line);
+        std::string key;
+        is >> key;
+        if (key == "count") is >> count;
+    }
+    std::vector<Gaussian3D> gs(count);
+    double rec[59];
+    for (Gaussian3D& g : gs) {
+        in.read(reinterpret_cast<char*>(rec), sizeof(rec));
+        flat_to_gaussian(rec, g);
+        int32_t deg = 0;
+        in.read(reinterpret_cast<char*>(&deg), sizeof(deg));
+        g.active_degree = deg;
+    }
+    if (!in) throw std::runtime_error("load_checkpoint: truncated file " + path);
+    GaussianMap map;
+    map.append(gs);
+    return map;
+}
+
+// ------------------------------------------------------------------ pipeline.cpp:34-64 (one frame)
+ImageD quantize_8bit(const ImageD& image) {
+    ImageD out = image;
+    for (size_t i = 0; i < out.size(); ++i)
+        out.data[i] = std::lround(std::clamp(out.data[i], 0.0, 1.0) * 255.0) / 255.0;
+    return out;
+}
+
+EvalMetrics evaluate_view(const GaussianMap& map, const Pose& pose, const CameraModel& cam, const ImageD& gt_color,
+                          const ImageD* gt_depth) {
+    const RenderOutput out = render(map, pose, cam);
+    const ImageD q = quantize_8bit(out.color);
+    EvalMetrics m;
+    m.psnr = psnr(q, gt_color);
+    m.ssim = ssim(q, gt_color);
+    m.depth_rmse = gt_depth ? depth_rmse(out.depth, *gt_depth) : std::numeric_limits<double>::quiet_NaN();
+    return m;
 }
 
 // ------------------------------------------------------------------ tests/support/brute_force.hpp

@@ -31,6 +31,8 @@ struct KnnGrid {
 };
 void launch_knn_bbox(const double* pts6, int64_t n, unsigned long long* out6 /* ordered min xyz, max xyz */,
                      cudaStream_t st);
+void launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h, int w,
+                 float* quant, float* wbuf, LossScalars* acc, cudaStream_t st);
 void launch_vis_filter(const double* pts6, int64_t n, const ViewParams& v, const float* vis, double tau,
                        int32_t* keep, cudaStream_t st);
 void launch_compact_points(const double* src6, int64_t n, const int32_t* keep, const int32_t* pos, double* dst6,

@@ -340,6 +340,54 @@ void launch_ssim(const float* color, const float* gt_color, int h, int w, double
     }
 }
 
+// ---------------------------------------------------------------------------- evaluation
+// evaluate_sequence (pipeline.cpp:41-64) per view: quantize_8bit of the render (pipeline.cpp:
+// 34-39: lround(clamp(c, 0, 1) * 255) / 255), psnr's squared error (metrics.cpp:165-175) and
+// depth_rmse over gt > 0 (metrics.cpp:183-197). The quantized planes feed the SSIM forward.
+__global__ void __launch_bounds__(256) eval_pixel_kernel(
+    const float* __restrict__ color, const float* __restrict__ depth, const float* __restrict__ gt_color,
+    const float* __restrict__ gt_depth, int P, float* __restrict__ quant, LossScalars* __restrict__ acc) {
+    __shared__ double scratch[8];
+    double sq = 0.0, dsq = 0.0;
+    unsigned long long nv = 0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double x = fmin(fmax(static_cast<double>(color[c * P + p]), 0.0), 1.0);
+            const double q = static_cast<double>(llround(x * 255.0)) / 255.0;
+            quant[c * P + p] = static_cast<float>(q);
+            const double d = q - static_cast<double>(gt_color[c * P + p]);
+            sq += d * d;
+        }
+        if (gt_depth) {
+            const double gd = gt_depth[p];
+            if (gd > 0.0) {
+                const double d = static_cast<double>(depth[p]) - gd;
+                dsq += d * d;
+                ++nv;
+            }
+        }
+    }
+    block_add(sq, &acc->sq_sum, scratch);
+    block_add(dsq, &acc->depth_abs_sum, scratch);
+    nv = warp_sum(nv);
+    if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&acc->n_valid, nv);
+}
+
+void launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h, int w,
+                 float* quant, float* wbuf, LossScalars* acc, cudaStream_t st) {
+    const int P = h * w;
+    eval_pixel_kernel<<<std::min(div_up(P, 256), 148 * 8), 256, 0, st>>>(color, depth, gt_color, gt_depth, P, quant,
+                                                                         acc);
+    if (h >= 11 && w >= 11) {
+        ensure_taps();
+        const int vh = h - kHalo, vw = w - kHalo;
+        const float inv_n = static_cast<float>(1.0 / (static_cast<double>(vh) * vw * 3));
+        dim3 gf(div_up(vw, kSx), div_up(vh, kSy), 3);
+        ssim_fwd_kernel<<<gf, 256, 0, st>>>(quant, gt_color, h, w, inv_n, wbuf, acc);
+    }
+}
+
 __global__ void loss_finalize_kernel(LossScalars* acc, double lambda_d) {
     const unsigned long long n = acc->n_valid;
     acc->depth_scale = n > 0 ? static_cast<float>(lambda_d / static_cast<double>(n)) : 0.f;

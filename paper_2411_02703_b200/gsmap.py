@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libgsmap_b200.so")
 
 GAUSS_DTYPE = np.dtype([("p", "<f8", (59,)), ("degree", "<i4"), ("pad", "<i4")])
 
-GS_OK, GS_EINVAL, GS_ELOGIC, GS_ECUDA, GS_ENCCL, GS_ENOMEM = range(6)
+GS_OK, GS_EINVAL, GS_ELOGIC, GS_ECUDA, GS_ENCCL, GS_ENOMEM, GS_ERUNTIME = range(7)
 
 
 class Camera(C.Structure):  # gsmap::CameraModel (core/types.hpp:15-45)
@@ -98,6 +98,8 @@ def _check(st: int):
         raise LogicError(msg)
     if st == GS_ENOMEM:
         raise MemoryError(msg)
+    if st == GS_ERUNTIME:
+        raise RuntimeError(msg)
     raise CudaError(msg)
 
 
@@ -183,13 +185,28 @@ def validate_camera(cam: Camera):
 class GaussianMap:
     """gsmap::GaussianMap (map/gaussian_map.hpp:44-96) resident on the GPU (fp32 SoA + Adam)."""
 
-    def __init__(self, ctx: Context | None = None, gaussians: np.ndarray | None = None):
+    def __init__(self, ctx: Context | None = None, gaussians: np.ndarray | None = None, _handle=None):
         self.ctx = ctx or default_context()
+        if _handle is not None:
+            self.h = _handle
+            return
         h = C.c_void_p()
         _check(lib().gs_map_create(_vp(self.ctx.h), C.byref(h)))
         self.h = h.value
         if gaussians is not None and len(gaussians):
             self.append(gaussians)
+
+    def save_checkpoint(self, path: str):
+        """save_checkpoint (io/checkpoint.cpp:17-35), format v1."""
+        _check(lib().gs_save_checkpoint(_vp(self.h), os.fsencode(path)))
+
+    @classmethod
+    def load_checkpoint(cls, path: str, ctx: Context | None = None) -> "GaussianMap":
+        """load_checkpoint (io/checkpoint.cpp:37-71): a new device map with fresh Adam state."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(lib().gs_load_checkpoint(_vp(ctx.h), os.fsencode(path), C.byref(h)))
+        return cls(ctx, _handle=h.value)
 
     def __del__(self):
         try:
@@ -429,6 +446,49 @@ class RenderOutput:
         c, d, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _check(lib().gs_frame_device_images(_vp(self.h), C.byref(c), C.byref(d), C.byref(v)))
         return c.value, d.value, v.value
+
+
+class EvalMetrics(C.Structure):
+    _fields_ = [("psnr", C.c_double), ("ssim", C.c_double), ("depth_rmse", C.c_double)]
+
+
+def save_checkpoint(path: str, m: GaussianMap):
+    m.save_checkpoint(path)
+
+
+def load_checkpoint(path: str, ctx: Context | None = None) -> GaussianMap:
+    return GaussianMap.load_checkpoint(path, ctx)
+
+
+def evaluate_view(m: GaussianMap, pose: Pose, cam: Camera, gt_color: np.ndarray,
+                  gt_depth: np.ndarray | None = None) -> dict:
+    """One frame of evaluate_sequence (pipeline.cpp:46-60) on the device: psnr / ssim of the
+    quantize_8bit render against gt_color (HWC) and depth_rmse against gt_depth (NaN if None)."""
+    gc = np.ascontiguousarray(gt_color, np.float64)
+    if gc.shape != (cam.height, cam.width, 3):
+        raise ValueError("evaluate_view: gt colour shape does not match the camera")
+    gd = None if gt_depth is None else np.ascontiguousarray(gt_depth, np.float64)
+    if gd is not None and gd.shape != (cam.height, cam.width):
+        raise ValueError("evaluate_view: gt depth shape does not match the camera")
+    r = EvalMetrics()
+    _check(lib().gs_evaluate_view(_vp(m.h), C.byref(pose), C.byref(cam), _p(gc), _p(gd), C.byref(r)))
+    return dict(psnr=r.psnr, ssim=r.ssim, depth_rmse=r.depth_rmse)
+
+
+def evaluate_sequence(m: GaussianMap, frames, cam: Camera) -> list[dict]:
+    """evaluate_sequence (pipeline.cpp:41-64): frames yields (pose, colour HWC, gt depth or
+    None, LiDAR points or None); without gt depth the frame's cloud is projected
+    (project_sparse_depth) as the reference does. Returns EvalRecord dicts."""
+    import time
+    start = time.monotonic()
+    out = []
+    for i, (pose, color, gt_depth, cloud) in enumerate(frames):
+        if gt_depth is None and cloud is not None:
+            gt_depth = project_sparse_depth(cloud, pose, cam, m.ctx)
+        r = evaluate_view(m, pose, cam, color, gt_depth)
+        r.update(frame=i, iteration=m.global_step, wall_time_s=time.monotonic() - start)
+        out.append(r)
+    return out
 
 
 def filter_points_by_visibility(points6: np.ndarray, m: GaussianMap, pose: Pose, cam: Camera,
