@@ -154,9 +154,13 @@ struct RenderGradients {  // rasterizer.hpp:62-64, device-resident
 class GaussianMap {
 public:
     explicit GaussianMap(Context& ctx = Context::default_context()) : ctx_(&ctx) { check(gs_map_create(ctx.get(), &h_)); }
-    ~GaussianMap() { gs_map_destroy(h_); }
+    GaussianMap(Context& ctx, gs_map* adopt) : ctx_(&ctx), h_(adopt) {}  // takes ownership of a C-ABI handle
+    ~GaussianMap() {
+        if (h_) gs_map_destroy(h_);
+    }
     GaussianMap(const GaussianMap&) = delete;
     GaussianMap& operator=(const GaussianMap&) = delete;
+    GaussianMap(GaussianMap&& o) noexcept : ctx_(o.ctx_), h_(o.h_) { o.h_ = nullptr; }
 
     size_t size() const {
         int64_t n = 0;
@@ -197,6 +201,11 @@ public:
         return e;
     }
     void raise_sh_degree(int d) { check(gs_map_raise_sh_degree(h_, d)); }
+    int max_active_degree() const {  // gaussian_map.hpp:84
+        int d = 0;
+        check(gs_map_max_active_degree(h_, &d));
+        return d;
+    }
     std::size_t prune(double opacity_threshold) {  // gaussian_map.hpp:79
         int64_t removed = 0;
         check(gs_map_prune(h_, opacity_threshold, &removed));
@@ -291,6 +300,31 @@ inline std::size_t init_gaussians_from_points(GaussianMap& map, const std::vecto
     return static_cast<std::size_t>(added);
 }
 
+class Keyframe;
+// keyframe.cpp:49-74: the points (in order) behind the near plane, outside the image, or on a
+// pixel whose rendered visibility is <= tau_alpha
+inline std::vector<ColoredPoint> filter_points_by_visibility(const std::vector<ColoredPoint>& points,
+                                                             const Keyframe& kf, const GaussianMap& map,
+                                                             const CameraModel& cam, double tau_alpha,
+                                                             ThreadPool* = nullptr);
+
+// mapper.cpp:240-246 (sh_interval = TrainConfig::sh_interval in the reference); returns the degree
+inline int maybe_upgrade_sh(GaussianMap& map, int sh_interval) {
+    int d = 0;
+    check(gs_maybe_upgrade_sh(map.get(), sh_interval, &d));
+    return d;
+}
+
+// io/checkpoint.hpp (checkpoint.cpp:17-73), format v1
+inline void save_checkpoint(const std::string& path, const GaussianMap& map) {
+    check(gs_save_checkpoint(map.get(), path.c_str()));
+}
+inline GaussianMap load_checkpoint(const std::string& path, Context& ctx = Context::default_context()) {
+    gs_map* h = nullptr;
+    check(gs_load_checkpoint(ctx.get(), path.c_str(), &h));
+    return GaussianMap(ctx, h);
+}
+
 // rasterizer.hpp:69-70
 inline RenderOutput render(const GaussianMap& map, const Pose& pose, const CameraModel& cam, ThreadPool* = nullptr) {
     RenderOutput out{make_frame(map.context()), cam};
@@ -349,6 +383,40 @@ private:
     Pose pose_;
     gs_keyframe* h_ = nullptr;
 };
+
+inline std::vector<ColoredPoint> filter_points_by_visibility(const std::vector<ColoredPoint>& points,
+                                                             const Keyframe& kf, const GaussianMap& map,
+                                                             const CameraModel& cam, double tau_alpha, ThreadPool*) {
+    std::vector<double> flat(points.size() * 6), kept(points.size() * 6);
+    for (size_t i = 0; i < points.size(); ++i) {
+        for (int k = 0; k < 3; ++k) flat[6 * i + k] = points[i].position[k];
+        for (int k = 0; k < 3; ++k) flat[6 * i + 3 + k] = points[i].color[k];
+    }
+    const gs_pose p = kf.pose().p();
+    const gs_camera c = cam.c();
+    int64_t n = 0;
+    check(gs_filter_points_by_visibility(map.get(), flat.data(), static_cast<int64_t>(points.size()), &p, &c,
+                                         tau_alpha, kept.data(), &n));
+    std::vector<ColoredPoint> out(static_cast<size_t>(n));
+    for (size_t i = 0; i < out.size(); ++i) {
+        for (int k = 0; k < 3; ++k) out[i].position[k] = kept[6 * i + k];
+        for (int k = 0; k < 3; ++k) out[i].color[k] = kept[6 * i + 3 + k];
+    }
+    return out;
+}
+
+// evaluate_sequence (pipeline.cpp:41-64), one frame: EvalRecord's metric fields
+struct EvalMetrics {
+    double psnr = 0, ssim = 0, depth_rmse = 0;
+};
+inline EvalMetrics evaluate_view(const GaussianMap& map, const Pose& pose, const CameraModel& cam,
+                                 const ImageD& gt_color, const ImageD* gt_depth) {
+    const gs_pose p = pose.p();
+    const gs_camera c = cam.c();
+    gs_eval_metrics m{};
+    check(gs_evaluate_view(map.get(), &p, &c, gt_color.data.data(), gt_depth ? gt_depth->data.data() : nullptr, &m));
+    return EvalMetrics{m.psnr, m.ssim, m.depth_rmse};
+}
 
 struct LossResult {  // mapper.hpp:52-60
     double total = 0, color_loss = 0, depth_loss = 0, l1 = 0, ssim = 0;

@@ -137,6 +137,111 @@ static void level_schedule_and_loss_decrease() {  // test_mapper.cpp:206-276
     CHECK(last < first);  // training decreases the level-0 loss
 }
 
+static Gaussian3D opaque_blob(Vec3 pos, double opacity) {  // test_keyframe.cpp:22-30
+    return make_blob(pos, opacity, {0.8, 0.2, 0.2}, std::log(0.5));
+}
+
+static void filter_points_kats() {  // test_keyframe.cpp:98-136
+    const CameraModel cam{100, 100, 31.5, 23.5, 64, 48};
+    const ImageD blank(48, 64, 3, 0.5), nodepth(48, 64, 1, 0.0);
+    Keyframe kf(Context::default_context(), Pose{}, blank, nodepth, 1, 0);
+    std::mt19937 gen(1);
+    std::uniform_real_distribution<double> u(-1, 1);
+    std::vector<ColoredPoint> pts(20);
+    for (auto& p : pts) p.position = {u(gen), u(gen), 3.0 + u(gen)};
+    GaussianMap empty;
+    CHECK(filter_points_by_visibility(pts, kf, empty, cam, 0.5).size() == pts.size());
+
+    GaussianMap map;
+    std::vector<Gaussian3D> wall;
+    for (double x = -2.0; x <= 2.0; x += 0.25)
+        for (double y = -1.5; y <= 1.5; y += 0.25) wall.push_back(opaque_blob({x, y, 4.0}, 0.95));
+    map.append(wall);
+    std::vector<ColoredPoint> q(3);
+    q[0].position = {0, 0, 3.0};
+    q[1].position = {50, 0, 3.0};
+    q[2].position = {0, 0, -3.0};
+    const auto kept = filter_points_by_visibility(q, kf, map, cam, 0.5);
+    CHECK(kept.size() == 2);
+    if (kept.size() == 2) {
+        CHECK(kept[0].position[0] == 50);
+        CHECK(kept[1].position[2] == -3.0);
+    }
+    bool threw = false;
+    try {
+        filter_points_by_visibility(q, kf, map, cam, 1.5);
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    CHECK(threw);
+}
+
+static void checkpoint_round_trip() {  // test_io.cpp:190-207
+    const CameraModel cam{100, 100, 31.5, 23.5, 64, 48};
+    GaussianMap map;
+    std::vector<Gaussian3D> gs;
+    std::mt19937 gen(4);
+    std::uniform_real_distribution<double> u(-1, 1);
+    for (int i = 0; i < 50; ++i) {
+        Gaussian3D g = make_blob({u(gen), u(gen), 3.0 + u(gen)}, 0.3 + 0.3 * (u(gen) + 1), {0.5 + 0.4 * u(gen), 0.5, 0.3});
+        g.active_degree = i % 4;
+        gs.push_back(g);
+    }
+    map.append(gs);
+    map.raise_sh_degree(2);
+    const std::string path = "/tmp/gsmap_b200_shim_ckpt.gsmap";
+    save_checkpoint(path, map);
+    const GaussianMap loaded = load_checkpoint(path);
+    CHECK(loaded.size() == map.size());
+    CHECK(loaded.max_active_degree() == 3);
+    const RenderOutput a = render(map, Pose{}, cam);
+    const RenderOutput b = render(loaded, Pose{}, cam);
+    const ImageD ca = a.color(), cb = b.color(), da = a.depth(), db = b.depth();
+    bool same = true;
+    for (size_t i = 0; i < ca.data.size(); ++i) same = same && ca.data[i] == cb.data[i];
+    for (size_t i = 0; i < da.data.size(); ++i) same = same && da.data[i] == db.data[i];
+    CHECK(same);
+    int threw = 0;
+    try {
+        load_checkpoint("/tmp/gsmap_b200_shim_missing.gsmap");
+    } catch (const std::runtime_error&) {
+        ++threw;
+    }
+    {
+        std::FILE* f = std::fopen("/tmp/gsmap_b200_shim_junk.gsmap", "w");
+        std::fputs("not a checkpoint\n", f);
+        std::fclose(f);
+    }
+    try {
+        load_checkpoint("/tmp/gsmap_b200_shim_junk.gsmap");
+    } catch (const std::runtime_error&) {
+        ++threw;
+    }
+    CHECK(threw == 2);
+}
+
+static void evaluate_and_sh_schedule() {  // test_pipeline.cpp:128-146, test_mapper.cpp:278-296
+    const CameraModel cam{55, 55, 31.5, 23.5, 64, 48};
+    GaussianMap map;
+    std::vector<Gaussian3D> gs;
+    for (double x = -0.6; x <= 0.6; x += 0.3)
+        for (double y = -0.4; y <= 0.4; y += 0.2) gs.push_back(make_blob({x, y, 3.0}, 0.6, {0.7, 0.4, 0.2}, -2.0));
+    map.append(gs);
+    const RenderOutput out = render(map, Pose{}, cam);
+    ImageD stored = out.color();
+    for (double& v : stored.data) v = std::lround(std::min(std::max(v, 0.0), 1.0) * 255.0) / 255.0;
+    const ImageD depth = out.depth();
+    const EvalMetrics m = evaluate_view(map, Pose{}, cam, stored, &depth);
+    CHECK(m.psnr == 100.0 || m.psnr > 80.0);
+    CHECK(APPROX(m.ssim, 1.0, 1e-5));
+    CHECK(APPROX(m.depth_rmse, 0.0, 1e-5));
+    CHECK(std::isnan(evaluate_view(map, Pose{}, cam, stored, nullptr).depth_rmse));
+    map.set_global_step(250);
+    CHECK(maybe_upgrade_sh(map, 100) == 2);
+    CHECK(map.max_active_degree() == 2);
+    CHECK(maybe_upgrade_sh(map, 0) == 2);
+}
+
 int main() {
     struct Case {
         const char* name;
@@ -146,7 +251,10 @@ int main() {
                  {"two stacked Gaussians composite front to back", two_stacked},
                  {"render_backward known answers and shape checks", backward_kats},
                  {"camera validation and pyramid scaling", camera_validation},
-                 {"coarse-to-fine schedule and loss decrease", level_schedule_and_loss_decrease}};
+                 {"coarse-to-fine schedule and loss decrease", level_schedule_and_loss_decrease},
+                 {"filter_points_by_visibility known answers", filter_points_kats},
+                 {"checkpoint round trip renders bit-exactly", checkpoint_round_trip},
+                 {"evaluation sentinel and SH schedule", evaluate_and_sh_schedule}};
     for (const auto& c : cases) {
         const int before = g_fail;
         try {

@@ -16,4 +16,4 @@ def test_cpp_shim_kats():
                        timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 6
+    assert r.stdout.count("PASS") == 9
