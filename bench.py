@@ -8,6 +8,8 @@ view per iteration at its scheduled pyramid level) and Mpix/s, 1M Gaussians at 1
   python bench.py [--steps K] [--warmup W] [--impl ours|reference] [--sh-degree 0|3]
   torchrun --nproc-per-node N bench.py --gpus N      (C4: 8-view batch sharded over N GPUs,
                                                       NCCL all-reduce of the gradient SoA)
+  python bench.py --workload c5                       (C5: the mapping loop growing a map from
+                                                      8 LiDAR keyframes at 1920x1080; §8f rows)
 
 Workload: synthetic scene = proj/src/io/synthetic.cpp restated (fixtures/),
 focal 0.8125*W, extent 18, line trajectory, 8 frames, seed 1, LiDAR noise 0.06 m; the
@@ -48,6 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines)")
     ap.add_argument("--batch", action="store_true", help="C4 batch path even at world size 1 (testing)")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
+                    help="c5: the single-thread mapping loop (integrate -> train -> housekeeping) at 1920x1080")
+    ap.add_argument("--c5-gaussians", type=int, default=2_000_000, help="C5 GT scene size")
+    ap.add_argument("--c5-budget", type=int, default=60, help="C5 iter_budget per keyframe (keyframe.hpp:43)")
     return ap.parse_args()
 
 
@@ -398,6 +404,97 @@ def cpu_sample(scene, train, gt_levels, threads=0):
             "seconds": round(dt, 2)}
 
 
+# ----------------------------------------------------------------------------- C5 mapping loop
+def run_c5(args):
+    """the reference's single-thread mapping loop (pipeline.cpp:130-203)
+    over the device map, growing it from 8 LiDAR keyframes at 1920x1080 (GT scene of
+    --c5-gaussians). Integrate = filter_points_by_visibility + init_gaussians_from_points +
+    project_sparse_depth + pyramid + one step; then sampled steps until every keyframe's
+    iter_budget is spent; housekeeping = maybe_upgrade_sh (300) + prune every 50 steps. Then
+    evaluate_sequence over the 8 frames and a checkpoint save + load of the final map.
+    value = train steps / wall time of the whole loop (integration and housekeeping inside)."""
+    import torch
+    from fixtures import pyfixture as F
+    from paper_2411_02703_b200 import gsmap as G
+    from paper_2411_02703_b200.mapping import MappingConfig, MappingLoop
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx = G.Context(dev, stream.cuda_stream)
+    t = time.time()
+    scene = F.Scene(n_gaussians=args.c5_gaussians, width=1920, height=1080, n_frames=N_FRAMES, seed=1)
+    clouds = [scene.cloud(f) for f in range(N_FRAMES)]
+    fx, fy, cx, cy, W, H = scene.camera
+    cam = G.Camera(fx, fy, cx, cy, W, H)
+    poses = [G.Pose(*p) for p in scene.poses]
+    gt_map = G.GaussianMap(ctx, scene.gaussians)
+    fr = G.RenderOutput(ctx)
+    colors = []
+    for f in range(N_FRAMES):
+        G.render(gt_map, poses[f], cam, fr)
+        colors.append(np.floor(np.clip(fr.color, 0.0, 1.0) * 255.0 + 0.5) / 255.0)  # stored as 8-bit images
+    del gt_map, fr
+    t_fix = time.time() - t
+    mk = lambda budget: MappingConfig(iter_budget=budget, train=G.TrainConfig.make(0.2, 0.5, LEVELS))
+    # warm-up: a short loop on a throw-away map (allocations, CUB temp sizes, first launches)
+    MappingLoop(G.GaussianMap(ctx), cam, mk(3)).run(list(zip(poses, colors, clouds))[:3])
+    torch.cuda.synchronize()
+    m = G.GaussianMap(ctx)
+    loop = MappingLoop(m, cam, mk(args.c5_budget), timed=True)
+    launches0 = ctx.launches
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        steps = loop.run(zip(poses, colors, clouds))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    dev_ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    # evaluate_sequence (gt depth = the projected cloud, as without a gt depth file)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    recs = G.evaluate_sequence(m, [(poses[f], colors[f], None, clouds[f]) for f in range(N_FRAMES)], cam)
+    torch.cuda.synchronize()
+    t_eval = time.perf_counter() - t
+    path = os.path.join("/tmp", f"gsmap_c5_{os.getpid()}.gsmap")
+    t = time.perf_counter()
+    m.save_checkpoint(path)
+    t_save = time.perf_counter() - t
+    t = time.perf_counter()
+    m2 = G.load_checkpoint(path, ctx)
+    t_load = time.perf_counter() - t
+    ck_bytes = os.path.getsize(path)
+    os.remove(path)
+    assert len(m2) == len(m)
+    del m2
+    rows = {k: {"calls": loop.calls[k], "ms_total": round(loop.times[k] * 1e3, 2),
+                "ms_per_call": round(loop.times[k] * 1e3 / loop.calls[k], 3)} for k in sorted(loop.times)}
+    rows["host_bookkeeping"] = {"ms_total": round((wall - sum(loop.times.values())) * 1e3, 2)}
+    psnr = [r["psnr"] for r in recs]
+    return {"metric": "C5 mapping loop: train iterations/s including keyframe integration and housekeeping",
+            "value": round(steps / wall, 3), "unit": "iters/s", "n_gpus": 1, "steps": steps, "warmup": 1,
+            "ms_per_step": round(wall / steps * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp64 geometry, fp64 transmittance)",
+            "data": "synthetic (reference synthetic.cpp scene; the map grows from the frames' LiDAR clouds)",
+            "config": {"workload": "C5: map expansion stream, 8 keyframes, 1920x1080, 3-level pyramid",
+                       "gt_gaussians": args.c5_gaussians, "iter_budget": args.c5_budget, "tau_alpha": 0.5,
+                       "prune_interval": 50, "sh_interval": 300, "cloud_points": [len(c) for c in clouds]},
+            "device_ms": round(dev_ms, 2), "wall_ms": round(wall * 1e3, 2), "gpu_launches": launches,
+            "map": {"final_gaussians": len(m), "added_per_keyframe": loop.added, "pruned": loop.pruned,
+                    "max_sh_degree": m.max_active_degree()},
+            "rows": rows,
+            "evaluate": {"frames": len(recs), "ms_per_frame": round(t_eval * 1e3 / len(recs), 3),
+                         "mean_psnr": round(float(np.mean(psnr)), 4),
+                         "mean_ssim": round(float(np.mean([r["ssim"] for r in recs])), 5)},
+            "checkpoint": {"bytes": ck_bytes, "save_ms": round(t_save * 1e3, 1), "load_ms": round(t_load * 1e3, 1),
+                           "save_gbs": round(ck_bytes / t_save / 1e9, 3), "load_gbs": round(ck_bytes / t_load / 1e9, 3)},
+            "clocks": clk.summary(), "fixture_s": round(t_fix, 2)}
+
+
 def run_reference(args, rank):
     """--impl reference: the reference's CPU path (oracle restatement; the C++ reference itself
     cannot be built here: no Eigen/libpng/doctest) on this host's cores."""
@@ -446,6 +543,13 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.workload == "c5":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "C5 is measured on the device arm only "
+                              "(the oracle's O(n^2) 3-NN init at 566k points per keyframe does not finish)"}))
+            return
+        print(json.dumps(run_c5(args)), flush=True)
+        return
     if args.impl == "reference":
         res = run_reference(args, rank)
         if res is not None:

@@ -256,6 +256,9 @@ class OracleMap:
     def raise_sh_degree(self, d: int):
         lib().orc_map_raise_sh_degree(C.c_void_p(self.h), d)
 
+    def max_active_degree(self) -> int:
+        return lib().orc_map_max_active_degree(C.c_void_p(self.h))
+
     def maybe_upgrade_sh(self, interval: int) -> int:
         return lib().orc_maybe_upgrade_sh(C.c_void_p(self.h), interval)
 

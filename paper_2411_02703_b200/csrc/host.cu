@@ -215,6 +215,22 @@ struct gs_map {
     int64_t adam_count = 0;  // updates applied to this map; Gaussian i's Adam step = adam_count - birth[i]
     DevBuf minmax;
 
+    int min_degree = 0;
+    // prune's compaction target: a second set of planes of the same capacity, swapped with the
+    // live one (no per-prune cudaMalloc / cudaFree of ~1.8 GB at 2.5M capacity)
+    struct Planes {
+        float *params = nullptr, *m = nullptr, *v = nullptr;
+        int32_t* birth = nullptr;
+        int8_t* degree = nullptr;
+        int64_t cap = 0;
+        void free_all() {
+            for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
+                            static_cast<void*>(birth), static_cast<void*>(degree)})
+                if (p) cudaFree(p);
+            *this = Planes{};
+        }
+    } spare;
+
     void free_all() {
         for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
                         static_cast<void*>(birth), static_cast<void*>(degree)})
@@ -222,11 +238,16 @@ struct gs_map {
         params = m = v = nullptr;
         birth = nullptr;
         degree = nullptr;
+        spare.free_all();
     }
     void recompute_max_degree() {
-        int d = 0;
-        for (int8_t x : deg_host) d = std::max<int>(d, x);
+        int d = 0, lo = 3;
+        for (int8_t x : deg_host) {
+            d = std::max<int>(d, x);
+            lo = std::min<int>(lo, x);
+        }
         max_degree = d;
+        min_degree = deg_host.empty() ? 0 : lo;
     }
 };
 
@@ -354,7 +375,7 @@ void map_reserve(gs_map* M, int64_t need) {
         ck(cudaMemcpyAsync(d, M->degree, sizeof(int8_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy degree");
     }
     ck(cudaStreamSynchronize(st), "sync");
-    M->free_all();
+    M->free_all();  // also drops prune's spare planes (sized for the old capacity)
     M->params = p; M->m = m; M->v = v; M->birth = s; M->degree = d;
     M->cap = nc;
 }
@@ -1106,6 +1127,10 @@ int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // m
         }
         const int target = static_cast<int>(std::min<int64_t>(3, M->global_step / sh_interval));
         const int d = std::clamp(target, 0, 3);
+        if (d <= M->min_degree) {  // every Gaussian is already there (the common case): O(1)
+            *degree = target;
+            return;
+        }
         bool change = false;
         for (auto& x : M->deg_host)
             if (x < d) {
@@ -1418,39 +1443,39 @@ int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // ga
         cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st);
         ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st), "scan");
         int32_t kept = 0;
-        std::vector<int32_t> flags(n);
         ck(cudaMemcpyAsync(&kept, pos.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaMemcpyAsync(flags.data(), keep.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
         C->launched(2);
         if (kept == n) return;
-        // stable compaction into fresh arrays of the same capacity
+        // stable compaction into the spare planes, then swap (entries past `kept` are don't-care:
+        // append / init reset the optimizer state of every range they fill)
         const int64_t cap = M->cap;
-        float *p = nullptr, *m = nullptr, *v = nullptr;
-        int32_t* b = nullptr;
-        int8_t* d = nullptr;
-        ck(cudaMalloc(&p, sizeof(float) * kNumParams * cap), "cudaMalloc params");
-        ck(cudaMalloc(&m, sizeof(float) * kNumParams * cap), "cudaMalloc adam m");
-        ck(cudaMalloc(&v, sizeof(float) * kNumParams * cap), "cudaMalloc adam v");
-        ck(cudaMalloc(&b, sizeof(int32_t) * cap), "cudaMalloc birth");
-        ck(cudaMalloc(&d, sizeof(int8_t) * cap), "cudaMalloc degree");
-        ck(cudaMemsetAsync(p, 0, sizeof(float) * kNumParams * cap, st), "memset");
-        ck(cudaMemsetAsync(m, 0, sizeof(float) * kNumParams * cap, st), "memset");
-        ck(cudaMemsetAsync(v, 0, sizeof(float) * kNumParams * cap, st), "memset");
-        launch_compact(M->params, p, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
-        launch_compact(M->m, m, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
-        launch_compact(M->v, v, cap, cap, kNumParams, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
-        launch_compact(M->birth, b, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
-        launch_compact(M->degree, d, n, keep.as<int32_t>(), pos.as<int32_t>(), st);
+        auto& S = M->spare;
+        if (S.cap != cap) {
+            S.free_all();
+            ck(cudaMalloc(&S.params, sizeof(float) * kNumParams * cap), "cudaMalloc params");
+            ck(cudaMalloc(&S.m, sizeof(float) * kNumParams * cap), "cudaMalloc adam m");
+            ck(cudaMalloc(&S.v, sizeof(float) * kNumParams * cap), "cudaMalloc adam v");
+            ck(cudaMalloc(&S.birth, sizeof(int32_t) * cap), "cudaMalloc birth");
+            ck(cudaMalloc(&S.degree, sizeof(int8_t) * cap), "cudaMalloc degree");
+            S.cap = cap;
+        }
+        const int32_t* kp = keep.as<int32_t>();
+        const int32_t* ps = pos.as<int32_t>();
+        launch_compact(M->params, S.params, cap, cap, kNumParams, n, kp, ps, st);
+        launch_compact(M->m, S.m, cap, cap, kNumParams, n, kp, ps, st);
+        launch_compact(M->v, S.v, cap, cap, kNumParams, n, kp, ps, st);
+        launch_compact(M->birth, S.birth, n, kp, ps, st);
+        launch_compact(M->degree, S.degree, n, kp, ps, st);
         C->launched(5);
+        std::swap(M->params, S.params);
+        std::swap(M->m, S.m);
+        std::swap(M->v, S.v);
+        std::swap(M->birth, S.birth);
+        std::swap(M->degree, S.degree);
+        M->deg_host.resize(kept);
+        ck(cudaMemcpyAsync(M->deg_host.data(), M->degree, kept, cudaMemcpyDeviceToHost, st), "d2h degree");
         ck(cudaStreamSynchronize(st), "sync");
-        M->free_all();
-        M->params = p; M->m = m; M->v = v; M->birth = b; M->degree = d;
-        std::vector<int8_t> deg;
-        deg.reserve(kept);
-        for (int i = 0; i < n; ++i)
-            if (flags[i]) deg.push_back(M->deg_host[i]);
-        M->deg_host = std::move(deg);
         M->recompute_max_degree();
         M->n = kept;
         *removed = n - kept;

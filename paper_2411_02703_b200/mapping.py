@@ -1,0 +1,122 @@
+"""The reference's single-thread mapping loop around the hot path, driving the device map.
+
+This mirrors PipelineState's optimizer role (pipeline.cpp:130-180, single_thread mode
+:196-203). It is not a pipeline: keyframe admission, the voxel store, sequence IO and threads
+stay out of scope. Each keyframe arrives with its pose, colour image and LiDAR
+cloud (the reference drains the voxel store instead: `kf->points`, pipeline.cpp:116):
+
+  integrate_keyframe (pipeline.cpp:148-160):
+      filter_points_by_visibility -> init_gaussians_from_points   (gs_map_integrate_points)
+      project_sparse_depth + build_keyframe_pyramid               (gs_project_sparse_depth, gs_keyframe_create)
+      one train_keyframe_step + housekeeping
+  optimize_once (pipeline.cpp:163-173): a uniformly sampled keyframe with budget left
+      (KeyframeQueue::sample_for_optimization, keyframe.cpp:122-138) -> train step + housekeeping
+  housekeeping (pipeline.cpp:133-145): maybe_upgrade_sh; prune every prune_interval steps
+
+Every call runs on the device; the loop itself is host bookkeeping.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import gsmap as G
+
+
+@dataclass
+class MappingConfig:
+    """The PipelineConfig / KeyframeConfig / TrainConfig fields the loop reads (defaults:
+    keyframe.hpp:41-43, config.hpp:27, mapper.hpp:17-24)."""
+    iter_budget: int = 60
+    tau_alpha: float = 0.5
+    prune_interval: int = 50
+    prune_threshold: float = 0.005
+    sh_interval: int = 300
+    seed: int = 1
+    train: G.TrainConfig = field(default_factory=G.TrainConfig.make)
+
+
+class _Entry:
+    __slots__ = ("kf", "remaining", "index")
+
+    def __init__(self, kf, remaining, index):
+        self.kf, self.remaining, self.index = kf, remaining, index
+
+
+class MappingLoop:
+    def __init__(self, m: G.GaussianMap, cam: G.Camera, cfg: MappingConfig | None = None, timed: bool = False):
+        self.m, self.cam, self.cfg = m, cam, cfg or MappingConfig()
+        self.active: list[_Entry] = []
+        self.rng = np.random.default_rng(self.cfg.seed)
+        self.reports: list[tuple[int, dict]] = []  # (keyframe index, StepReport)
+        self.timed = timed
+        self.times: dict[str, float] = {}
+        self.calls: dict[str, int] = {}
+        self.added: list[int] = []
+        self.pruned = 0
+        self.n_keyframes = 0
+
+    def _clock(self, name, fn, *a):
+        if not self.timed:
+            return fn(*a)
+        import torch
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        r = fn(*a)
+        torch.cuda.synchronize()
+        self.times[name] = self.times.get(name, 0.0) + time.perf_counter() - t
+        self.calls[name] = self.calls.get(name, 0) + 1
+        return r
+
+    def _step(self, e: _Entry):
+        rep = self._clock("train_step", G.train_keyframe_step, self.m, e.kf, self.cfg.train, self.cam)
+        if rep is not None:
+            self.reports.append((e.index, rep))
+            self.housekeeping()
+        return rep
+
+    def housekeeping(self):
+        self._clock("maybe_upgrade_sh", self.m.maybe_upgrade_sh, self.cfg.sh_interval)
+        step = self.m.global_step
+        if self.cfg.prune_interval > 0 and step > 0 and step % self.cfg.prune_interval == 0:
+            self.pruned += self._clock("prune", self.m.prune, self.cfg.prune_threshold)
+
+    def integrate_keyframe(self, pose: G.Pose, color: np.ndarray, cloud6: np.ndarray) -> G.Keyframe:
+        cfg = self.cfg
+        self.added.append(self._clock("integrate_points", self.m.integrate_points, cloud6, pose, self.cam,
+                                      cfg.tau_alpha))
+        sparse = self._clock("project_sparse_depth", G.project_sparse_depth, cloud6, pose, self.cam, self.m.ctx)
+        kf = self._clock("build_keyframe_pyramid", lambda: G.Keyframe(
+            pose, color, sparse, initial_iters=cfg.iter_budget, levels=cfg.train.pyramid_levels, ctx=self.m.ctx))
+        e = _Entry(kf, cfg.iter_budget, self.n_keyframes)
+        self.n_keyframes += 1
+        if e.remaining > 0:
+            e.remaining -= 1
+            self._step(e)
+        if e.remaining > 0:
+            self.active.append(e)
+        return kf
+
+    def optimize_once(self) -> bool:
+        eligible = [i for i, e in enumerate(self.active) if e.remaining > 0]
+        if not eligible:
+            return False
+        i = eligible[int(self.rng.integers(len(eligible)))]
+        e = self.active[i]
+        e.remaining -= 1
+        if e.remaining == 0:
+            del self.active[i]
+        self._step(e)
+        return True
+
+    def run(self, frames) -> int:
+        """frames: iterable of (pose, colour HWC, cloud [n][6]); integrates every frame, then
+        optimizes until every budget is spent. Returns the number of train steps."""
+        n0 = len(self.reports)
+        for pose, color, cloud in frames:
+            self.integrate_keyframe(pose, color, cloud)
+        while self.optimize_once():
+            pass
+        return len(self.reports) - n0

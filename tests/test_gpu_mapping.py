@@ -1,0 +1,97 @@
+"""The single-thread mapping loop (pipeline.cpp:130-203) over the device map against the same
+loop over the CPU oracle: integrate (filter -> init -> sparse depth -> pyramid -> one step),
+sampled optimisation, SH schedule and periodic prune."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from tests._common import gpu_cam, gpu_pose, round32
+
+pytestmark = pytest.mark.gpu
+
+
+def G():
+    from paper_2411_02703_b200 import gsmap
+    return gsmap
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+class OracleLoop:
+    """The same bookkeeping as paper_2411_02703_b200.mapping.MappingLoop over the oracle."""
+
+    def __init__(self, cam, cfg, mcfg):
+        self.m, self.cam, self.cfg, self.mcfg = O.OracleMap(), cam, cfg, mcfg
+        self.active, self.rng, self.reports, self.added, self.pruned, self.n = [], np.random.default_rng(mcfg.seed), [], [], 0, 0
+
+    def step(self, e):
+        r = O.train_keyframe_step(self.m, e[0], self.cfg, self.cam)
+        if r is not None:
+            self.reports.append((e[2], r))
+            self.m.maybe_upgrade_sh(self.mcfg.sh_interval)
+            s = self.m.global_step
+            if self.mcfg.prune_interval > 0 and s > 0 and s % self.mcfg.prune_interval == 0:
+                self.pruned += self.m.prune(self.mcfg.prune_threshold)
+
+    def integrate(self, pose, color, cloud):
+        kept = O.filter_points_by_visibility(cloud, self.m, pose, self.cam, self.mcfg.tau_alpha)
+        self.added.append(self.m.init_from_points(cloud[kept]) if len(kept) else 0)
+        sparse = O.project_sparse_depth(cloud, pose, self.cam)
+        e = [O.Keyframe(pose, color, sparse, self.mcfg.iter_budget, self.cfg.pyramid_levels), self.mcfg.iter_budget, self.n]
+        self.n += 1
+        e[1] -= 1
+        self.step(e)
+        if e[1] > 0:
+            self.active.append(e)
+
+    def optimize_once(self):
+        eligible = [i for i, e in enumerate(self.active) if e[1] > 0]
+        if not eligible:
+            return False
+        i = eligible[int(self.rng.integers(len(eligible)))]
+        e = self.active[i]
+        e[1] -= 1
+        if e[1] == 0:
+            del self.active[i]
+        self.step(e)
+        return True
+
+
+def test_mapping_loop_tracks_oracle():
+    from fixtures import pyfixture as F
+    from paper_2411_02703_b200.mapping import MappingConfig, MappingLoop
+    scene = F.Scene(n_gaussians=3000, width=160, height=128, n_frames=3, seed=1)
+    cam = O.camera(*scene.camera)
+    poses = [O.pose(p[0], p[1], p[2], p[3], t=p[4:7]) for p in scene.poses]
+    gt = O.OracleMap(round32(scene.gaussians))
+    colors = [f32(O.render(gt, p, cam).color) for p in poses]
+    clouds = [scene.cloud(f) for f in range(3)]
+    mcfg = MappingConfig(iter_budget=6, prune_interval=5, prune_threshold=0.098, sh_interval=4, seed=3,
+                         train=G().TrainConfig.make(0.2, 0.5, 2))
+    ocfg = O.make_cfg(0.2, 0.5, 2)
+    gm = G().GaussianMap(None)
+    loop = MappingLoop(gm, gpu_cam(cam), mcfg)
+    ref = OracleLoop(cam, ocfg, mcfg)
+    for f in range(3):
+        loop.integrate_keyframe(gpu_pose(poses[f]), colors[f], clouds[f])
+        ref.integrate(poses[f], colors[f], clouds[f])
+        assert loop.added == ref.added
+        assert len(gm) == len(ref.m)
+    assert ref.added[0] == len(clouds[0]) and 0 < ref.added[1] < len(clouds[1])
+    while True:
+        a, b = loop.optimize_once(), ref.optimize_once()
+        assert a == b
+        if not a:
+            break
+    assert len(loop.reports) == len(ref.reports) == 18 and gm.global_step == ref.m.global_step == 18
+    for (ka, ra), (kb, rb) in zip(loop.reports, ref.reports):
+        assert ka == kb and ra["level"] == rb["level"]
+        assert ra["loss"] == pytest.approx(rb["loss"], rel=2e-3)
+    assert ref.pruned > 0 and loop.pruned == ref.pruned and len(gm) == len(ref.m)
+    assert gm.max_active_degree() == ref.m.max_active_degree() == 3
+    np.testing.assert_array_equal(gm.gaussians["degree"], ref.m.gaussians["degree"])
+    lr = np.array([1.6e-4 * ref.m.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
+    d = np.abs(gm.gaussians["p"] - ref.m.gaussians["p"])
+    assert np.mean(d <= 0.05 * lr + 1e-6) > 0.95
