@@ -23,6 +23,7 @@ Inputs (1M-Gaussian params + Adam state ~ 240 MB at d=0) exceed the 126 MB L2: n
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -54,6 +55,7 @@ def parse():
                     help="c5: the single-thread mapping loop (integrate -> train -> housekeeping) at 1920x1080")
     ap.add_argument("--c5-gaussians", type=int, default=2_000_000, help="C5 GT scene size")
     ap.add_argument("--c5-budget", type=int, default=60, help="C5 iter_budget per keyframe (keyframe.hpp:43)")
+    ap.add_argument("--c5-phases", action="store_true", help="C5: per-phase event table of the integration calls")
     return ap.parse_args()
 
 
@@ -232,6 +234,8 @@ def run_ours(args, rank, world):
         torch.cuda.cudart().cudaProfilerStart()
     launches0 = ctx.launches
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.freeze()  # setup objects leave the collector's generations: no multi-ms gen-2 pauses in the timed loop
     with ClockSampler(dev) as clk:
         e0.record(stream)
         views = pix = 0
@@ -442,8 +446,12 @@ def run_c5(args):
     torch.cuda.synchronize()
     m = G.GaussianMap(ctx)
     loop = MappingLoop(m, cam, mk(args.c5_budget), timed=True)
+    if args.c5_phases:
+        ctx.profile(True)  # per-phase CUDA-event table of the integration calls (train steps included)
     launches0 = ctx.launches
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.freeze()  # setup objects leave the collector's generations: no multi-ms gen-2 pauses in the timed loop
     with ClockSampler(dev) as clk:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
@@ -454,6 +462,11 @@ def run_c5(args):
         wall = time.perf_counter() - w0
     dev_ms = e0.elapsed_time(e1)
     launches = ctx.launches - launches0
+    phases = None
+    if args.c5_phases:
+        phases = {k: {"ms": round(v[0], 2), "calls": v[1]} for k, v in ctx.profile_read().items()
+                  if k.startswith("kf_") or k == "map_reserve"}
+        ctx.profile(False)
     # evaluate_sequence (gt depth = the projected cloud, as without a gt depth file)
     torch.cuda.synchronize()
     t = time.perf_counter()
@@ -486,7 +499,7 @@ def run_c5(args):
             "device_ms": round(dev_ms, 2), "wall_ms": round(wall * 1e3, 2), "gpu_launches": launches,
             "map": {"final_gaussians": len(m), "added_per_keyframe": loop.added, "pruned": loop.pruned,
                     "max_sh_degree": m.max_active_degree()},
-            "rows": rows,
+            "rows": rows, "integrate_phases": phases,
             "evaluate": {"frames": len(recs), "ms_per_frame": round(t_eval * 1e3 / len(recs), 3),
                          "mean_psnr": round(float(np.mean(psnr)), 4),
                          "mean_ssim": round(float(np.mean([r["ssim"] for r in recs])), 5)},

@@ -162,6 +162,14 @@ int gs_filter_points_by_visibility(gs_map* map, const double* points6, int64_t n
    filter_points_by_visibility then init_gaussians_from_points; *added = the kept count */
 int gs_map_integrate_points(gs_map* map, const double* points6, int64_t n, const gs_pose* pose,
                             const gs_camera* cam, double tau_alpha, int64_t* added);
+/* integrate_keyframe (pipeline.cpp:148-155) in one call: the frame's cloud is uploaded once;
+   filter_points_by_visibility -> init_gaussians_from_points append to the map, and the new
+   keyframe (*out_kf, destroy with gs_keyframe_destroy) gets project_sparse_depth of the same
+   cloud and the colour image (H x W x 3 HWC) as its pyramid (build_keyframe_pyramid).
+   *added = Gaussians appended. The step that follows is the caller's (gs_train_step). */
+int gs_integrate_keyframe(gs_map* map, const gs_pose* pose, const gs_camera* cam, const double* color,
+                          const double* points6, int64_t n, double tau_alpha, int32_t initial_iters, int32_t levels,
+                          gs_keyframe** out_kf, int64_t* added);
 /* GaussianMap::prune (gaussian_map.hpp:79, gaussian_map.cpp:56-73): drop every Gaussian with
    sigmoid(opacity_logit) < threshold, compacting parameters and optimizer state in order;
    threshold outside (0, 1) -> GS_EINVAL. *removed = the number dropped. */

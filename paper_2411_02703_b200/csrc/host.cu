@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <optional>
 #include <fstream>
 #include <limits>
 #include <sstream>
@@ -58,23 +59,37 @@ int guard(F&& f) {
     }
 }
 
-// Grow-only device buffer (no per-iteration cudaMalloc on the hot path).
+// Grow-only device buffer (no per-iteration cudaMalloc on the hot path). Buffers of objects
+// created and destroyed in the mapping loop (keyframes) come from the device's stream-ordered
+// memory pool instead (`pool` = the stream they are used on): their frees return memory to the
+// pool without the device-wide synchronisation and unmapping of cudaFree (~50 ms per keyframe).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t pool = nullptr;
+    bool pooled = false;
     template <class T>
     T* as() const { return static_cast<T*>(p); }
     void ensure(size_t need) {
         if (need <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
+        release();
         const size_t alloc = std::max<size_t>(need + need / 4, 256);
-        ck(cudaMalloc(&p, alloc), "cudaMalloc");
+        if (pool) {
+            ck(cudaMallocAsync(&p, alloc, pool), "cudaMallocAsync");
+            // usable by every stream from here on (keyframe uploads run on the copy stream)
+            ck(cudaStreamSynchronize(pool), "sync");
+            pooled = true;
+        } else {
+            ck(cudaMalloc(&p, alloc), "cudaMalloc");
+            pooled = false;
+        }
         bytes = alloc;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pooled) cudaFreeAsync(p, pool);
+            else cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -130,11 +145,20 @@ int n_active_planes(int max_degree) { return kGeomParams + 3 * (max_degree + 1) 
 }  // namespace
 
 // ============================================================================ handles
+// grow-only scratch of the per-keyframe mapping calls (filter / init / sparse depth / prune):
+// one slot per role, so nested calls never share a slot and no call pays cudaMalloc twice
+enum ScratchSlot {
+    kScPoints, kScKept, kScKeep, kScPos, kScKeys, kScKeys2, kScIdx, kScIdx2, kScBBox, kScHashK, kScHashV,
+    kScDepth, kScColor, kScPruneKeep, kScPrunePos, kScPruneTmp, kNumScratch
+};
+
 struct gs_context {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     DevBuf cub_tmp;
+    DevBuf scratch[kNumScratch];
+    DevBuf& sc(ScratchSlot s) { return scratch[s]; }
     PinnedBuf pinned;
     cudaStream_t copy_stream = nullptr;  // host uploads (overlap the compute stream)
     bool defer_sync = false;             // diagnostics: train steps skip the loss read-back
@@ -200,6 +224,20 @@ struct Scope {
 };
 }  // namespace
 
+// Map-sized arrays (planes, Adam state, gradients) and the mapping calls' scratch come from the device's
+// stream-ordered pool on the context stream: the map grows in the mapping loop, and pooled
+// frees / reallocations skip cudaFree's device-wide synchronisation and unmapping (measured:
+// 16 ms to 1 s per growth with cudaMalloc / cudaFree, run to run).
+template <class T>
+T* pool_alloc(size_t count, cudaStream_t st, const char* what) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, sizeof(T) * count, st), what);
+    return static_cast<T*>(p);
+}
+inline void pool_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
 struct gs_map {
     gs_context* ctx = nullptr;
     int64_t n = 0, cap = 0;
@@ -216,29 +254,14 @@ struct gs_map {
     DevBuf minmax;
 
     int min_degree = 0;
-    // prune's compaction target: a second set of planes of the same capacity, swapped with the
-    // live one (no per-prune cudaMalloc / cudaFree of ~1.8 GB at 2.5M capacity)
-    struct Planes {
-        float *params = nullptr, *m = nullptr, *v = nullptr;
-        int32_t* birth = nullptr;
-        int8_t* degree = nullptr;
-        int64_t cap = 0;
-        void free_all() {
-            for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
-                            static_cast<void*>(birth), static_cast<void*>(degree)})
-                if (p) cudaFree(p);
-            *this = Planes{};
-        }
-    } spare;
-
     void free_all() {
+        cudaStream_t st = ctx->stream;
         for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
                         static_cast<void*>(birth), static_cast<void*>(degree)})
-            if (p) cudaFree(p);
+            pool_free(p, st);
         params = m = v = nullptr;
         birth = nullptr;
         degree = nullptr;
-        spare.free_all();
     }
     void recompute_max_degree() {
         int d = 0, lo = 3;
@@ -300,10 +323,10 @@ struct gs_grads {
     void ensure(int64_t need) {
         if (need <= cap) return;
         if (external) fail(GS_EINVAL, "gs_grads: external buffer too small for the map");
-        if (planes) cudaFree(planes);
+        pool_free(planes, ctx->stream);
         planes = nullptr;
         const int64_t c = (std::max<int64_t>(need + need / 4, 1024) + 63) / 64 * 64;
-        ck(cudaMalloc(&planes, sizeof(float) * kNumParams * c), "cudaMalloc grads");
+        planes = pool_alloc<float>(kNumParams * c, ctx->stream, "alloc grads");
         ck(cudaMemsetAsync(planes, 0, sizeof(float) * kNumParams * c, ctx->stream), "memset grads");
         cap = c;
     }
@@ -350,17 +373,18 @@ namespace {
 
 void map_reserve(gs_map* M, int64_t need) {
     if (need <= M->cap) return;
+    Scope sc(M->ctx, "map_reserve");
     // multiples of 64: every plane base stays 16-byte aligned (vectorised Adam)
     const int64_t nc = (std::max<int64_t>(need, M->cap + M->cap / 2) + 63) / 64 * 64;
     cudaStream_t st = M->ctx->stream;
     float *p = nullptr, *m = nullptr, *v = nullptr;
     int32_t* s = nullptr;
     int8_t* d = nullptr;
-    ck(cudaMalloc(&p, sizeof(float) * kNumParams * nc), "cudaMalloc params");
-    ck(cudaMalloc(&m, sizeof(float) * kNumParams * nc), "cudaMalloc adam m");
-    ck(cudaMalloc(&v, sizeof(float) * kNumParams * nc), "cudaMalloc adam v");
-    ck(cudaMalloc(&s, sizeof(int32_t) * nc), "cudaMalloc step");
-    ck(cudaMalloc(&d, sizeof(int8_t) * nc), "cudaMalloc degree");
+    p = pool_alloc<float>(kNumParams * nc, st, "alloc params");
+    m = pool_alloc<float>(kNumParams * nc, st, "alloc adam m");
+    v = pool_alloc<float>(kNumParams * nc, st, "alloc adam v");
+    s = pool_alloc<int32_t>(nc, st, "alloc birth");
+    d = pool_alloc<int8_t>(nc, st, "alloc degree");
     ck(cudaMemsetAsync(m, 0, sizeof(float) * kNumParams * nc, st), "memset");
     ck(cudaMemsetAsync(v, 0, sizeof(float) * kNumParams * nc, st), "memset");
     ck(cudaMemsetAsync(p, 0, sizeof(float) * kNumParams * nc, st), "memset");
@@ -375,7 +399,7 @@ void map_reserve(gs_map* M, int64_t need) {
         ck(cudaMemcpyAsync(d, M->degree, sizeof(int8_t) * M->n, cudaMemcpyDeviceToDevice, st), "copy degree");
     }
     ck(cudaStreamSynchronize(st), "sync");
-    M->free_all();  // also drops prune's spare planes (sized for the old capacity)
+    M->free_all();
     M->params = p; M->m = m; M->v = v; M->birth = s; M->degree = d;
     M->cap = nc;
 }
@@ -740,11 +764,14 @@ void keyframe_build(gs_keyframe* K, const float* color0, const float* depth0, in
     if (levels < 0) fail(GS_EINVAL, "build_pyramid: levels must be >= 0");
     if (h < (1 << levels) || w < (1 << levels)) fail(GS_EINVAL, "build_pyramid: image too small for requested levels");
     cudaStream_t st = K->ctx->stream;
-    K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(h) * w);  // host-upload staging, sized once
     K->hs.assign(levels + 1, 0);
     K->ws.assign(levels + 1, 0);
     K->color.resize(levels + 1);
     K->depth.resize(levels + 1);
+    for (auto* v : {&K->color, &K->depth})
+        for (DevBuf& b : *v) b.pool = st;
+    K->stage.pool = st;
+    if (!device_src) K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(h) * w);  // host-upload staging
     int ch = h, cw = w;
     for (int l = 0; l <= levels; ++l) {
         K->hs[l] = ch;
@@ -805,12 +832,19 @@ int gs_context_create(int device, void* stream, gs_context** out) {
         C->device = device;
         try {
             C->use();
+            // freed pool memory stays reserved for reuse (keyframes come and go in the mapping loop)
+            cudaMemPool_t mp = nullptr;
+            if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
             if (stream) {
                 C->stream = static_cast<cudaStream_t>(stream);
             } else {
                 ck(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking), "cudaStreamCreate");
                 C->own_stream = true;
             }
+            for (DevBuf& b : C->scratch) b.pool = C->stream;
         } catch (...) {
             delete C;
             throw;
@@ -825,13 +859,15 @@ int gs_context_destroy(gs_context* C) {
         C->use();
         cudaStreamSynchronize(C->stream);
         delete C->scratch_frame;
-        if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external) cudaFree(C->scratch_grads->planes);
+        if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external)
+            pool_free(C->scratch_grads->planes, C->stream);
         delete C->scratch_grads;
         if (C->copy_stream) {
             cudaStreamSynchronize(C->copy_stream);
             cudaStreamDestroy(C->copy_stream);
         }
         C->cub_tmp.release();
+        for (DevBuf& b : C->scratch) b.release();
         if (C->own_stream) cudaStreamDestroy(C->stream);
         delete C;
     });
@@ -1104,7 +1140,7 @@ int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int3
         cudaStream_t st = C->stream;
         const ViewParams v = make_view(*pose, *cam);
         const size_t P = static_cast<size_t>(cam->width) * cam->height;
-        DevBuf pts, out;
+        DevBuf &pts = C->sc(kScPoints), &out = C->sc(kScDepth);
         pts.ensure(sizeof(double) * static_cast<size_t>(std::max<int64_t>(n, 1)) * stride);
         out.ensure(sizeof(double) * P);
         if (n > 0)
@@ -1114,8 +1150,6 @@ int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int3
         C->launched(3);
         ck(cudaMemcpyAsync(depth, out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "d2h depth");
         ck(cudaStreamSynchronize(st), "sync");
-        pts.release();
-        out.release();
     });
 }
 
@@ -1151,7 +1185,8 @@ int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // m
 void init_points_device(gs_map* M, const double* dpts, int64_t n) {
         gs_context* C = M->ctx;
         cudaStream_t st = C->stream;
-        DevBuf keys, keys2, idx, idx2, bb, hk, hv;
+        DevBuf &keys = C->sc(kScKeys), &keys2 = C->sc(kScKeys2), &idx = C->sc(kScIdx), &idx2 = C->sc(kScIdx2),
+               &bb = C->sc(kScBBox), &hk = C->sc(kScHashK), &hv = C->sc(kScHashV);
         keys.ensure(sizeof(uint64_t) * n);
         keys2.ensure(sizeof(uint64_t) * n);
         idx.ensure(sizeof(int32_t) * n);
@@ -1229,7 +1264,7 @@ int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* a
         if (n <= 0) return;  // points.empty() -> 0
         if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
         M->ctx->use();
-        DevBuf pts;
+        DevBuf& pts = M->ctx->sc(kScPoints);
         pts.ensure(sizeof(double) * 6 * n);
         ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d points");
         init_points_device(M, pts.as<double>(), n);
@@ -1247,7 +1282,7 @@ int64_t filter_points_device(gs_map* M, const double* dpts, int64_t n, const gs_
     cudaStream_t st = C->stream;
     gs_frame* F = scratch_frame(C);
     render_impl(M, pose, cam, F, true, false);
-    DevBuf keep, pos;
+    DevBuf &keep = C->sc(kScKeep), &pos = C->sc(kScPos);
     keep.ensure(sizeof(int32_t) * (n + 1));
     pos.ensure(sizeof(int32_t) * (n + 1));
     ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
@@ -1344,6 +1379,68 @@ int gs_load_checkpoint(gs_context* C, const char* path, gs_map** out) {
     });
 }
 
+int gs_integrate_keyframe(gs_map* M, const gs_pose* pose, const gs_camera* cam, const double* color,
+                          const double* points6, int64_t n, double tau_alpha, int32_t initial_iters, int32_t levels,
+                          gs_keyframe** out_kf, int64_t* added) {
+    return guard([&] {  // pipeline.cpp:148-155 (+ the keyframe's sparse depth, pipeline.cpp:108)
+        validate_camera(*cam);
+        gs_context* C = M->ctx;
+        C->use();
+        *out_kf = nullptr;
+        *added = 0;
+        if (tau_alpha < 0.0 || tau_alpha > 1.0)
+            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
+        if (n < 0 || n > 0x7fffffff) fail(GS_EINVAL, "integrate_keyframe: bad point count");
+        if (!color) fail(GS_EINVAL, "integrate_keyframe: missing colour image");
+        cudaStream_t st = C->stream;
+        const int h = cam->height, w = cam->width;
+        const size_t P = static_cast<size_t>(h) * w;
+        // the cloud crosses once: filter -> init, and the sparse depth, read the same device copy
+        DevBuf &pts = C->sc(kScPoints), &kept = C->sc(kScKept), &dd = C->sc(kScDepth), &cs = C->sc(kScColor);
+        std::optional<Scope> sc_up(std::in_place, C, "kf_upload_sparse_depth");
+        pts.ensure(sizeof(double) * 6 * std::max<int64_t>(n, 1));
+        if (n > 0)
+            ck(cudaMemcpyAsync(pts.p, points6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st), "h2d points");
+        // sparse depth first: project_sparse_depth reads the frame's full cloud (sequence.cpp:246-259)
+        dd.ensure(sizeof(double) * P + sizeof(float) * P);
+        launch_sparse_depth(pts.as<double>(), 6, n, make_view(*pose, *cam), dd.as<double>(), st);
+        float* depth_f = reinterpret_cast<float*>(dd.as<double>() + P);
+        launch_from_hwc_double(dd.as<double>(), h, w, 1, depth_f, st);
+        cs.ensure(sizeof(double) * 3 * P + sizeof(float) * 3 * P);
+        ck(cudaMemcpyAsync(cs.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d colour");
+        float* color_f = reinterpret_cast<float*>(cs.as<double>() + 3 * P);
+        launch_from_hwc_double(cs.as<double>(), h, w, 3, color_f, st);
+        C->launched(5);
+        sc_up.reset();
+        auto* K = new gs_keyframe();
+        K->ctx = C;
+        K->pose = *pose;
+        K->initial_iters = initial_iters;
+        try {
+            {
+                Scope sc(C, "kf_pyramid");
+                keyframe_build(K, color_f, depth_f, h, w, levels, true);
+            }
+            if (n > 0) {
+                int64_t k = 0;
+                {
+                    Scope sc(C, "kf_filter_points");
+                    k = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, kept);
+                }
+                if (k > 0) {
+                    Scope sc(C, "kf_init_gaussians");
+                    init_points_device(M, kept.as<double>(), k);
+                }
+                *added = k;
+            }
+        } catch (...) {
+            delete K;
+            throw;
+        }
+        *out_kf = K;
+    });
+}
+
 int gs_evaluate_view(gs_map* M, const gs_pose* pose, const gs_camera* cam, const double* gt_color,
                      const double* gt_depth, gs_eval_metrics* out) {
     return guard([&] {  // evaluate_sequence (pipeline.cpp:41-64), one frame
@@ -1394,7 +1491,7 @@ int gs_filter_points_by_visibility(gs_map* M, const double* pts6, int64_t n, con
         if (tau_alpha < 0.0 || tau_alpha > 1.0)
             fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
         if (n <= 0) return;
-        DevBuf pts, out;
+        DevBuf &pts = M->ctx->sc(kScPoints), &out = M->ctx->sc(kScKept);
         pts.ensure(sizeof(double) * 6 * n);
         ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
         const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
@@ -1415,7 +1512,7 @@ int gs_map_integrate_points(gs_map* M, const double* pts6, int64_t n, const gs_p
             fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
         if (n <= 0) return;
         if (n > 0x7fffffff) fail(GS_EINVAL, "integrate_points: too many points");
-        DevBuf pts, out;
+        DevBuf &pts = M->ctx->sc(kScPoints), &out = M->ctx->sc(kScKept);
         pts.ensure(sizeof(double) * 6 * n);
         ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
         const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
@@ -1434,7 +1531,7 @@ int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // ga
         if (n == 0) return;
         gs_context* C = M->ctx;
         cudaStream_t st = C->stream;
-        DevBuf keep, pos;
+        DevBuf &keep = C->sc(kScPruneKeep), &pos = C->sc(kScPrunePos);
         keep.ensure(sizeof(int32_t) * (n + 1));
         pos.ensure(sizeof(int32_t) * (n + 1));
         ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
@@ -1447,32 +1544,29 @@ int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // ga
         ck(cudaStreamSynchronize(st), "sync");
         C->launched(2);
         if (kept == n) return;
-        // stable compaction into the spare planes, then swap (entries past `kept` are don't-care:
-        // append / init reset the optimizer state of every range they fill)
+        // stable compaction through a staging block of kChunk planes (context scratch, reused):
+        // compact a block of planes into it, copy the kept prefix back; no map-sized allocation.
+        // Entries past `kept` are don't-care (append / init reset every range they fill).
+        constexpr int kChunk = 16;
         const int64_t cap = M->cap;
-        auto& S = M->spare;
-        if (S.cap != cap) {
-            S.free_all();
-            ck(cudaMalloc(&S.params, sizeof(float) * kNumParams * cap), "cudaMalloc params");
-            ck(cudaMalloc(&S.m, sizeof(float) * kNumParams * cap), "cudaMalloc adam m");
-            ck(cudaMalloc(&S.v, sizeof(float) * kNumParams * cap), "cudaMalloc adam v");
-            ck(cudaMalloc(&S.birth, sizeof(int32_t) * cap), "cudaMalloc birth");
-            ck(cudaMalloc(&S.degree, sizeof(int8_t) * cap), "cudaMalloc degree");
-            S.cap = cap;
-        }
+        DevBuf& tmp = C->sc(kScPruneTmp);
+        tmp.ensure(sizeof(float) * kChunk * cap);
         const int32_t* kp = keep.as<int32_t>();
         const int32_t* ps = pos.as<int32_t>();
-        launch_compact(M->params, S.params, cap, cap, kNumParams, n, kp, ps, st);
-        launch_compact(M->m, S.m, cap, cap, kNumParams, n, kp, ps, st);
-        launch_compact(M->v, S.v, cap, cap, kNumParams, n, kp, ps, st);
-        launch_compact(M->birth, S.birth, n, kp, ps, st);
-        launch_compact(M->degree, S.degree, n, kp, ps, st);
-        C->launched(5);
-        std::swap(M->params, S.params);
-        std::swap(M->m, S.m);
-        std::swap(M->v, S.v);
-        std::swap(M->birth, S.birth);
-        std::swap(M->degree, S.degree);
+        for (float* arr : {M->params, M->m, M->v}) {
+            for (int c0 = 0; c0 < kNumParams; c0 += kChunk) {
+                const int np = std::min(kChunk, kNumParams - c0);
+                launch_compact(arr + c0 * cap, tmp.as<float>(), cap, cap, np, n, kp, ps, st);
+                ck(cudaMemcpy2DAsync(arr + c0 * cap, sizeof(float) * cap, tmp.p, sizeof(float) * cap,
+                                     sizeof(float) * kept, np, cudaMemcpyDeviceToDevice, st), "copy back");
+                C->launched();
+            }
+        }
+        launch_compact(M->birth, tmp.as<int32_t>(), n, kp, ps, st);
+        ck(cudaMemcpyAsync(M->birth, tmp.p, sizeof(int32_t) * kept, cudaMemcpyDeviceToDevice, st), "copy back");
+        launch_compact(M->degree, reinterpret_cast<int8_t*>(tmp.p), n, kp, ps, st);
+        ck(cudaMemcpyAsync(M->degree, tmp.p, kept, cudaMemcpyDeviceToDevice, st), "copy back");
+        C->launched(2);
         M->deg_host.resize(kept);
         ck(cudaMemcpyAsync(M->deg_host.data(), M->degree, kept, cudaMemcpyDeviceToHost, st), "d2h degree");
         ck(cudaStreamSynchronize(st), "sync");
@@ -1689,10 +1783,7 @@ int gs_grads_create_external(gs_context* C, float* ptr, int64_t capacity, gs_gra
 int gs_grads_destroy(gs_grads* G) {
     return guard([&] {
         if (!G) return;
-        if (G->planes && !G->external) {
-            cudaStreamSynchronize(G->ctx->stream);
-            cudaFree(G->planes);
-        }
+        if (G->planes && !G->external) pool_free(G->planes, G->ctx->stream);
         delete G;
     });
 }

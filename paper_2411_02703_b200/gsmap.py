@@ -294,6 +294,22 @@ class GaussianMap:
                                              C.c_double(tau_alpha), C.byref(added)))
         return added.value
 
+    def integrate_keyframe(self, pose: Pose, cam: Camera, color: np.ndarray, points6: np.ndarray, tau_alpha: float,
+                           initial_iters: int, levels: int) -> tuple["Keyframe", int]:
+        """integrate_keyframe (pipeline.cpp:148-155) in one device call: the cloud is uploaded once,
+        filtered by visibility and initialised into the map; the returned Keyframe holds the
+        pyramid of `color` and of the cloud's project_sparse_depth. Returns (keyframe, added)."""
+        col = np.ascontiguousarray(color, np.float64)
+        if col.shape != (cam.height, cam.width, 3):
+            raise ValueError("integrate_keyframe: colour shape does not match the camera")
+        pts = np.ascontiguousarray(points6, np.float64).reshape(-1, 6)
+        h = C.c_void_p()
+        added = C.c_int64()
+        _check(lib().gs_integrate_keyframe(_vp(self.h), C.byref(pose), C.byref(cam), _p(col), _p(pts),
+                                           C.c_int64(len(pts)), C.c_double(tau_alpha), initial_iters, levels,
+                                           C.byref(h), C.byref(added)))
+        return Keyframe(pose, ctx=self.ctx, hw=(cam.height, cam.width), _handle=h.value), added.value
+
     def prune(self, opacity_threshold: float) -> int:
         """GaussianMap::prune (gaussian_map.cpp:56-73): removed count; state stays aligned."""
         removed = C.c_int64()
@@ -544,9 +560,14 @@ class Keyframe:
     """gsmap::Keyframe hot-path fields (map/keyframe.hpp:23-34) with its pyramid on the device."""
 
     def __init__(self, pose: Pose, color=None, sparse_depth=None, initial_iters: int = 0, levels: int = 2,
-                 ctx: Context | None = None, device_planes: tuple | None = None, hw: tuple | None = None):
+                 ctx: Context | None = None, device_planes: tuple | None = None, hw: tuple | None = None,
+                 _handle=None):
         self.ctx = ctx or default_context()
         self.pose = pose
+        if _handle is not None:  # adopted from gs_integrate_keyframe
+            self.h = _handle
+            self.shape = hw
+            return
         h = C.c_void_p()
         if device_planes is not None:
             H, W = hw
@@ -562,11 +583,15 @@ class Keyframe:
         self.h = h.value
         self.shape = (H, W)
 
+    def close(self):
+        """Release the keyframe's device pyramid now (otherwise at garbage collection)."""
+        if getattr(self, "h", None):
+            h, self.h = self.h, None
+            _check(lib().gs_keyframe_destroy(_vp(h)))
+
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                lib().gs_keyframe_destroy(_vp(self.h))
-                self.h = None
+            self.close()
         except Exception:
             pass
 

@@ -5,10 +5,9 @@ This mirrors PipelineState's optimizer role (pipeline.cpp:130-180, single_thread
 stay out of scope. Each keyframe arrives with its pose, colour image and LiDAR
 cloud (the reference drains the voxel store instead: `kf->points`, pipeline.cpp:116):
 
-  integrate_keyframe (pipeline.cpp:148-160):
-      filter_points_by_visibility -> init_gaussians_from_points   (gs_map_integrate_points)
-      project_sparse_depth + build_keyframe_pyramid               (gs_project_sparse_depth, gs_keyframe_create)
-      one train_keyframe_step + housekeeping
+  integrate_keyframe (pipeline.cpp:148-160), one device call (gs_integrate_keyframe):
+      filter_points_by_visibility -> init_gaussians_from_points, project_sparse_depth +
+      build_keyframe_pyramid; then one train_keyframe_step + housekeeping
   optimize_once (pipeline.cpp:163-173): a uniformly sampled keyframe with budget left
       (KeyframeQueue::sample_for_optimization, keyframe.cpp:122-138) -> train step + housekeeping
   housekeeping (pipeline.cpp:133-145): maybe_upgrade_sh; prune every prune_interval steps
@@ -79,17 +78,16 @@ class MappingLoop:
 
     def housekeeping(self):
         self._clock("maybe_upgrade_sh", self.m.maybe_upgrade_sh, self.cfg.sh_interval)
-        step = self.m.global_step
+        step = self._clock("global_step", lambda: self.m.global_step)
         if self.cfg.prune_interval > 0 and step > 0 and step % self.cfg.prune_interval == 0:
             self.pruned += self._clock("prune", self.m.prune, self.cfg.prune_threshold)
 
     def integrate_keyframe(self, pose: G.Pose, color: np.ndarray, cloud6: np.ndarray) -> G.Keyframe:
         cfg = self.cfg
-        self.added.append(self._clock("integrate_points", self.m.integrate_points, cloud6, pose, self.cam,
-                                      cfg.tau_alpha))
-        sparse = self._clock("project_sparse_depth", G.project_sparse_depth, cloud6, pose, self.cam, self.m.ctx)
-        kf = self._clock("build_keyframe_pyramid", lambda: G.Keyframe(
-            pose, color, sparse, initial_iters=cfg.iter_budget, levels=cfg.train.pyramid_levels, ctx=self.m.ctx))
+        # filter -> init, sparse depth and pyramid in one device call (the cloud crosses once)
+        kf, added = self._clock("integrate_keyframe", self.m.integrate_keyframe, pose, self.cam, color, cloud6,
+                                cfg.tau_alpha, cfg.iter_budget, cfg.train.pyramid_levels)
+        self.added.append(added)
         e = _Entry(kf, cfg.iter_budget, self.n_keyframes)
         self.n_keyframes += 1
         if e.remaining > 0:
@@ -109,6 +107,8 @@ class MappingLoop:
         if e.remaining == 0:
             del self.active[i]
         self._step(e)
+        if e.remaining == 0:  # retired (keyframe.cpp:133-136): its device pyramid is freed now
+            self._clock("retire_keyframe", e.kf.close)
         return True
 
     def run(self, frames) -> int:

@@ -111,5 +111,7 @@ def test_evaluate_sequence_records():  # pipeline.cpp:41-64: records per frame, 
     assert [r["frame"] for r in recs] == [0, 1]
     sparse = G().project_sparse_depth(cloud, gpu_pose(O.pose()), gpu_cam(cam))
     r0 = G().evaluate_view(gm, gpu_pose(O.pose()), gpu_cam(cam), np.full((48, 64, 3), 0.5), sparse)
-    assert recs[0]["depth_rmse"] == r0["depth_rmse"] and recs[0]["psnr"] == r0["psnr"]
+    # fp64 block sums meet in atomics: equal to the last few ulps, not bit for bit
+    assert recs[0]["depth_rmse"] == pytest.approx(r0["depth_rmse"], rel=1e-12)
+    assert recs[0]["psnr"] == pytest.approx(r0["psnr"], rel=1e-12)
     assert recs[1]["iteration"] == gm.global_step and recs[1]["wall_time_s"] >= recs[0]["wall_time_s"]

@@ -95,3 +95,27 @@ def test_mapping_loop_tracks_oracle():
     lr = np.array([1.6e-4 * ref.m.scene_extent] * 3 + [1e-3] * 4 + [5e-3] * 3 + [5e-2] + [2.5e-3] * 48)
     d = np.abs(gm.gaussians["p"] - ref.m.gaussians["p"])
     assert np.mean(d <= 0.05 * lr + 1e-6) > 0.95
+
+
+def test_integrate_keyframe_equals_separate_calls():  # pipeline.cpp:148-155 in one call
+    from fixtures import pyfixture as F
+    scene = F.Scene(n_gaussians=3000, width=160, height=128, n_frames=2, seed=1)
+    cam = O.camera(*scene.camera)
+    poses = [O.pose(p[0], p[1], p[2], p[3], t=p[4:7]) for p in scene.poses]
+    gt = O.OracleMap(round32(scene.gaussians))
+    color = f32(O.render(gt, poses[1], cam).color)
+    cloud0, cloud1 = scene.cloud(0), scene.cloud(1)
+    a, b = G().GaussianMap(None), G().GaussianMap(None)
+    a.init_from_points(cloud0); b.init_from_points(cloud0)
+    kf, added = a.integrate_keyframe(gpu_pose(poses[1]), gpu_cam(cam), color, cloud1, 0.5, 6, 2)
+    assert added == b.integrate_points(cloud1, gpu_pose(poses[1]), gpu_cam(cam), 0.5)
+    np.testing.assert_array_equal(a.gaussians["p"], b.gaussians["p"])
+    sparse = G().project_sparse_depth(cloud1, gpu_pose(poses[1]), gpu_cam(cam))
+    ref = G().Keyframe(gpu_pose(poses[1]), color, sparse, 6, 2)
+    for l in range(3):
+        c0, d0 = kf.level(l)
+        c1, d1 = ref.level(l)
+        np.testing.assert_array_equal(c0, c1)
+        np.testing.assert_array_equal(d0, d1)
+    with pytest.raises(ValueError, match="tau_alpha"):
+        a.integrate_keyframe(gpu_pose(poses[1]), gpu_cam(cam), color, cloud1, 1.5, 6, 2)
