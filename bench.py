@@ -42,8 +42,8 @@ N_GAUSS, W0, H0, N_FRAMES, LEVELS = 1_000_000, 1280, 1024, 8, 2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=48)
-    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--steps", type=int, default=240)
+    ap.add_argument("--warmup", type=int, default=24)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sh-degree", type=int, default=0)
     ap.add_argument("--n-gaussians", type=int, default=N_GAUSS)
@@ -236,15 +236,26 @@ def run_ours(args, rank, world):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.freeze()  # setup objects leave the collector's generations: no multi-ms gen-2 pauses in the timed loop
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(dev) as clk:
         e0.record(stream)
         views = pix = 0
         for s in range(args.steps):
             v, p = step(args.warmup + s)
             views += v; pix += p
+            step_ev[s].record(stream)
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
+    # per-level step times (per-level rates)
+    lvl_ms = {}
+    for s in range(args.steps):
+        d = step_ev[s - 1].elapsed_time(step_ev[s]) if s else e0.elapsed_time(step_ev[0])
+        lvl = (LEVELS - ((args.warmup + s) % 3)) if batch else schedule(args.warmup + s)[1]
+        lvl_ms.setdefault(lvl, []).append(d)
+    per_level = {f"L{l}": {"ms_per_step": round(float(np.mean(v)), 4), "steps": len(v),
+                           "mpix_per_s": round(shapes[l][0] * shapes[l][1] * views_per_rank * world / (np.mean(v) / 1e3) / 1e6, 2)}
+                 for l, v in sorted(lvl_ms.items())}
     launches = ctx.launches - launches0
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()
@@ -266,7 +277,7 @@ def run_ours(args, rank, world):
                             "one keyframe view: render + loss + backward + Adam at its scheduled level"),
               "dtype": "f32 (fp64 geometry, fp64 transmittance)",
               "data": "synthetic (reference synthetic.cpp scene, colourised-LiDAR-initialised map)",
-              "mpix_per_s": round(total_pix / (ms_max / 1e3) / 1e6, 3),
+              "mpix_per_s": round(total_pix / (ms_max / 1e3) / 1e6, 3), "per_level": per_level,
               "config": {"workload": ("C4: 8-keyframe batch sharded over ranks, NCCL all-reduce" if batch else
                                       "C3: 1M Gaussians 1280x1024, 3-level pyramid (L2,L1,L0 in turn), L1+SSIM+depth loss"),
                          "n_gaussians": len(m), "width": W0, "height": H0, "pyramid_levels": LEVELS + 1,
