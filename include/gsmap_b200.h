@@ -142,6 +142,11 @@ int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64
    a missing / foreign / wrong-version / truncated file, with the reference's messages. */
 int gs_save_checkpoint(gs_map* map, const char* path);
 int gs_load_checkpoint(gs_context* ctx, const char* path, gs_map** out);
+/* optimizer state beside a checkpoint, for a true resume (the v1 format carries none):
+   per Gaussian Adam m / v (59 each) and step, plus the map's global_step and scene_extent. load requires a map of
+   the same size (e.g. fresh from gs_load_checkpoint). */
+int gs_save_training_state(gs_map* map, const char* path);
+int gs_load_training_state(gs_map* map, const char* path);
 /* evaluate_sequence (pipeline.cpp:41-64) for one frame: render at the pose, quantize_8bit the
    colour (pipeline.cpp:34-39), psnr / ssim against gt_color (H x W x 3, HWC) and depth_rmse of
    the raw depth against gt_depth (H x W; NULL -> depth_rmse = NaN, as with no valid pixel). */

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <optional>
 #include <fstream>
+#include <iomanip>
 #include <limits>
 #include <sstream>
 #include <cstring>
@@ -1376,6 +1377,74 @@ int gs_load_checkpoint(gs_context* C, const char* path, gs_map** out) {
             fail(st, msg);
         }
         *out = M;
+    });
+}
+
+// Optimizer state beside a v1 checkpoint ("add Adam state for true resume"; the
+// reference's format has none, load_checkpoint starts Adam afresh): text header, then per
+// Gaussian m[59], v[59] (fp64 widening of the device's fp32 moments) and the int64 Adam step.
+int gs_save_training_state(gs_map* M, const char* path) {
+    return guard([&] {
+        M->ctx->use();
+        const int64_t n = M->n;
+        std::vector<double> m(static_cast<size_t>(kNumParams) * n), v(m.size());
+        std::vector<int64_t> step(n);
+        if (n > 0) {
+            const int st = gs_map_get_adam(M, m.data(), v.data(), step.data(), n);
+            if (st != GS_OK) fail(st, g_err);
+        }
+        std::ofstream out(path, std::ios::binary);
+        if (!out) fail(GS_ERUNTIME, std::string("save_training_state: cannot open ") + path);
+        // scene_extent too: the reference refreshes it only on append (gaussian_map.cpp:87-99), so a
+        // reloaded map would otherwise rescale the position learning rate by its trained extent
+        out << "gsmap-adam-state 1\ncount " << n << "\nglobal_step " << M->global_step << "\nscene_extent "
+            << std::setprecision(17) << M->scene_extent << "\nend_header\n";
+        for (int64_t i = 0; i < n; ++i) {
+            out.write(reinterpret_cast<const char*>(&m[kNumParams * i]), sizeof(double) * kNumParams);
+            out.write(reinterpret_cast<const char*>(&v[kNumParams * i]), sizeof(double) * kNumParams);
+            out.write(reinterpret_cast<const char*>(&step[i]), sizeof(int64_t));
+        }
+        if (!out) fail(GS_ERUNTIME, std::string("save_training_state: write failed for ") + path);
+    });
+}
+
+int gs_load_training_state(gs_map* M, const char* path) {
+    return guard([&] {
+        M->ctx->use();
+        std::ifstream in(path, std::ios::binary);
+        if (!in) fail(GS_ERUNTIME, std::string("load_training_state: cannot open ") + path);
+        std::string line, magic;
+        std::getline(in, line);
+        std::istringstream head(line);
+        int version = 0;
+        head >> magic >> version;
+        if (magic != "gsmap-adam-state" || version != 1)
+            fail(GS_ERUNTIME, std::string("load_training_state: not an optimizer state file: ") + path);
+        int64_t count = -1, gstep = 0;
+        double extent = M->scene_extent;
+        while (std::getline(in, line) && line != "end_header") {
+            std::istringstream is(line);
+            std::string key;
+            is >> key;
+            if (key == "count") is >> count;
+            if (key == "global_step") is >> gstep;
+            if (key == "scene_extent") is >> extent;
+        }
+        if (count != M->n) fail(GS_EINVAL, "load_training_state: Gaussian count does not match the map");
+        std::vector<double> m(static_cast<size_t>(kNumParams) * count), v(m.size());
+        std::vector<int64_t> step(count);
+        for (int64_t i = 0; i < count; ++i) {
+            in.read(reinterpret_cast<char*>(&m[kNumParams * i]), sizeof(double) * kNumParams);
+            in.read(reinterpret_cast<char*>(&v[kNumParams * i]), sizeof(double) * kNumParams);
+            in.read(reinterpret_cast<char*>(&step[i]), sizeof(int64_t));
+        }
+        if (!in) fail(GS_ERUNTIME, std::string("load_training_state: truncated file ") + path);
+        if (count > 0) {
+            const int st = gs_map_set_adam(M, m.data(), v.data(), step.data(), count);
+            if (st != GS_OK) fail(st, g_err);
+        }
+        M->global_step = gstep;
+        M->scene_extent = extent;
     });
 }
 

@@ -200,6 +200,13 @@ class GaussianMap:
         """save_checkpoint (io/checkpoint.cpp:17-35), format v1."""
         _check(lib().gs_save_checkpoint(_vp(self.h), os.fsencode(path)))
 
+    def save_training_state(self, path: str):
+        """Adam m / v / step and global_step beside a checkpoint (true resume)."""
+        _check(lib().gs_save_training_state(_vp(self.h), os.fsencode(path)))
+
+    def load_training_state(self, path: str):
+        _check(lib().gs_load_training_state(_vp(self.h), os.fsencode(path)))
+
     @classmethod
     def load_checkpoint(cls, path: str, ctx: Context | None = None) -> "GaussianMap":
         """load_checkpoint (io/checkpoint.cpp:37-71): a new device map with fresh Adam state."""

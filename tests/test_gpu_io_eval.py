@@ -115,3 +115,32 @@ def test_evaluate_sequence_records():  # pipeline.cpp:41-64: records per frame, 
     assert recs[0]["depth_rmse"] == pytest.approx(r0["depth_rmse"], rel=1e-12)
     assert recs[0]["psnr"] == pytest.approx(r0["psnr"], rel=1e-12)
     assert recs[1]["iteration"] == gm.global_step and recs[1]["wall_time_s"] >= recs[0]["wall_time_s"]
+
+
+def test_training_state_resume_is_exact(tmp_path):  # checkpoint + optimizer state = a true resume
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    gt = O.random_scene(O.Rng(21), 40, cam, O.pose(), 1.0, 2.0)
+    color = np.asarray(O.render(gt, O.pose(), cam).color, np.float32).astype(np.float64)
+    g = gt.gaussians
+    g["p"][:, 10] = np.log(0.1 / 0.9)
+    _, a = pair(g)
+    cfg = G().TrainConfig.make(0.2, 0.5, 0)
+    mk = lambda: G().Keyframe(gpu_pose(O.pose()), color, np.zeros((48, 64)), 100, 0)
+    ka = mk()
+    for _ in range(3):
+        G().train_keyframe_step(a, ka, cfg, gpu_cam(cam))
+    a.save_checkpoint(str(tmp_path / "m.gsmap"))
+    a.save_training_state(str(tmp_path / "m.adam"))
+    b = G().load_checkpoint(str(tmp_path / "m.gsmap"), a.ctx)
+    b.load_training_state(str(tmp_path / "m.adam"))
+    assert b.global_step == a.global_step == 3 and b.scene_extent == a.scene_extent
+    for x, y in zip(a.adam_state(), b.adam_state()):
+        np.testing.assert_array_equal(x, y)
+    kb = mk()
+    for _ in range(2):
+        ra = G().train_keyframe_step(a, ka, cfg, gpu_cam(cam))
+        rb = G().train_keyframe_step(b, kb, cfg, gpu_cam(cam))
+        assert ra["loss"] == pytest.approx(rb["loss"], rel=1e-12)
+    np.testing.assert_array_equal(a.gaussians["p"], b.gaussians["p"])
+    with pytest.raises(ValueError, match="count"):
+        G().GaussianMap(a.ctx).load_training_state(str(tmp_path / "m.adam"))
