@@ -307,6 +307,7 @@ struct gs_frame {
     DevBuf seg_scratch;  // segmented forward: per-segment local states, Tl and stop segment
     int nseg = 1;
     DevBuf loss;  // LossScalars
+    DevBuf rank_of;  // K8b: depth rank per map index (-1 = culled)
     DevBuf eval_quant, eval_gt, eval_stage;  // evaluate_view scratch
     bool has_cotangent = false;
     bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)
@@ -672,11 +673,15 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     }
     {
         Scope sc(C, "preprocess_bwd");
+        // map-order K8b once SH planes are active (coalesced plane traffic), rank order at degree 0
+        const bool by_gid = M->max_degree > 0;
+        if (by_gid) F->rank_of.ensure(sizeof(int32_t) * std::max<int64_t>(M->n, 1));
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
                               F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
-                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, st);
+                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, by_gid,
+                              F->rank_of.as<int32_t>(), static_cast<int>(M->n), st);
         G->clean = false;
-        C->launched();
+        C->launched(by_gid ? 3 : 2);  // K8a reduce, (rank scatter,) K8b
     }
 }
 

@@ -17,7 +17,8 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
                            double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
-                           int max_ranks, float* grads, int64_t gcap, bool accumulate, cudaStream_t st);
+                           int max_ranks, float* grads, int64_t gcap, bool accumulate, bool by_gid,
+                           int32_t* rank_of /* [n_map] scratch */, int n_map, cudaStream_t st);
 
 // project_sparse_depth: points [n][stride] (x, y, z first, fp64, device) -> depth [h][w] fp64
 void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,
