@@ -589,6 +589,13 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
     result, ctxdata = run_ours(args, rank, world)
+    if world == 1 and not args.batch and args.sh_degree == 0 and not args.profile_only:
+        # d = 0 and d = 3 reported separately (same workload, every SH band active)
+        import copy
+        a3 = copy.copy(args)
+        a3.sh_degree, a3.no_e2e = 3, True
+        r3, _ = run_ours(a3, rank, world)
+        result["sh_degree_3"] = {k: r3[k] for k in ("value", "ms_per_step", "mpix_per_s", "per_level", "kernels")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         scene, train, kfs, host_levels = ctxdata
         c0, d0 = host_levels[0][0]
