@@ -368,9 +368,13 @@ public:
         check(gs_keyframe_create(ctx.get(), &p, color.data.data(), sparse_depth.data.data(), color.h, color.w,
                                  initial_iters, levels, &h_));
     }
-    ~Keyframe() { gs_keyframe_destroy(h_); }
+    Keyframe(const Pose& pose, gs_keyframe* adopt) : pose_(pose), h_(adopt) {}  // owns a C-ABI handle
+    ~Keyframe() {
+        if (h_) gs_keyframe_destroy(h_);
+    }
     Keyframe(const Keyframe&) = delete;
     Keyframe& operator=(const Keyframe&) = delete;
+    Keyframe(Keyframe&& o) noexcept : pose_(o.pose_), h_(o.h_) { o.h_ = nullptr; }
     int consumed_iters() const {
         int32_t c = 0;
         check(gs_keyframe_consumed(h_, &c));
@@ -403,6 +407,35 @@ inline std::vector<ColoredPoint> filter_points_by_visibility(const std::vector<C
         for (int k = 0; k < 3; ++k) out[i].color[k] = kept[6 * i + 3 + k];
     }
     return out;
+}
+
+// integrate_keyframe (pipeline.cpp:148-155) in one device call: filter the frame's cloud by the
+// map's visibility, initialise Gaussians from the kept points, and build the keyframe (pyramid of
+// `color` and of the cloud's project_sparse_depth). Returns the keyframe; *added = Gaussians added.
+inline Keyframe integrate_keyframe(GaussianMap& map, const Pose& pose, const CameraModel& cam, const ImageD& color,
+                                   const std::vector<ColoredPoint>& points, double tau_alpha, int initial_iters,
+                                   int levels, std::size_t* added = nullptr) {
+    std::vector<double> flat(points.size() * 6);
+    for (size_t i = 0; i < points.size(); ++i) {
+        for (int k = 0; k < 3; ++k) flat[6 * i + k] = points[i].position[k];
+        for (int k = 0; k < 3; ++k) flat[6 * i + 3 + k] = points[i].color[k];
+    }
+    const gs_pose p = pose.p();
+    const gs_camera c = cam.c();
+    gs_keyframe* h = nullptr;
+    int64_t n = 0;
+    check(gs_integrate_keyframe(map.get(), &p, &c, color.data.data(), flat.data(), static_cast<int64_t>(points.size()),
+                                tau_alpha, initial_iters, levels, &h, &n));
+    if (added) *added = static_cast<std::size_t>(n);
+    return Keyframe(pose, h);
+}
+
+// optimizer state beside a checkpoint (true resume; the v1 format has none)
+inline void save_training_state(const std::string& path, const GaussianMap& map) {
+    check(gs_save_training_state(map.get(), path.c_str()));
+}
+inline void load_training_state(const std::string& path, GaussianMap& map) {
+    check(gs_load_training_state(map.get(), path.c_str()));
 }
 
 // evaluate_sequence (pipeline.cpp:41-64), one frame: EvalRecord's metric fields

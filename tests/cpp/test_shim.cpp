@@ -236,6 +236,21 @@ static void evaluate_and_sh_schedule() {  // test_pipeline.cpp:128-146, test_map
     CHECK(APPROX(m.ssim, 1.0, 1e-5));
     CHECK(APPROX(m.depth_rmse, 0.0, 1e-5));
     CHECK(std::isnan(evaluate_view(map, Pose{}, cam, stored, nullptr).depth_rmse));
+    // one-call keyframe integration: a cloud behind the blobs (points on pixels they cover filter out)
+    std::vector<ColoredPoint> cloud;
+    for (double x = -2.5; x <= 2.5; x += 0.05)  // wider than the blobs' footprint: the rim is kept
+        for (double y = -1.8; y <= 1.8; y += 0.05) {
+            ColoredPoint q;
+            q.position = {x, y, 5.0};
+            q.color = {0.3, 0.6, 0.9};
+            cloud.push_back(q);
+        }
+    const std::size_t before = map.size();
+    std::size_t added = 0;
+    Keyframe kf = integrate_keyframe(map, Pose{}, cam, stored, cloud, 0.5, 10, 1, &added);
+    CHECK(added > 0 && added < cloud.size());
+    CHECK(map.size() == before + added);
+    CHECK(kf.consumed_iters() == 0);
     map.set_global_step(250);
     CHECK(maybe_upgrade_sh(map, 100) == 2);
     CHECK(map.max_active_degree() == 2);

@@ -108,6 +108,7 @@ def test_integrate_keyframe_equals_separate_calls():  # pipeline.cpp:148-155 in 
     a, b = G().GaussianMap(None), G().GaussianMap(None)
     a.init_from_points(cloud0); b.init_from_points(cloud0)
     kf, added = a.integrate_keyframe(gpu_pose(poses[1]), gpu_cam(cam), color, cloud1, 0.5, 6, 2)
+    assert 0 < added < len(cloud1)
     assert added == b.integrate_points(cloud1, gpu_pose(poses[1]), gpu_cam(cam), 0.5)
     np.testing.assert_array_equal(a.gaussians["p"], b.gaussians["p"])
     sparse = G().project_sparse_depth(cloud1, gpu_pose(poses[1]), gpu_cam(cam))
