@@ -99,7 +99,9 @@ def test_mapping_loop_tracks_oracle():
 
 def test_integrate_keyframe_equals_separate_calls():  # pipeline.cpp:148-155 in one call
     from fixtures import pyfixture as F
-    scene = F.Scene(n_gaussians=3000, width=160, height=128, n_frames=2, seed=1)
+    # 8 frames along the line: neighbouring frames overlap, so the map built from frame 0's cloud
+    # covers part of frame 1 and the visibility filter drops those points
+    scene = F.Scene(n_gaussians=3000, width=160, height=128, n_frames=8, seed=1)
     cam = O.camera(*scene.camera)
     poses = [O.pose(p[0], p[1], p[2], p[3], t=p[4:7]) for p in scene.poses]
     gt = O.OracleMap(round32(scene.gaussians))
