@@ -136,6 +136,9 @@ int gs_maybe_upgrade_sh(gs_map* map, int32_t sh_interval, int32_t* degree);
    distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;
    degree 0; fresh optimizer state). *added = n. */
 int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64_t* added);
+/* diagnostics: thread order of the per-Gaussian VJP kernel (0 depth rank, 1 map index, 2 the
+   visible list; -1 = automatic: the visible list) */
+int gs_debug_set_k8_order(int order);
 /* checkpoint format v1 (io/checkpoint.cpp:17-73): text header + 476-byte fp64 AoS records.
    save_checkpoint writes the device map's parameters (exact fp64 widening of the fp32 store);
    load_checkpoint returns a NEW map (fresh Adam state, GaussianMap::append) or GS_ERUNTIME for

@@ -506,27 +506,36 @@ __global__ void rank_scatter_kernel(const Splat* __restrict__ rec, const unsigne
     if (r < static_cast<int>(cnt[kCntVisible]) && !overflowed(cnt)) rank_of[rec[r].gid] = r;
 }
 
-// K8b, one thread per visible Gaussian. BY_GID = false: threads in depth-rank order (the
-// Gaussian's map index from its record; its parameter and gradient plane accesses scatter, one
-// 32-byte sector per 4-byte value). BY_GID = true: threads in map order over every Gaussian
-// (rank looked up, culled ones exit), so the planes are read and written by consecutive threads
-// at consecutive addresses — at SH degree 3 (48 more planes each way) 2.9x faster; at degree 0
-// the idle lanes of culled Gaussians cost more than the scatter (measured), so the host picks
-// BY_GID only for degree >= 1.
-template <bool ACC, bool BY_GID>
+// K8b, one thread per visible Gaussian; ORDER picks which thread takes which Gaussian.
+//   kByRank: depth-rank order (map index from the record): the parameter and gradient plane
+//            accesses scatter, one 32-byte sector per 4-byte value;
+//   kByMap: map order over every Gaussian (rank looked up, culled ones exit): coalesced planes
+//           but ~70% idle lanes;
+//   kByVisList: the visible list K1 appended (ascending map-index runs, rank looked up): full
+//           warps and mostly coalesced planes — the default (3.3x faster than rank order at SH
+//           degree 3, where 48 more planes move each way).
+enum K8Order : int { kByRank = 0, kByMap = 1, kByVisList = 2 };
+int g_k8_order = -1;  // diagnostics override (-1 = automatic)
+
+template <bool ACC, int ORDER>
 __global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
     const double* __restrict__ sums, const unsigned long long* __restrict__ cnt, float* __restrict__ grads,
-    int64_t gcap, const int32_t* __restrict__ rank_of, int n_map) {
+    int64_t gcap, const int32_t* __restrict__ rank_of, int n_map, const int32_t* __restrict__ vis_gid) {
     const int t = blockIdx.x * kBwdRanks + threadIdx.x;
     if (overflowed(cnt)) return;
     int r, i;
-    if (BY_GID) {
+    if (ORDER == kByMap) {
         if (t >= n_map) return;
         i = t;
         r = rank_of[i];
         if (r < 0) return;  // culled: never touched
+    } else if (ORDER == kByVisList) {
+        // the visible list in append order: runs of ascending map indices (one run per K1 warp)
+        if (t >= static_cast<int>(cnt[kCntVisible])) return;
+        i = vis_gid[t];
+        r = rank_of[i];
     } else {
         if (t >= static_cast<int>(cnt[kCntVisible])) return;
         r = t;
@@ -903,29 +912,37 @@ void launch_knn_init(const double* pts, int64_t n, int k, const KnnGrid& g, cons
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
                            const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,
-                           bool accumulate, bool by_gid, int32_t* rank_of, int n_map, cudaStream_t st) {
+                           bool accumulate, bool by_gid, int32_t* rank_of, int n_map, const int32_t* vis_gid,
+                           cudaStream_t st) {
     if (max_ranks <= 0 || n_map <= 0) return;
     const int blocks = div_up(max_ranks, kBwdRanks);
     reduce_partials_kernel<<<blocks, kBwdRanks, 0, st>>>(emit_off, partials, cnt, sums);
     // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
     // read-modify-write of the gradient entries
-    if (by_gid) {
+    // visible-list order measured best at every SH degree (C3, B200): rank order 0.113 / 0.515 ms,
+    // map order 0.139 / 0.175 ms, visible list 0.108 / 0.158 ms at degree 0 / 3
+    (void)by_gid;
+    const int order = g_k8_order >= 0 ? g_k8_order : kByVisList;
+    if (order != kByRank) {
         cudaMemsetAsync(rank_of, 0xff, sizeof(int32_t) * static_cast<size_t>(n_map), st);
         rank_scatter_kernel<<<div_up(max_ranks, 256), 256, 0, st>>>(rec, cnt, rank_of);
-        const int gblocks = div_up(n_map, kBwdRanks);
-        if (accumulate)
-            preprocess_bwd_kernel<true, true><<<gblocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off,
-                                                                             sums, cnt, grads, gcap, rank_of, n_map);
-        else
-            preprocess_bwd_kernel<false, true><<<gblocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off,
-                                                                              sums, cnt, grads, gcap, rank_of, n_map);
-    } else if (accumulate) {
-        preprocess_bwd_kernel<true, false><<<blocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, sums,
-                                                                         cnt, grads, gcap, nullptr, 0);
-    } else {
-        preprocess_bwd_kernel<false, false><<<blocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, sums,
-                                                                          cnt, grads, gcap, nullptr, 0);
     }
+    const int gblocks = order == kByMap ? div_up(n_map, kBwdRanks) : blocks;
+#define GS_K8(ACC_, ORD_)                                                                              \
+    preprocess_bwd_kernel<ACC_, ORD_><<<gblocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, \
+                                                                    sums, cnt, grads, gcap, rank_of, n_map, vis_gid)
+    if (accumulate) {
+        if (order == kByMap) GS_K8(true, kByMap);
+        else if (order == kByVisList) GS_K8(true, kByVisList);
+        else GS_K8(true, kByRank);
+    } else {
+        if (order == kByMap) GS_K8(false, kByMap);
+        else if (order == kByVisList) GS_K8(false, kByVisList);
+        else GS_K8(false, kByRank);
+    }
+#undef GS_K8
 }
+
+void set_k8_order(int order) { g_k8_order = order; }
 
 }  // namespace gsb

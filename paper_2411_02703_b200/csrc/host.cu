@@ -673,15 +673,14 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     }
     {
         Scope sc(C, "preprocess_bwd");
-        // map-order K8b once SH planes are active (coalesced plane traffic), rank order at degree 0
-        const bool by_gid = M->max_degree > 0;
-        if (by_gid) F->rank_of.ensure(sizeof(int32_t) * std::max<int64_t>(M->n, 1));
+        const bool by_gid = true;  // K8b in visible-list order (coalesced plane traffic), see geometry.cu
+        F->rank_of.ensure(sizeof(int32_t) * std::max<int64_t>(M->n, 1));
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
                               F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
                               dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, by_gid,
-                              F->rank_of.as<int32_t>(), static_cast<int>(M->n), st);
+                              F->rank_of.as<int32_t>(), static_cast<int>(M->n), F->vis_gid.as<int32_t>(), st);
         G->clean = false;
-        C->launched(by_gid ? 3 : 2);  // K8a reduce, (rank scatter,) K8b
+        C->launched(3);  // K8a reduce, rank scatter, K8b
     }
 }
 
@@ -1513,6 +1512,11 @@ int gs_integrate_keyframe(gs_map* M, const gs_pose* pose, const gs_camera* cam, 
         }
         *out_kf = K;
     });
+}
+
+// diagnostics: K8b thread order (0 rank, 1 map, 2 visible list; -1 = automatic)
+int gs_debug_set_k8_order(int order) {
+    return guard([&] { set_k8_order(order); });
 }
 
 int gs_evaluate_view(gs_map* M, const gs_pose* pose, const gs_camera* cam, const double* gt_color,

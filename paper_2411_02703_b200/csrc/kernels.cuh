@@ -18,7 +18,9 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
                            double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
                            int max_ranks, float* grads, int64_t gcap, bool accumulate, bool by_gid,
-                           int32_t* rank_of /* [n_map] scratch */, int n_map, cudaStream_t st);
+                           int32_t* rank_of /* [n_map] scratch */, int n_map, const int32_t* vis_gid,
+                           cudaStream_t st);
+void set_k8_order(int order);  // diagnostics: 0 rank order, 1 map order, 2 visible-list order, -1 auto
 
 // project_sparse_depth: points [n][stride] (x, y, z first, fp64, device) -> depth [h][w] fp64
 void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,
