@@ -255,6 +255,14 @@ int gs_render_backward_frame(gs_map* map, const gs_pose* pose, const gs_camera* 
 /* train_keyframe_step (mapper.cpp:214-238): level schedule, render, loss, backward, Adam, psnr */
 int gs_train_step(gs_map* map, gs_keyframe* kf, const gs_train_config* cfg, const gs_camera* cam,
                   gs_step_report* report);
+/* gs_train_step plus the NEXT step's input upload (gs_keyframe_upload_level of next_kf's
+   next_level from host fp64 HWC buffers), issued on the copy stream right behind this step's
+   enqueued work so that the copy and its API calls overlap this step's compute (a data-loader
+   prefetch; next_kf = NULL: plain gs_train_step). The host buffers must stay valid until the
+   next synchronising call on the context. */
+int gs_train_step_prefetch(gs_map* map, gs_keyframe* kf, const gs_train_config* cfg, const gs_camera* cam,
+                           gs_keyframe* next_kf, int32_t next_level, const double* next_color,
+                           const double* next_depth, gs_step_report* report);
 /* keyframe-batch step: grads of every view summed (GaussianGrad::add), then the
  * caller may all-reduce gs_grads planes across ranks, then gs_apply_gradients. This call does
  * render+loss+backward for one view at its scheduled level and accumulates into grads.

@@ -1992,8 +1992,14 @@ int gs_keyframe_consumed(gs_keyframe* K, int32_t* c) { return guard([&] { *c = K
 int gs_keyframe_set_consumed(gs_keyframe* K, int32_t c) { return guard([&] { K->consumed = c; }); }
 int gs_keyframe_levels(gs_keyframe* K, int32_t* n) { return guard([&] { *n = static_cast<int32_t>(K->hs.size()); }); }
 
+void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const double* depth);
+
 int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
-    return guard([&] {
+    return guard([&] { upload_level_impl(K, level, color, depth); });
+}
+
+void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
+    {
         if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
         const int h = K->hs[level], w = K->ws[level];
         const size_t P = static_cast<size_t>(h) * w;
@@ -2015,7 +2021,7 @@ int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color,
         if (!K->ready[level]) ck(cudaEventCreateWithFlags(&K->ready[level], cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventRecord(K->ready[level], st), "record upload");
         K->pending[level] = 1;
-    });
+    }
 }
 
 int gs_keyframe_read_level(gs_keyframe* K, int32_t level, double* color, double* depth) {
@@ -2075,22 +2081,56 @@ int gs_render_backward_frame(gs_map* M, const gs_pose* pose, const gs_camera* ca
     });
 }
 
+struct Prefetch {
+    gs_keyframe* K = nullptr;
+    int32_t level = 0;
+    const double *color = nullptr, *depth = nullptr;
+};
+void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
+                     gs_step_report* report, const Prefetch* pf);
+
 int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_step_report* report) {
+    return guard([&] { train_step_impl(M, K, cfg, cam, report, nullptr); });
+}
+
+int gs_train_step_prefetch(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
+                           gs_keyframe* next_kf, int32_t next_level, const double* next_color,
+                           const double* next_depth, gs_step_report* report) {
     return guard([&] {
+        Prefetch pf{next_kf, next_level, next_color, next_depth};
+        train_step_impl(M, K, cfg, cam, report, next_kf ? &pf : nullptr);
+    });
+}
+
+void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
+                     gs_step_report* report, const Prefetch* pf) {
+    {
         M->ctx->use();
         *report = gs_step_report{};
         if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
-        if (K->consumed >= K->initial_iters) return;  // std::nullopt (mapper.cpp:219)
+        if (K->consumed >= K->initial_iters) {  // std::nullopt (mapper.cpp:219)
+            if (pf) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+            return;
+        }
         gs_frame* F = scratch_frame(M->ctx);
         gs_grads* G = scratch_grads(M->ctx);
         int level = 0;
         gs_loss_result lr{};
+        bool prefetched = false;
         // one host round trip per step (the loss read); a step whose render overflowed the
         // remembered pair capacity changed nothing on the device and is re-run at exact size
         for (int attempt = 0;; ++attempt) {
             grads_zero(G, M);
             train_view(M, K, *cfg, *cam, F, G, &level, attempt > 0);
             adam_impl(M, G, cfg->lr, dev_counters(F));
+            // the next step's input upload is issued behind this step's enqueued work, on the
+            // copy stream (it waits for this step's last read of that level buffer); a level
+            // this very step reads is uploaded only after the step is final (an overflow re-run
+            // must not see the next input)
+            if (pf && !prefetched && !(pf->K == K && pf->level == level)) {
+                upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+                prefetched = true;
+            }
             if (M->ctx->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
                 lr.total = lr.psnr = std::nan("");
                 break;
@@ -2101,12 +2141,13 @@ int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const g
             --M->global_step;
             if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
         }
+        if (pf && !prefetched) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
         ++K->consumed;
         report->ran = 1;
         report->level = level;
         report->loss = lr.total;
         report->psnr = lr.psnr;
-    });
+    }
 }
 
 int gs_train_accumulate(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_frame* F,

@@ -637,10 +637,22 @@ def compute_loss(out: RenderOutput, kf: Keyframe, level: int, cfg: TrainConfig, 
     return res
 
 
-def train_keyframe_step(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera, pool=None):
-    """mapper.cpp:214-238. Returns dict(level, loss, psnr) or None when the budget is spent."""
+def train_keyframe_step(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera, pool=None,
+                        prefetch: tuple | None = None):
+    """mapper.cpp:214-238. Returns dict(level, loss, psnr) or None when the budget is spent.
+    prefetch = (next_keyframe, level, colour HWC fp64, depth fp64): that upload is issued on the
+    copy stream behind this step's work (gs_train_step_prefetch); the arrays must stay alive
+    until the next call."""
     rep = StepReport()
-    _check(lib().gs_train_step(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), C.byref(rep)))
+    if prefetch is not None:
+        nk, nl, nc, nd = prefetch
+        for a in (nc, nd):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("train_keyframe_step: prefetch images must be C-contiguous float64")
+        _check(lib().gs_train_step_prefetch(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), _vp(nk.h), int(nl),
+                                            _p(nc), _p(nd), C.byref(rep)))
+    else:
+        _check(lib().gs_train_step(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), C.byref(rep)))
     if not rep.ran:
         return None
     return dict(level=rep.level, loss=rep.loss, psnr=rep.psnr)

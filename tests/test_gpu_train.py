@@ -526,3 +526,39 @@ def test_batch_trainer_matches_summed_oracle_views():  # sum of per
     assert np.all(d <= 2 * lr + 1e-6)
     assert np.mean(d <= 0.05 * lr + 1e-6) > 0.95
     assert gm.global_step == 1
+
+
+def test_train_step_prefetch_matches_upload_then_step():  # gs_train_step_prefetch
+    """Uploading step s+1's level behind step s (copy stream) gives the same training as
+    uploading each level right before its step; the prefetched data is what step s+1 reads."""
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    gt = O.random_scene(O.Rng(21), 40, cam, O.pose(), 1.0, 2.0)
+    g = gt.gaussians
+    g["p"][:, 10] = np.log(0.1 / 0.9)
+    color_x = f32(O.render(gt, O.pose(), cam).color)
+    gen = np.random.default_rng(4)
+    color_y = f32(np.clip(color_x + gen.normal(0, 0.05, color_x.shape), 0, 1))
+    sparse = np.zeros((48, 64))
+    ky = G().Keyframe(gpu_pose(O.pose()), color_y, sparse, 100, 2)
+    host = [tuple(np.ascontiguousarray(a, np.float64) for a in ky.level(l)) for l in range(3)]
+    cfg = G().TrainConfig.make(0.2, 0.5, 2, 1)
+    lv = lambda s: 2 - (s % 3)
+    _, m1 = pair(g)
+    _, m2 = pair(g)
+    k1 = G().Keyframe(gpu_pose(O.pose()), color_x, sparse, 100, 2)
+    k2 = G().Keyframe(gpu_pose(O.pose()), color_x, sparse, 100, 2)
+    r1, r2 = [], []
+    for s in range(6):
+        k1.consumed_iters = 2 - lv(s)
+        k1.upload_level(lv(s), *host[lv(s)])
+        r1.append(G().train_keyframe_step(m1, k1, cfg, gpu_cam(cam)))
+    k2.upload_level(lv(0), *host[lv(0)])
+    for s in range(6):
+        k2.consumed_iters = 2 - lv(s)
+        pf = (k2, lv(s + 1), *host[lv(s + 1)]) if s < 5 else None
+        r2.append(G().train_keyframe_step(m2, k2, cfg, gpu_cam(cam), prefetch=pf))
+    for a, b in zip(r1, r2):
+        assert a["level"] == b["level"] and a["loss"] == pytest.approx(b["loss"], rel=1e-12)
+    np.testing.assert_array_equal(m1.gaussians["p"], m2.gaussians["p"])
+    with pytest.raises(ValueError, match="float64"):
+        G().train_keyframe_step(m2, k2, cfg, gpu_cam(cam), prefetch=(k2, 0, host[0][0].astype(np.float32), host[0][1]))
