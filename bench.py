@@ -219,7 +219,11 @@ def run_ours(args, rank, world):
             if e2e:
                 kf.upload_level(lvl, *host_levels[k][lvl])
             px += shapes[lvl][0] * shapes[lvl][1]
-        trainer.step(kfs, my_views, cfg, cam)
+        after = None
+        if prefetch is not None:  # batch `prefetch`'s inputs, uploaded behind this batch's views
+            nl = LEVELS - (prefetch % 3)
+            after = lambda: [kfs[k].upload_level(nl, *host_levels[k][nl]) for k in my_views]
+        trainer.step(kfs, my_views, cfg, cam, after_accumulate=after)
         torch.cuda.current_stream().synchronize()
         return views_per_rank, px
 
@@ -369,11 +373,12 @@ def run_ours(args, rank, world):
             # (step 0's included) and each train step waits for its own level's upload
             k0, l0 = schedule(0)
             kfs[k0].upload_level(l0, *host_levels[k0][l0])
+        else:
+            l0 = LEVELS - 0 % 3
+            for k in my_views:
+                kfs[k].upload_level(l0, *host_levels[k][l0])
         for s in range(args.steps):
-            if not batch:
-                v, _ = step(s, e2e=False, prefetch=s + 1 if s + 1 < args.steps else None)
-            else:
-                v, _ = step(s, e2e=True)
+            v, _ = step(s, e2e=False, prefetch=s + 1 if s + 1 < args.steps else None)
             views += v
             lvl = LEVELS - (s % 3)
             h2d += 32 * shapes[lvl][0] * shapes[lvl][1] * (views_per_rank if batch else 1)

@@ -65,14 +65,18 @@ class BatchTrainer:
         self.buf = torch.zeros(N_PARAMS * self.cap, dtype=torch.float32, device=self.device)
         self.grads = self.G.RenderGradients(self.ctx, external_ptr=self.buf.data_ptr(), capacity=self.cap)
 
-    def step(self, keyframes, views, cfg, cam, lr=None) -> int:
+    def step(self, keyframes, views, cfg, cam, lr=None, after_accumulate=None) -> int:
         """Accumulate `views` (indices into keyframes, already at their scheduled level), reduce,
-        apply Adam; returns the number of local views rendered."""
+        apply Adam; returns the number of local views rendered. `after_accumulate()` runs once the
+        views' work is enqueued, before the collective (e.g. the next batch's input uploads on
+        the copy stream, overlapping this batch's compute)."""
         if len(self.m) > self.cap:  # the map grew since the buffer was sized
             self._alloc()
         self.grads.zero(self.m)
         for k in views:
             self.G.train_accumulate(self.m, keyframes[k], cfg, cam, self.grads, self.frame, sync=False)
+        if after_accumulate is not None:
+            after_accumulate()
         reduce_gradient_planes(self.buf, active_planes(self.m.max_active_degree()), self.cap, self.group)
         self.m.apply_gradients(self.grads, lr if lr is not None else cfg.lr)
         return len(views)
