@@ -196,7 +196,7 @@ def run_ours(args, rank, world):
         my_views = rank_views(N_FRAMES, rank, world)
         views_per_rank = len(my_views)
 
-    def step(s, e2e=False, prefetch=None):
+    def step(s, e2e=False, prefetch=None, hint=None):
         if not batch:
             k, lvl = schedule(s)
             kf = kfs[k]
@@ -208,6 +208,9 @@ def run_ours(args, rank, world):
             if prefetch is not None:  # step `prefetch`'s input, uploaded behind this step's work
                 nk, nl = schedule(prefetch)
                 pf = (kfs[nk], nl, *host_levels[nk][nl])
+            elif hint is not None:  # the next step (its render is enqueued during this read-back)
+                nk, nl = schedule(hint)
+                pf = (kfs[nk], nl)
             rep = G.train_keyframe_step(m, kf, cfg, cam, prefetch=pf)
             assert rep is not None and rep["level"] == lvl
             return 1, shapes[lvl][0] * shapes[lvl][1]
@@ -233,8 +236,8 @@ def run_ours(args, rank, world):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for s in range(args.warmup):
-        step(s)
+    for s in range(args.warmup):  # (no hint past the warm-up: the timed region renders all its steps)
+        step(s, hint=s + 1 if s + 1 < args.warmup else None)
     barrier()
     # GS_PROFILE_RANGE=1: restrict an `ncu --profile-from-start off` capture to the timed steps
     prof_range = os.environ.get("GS_PROFILE_RANGE") == "1"
@@ -249,7 +252,7 @@ def run_ours(args, rank, world):
         e0.record(stream)
         views = pix = 0
         for s in range(args.steps):
-            v, p = step(args.warmup + s)
+            v, p = step(args.warmup + s, hint=args.warmup + s + 1 if s + 1 < args.steps else None)
             views += v; pix += p
             step_ev[s].record(stream)
         e1.record(stream)

@@ -139,6 +139,8 @@ int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64
 /* diagnostics: thread order of the per-Gaussian VJP kernel (0 depth rank, 1 map index, 2 the
    visible list; -1 = automatic: the visible list) */
 int gs_debug_set_k8_order(int order);
+/* diagnostics: speculative next-step renders enqueued / used on this context (gs_train_step_prefetch) */
+int gs_debug_speculation(gs_context* ctx, int64_t* out2);
 /* checkpoint format v1 (io/checkpoint.cpp:17-73): text header + 476-byte fp64 AoS records.
    save_checkpoint writes the device map's parameters (exact fp64 widening of the fp32 store);
    load_checkpoint returns a NEW map (fresh Adam state, GaussianMap::append) or GS_ERUNTIME for

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <optional>
 #include <fstream>
 #include <iomanip>
@@ -169,6 +170,21 @@ struct gs_context {
     }
     int64_t launches = 0;
     gs_frame* scratch_frame = nullptr;
+    // train steps alternate between two frames: while step s's report is read back, the next
+    // step's render (known from gs_train_step_prefetch) is already enqueued into the other frame
+    gs_frame* train_frames[2] = {nullptr, nullptr};
+    int train_parity = 0;
+    cudaEvent_t loss_ready = nullptr;  // the step's read-back copies (waited on instead of the stream)
+    int64_t spec_enqueued = 0, spec_used = 0;  // diagnostics
+    struct Speculation {
+        bool valid = false;
+        const gs_map* map = nullptr;
+        const gs_keyframe* kf = nullptr;
+        int level = -1;
+        uint64_t version = 0;
+        gs_camera cam{};
+        int frame = 0;
+    } spec;
     gs_grads* scratch_grads = nullptr;
     // optional per-kernel event timing (bench roofline); events are pooled
     bool profile = false;
@@ -252,6 +268,7 @@ struct gs_map {
     double scene_extent = 1.0;
     int64_t global_step = 0;
     int64_t adam_count = 0;  // updates applied to this map; Gaussian i's Adam step = adam_count - birth[i]
+    uint64_t version = 0;    // bumped by every change a render would see (speculative renders check it)
     DevBuf minmax;
 
     int min_degree = 0;
@@ -264,7 +281,8 @@ struct gs_map {
         birth = nullptr;
         degree = nullptr;
     }
-    void recompute_max_degree() {
+    void recompute_max_degree() {  // called after every host-visible change of the Gaussians
+        ++version;
         int d = 0, lo = 3;
         for (int8_t x : deg_host) {
             d = std::max<int>(d, x);
@@ -692,6 +710,7 @@ void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsign
     launch_adam(M->params, M->m, M->v, M->birth, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
                 M->scene_extent, M->adam_count + 1, counters, M->max_degree, M->ctx->stream);
     ++M->adam_count;
+    ++M->version;
     M->ctx->launched();
     ++M->global_step;
 }
@@ -732,7 +751,9 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
 }
 
 // loss scalars and the frame's counts in one round trip
-gs_loss_result read_loss(gs_frame* F) {
+// `between` (optional) enqueues more work after the read-back copies and before the host waits
+// for them (the next step's speculative render): the host then waits on the copies alone
+gs_loss_result read_loss(gs_frame* F, const std::function<void()>& between = {}) {
     gs_context* C = F->ctx;
     C->pinned.ensure(sizeof(LossScalars) + 64);
     char* pin = static_cast<char*>(C->pinned.p);
@@ -740,7 +761,14 @@ gs_loss_result read_loss(gs_frame* F) {
     if (!F->counts_known)
         ck(cudaMemcpyAsync(pin + sizeof(LossScalars), F->counters.p, kNumCounters * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, C->stream), "d2h counters");
-    ck(cudaStreamSynchronize(C->stream), "sync loss");
+    if (between) {
+        if (!C->loss_ready) ck(cudaEventCreateWithFlags(&C->loss_ready, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(C->loss_ready, C->stream), "record read-back");
+        between();
+        ck(cudaEventSynchronize(C->loss_ready), "sync loss");
+    } else {
+        ck(cudaStreamSynchronize(C->stream), "sync loss");
+    }
     if (!F->counts_known) take_counts(F, reinterpret_cast<const unsigned long long*>(pin + sizeof(LossScalars)));
     LossScalars s;
     std::memcpy(&s, pin, sizeof(s));
@@ -805,6 +833,14 @@ gs_frame* scratch_frame(gs_context* C) {
     return C->scratch_frame;
 }
 
+gs_frame* train_frame(gs_context* C, int i) {
+    if (!C->train_frames[i]) {
+        C->train_frames[i] = new gs_frame();
+        C->train_frames[i]->ctx = C;
+    }
+    return C->train_frames[i];
+}
+
 gs_grads* scratch_grads(gs_context* C) {
     if (!C->scratch_grads) {
         C->scratch_grads = new gs_grads();
@@ -864,6 +900,9 @@ int gs_context_destroy(gs_context* C) {
         C->use();
         cudaStreamSynchronize(C->stream);
         delete C->scratch_frame;
+        delete C->train_frames[0];
+        delete C->train_frames[1];
+        if (C->loss_ready) cudaEventDestroy(C->loss_ready);
         if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external)
             pool_free(C->scratch_grads->planes, C->stream);
         delete C->scratch_grads;
@@ -1515,6 +1554,14 @@ int gs_integrate_keyframe(gs_map* M, const gs_pose* pose, const gs_camera* cam, 
 }
 
 // diagnostics: K8b thread order (0 rank, 1 map, 2 visible list; -1 = automatic)
+// diagnostics: speculative next-step renders enqueued / used so far on this context
+int gs_debug_speculation(gs_context* C, int64_t* out2) {
+    return guard([&] {
+        out2[0] = C->spec_enqueued;
+        out2[1] = C->spec_used;
+    });
+}
+
 int gs_debug_set_k8_order(int order) {
     return guard([&] { set_k8_order(order); });
 }
@@ -2097,51 +2144,91 @@ int gs_train_step_prefetch(gs_map* M, gs_keyframe* K, const gs_train_config* cfg
                            gs_keyframe* next_kf, int32_t next_level, const double* next_color,
                            const double* next_depth, gs_step_report* report) {
     return guard([&] {
+        if (next_kf && (next_color == nullptr) != (next_depth == nullptr))
+            fail(GS_EINVAL, "train_step_prefetch: pass both next images or neither");
         Prefetch pf{next_kf, next_level, next_color, next_depth};
         train_step_impl(M, K, cfg, cam, report, next_kf ? &pf : nullptr);
     });
 }
 
+bool same_camera(const gs_camera& a, const gs_camera& b) {
+    return a.fx == b.fx && a.fy == b.fy && a.cx == b.cx && a.cy == b.cy && a.width == b.width && a.height == b.height;
+}
+
 void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
                      gs_step_report* report, const Prefetch* pf) {
     {
-        M->ctx->use();
+        gs_context* C = M->ctx;
+        C->use();
         *report = gs_step_report{};
         if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
+        auto upload = [&] {
+            if (pf && pf->color) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+        };
         if (K->consumed >= K->initial_iters) {  // std::nullopt (mapper.cpp:219)
-            if (pf) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+            upload();
             return;
         }
-        gs_frame* F = scratch_frame(M->ctx);
-        gs_grads* G = scratch_grads(M->ctx);
-        int level = 0;
+        gs_grads* G = scratch_grads(C);
+        const int level = schedule_level(K, *cfg);
+        const gs_camera lc = scaled(*cam, level);
+        // this step's render was enqueued speculatively by the previous call when it predicted
+        // this (keyframe, level, camera) and the map has not changed since
+        auto& sp = C->spec;
+        const bool have = sp.valid && sp.map == M && sp.kf == K && sp.level == level && sp.version == M->version &&
+                          same_camera(sp.cam, *cam);
+        const int fi = have ? sp.frame : C->train_parity;
+        sp.valid = false;
+        C->spec_used += have;
+        gs_frame* F = train_frame(C, fi);
+        C->train_parity = fi ^ 1;  // the next step renders into the other frame
         gs_loss_result lr{};
         bool prefetched = false;
+        // a level this very step reads is uploaded only after the step is final (an overflow
+        // re-run must not see the next input)
+        const bool late_upload = pf && pf->K == K && pf->level == level;
+        // the next step's render, enqueued while this step's read-back is in flight: the host's
+        // return, report and next call then overlap device work instead of idling it
+        auto speculate = [&] {
+            if (!pf || !pf->K || pf->K->hs.empty() || pf->level < 0 ||
+                pf->level >= static_cast<int>(pf->K->hs.size()) || M->n == 0)
+                return;
+            const gs_camera nc = scaled(*cam, pf->level);
+            gs_frame* B = train_frame(C, fi ^ 1);
+            const gs_frame::Caps& cs = B->cap_slot(nc.width, nc.height);
+            if (cs.pairs == 0) return;  // first render at this size needs exact counts (a sync)
+            render_impl(M, pf->K->pose, nc, B, false, false);
+            sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, fi ^ 1};
+            ++C->spec_enqueued;
+        };
         // one host round trip per step (the loss read); a step whose render overflowed the
         // remembered pair capacity changed nothing on the device and is re-run at exact size
         for (int attempt = 0;; ++attempt) {
             grads_zero(G, M);
-            train_view(M, K, *cfg, *cam, F, G, &level, attempt > 0);
+            if (!(have && attempt == 0)) render_impl(M, K->pose, lc, F, attempt > 0, false);
+            loss_impl(F, K, level, *cfg);
+            backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
+                          &F->loss.as<LossScalars>()->depth_scale, G);
             adam_impl(M, G, cfg->lr, dev_counters(F));
             // the next step's input upload is issued behind this step's enqueued work, on the
-            // copy stream (it waits for this step's last read of that level buffer); a level
-            // this very step reads is uploaded only after the step is final (an overflow re-run
-            // must not see the next input)
-            if (pf && !prefetched && !(pf->K == K && pf->level == level)) {
-                upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+            // copy stream (it waits for this step's last read of that level buffer)
+            if (!prefetched && !late_upload) {
+                upload();
                 prefetched = true;
             }
-            if (M->ctx->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
+            if (C->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
                 lr.total = lr.psnr = std::nan("");
                 break;
             }
-            lr = read_loss(F);
+            if (attempt == 0 && pf) lr = read_loss(F, speculate);
+            else lr = read_loss(F);
             if (!F->overflow) break;
+            sp.valid = false;  // rendered from the map before this step's (re-run) update
             --M->adam_count;
             --M->global_step;
             if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
         }
-        if (pf && !prefetched) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+        if (!prefetched) upload();
         ++K->consumed;
         report->ran = 1;
         report->level = level;

@@ -640,14 +640,15 @@ def compute_loss(out: RenderOutput, kf: Keyframe, level: int, cfg: TrainConfig, 
 def train_keyframe_step(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera, pool=None,
                         prefetch: tuple | None = None):
     """mapper.cpp:214-238. Returns dict(level, loss, psnr) or None when the budget is spent.
-    prefetch = (next_keyframe, level, colour HWC fp64, depth fp64): that upload is issued on the
-    copy stream behind this step's work (gs_train_step_prefetch); the arrays must stay alive
-    until the next call."""
+    prefetch = (next_keyframe, level[, colour HWC fp64, depth fp64]) names the NEXT step
+    (gs_train_step_prefetch): its render is enqueued while this step's report is read back (and
+    used by the next call if the map and camera are unchanged), and the images, if given, are
+    uploaded on the copy stream behind this step's work; they must stay alive until the next call."""
     rep = StepReport()
     if prefetch is not None:
-        nk, nl, nc, nd = prefetch
+        nk, nl, nc, nd = (tuple(prefetch) + (None, None))[:4]  # (keyframe, level[, colour, depth])
         for a in (nc, nd):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
+            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous):
                 raise ValueError("train_keyframe_step: prefetch images must be C-contiguous float64")
         _check(lib().gs_train_step_prefetch(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), _vp(nk.h), int(nl),
                                             _p(nc), _p(nd), C.byref(rep)))

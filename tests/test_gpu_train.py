@@ -562,3 +562,75 @@ def test_train_step_prefetch_matches_upload_then_step():  # gs_train_step_prefet
     np.testing.assert_array_equal(m1.gaussians["p"], m2.gaussians["p"])
     with pytest.raises(ValueError, match="float64"):
         G().train_keyframe_step(m2, k2, cfg, gpu_cam(cam), prefetch=(k2, 0, host[0][0].astype(np.float32), host[0][1]))
+
+
+def test_speculative_next_render_changes_nothing():  # gs_train_step_prefetch with a (keyframe, level) hint
+    """Naming the next step lets the library enqueue its render during this step's read-back.
+    Training with correct hints, wrong hints, and a host edit of the map between steps gives
+    exactly the training without hints."""
+    cam = O.camera(100, 100, 31.5, 23.5, 64, 48)
+    gt = O.random_scene(O.Rng(23), 60, cam, O.pose(), 1.0, 2.0)
+    g = gt.gaussians
+    g["p"][:, 10] = np.log(0.2 / 0.8)
+    poses = [O.pose(), O.pose(1, 0.0, 0.02, 0.0, t=(0.05, 0.0, 0.0))]
+    colors = [f32(O.render(gt, p, cam).color) for p in poses]
+    cfg = G().TrainConfig.make(0.2, 0.5, 2, 1)
+    sched = [(k, 2 - s % 3) for k in (0, 1, 0, 1) for s in range(3)]
+
+    def run(mode):
+        _, m = pair(g)
+        kfs = [G().Keyframe(gpu_pose(poses[k]), colors[k], np.zeros((48, 64)), 3, 2) for k in (0, 1)]
+        reps = []
+        for i, (k, lvl) in enumerate(sched):
+            if kfs[k].consumed_iters >= 3:
+                kfs[k].consumed_iters = 0
+            hint = None
+            if i + 1 < len(sched):
+                nk, nl = sched[i + 1]
+                if mode == "hint":
+                    hint = (kfs[nk], nl)
+                elif mode == "wrong":
+                    hint = (kfs[1 - nk], (nl + 1) % 3)
+                elif mode == "edit":
+                    hint = (kfs[nk], nl)
+            rep = G().train_keyframe_step(m, kfs[k], cfg, gpu_cam(cam), prefetch=hint)
+            assert rep["level"] == lvl
+            reps.append(rep["loss"])
+            if mode == "edit" and i == 4:  # host edit between steps: the speculation is stale
+                gg = m.gaussians
+                gg["p"][:, 10] -= 0.01
+                m.gaussians = gg
+        return reps, m.gaussians["p"]
+
+    import ctypes
+    ctx = G().default_context()
+    cnt = np.zeros(2, np.int64)
+    spec = lambda: (G().lib().gs_debug_speculation(ctypes.c_void_p(ctx.h), cnt.ctypes.data_as(ctypes.c_void_p)),
+                    cnt.copy())[1]
+    base_l, base_p = run(None)
+    for mode in ("hint", "wrong"):
+        before = spec()
+        l, p = run(mode)
+        after = spec()
+        if mode == "hint":
+            assert after[1] - before[1] >= 4  # speculative renders were actually used
+        else:
+            assert after[1] == before[1]      # mispredicted: enqueued, never used
+        np.testing.assert_allclose(l, base_l, rtol=1e-12)
+        np.testing.assert_array_equal(p, base_p)
+    # the edited run differs from the base but must equal an edited run without hints
+    l_e, p_e = run("edit")
+    _, m2 = pair(g)
+    # replay "edit" without hints
+    kfs = [G().Keyframe(gpu_pose(poses[k]), colors[k], np.zeros((48, 64)), 3, 2) for k in (0, 1)]
+    ref = []
+    for i, (k, lvl) in enumerate(sched):
+        if kfs[k].consumed_iters >= 3:
+            kfs[k].consumed_iters = 0
+        ref.append(G().train_keyframe_step(m2, kfs[k], cfg, gpu_cam(cam))["loss"])
+        if i == 4:
+            gg = m2.gaussians
+            gg["p"][:, 10] -= 0.01
+            m2.gaussians = gg
+    np.testing.assert_allclose(l_e, ref, rtol=1e-12)
+    np.testing.assert_array_equal(p_e, m2.gaussians["p"])
