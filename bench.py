@@ -289,6 +289,8 @@ def run_ours(args, rank, world):
               "dtype": "f32 (fp64 geometry, fp64 transmittance)",
               "data": "synthetic (reference synthetic.cpp scene, colourised-LiDAR-initialised map)",
               "mpix_per_s": round(total_pix / (ms_max / 1e3) / 1e6, 3), "per_level": per_level,
+              "per_level_note": "intervals between consecutive step reports; each step names the next, whose render "
+                                "is enqueued during this step's read-back and so falls in this step's interval",
               "config": {"workload": ("C4: 8-keyframe batch sharded over ranks, NCCL all-reduce" if batch else
                                       "C3: 1M Gaussians 1280x1024, 3-level pyramid (L2,L1,L0 in turn), L1+SSIM+depth loss"),
                          "n_gaussians": len(m), "width": W0, "height": H0, "pyramid_levels": LEVELS + 1,
