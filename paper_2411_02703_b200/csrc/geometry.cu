@@ -284,7 +284,9 @@ void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, i
 // monotone non-decreasing function of the depth) and the map index. Counts the visible set and the (tile, gaussian) pairs.
 // Reference: rasterizer.cpp:37-68 (project_visible) + projection.cpp:17-40 + sh.cpp:82-92 +
 // rasterizer.cpp:81-88 (pixel rect -> tile rect).
-__global__ void __launch_bounds__(256) preprocess_fwd_kernel(
+// 3 CTAs per SM (80 registers, 80 B of L1-resident spills) beat the unconstrained 128-register
+// build: the fp64 chain is latency-bound and the extra warps hide it (measured -6%)
+__global__ void __launch_bounds__(256, 3) preprocess_fwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree,
     const int32_t* __restrict__ cand, ViewParams v, Splat* __restrict__ rec_by_gid,
     unsigned long long* __restrict__ depth_key, int32_t* __restrict__ vis_gid, uint32_t* __restrict__ key32,
