@@ -2181,7 +2181,9 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
         sp.valid = false;
         C->spec_used += have;
         gs_frame* F = train_frame(C, fi);
-        C->train_parity = fi ^ 1;  // the next step renders into the other frame
+        // with a named next step, its render goes to the other frame; without one, steps stay on
+        // one frame (its remembered capacities then track a growing map step by step)
+        C->train_parity = pf ? fi ^ 1 : fi;
         gs_loss_result lr{};
         bool prefetched = false;
         // a level this very step reads is uploaded only after the step is final (an overflow
