@@ -183,6 +183,7 @@ struct gs_context {
         int level = -1;
         uint64_t version = 0;
         gs_camera cam{};
+        gs_pose pose{};
         int frame = 0;
     } spec;
     gs_grads* scratch_grads = nullptr;
@@ -1053,6 +1054,7 @@ int gs_map_create(gs_context* C, gs_map** out) {
 int gs_map_destroy(gs_map* M) {
     return guard([&] {
         if (!M) return;
+        if (M->ctx->spec.map == M) M->ctx->spec.valid = false;
         M->ctx->use();
         cudaStreamSynchronize(M->ctx->stream);
         M->free_all();
@@ -2029,6 +2031,7 @@ int gs_keyframe_create_device(gs_context* C, const gs_pose* pose, const float* c
 int gs_keyframe_destroy(gs_keyframe* K) {
     return guard([&] {
         if (!K) return;
+        if (K->ctx->spec.kf == K) K->ctx->spec.valid = false;  // no stale match on a reused address
         cudaStreamSynchronize(K->ctx->stream);
         if (K->ctx->copy_stream) cudaStreamSynchronize(K->ctx->copy_stream);
         delete K;
@@ -2176,7 +2179,7 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
         // this (keyframe, level, camera) and the map has not changed since
         auto& sp = C->spec;
         const bool have = sp.valid && sp.map == M && sp.kf == K && sp.level == level && sp.version == M->version &&
-                          same_camera(sp.cam, *cam);
+                          same_camera(sp.cam, *cam) && std::memcmp(&sp.pose, &K->pose, sizeof(gs_pose)) == 0;
         const int fi = have ? sp.frame : C->train_parity;
         sp.valid = false;
         C->spec_used += have;
@@ -2200,7 +2203,7 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
             const gs_frame::Caps& cs = B->cap_slot(nc.width, nc.height);
             if (cs.pairs == 0) return;  // first render at this size needs exact counts (a sync)
             render_impl(M, pf->K->pose, nc, B, false, false);
-            sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, fi ^ 1};
+            sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, pf->K->pose, fi ^ 1};
             ++C->spec_enqueued;
         };
         // one host round trip per step (the loss read); a step whose render overflowed the
