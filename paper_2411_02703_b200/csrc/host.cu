@@ -1,396 +1,13 @@
-// Host side of the C-ABI (include/gsmap_b200.h): device state, buffer management and the
-// orchestration of the hot step train_keyframe_step (mapper.cpp:214-238) over the kernels.
-// Exceptions never cross the boundary: every entry point returns a status and keeps a
-// thread-local message (gs_last_error).
-#include <cub/cub.cuh>
-
-#include <algorithm>
-#include <chrono>
-#include <cmath>
-#include <functional>
-#include <optional>
-#include <fstream>
-#include <iomanip>
-#include <limits>
-#include <sstream>
-#include <cstring>
-#include <stdexcept>
-#include <string>
-#include <vector>
-
-#include "../../include/gsmap_b200.h"
-#include "common.cuh"
-#include "kernels.cuh"
-#include "blend_common.cuh"
-
-using namespace gsb;
-
-namespace {
-
-thread_local std::string g_err;
-
-struct GsError : std::runtime_error {
-    int code;
-    GsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw GsError(code, msg); }
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        fail(e == cudaErrorMemoryAllocation ? GS_ENOMEM : GS_ECUDA,
-             std::string(what) + ": " + cudaGetErrorString(e));
-    }
-}
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return GS_OK;
-    } catch (const GsError& e) {
-        g_err = e.what();
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return GS_ENOMEM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return GS_ELOGIC;
-    }
-}
-
-// Grow-only device buffer (no per-iteration cudaMalloc on the hot path). Buffers of objects
-// created and destroyed in the mapping loop (keyframes) come from the device's stream-ordered
-// memory pool instead (`pool` = the stream they are used on): their frees return memory to the
-// pool without the device-wide synchronisation and unmapping of cudaFree (~50 ms per keyframe).
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    cudaStream_t pool = nullptr;
-    bool pooled = false;
-    template <class T>
-    T* as() const { return static_cast<T*>(p); }
-    void ensure(size_t need) {
-        if (need <= bytes) return;
-        release();
-        const size_t alloc = std::max<size_t>(need + need / 4, 256);
-        if (pool) {
-            ck(cudaMallocAsync(&p, alloc, pool), "cudaMallocAsync");
-            // usable by every stream from here on (keyframe uploads run on the copy stream)
-            ck(cudaStreamSynchronize(pool), "sync");
-            pooled = true;
-        } else {
-            ck(cudaMalloc(&p, alloc), "cudaMalloc");
-            pooled = false;
-        }
-        bytes = alloc;
-    }
-    void release() {
-        if (p) {
-            if (pooled) cudaFreeAsync(p, pool);
-            else cudaFree(p);
-        }
-        p = nullptr;
-        bytes = 0;
-    }
-};
-
-struct PinnedBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void ensure(size_t need) {
-        if (need <= bytes) return;
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-        ck(cudaMallocHost(&p, need), "cudaMallocHost");
-        bytes = need;
-    }
-    ~PinnedBuf() {
-        if (p) cudaFreeHost(p);
-    }
-};
-
-void validate_camera(const gs_camera& c) {  // core/types.hpp:22-29
-    if (c.fx <= 0.0 || c.fy <= 0.0) fail(GS_EINVAL, "CameraModel: focal lengths must be positive");
-    if (c.width <= 0 || c.height <= 0) fail(GS_EINVAL, "CameraModel: image size must be positive");
-    if (c.cx < 0.0 || c.cx >= c.width || c.cy < 0.0 || c.cy >= c.height)
-        fail(GS_EINVAL, "CameraModel: principal point outside image");
-}
-
-gs_camera scaled(const gs_camera& c, int level) {  // core/types.hpp:34-44
-    gs_camera s = c;
-    const double f = static_cast<double>(1 << level);
-    s.fx = c.fx / f;
-    s.fy = c.fy / f;
-    s.cx = (c.cx + 0.5) / f - 0.5;
-    s.cy = (c.cy + 0.5) / f - 0.5;
-    s.width = (c.width + (1 << level) - 1) >> level;
-    s.height = (c.height + (1 << level) - 1) >> level;
-    return s;
-}
-
-ViewParams make_view(const gs_pose& p, const gs_camera& c) {
-    ViewParams v;
-    v.qw = p.qw; v.qx = p.qx; v.qy = p.qy; v.qz = p.qz;
-    v.tx = p.tx; v.ty = p.ty; v.tz = p.tz;
-    v.fx = c.fx; v.fy = c.fy; v.cx = c.cx; v.cy = c.cy;
-    v.width = c.width; v.height = c.height;
-    v.tiles_x = div_up(c.width, kTile);
-    v.tiles_y = div_up(c.height, kTile);
-    return v;
-}
-
-int n_active_planes(int max_degree) { return kGeomParams + 3 * (max_degree + 1) * (max_degree + 1); }
-
-}  // namespace
-
-// ============================================================================ handles
-// grow-only scratch of the per-keyframe mapping calls (filter / init / sparse depth / prune):
-// one slot per role, so nested calls never share a slot and no call pays cudaMalloc twice
-enum ScratchSlot {
-    kScPoints, kScKept, kScKeep, kScPos, kScKeys, kScKeys2, kScIdx, kScIdx2, kScBBox, kScHashK, kScHashV,
-    kScDepth, kScColor, kScPruneKeep, kScPrunePos, kScPruneTmp, kNumScratch
-};
-
-struct gs_context {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    DevBuf cub_tmp;
-    DevBuf scratch[kNumScratch];
-    DevBuf& sc(ScratchSlot s) { return scratch[s]; }
-    PinnedBuf pinned;
-    cudaStream_t copy_stream = nullptr;  // host uploads (overlap the compute stream)
-    bool defer_sync = false;             // diagnostics: train steps skip the loss read-back
-    cudaStream_t copies() {
-        if (!copy_stream) ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
-        return copy_stream;
-    }
-    int64_t launches = 0;
-    gs_frame* scratch_frame = nullptr;
-    // train steps alternate between two frames: while step s's report is read back, the next
-    // step's render (known from gs_train_step_prefetch) is already enqueued into the other frame
-    gs_frame* train_frames[2] = {nullptr, nullptr};
-    int train_parity = 0;
-    cudaEvent_t loss_ready = nullptr;  // the step's read-back copies (waited on instead of the stream)
-    int64_t spec_enqueued = 0, spec_used = 0;  // diagnostics
-    struct Speculation {
-        bool valid = false;
-        const gs_map* map = nullptr;
-        const gs_keyframe* kf = nullptr;
-        int level = -1;
-        uint64_t version = 0;
-        gs_camera cam{};
-        gs_pose pose{};
-        int frame = 0;
-    } spec;
-    gs_grads* scratch_grads = nullptr;
-    // optional per-kernel event timing (bench roofline); events are pooled
-    bool profile = false;
-    struct ProfRec {
-        const char* name;
-        cudaEvent_t a, b;
-        double host_us;  // host time spent enqueueing the scope
-    };
-    std::vector<ProfRec> prof;
-    std::vector<cudaEvent_t> ev_pool;
-    size_t ev_next = 0;
-
-    cudaEvent_t ev() {
-        if (ev_next == ev_pool.size()) {
-            cudaEvent_t e;
-            ck(cudaEventCreate(&e), "cudaEventCreate");
-            ev_pool.push_back(e);
-        }
-        return ev_pool[ev_next++];
-    }
-    void use() { ck(cudaSetDevice(device), "cudaSetDevice"); }
-    void launched(int k = 1) {
-        launches += k;
-        ck(cudaGetLastError(), "kernel launch");
-    }
-    void* cub(size_t bytes) {
-        cub_tmp.ensure(bytes);
-        return cub_tmp.p;
-    }
-};
-
-namespace {
-// Brackets one kernel family with CUDA events on the context stream when profiling is on.
-struct Scope {
-    gs_context* C;
-    const char* name;
-    cudaEvent_t a = nullptr;
-    std::chrono::steady_clock::time_point h0;
-    Scope(gs_context* c, const char* n) : C(c), name(n) {
-        if (C->profile) {
-            h0 = std::chrono::steady_clock::now();
-            a = C->ev();
-            cudaEventRecord(a, C->stream);
-        }
-    }
-    ~Scope() {
-        if (C->profile && a) {
-            cudaEvent_t b = C->ev();
-            cudaEventRecord(b, C->stream);
-            const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
-            C->prof.push_back({name, a, b, us});
-        }
-    }
-};
-}  // namespace
-
-// Map-sized arrays (planes, Adam state, gradients) and the mapping calls' scratch come from the device's
-// stream-ordered pool on the context stream: the map grows in the mapping loop, and pooled
-// frees / reallocations skip cudaFree's device-wide synchronisation and unmapping (measured:
-// 16 ms to 1 s per growth with cudaMalloc / cudaFree, run to run).
-template <class T>
-T* pool_alloc(size_t count, cudaStream_t st, const char* what) {
-    void* p = nullptr;
-    ck(cudaMallocAsync(&p, sizeof(T) * count, st), what);
-    return static_cast<T*>(p);
-}
-inline void pool_free(void* p, cudaStream_t st) {
-    if (p) cudaFreeAsync(p, st);
-}
-
-struct gs_map {
-    gs_context* ctx = nullptr;
-    int64_t n = 0, cap = 0;
-    float* params = nullptr;
-    float* m = nullptr;
-    float* v = nullptr;
-    int32_t* birth = nullptr;  // per Gaussian: adam_count when its optimizer state was reset
-    int8_t* degree = nullptr;
-    std::vector<int8_t> deg_host;
-    int max_degree = 0;
-    double scene_extent = 1.0;
-    int64_t global_step = 0;
-    int64_t adam_count = 0;  // updates applied to this map; Gaussian i's Adam step = adam_count - birth[i]
-    uint64_t version = 0;    // bumped by every change a render would see (speculative renders check it)
-    DevBuf minmax;
-
-    int min_degree = 0;
-    void free_all() {
-        cudaStream_t st = ctx->stream;
-        for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
-                        static_cast<void*>(birth), static_cast<void*>(degree)})
-            pool_free(p, st);
-        params = m = v = nullptr;
-        birth = nullptr;
-        degree = nullptr;
-    }
-    void recompute_max_degree() {  // called after every host-visible change of the Gaussians
-        ++version;
-        int d = 0, lo = 3;
-        for (int8_t x : deg_host) {
-            d = std::max<int>(d, x);
-            lo = std::min<int>(lo, x);
-        }
-        max_degree = d;
-        min_degree = deg_host.empty() ? 0 : lo;
-    }
-};
-
-struct gs_frame {
-    gs_context* ctx = nullptr;
-    bool rendered = false;
-    ViewParams view{};
-    int64_t map_n = 0, n_vis = 0, n_pairs = 0;
-    // Device counts (Counter) are read back lazily: n_vis / n_pairs / overflow are valid only
-    // when counts_known. Pair buffers are sized by a capacity remembered per resolution.
-    DevBuf counters;
-    bool counts_known = false, overflow = false;
-    uint32_t pair_cap = 0;
-    int vis_cap = 0;  // ranks the depth sort and the rank-indexed kernels cover
-    struct Caps {
-        uint32_t pairs = 0;  // (tile, gaussian) pairs
-        int vis = 0;         // visible Gaussians
-    };
-    std::vector<std::pair<int64_t, Caps>> caps;  // (width << 32 | height) -> capacities
-    Caps& cap_slot(int w, int h) {
-        const int64_t key = (static_cast<int64_t>(w) << 32) | static_cast<uint32_t>(h);
-        for (auto& c : caps)
-            if (c.first == key) return c.second;
-        caps.emplace_back(key, Caps{});
-        return caps.back().second;
-    }
-    // per-Gaussian / per-rank / per-pair scratch
-    DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
-        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, rank_sums, depth_sorted;
-    // per-pixel
-    DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
-    DevBuf checkpoints;  // backward list-segment checkpoints [nseg - 1][5][pixels]
-    DevBuf seg_scratch;  // segmented forward: per-segment local states, Tl and stop segment
-    int nseg = 1;
-    DevBuf loss;  // LossScalars
-    DevBuf rank_of;  // K8b: depth rank per map index (-1 = culled)
-    DevBuf eval_quant, eval_gt, eval_stage;  // evaluate_view scratch
-    bool has_cotangent = false;
-    bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)
-    int loss_level = -1;
-    double loss_lambda = 0.0, loss_lambda_d = 0.0;
-};
-
-struct gs_grads {
-    gs_context* ctx = nullptr;
-    float* planes = nullptr;
-    int64_t cap = 0;
-    int64_t n = -1;      // Gaussians the gradient set describes (-1 = unset)
-    bool clean = false;  // all planes zero since the last gs_grads_zero (no backward yet)
-    bool external = false;
-    void ensure(int64_t need) {
-        if (need <= cap) return;
-        if (external) fail(GS_EINVAL, "gs_grads: external buffer too small for the map");
-        pool_free(planes, ctx->stream);
-        planes = nullptr;
-        const int64_t c = (std::max<int64_t>(need + need / 4, 1024) + 63) / 64 * 64;
-        planes = pool_alloc<float>(kNumParams * c, ctx->stream, "alloc grads");
-        ck(cudaMemsetAsync(planes, 0, sizeof(float) * kNumParams * c, ctx->stream), "memset grads");
-        cap = c;
-    }
-};
-
-struct gs_keyframe {
-    gs_context* ctx = nullptr;
-    gs_pose pose{};
-    int32_t initial_iters = 0, consumed = 0;
-    std::vector<int> hs, ws;
-    std::vector<DevBuf> color, depth;  // per level: planes [3][h][w] and [h][w]
-    DevBuf stage;                      // fp64 HWC staging for host uploads
-    // host uploads run on the context's copy stream: `ready[l]` marks level l's conversion,
-    // `used` the compute stream's last read of any level (an upload waits for it first)
-    std::vector<cudaEvent_t> ready;
-    std::vector<char> pending;
-    cudaEvent_t used = nullptr;
-    bool used_valid = false;
-    ~gs_keyframe() {
-        for (auto& b : color) b.release();
-        for (auto& b : depth) b.release();
-        stage.release();
-        for (cudaEvent_t e : ready)
-            if (e) cudaEventDestroy(e);
-        if (used) cudaEventDestroy(used);
-    }
-    // the compute stream must see level l's latest upload before reading it
-    void acquire(int l, cudaStream_t st) {
-        if (l < static_cast<int>(pending.size()) && pending[l]) {
-            ck(cudaStreamWaitEvent(st, ready[l], 0), "wait upload");
-            pending[l] = 0;
-        }
-    }
-    // after enqueueing reads of the level buffers on the compute stream
-    void release_reads(cudaStream_t st) {
-        if (!used) ck(cudaEventCreateWithFlags(&used, cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaEventRecord(used, st), "record use");
-        used_valid = true;
-    }
-};
+// Host side of the C-ABI (include/gsmap_b200.h): the handles (context, map, frame, gradients,
+// keyframe), buffer management and the orchestration of the hot step train_keyframe_step
+// (mapper.cpp:214-238) over the kernels. Mapping-loop helpers: host_mapping.cu; checkpoint,
+// optimizer state and evaluation: host_io.cu; shared declarations: host_internal.cuh.
+#include "host_internal.cuh"
 
 // ============================================================================ internals
-namespace {
+namespace gsb_host {
+
+thread_local std::string g_err;
 
 void map_reserve(gs_map* M, int64_t need) {
     if (need <= M->cap) return;
@@ -518,7 +135,7 @@ uint32_t grown_cap(int64_t pairs) {
 // exact_counts (or an unknown capacity) the pair count is read back first and the capacity
 // grown to fit, so the render cannot overflow.
 void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame* F, bool exact_counts,
-                 bool stats = true) {
+                 bool stats) {
     validate_camera(cam);
     gs_context* C = M->ctx;
     C->use();
@@ -704,7 +321,7 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
 }
 
 // counters: the frame whose gradients these are (the update is skipped if it overflowed)
-void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsigned long long* counters = nullptr) {
+void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsigned long long* counters) {
     if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
@@ -754,7 +371,7 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
 // loss scalars and the frame's counts in one round trip
 // `between` (optional) enqueues more work after the read-back copies and before the host waits
 // for them (the next step's speculative render): the host then waits on the copies alone
-gs_loss_result read_loss(gs_frame* F, const std::function<void()>& between = {}) {
+gs_loss_result read_loss(gs_frame* F, const std::function<void()>& between) {
     gs_context* C = F->ctx;
     C->pinned.ensure(sizeof(LossScalars) + 64);
     char* pin = static_cast<char*>(C->pinned.p);
@@ -860,7 +477,7 @@ void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_
     *level_out = level;
 }
 
-}  // namespace
+}  // namespace gsb_host
 
 // ============================================================================ C-ABI
 extern "C" {
@@ -1177,384 +794,6 @@ int gs_map_raise_sh_degree(gs_map* M, int degree) {  // gaussian_map.cpp:75-79
 
 int gs_map_max_active_degree(gs_map* M, int* degree) { return guard([&] { *degree = M->max_degree; }); }
 
-int gs_project_sparse_depth(gs_context* C, const double* points, int64_t n, int32_t stride, const gs_pose* pose,
-                            const gs_camera* cam, double* depth) {  // sequence.cpp:246-259
-    return guard([&] {
-        validate_camera(*cam);
-        if (n < 0 || stride < 3) fail(GS_EINVAL, "project_sparse_depth: bad point array");
-        C->use();
-        cudaStream_t st = C->stream;
-        const ViewParams v = make_view(*pose, *cam);
-        const size_t P = static_cast<size_t>(cam->width) * cam->height;
-        DevBuf &pts = C->sc(kScPoints), &out = C->sc(kScDepth);
-        pts.ensure(sizeof(double) * static_cast<size_t>(std::max<int64_t>(n, 1)) * stride);
-        out.ensure(sizeof(double) * P);
-        if (n > 0)
-            ck(cudaMemcpyAsync(pts.p, points, sizeof(double) * static_cast<size_t>(n) * stride, cudaMemcpyHostToDevice,
-                               st), "h2d points");
-        launch_sparse_depth(pts.as<double>(), stride, n, v, out.as<double>(), st);
-        C->launched(3);
-        ck(cudaMemcpyAsync(depth, out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st), "d2h depth");
-        ck(cudaStreamSynchronize(st), "sync");
-    });
-}
-
-int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // mapper.cpp:240-246
-    return guard([&] {
-        if (sh_interval <= 0) {
-            *degree = M->max_degree;
-            return;
-        }
-        const int target = static_cast<int>(std::min<int64_t>(3, M->global_step / sh_interval));
-        const int d = std::clamp(target, 0, 3);
-        if (d <= M->min_degree) {  // every Gaussian is already there (the common case): O(1)
-            *degree = target;
-            return;
-        }
-        bool change = false;
-        for (auto& x : M->deg_host)
-            if (x < d) {
-                x = static_cast<int8_t>(d);
-                change = true;
-            }
-        if (change && M->n > 0) {
-            M->ctx->use();
-            ck(cudaMemcpyAsync(M->degree, M->deg_host.data(), M->n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
-            ck(cudaStreamSynchronize(M->ctx->stream), "sync");
-        }
-        M->recompute_max_degree();
-        *degree = target;
-    });
-}
-
-// init_gaussians_from_points on device-resident points [n][6] (n > 0); appends to the map
-void init_points_device(gs_map* M, const double* dpts, int64_t n) {
-        gs_context* C = M->ctx;
-        cudaStream_t st = C->stream;
-        DevBuf &keys = C->sc(kScKeys), &keys2 = C->sc(kScKeys2), &idx = C->sc(kScIdx), &idx2 = C->sc(kScIdx2),
-               &bb = C->sc(kScBBox), &hk = C->sc(kScHashK), &hv = C->sc(kScHashV);
-        keys.ensure(sizeof(uint64_t) * n);
-        keys2.ensure(sizeof(uint64_t) * n);
-        idx.ensure(sizeof(int32_t) * n);
-        idx2.ensure(sizeof(int32_t) * n);
-        bb.ensure(sizeof(unsigned long long) * 8);
-        launch_knn_bbox(dpts, n, bb.as<unsigned long long>(), st);
-        unsigned long long enc[6];
-        ck(cudaMemcpyAsync(enc, bb.p, sizeof(enc), cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaStreamSynchronize(st), "sync");
-        double lo[3], hi[3];
-        auto dec = [](unsigned long long u) {
-            const unsigned long long b = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
-            double d;
-            std::memcpy(&d, &b, sizeof d);
-            return d;
-        };
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = dec(enc[a]);
-            hi[a] = dec(enc[3 + a]);
-        }
-        const double ext[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
-        const double vol = std::max(ext[0], 1e-9) * std::max(ext[1], 1e-9) * std::max(ext[2], 1e-9);
-        KnnGrid g{};
-        for (int a = 0; a < 3; ++a) g.lo[a] = lo[a];
-        g.cell = std::cbrt(vol / static_cast<double>(n)) * 1.5;
-        size_t tb = 0;
-        auto sort_keys = [&]() {
-            launch_knn_keys(dpts, n, g, keys.as<uint64_t>(), idx.as<int32_t>(), st);
-            tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(), idx.as<int32_t>(),
-                                            idx2.as<int32_t>(), static_cast<int>(n), 0, 64, st);
-            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, keys.as<uint64_t>(), keys2.as<uint64_t>(),
-                                               idx.as<int32_t>(), idx2.as<int32_t>(), static_cast<int>(n), 0, 64, st),
-               "knn sort");
-        };
-        // adapt the cell so occupied cells hold ~4 points (fixtures/synthetic.cpp init_from_points)
-        for (int it = 0; it < 2; ++it) {
-            sort_keys();
-            launch_knn_count_runs(keys2.as<uint64_t>(), n, bb.as<unsigned long long>() + 6, st);
-            unsigned long long runs = 1;
-            ck(cudaMemcpyAsync(&runs, bb.as<unsigned long long>() + 6, sizeof(runs), cudaMemcpyDeviceToHost, st), "d2h");
-            ck(cudaStreamSynchronize(st), "sync");
-            g.cell *= std::cbrt(4.0 / (static_cast<double>(n) / static_cast<double>(std::max(runs, 1ull))));
-        }
-        sort_keys();
-        g.max_ring = std::max({static_cast<int64_t>(ext[0] / g.cell) + 1, static_cast<int64_t>(ext[1] / g.cell) + 1,
-                               static_cast<int64_t>(ext[2] / g.cell) + 1});
-        uint32_t hsize = 1024;
-        while (hsize < 2 * static_cast<uint64_t>(n)) hsize <<= 1;
-        hk.ensure(sizeof(uint64_t) * hsize);
-        hv.ensure(sizeof(int2) * hsize);
-        launch_knn_table(keys2.as<uint64_t>(), n, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, st);
-        // new Gaussians at [first, first + n): fresh optimizer state, degree 0 (gaussian_map.cpp:33)
-        const int64_t first = M->n;
-        map_reserve(M, first + n);
-        ck(cudaMemset2DAsync(M->m + first, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
-        ck(cudaMemset2DAsync(M->v + first, sizeof(float) * M->cap, 0, sizeof(float) * n, kNumParams, st), "memset");
-        ck(cudaMemsetAsync(M->degree + first, 0, n, st), "memset");
-        const std::vector<int32_t> birth(n, static_cast<int32_t>(M->adam_count));
-        ck(cudaMemcpyAsync(M->birth + first, birth.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "h2d");
-        const int k = static_cast<int>(std::min<int64_t>(3, n - 1));
-        launch_knn_init(dpts, n, k, g, hk.as<uint64_t>(), hv.as<int2>(), hsize - 1, idx2.as<int32_t>(),
-                        M->params, M->cap, first, st);
-        C->launched(8);
-        ck(cudaStreamSynchronize(st), "sync");
-        M->deg_host.resize(first + n, 0);
-        M->n = first + n;
-        M->recompute_max_degree();
-        refresh_extent(M);
-}
-
-int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
-    return guard([&] {
-        *added = 0;
-        if (n <= 0) return;  // points.empty() -> 0
-        if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
-        M->ctx->use();
-        DevBuf& pts = M->ctx->sc(kScPoints);
-        pts.ensure(sizeof(double) * 6 * n);
-        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d points");
-        init_points_device(M, pts.as<double>(), n);
-        *added = n;
-    });
-}
-
-// filter_points_by_visibility on the device: render the map at the pose, flag, compact (stable);
-// returns the kept count, kept points in `out` (device, [kept][6])
-int64_t filter_points_device(gs_map* M, const double* dpts, int64_t n, const gs_pose& pose, const gs_camera& cam,
-                             double tau_alpha, DevBuf& out) {
-    if (tau_alpha < 0.0 || tau_alpha > 1.0)
-        fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
-    gs_context* C = M->ctx;
-    cudaStream_t st = C->stream;
-    gs_frame* F = scratch_frame(C);
-    render_impl(M, pose, cam, F, true, false);
-    DevBuf &keep = C->sc(kScKeep), &pos = C->sc(kScPos);
-    keep.ensure(sizeof(int32_t) * (n + 1));
-    pos.ensure(sizeof(int32_t) * (n + 1));
-    ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
-    launch_vis_filter(dpts, n, F->view, F->vis.as<float>(), tau_alpha, keep.as<int32_t>(), st);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st);
-    ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st), "scan");
-    int32_t kept = 0;
-    ck(cudaMemcpyAsync(&kept, pos.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
-    ck(cudaStreamSynchronize(st), "sync");
-    out.ensure(sizeof(double) * 6 * std::max<int64_t>(kept, 1));
-    launch_compact_points(dpts, n, keep.as<int32_t>(), pos.as<int32_t>(), out.as<double>(), st);
-    C->launched(3);
-    return kept;
-}
-
-// ------------------------------------------------------------------ checkpoint v1 (io/checkpoint.cpp)
-// Text header then one 476-byte record per Gaussian: the 59 parameters as fp64 in reference
-// order (position, rotation w x y z, log_scale, opacity_logit, sh[16][3]) and int32
-// active_degree. The device map holds fp32 parameters, so a save writes their exact fp64
-// widening and a load rounds to fp32 (a map saved here reloads bit-identically).
-int gs_save_checkpoint(gs_map* M, const char* path) {
-    return guard([&] {  // save_checkpoint, io/checkpoint.cpp:17-35
-        M->ctx->use();
-        std::ofstream out(path, std::ios::binary);
-        if (!out) fail(GS_ERUNTIME, std::string("save_checkpoint: cannot open ") + path);
-        const int64_t n = M->n;
-        int maxd = 0;
-        for (int64_t i = 0; i < n; ++i) maxd = std::max<int>(maxd, M->deg_host[i]);
-        out << "gsmap-checkpoint" << ' ' << 1 << '\n' << "count " << static_cast<size_t>(n) << '\n'
-            << "sh_degree " << maxd << '\n' << "end_header\n";
-        constexpr int64_t kChunk = 1 << 16;
-        constexpr size_t kRec = sizeof(double) * kNumParams + sizeof(int32_t);
-        std::vector<float> soa(static_cast<size_t>(kNumParams) * std::min(n, kChunk));
-        std::vector<char> rec(kRec * std::min(n, kChunk));
-        for (int64_t b = 0; b < n; b += kChunk) {
-            const int64_t m = std::min(kChunk, n - b);
-            ck(cudaMemcpy2DAsync(soa.data(), sizeof(float) * m, M->params + b, sizeof(float) * M->cap,
-                                 sizeof(float) * m, kNumParams, cudaMemcpyDeviceToHost, M->ctx->stream), "d2h params");
-            ck(cudaStreamSynchronize(M->ctx->stream), "sync");
-            for (int64_t i = 0; i < m; ++i) {
-                char* r = rec.data() + kRec * i;
-                for (int k = 0; k < kNumParams; ++k) {
-                    const double v = soa[static_cast<size_t>(k) * m + i];
-                    std::memcpy(r + sizeof(double) * k, &v, sizeof(double));
-                }
-                const int32_t deg = M->deg_host[b + i];
-                std::memcpy(r + sizeof(double) * kNumParams, &deg, sizeof(deg));
-            }
-            out.write(rec.data(), static_cast<std::streamsize>(kRec * m));
-        }
-        if (!out) fail(GS_ERUNTIME, std::string("save_checkpoint: write failed for ") + path);
-    });
-}
-
-int gs_load_checkpoint(gs_context* C, const char* path, gs_map** out) {
-    return guard([&] {  // load_checkpoint, io/checkpoint.cpp:37-71
-        *out = nullptr;
-        std::ifstream in(path, std::ios::binary);
-        if (!in) fail(GS_ERUNTIME, std::string("load_checkpoint: cannot open ") + path);
-        std::string line, magic;
-        std::getline(in, line);
-        std::istringstream head(line);
-        int version = 0;
-        head >> magic >> version;
-        if (magic != "gsmap-checkpoint") fail(GS_ERUNTIME, std::string("load_checkpoint: not a checkpoint file: ") + path);
-        if (version != 1) fail(GS_ERUNTIME, std::string("load_checkpoint: unsupported version in ") + path);
-        size_t count = 0;
-        while (std::getline(in, line) && line != "end_header") {
-            std::istringstream is(line);
-            std::string key;
-            is >> key;
-            if (key == "count") is >> count;
-        }
-        std::vector<gs_gaussian> gs(count);
-        for (gs_gaussian& g : gs) {
-            in.read(reinterpret_cast<char*>(g.p), sizeof(g.p));
-            int32_t deg = 0;
-            in.read(reinterpret_cast<char*>(&deg), sizeof(deg));
-            g.active_degree = deg;
-            g.pad = 0;
-        }
-        if (!in) fail(GS_ERUNTIME, std::string("load_checkpoint: truncated file ") + path);
-        gs_map* M = nullptr;
-        int st = gs_map_create(C, &M);
-        if (st != GS_OK) fail(st, g_err);
-        st = gs_map_append(M, gs.data(), static_cast<int64_t>(gs.size()));
-        if (st != GS_OK) {
-            const std::string msg = g_err;
-            gs_map_destroy(M);
-            fail(st, msg);
-        }
-        *out = M;
-    });
-}
-
-// Optimizer state beside a v1 checkpoint ("add Adam state for true resume"; the
-// reference's format has none, load_checkpoint starts Adam afresh): text header, then per
-// Gaussian m[59], v[59] (fp64 widening of the device's fp32 moments) and the int64 Adam step.
-int gs_save_training_state(gs_map* M, const char* path) {
-    return guard([&] {
-        M->ctx->use();
-        const int64_t n = M->n;
-        std::vector<double> m(static_cast<size_t>(kNumParams) * n), v(m.size());
-        std::vector<int64_t> step(n);
-        if (n > 0) {
-            const int st = gs_map_get_adam(M, m.data(), v.data(), step.data(), n);
-            if (st != GS_OK) fail(st, g_err);
-        }
-        std::ofstream out(path, std::ios::binary);
-        if (!out) fail(GS_ERUNTIME, std::string("save_training_state: cannot open ") + path);
-        // scene_extent too: the reference refreshes it only on append (gaussian_map.cpp:87-99), so a
-        // reloaded map would otherwise rescale the position learning rate by its trained extent
-        out << "gsmap-adam-state 1\ncount " << n << "\nglobal_step " << M->global_step << "\nscene_extent "
-            << std::setprecision(17) << M->scene_extent << "\nend_header\n";
-        for (int64_t i = 0; i < n; ++i) {
-            out.write(reinterpret_cast<const char*>(&m[kNumParams * i]), sizeof(double) * kNumParams);
-            out.write(reinterpret_cast<const char*>(&v[kNumParams * i]), sizeof(double) * kNumParams);
-            out.write(reinterpret_cast<const char*>(&step[i]), sizeof(int64_t));
-        }
-        if (!out) fail(GS_ERUNTIME, std::string("save_training_state: write failed for ") + path);
-    });
-}
-
-int gs_load_training_state(gs_map* M, const char* path) {
-    return guard([&] {
-        M->ctx->use();
-        std::ifstream in(path, std::ios::binary);
-        if (!in) fail(GS_ERUNTIME, std::string("load_training_state: cannot open ") + path);
-        std::string line, magic;
-        std::getline(in, line);
-        std::istringstream head(line);
-        int version = 0;
-        head >> magic >> version;
-        if (magic != "gsmap-adam-state" || version != 1)
-            fail(GS_ERUNTIME, std::string("load_training_state: not an optimizer state file: ") + path);
-        int64_t count = -1, gstep = 0;
-        double extent = M->scene_extent;
-        while (std::getline(in, line) && line != "end_header") {
-            std::istringstream is(line);
-            std::string key;
-            is >> key;
-            if (key == "count") is >> count;
-            if (key == "global_step") is >> gstep;
-            if (key == "scene_extent") is >> extent;
-        }
-        if (count != M->n) fail(GS_EINVAL, "load_training_state: Gaussian count does not match the map");
-        std::vector<double> m(static_cast<size_t>(kNumParams) * count), v(m.size());
-        std::vector<int64_t> step(count);
-        for (int64_t i = 0; i < count; ++i) {
-            in.read(reinterpret_cast<char*>(&m[kNumParams * i]), sizeof(double) * kNumParams);
-            in.read(reinterpret_cast<char*>(&v[kNumParams * i]), sizeof(double) * kNumParams);
-            in.read(reinterpret_cast<char*>(&step[i]), sizeof(int64_t));
-        }
-        if (!in) fail(GS_ERUNTIME, std::string("load_training_state: truncated file ") + path);
-        if (count > 0) {
-            const int st = gs_map_set_adam(M, m.data(), v.data(), step.data(), count);
-            if (st != GS_OK) fail(st, g_err);
-        }
-        M->global_step = gstep;
-        M->scene_extent = extent;
-    });
-}
-
-int gs_integrate_keyframe(gs_map* M, const gs_pose* pose, const gs_camera* cam, const double* color,
-                          const double* points6, int64_t n, double tau_alpha, int32_t initial_iters, int32_t levels,
-                          gs_keyframe** out_kf, int64_t* added) {
-    return guard([&] {  // pipeline.cpp:148-155 (+ the keyframe's sparse depth, pipeline.cpp:108)
-        validate_camera(*cam);
-        gs_context* C = M->ctx;
-        C->use();
-        *out_kf = nullptr;
-        *added = 0;
-        if (tau_alpha < 0.0 || tau_alpha > 1.0)
-            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
-        if (n < 0 || n > 0x7fffffff) fail(GS_EINVAL, "integrate_keyframe: bad point count");
-        if (!color) fail(GS_EINVAL, "integrate_keyframe: missing colour image");
-        cudaStream_t st = C->stream;
-        const int h = cam->height, w = cam->width;
-        const size_t P = static_cast<size_t>(h) * w;
-        // the cloud crosses once: filter -> init, and the sparse depth, read the same device copy
-        DevBuf &pts = C->sc(kScPoints), &kept = C->sc(kScKept), &dd = C->sc(kScDepth), &cs = C->sc(kScColor);
-        std::optional<Scope> sc_up(std::in_place, C, "kf_upload_sparse_depth");
-        pts.ensure(sizeof(double) * 6 * std::max<int64_t>(n, 1));
-        if (n > 0)
-            ck(cudaMemcpyAsync(pts.p, points6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, st), "h2d points");
-        // sparse depth first: project_sparse_depth reads the frame's full cloud (sequence.cpp:246-259)
-        dd.ensure(sizeof(double) * P + sizeof(float) * P);
-        launch_sparse_depth(pts.as<double>(), 6, n, make_view(*pose, *cam), dd.as<double>(), st);
-        float* depth_f = reinterpret_cast<float*>(dd.as<double>() + P);
-        launch_from_hwc_double(dd.as<double>(), h, w, 1, depth_f, st);
-        cs.ensure(sizeof(double) * 3 * P + sizeof(float) * 3 * P);
-        ck(cudaMemcpyAsync(cs.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d colour");
-        float* color_f = reinterpret_cast<float*>(cs.as<double>() + 3 * P);
-        launch_from_hwc_double(cs.as<double>(), h, w, 3, color_f, st);
-        C->launched(5);
-        sc_up.reset();
-        auto* K = new gs_keyframe();
-        K->ctx = C;
-        K->pose = *pose;
-        K->initial_iters = initial_iters;
-        try {
-            {
-                Scope sc(C, "kf_pyramid");
-                keyframe_build(K, color_f, depth_f, h, w, levels, true);
-            }
-            if (n > 0) {
-                int64_t k = 0;
-                {
-                    Scope sc(C, "kf_filter_points");
-                    k = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, kept);
-                }
-                if (k > 0) {
-                    Scope sc(C, "kf_init_gaussians");
-                    init_points_device(M, kept.as<double>(), k);
-                }
-                *added = k;
-            }
-        } catch (...) {
-            delete K;
-            throw;
-        }
-        *out_kf = K;
-    });
-}
-
 // diagnostics: K8b thread order (0 rank, 1 map, 2 visible list; -1 = automatic)
 // diagnostics: speculative next-step renders enqueued / used so far on this context
 int gs_debug_speculation(gs_context* C, int64_t* out2) {
@@ -1566,141 +805,6 @@ int gs_debug_speculation(gs_context* C, int64_t* out2) {
 
 int gs_debug_set_k8_order(int order) {
     return guard([&] { set_k8_order(order); });
-}
-
-int gs_evaluate_view(gs_map* M, const gs_pose* pose, const gs_camera* cam, const double* gt_color,
-                     const double* gt_depth, gs_eval_metrics* out) {
-    return guard([&] {  // evaluate_sequence (pipeline.cpp:41-64), one frame
-        gs_context* C = M->ctx;
-        C->use();
-        validate_camera(*cam);
-        if (!gt_color) fail(GS_EINVAL, "evaluate_view: missing ground-truth colour");
-        if (cam->width < 11 || cam->height < 11) fail(GS_EINVAL, "ssim: image smaller than the 11x11 window");
-        gs_frame* F = scratch_frame(C);
-        render_checked(M, *pose, *cam, F);
-        cudaStream_t st = C->stream;
-        const int h = cam->height, w = cam->width;
-        const size_t P = static_cast<size_t>(h) * w;
-        F->eval_quant.ensure(sizeof(float) * 3 * P);
-        F->eval_gt.ensure(sizeof(float) * 4 * P);
-        F->eval_stage.ensure(sizeof(double) * 4 * P);
-        F->wbuf.ensure(sizeof(float) * 9 * static_cast<size_t>(h - 10) * (w - 10));
-        double* stage = F->eval_stage.as<double>();
-        float* gt = F->eval_gt.as<float>();
-        ck(cudaMemcpyAsync(stage, gt_color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d gt colour");
-        launch_from_hwc_double(stage, h, w, 3, gt, st);
-        if (gt_depth) {
-            ck(cudaMemcpyAsync(stage + 3 * P, gt_depth, sizeof(double) * P, cudaMemcpyHostToDevice, st), "h2d gt depth");
-            launch_from_hwc_double(stage + 3 * P, h, w, 1, gt + 3 * P, st);
-        }
-        ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset");
-        launch_eval(F->color.as<float>(), F->depth.as<float>(), gt, gt_depth ? gt + 3 * P : nullptr, h, w,
-                    F->eval_quant.as<float>(), F->wbuf.as<float>(), F->loss.as<LossScalars>(), st);
-        C->launched(gt_depth ? 4 : 3);
-        LossScalars r;
-        ck(cudaMemcpyAsync(&r, F->loss.p, sizeof(r), cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaStreamSynchronize(st), "sync");
-        F->has_cotangent = false;
-        const double mse = r.sq_sum / (3.0 * static_cast<double>(P));
-        out->psnr = mse == 0.0 ? 100.0 : 10.0 * std::log10(1.0 / mse);  // metrics.cpp:165-175
-        out->ssim = r.ssim_sum / (3.0 * static_cast<double>(h - 10) * (w - 10));
-        out->depth_rmse = r.n_valid ? std::sqrt(r.depth_abs_sum / static_cast<double>(r.n_valid))
-                                    : std::numeric_limits<double>::quiet_NaN();
-    });
-}
-
-int gs_filter_points_by_visibility(gs_map* M, const double* pts6, int64_t n, const gs_pose* pose,
-                                   const gs_camera* cam, double tau_alpha, double* kept6, int64_t* n_kept) {
-    return guard([&] {  // keyframe.cpp:49-74
-        validate_camera(*cam);
-        M->ctx->use();
-        *n_kept = 0;
-        if (tau_alpha < 0.0 || tau_alpha > 1.0)
-            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
-        if (n <= 0) return;
-        DevBuf &pts = M->ctx->sc(kScPoints), &out = M->ctx->sc(kScKept);
-        pts.ensure(sizeof(double) * 6 * n);
-        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
-        const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
-        if (kept > 0)
-            ck(cudaMemcpyAsync(kept6, out.p, sizeof(double) * 6 * kept, cudaMemcpyDeviceToHost, M->ctx->stream), "d2h");
-        ck(cudaStreamSynchronize(M->ctx->stream), "sync");
-        *n_kept = kept;
-    });
-}
-
-int gs_map_integrate_points(gs_map* M, const double* pts6, int64_t n, const gs_pose* pose, const gs_camera* cam,
-                            double tau_alpha, int64_t* added) {
-    return guard([&] {  // pipeline.cpp:151-155: filter_points_by_visibility -> init_gaussians_from_points
-        validate_camera(*cam);
-        M->ctx->use();
-        *added = 0;
-        if (tau_alpha < 0.0 || tau_alpha > 1.0)
-            fail(GS_EINVAL, "filter_points_by_visibility: tau_alpha must be in [0,1]");
-        if (n <= 0) return;
-        if (n > 0x7fffffff) fail(GS_EINVAL, "integrate_points: too many points");
-        DevBuf &pts = M->ctx->sc(kScPoints), &out = M->ctx->sc(kScKept);
-        pts.ensure(sizeof(double) * 6 * n);
-        ck(cudaMemcpyAsync(pts.p, pts6, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, M->ctx->stream), "h2d");
-        const int64_t kept = filter_points_device(M, pts.as<double>(), n, *pose, *cam, tau_alpha, out);
-        if (kept > 0) init_points_device(M, out.as<double>(), kept);
-        *added = kept;
-    });
-}
-
-int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // gaussian_map.cpp:56-73
-    return guard([&] {
-        if (opacity_threshold <= 0.0 || opacity_threshold >= 1.0)
-            fail(GS_EINVAL, "prune: threshold must be in (0, 1)");
-        M->ctx->use();
-        *removed = 0;
-        const int n = static_cast<int>(M->n);
-        if (n == 0) return;
-        gs_context* C = M->ctx;
-        cudaStream_t st = C->stream;
-        DevBuf &keep = C->sc(kScPruneKeep), &pos = C->sc(kScPrunePos);
-        keep.ensure(sizeof(int32_t) * (n + 1));
-        pos.ensure(sizeof(int32_t) * (n + 1));
-        ck(cudaMemsetAsync(keep.as<int32_t>() + n, 0, sizeof(int32_t), st), "memset");
-        launch_prune_flags(M->params, M->cap, n, opacity_threshold, keep.as<int32_t>(), st);
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st);
-        ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, keep.as<int32_t>(), pos.as<int32_t>(), n + 1, st), "scan");
-        int32_t kept = 0;
-        ck(cudaMemcpyAsync(&kept, pos.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
-        ck(cudaStreamSynchronize(st), "sync");
-        C->launched(2);
-        if (kept == n) return;
-        // stable compaction through a staging block of kChunk planes (context scratch, reused):
-        // compact a block of planes into it, copy the kept prefix back; no map-sized allocation.
-        // Entries past `kept` are don't-care (append / init reset every range they fill).
-        constexpr int kChunk = 16;
-        const int64_t cap = M->cap;
-        DevBuf& tmp = C->sc(kScPruneTmp);
-        tmp.ensure(sizeof(float) * kChunk * cap);
-        const int32_t* kp = keep.as<int32_t>();
-        const int32_t* ps = pos.as<int32_t>();
-        for (float* arr : {M->params, M->m, M->v}) {
-            for (int c0 = 0; c0 < kNumParams; c0 += kChunk) {
-                const int np = std::min(kChunk, kNumParams - c0);
-                launch_compact(arr + c0 * cap, tmp.as<float>(), cap, cap, np, n, kp, ps, st);
-                ck(cudaMemcpy2DAsync(arr + c0 * cap, sizeof(float) * cap, tmp.p, sizeof(float) * cap,
-                                     sizeof(float) * kept, np, cudaMemcpyDeviceToDevice, st), "copy back");
-                C->launched();
-            }
-        }
-        launch_compact(M->birth, tmp.as<int32_t>(), n, kp, ps, st);
-        ck(cudaMemcpyAsync(M->birth, tmp.p, sizeof(int32_t) * kept, cudaMemcpyDeviceToDevice, st), "copy back");
-        launch_compact(M->degree, reinterpret_cast<int8_t*>(tmp.p), n, kp, ps, st);
-        ck(cudaMemcpyAsync(M->degree, tmp.p, kept, cudaMemcpyDeviceToDevice, st), "copy back");
-        C->launched(2);
-        M->deg_host.resize(kept);
-        ck(cudaMemcpyAsync(M->deg_host.data(), M->degree, kept, cudaMemcpyDeviceToHost, st), "d2h degree");
-        ck(cudaStreamSynchronize(st), "sync");
-        M->recompute_max_degree();
-        M->n = kept;
-        *removed = n - kept;
-    });
 }
 
 int gs_map_device_planes(gs_map* M, float** params, float** m, float** v, int64_t* cap) {
