@@ -477,6 +477,129 @@ void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_
     *level_out = level;
 }
 
+// host upload of one pyramid level on the copy stream (gs_keyframe_upload_level, and the
+// prefetch of gs_train_step_prefetch)
+void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
+    {
+        if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
+        const int h = K->hs[level], w = K->ws[level];
+        const size_t P = static_cast<size_t>(h) * w;
+        // asynchronous on the copy stream (host buffers must stay valid until the next
+        // synchronising call on this keyframe's context): overlaps the compute stream's work
+        cudaStream_t st = K->ctx->copies();
+        if (K->used_valid) ck(cudaStreamWaitEvent(st, K->used, 0), "wait last use");
+        K->stage.ensure(sizeof(double) * 4 * P);
+        ck(cudaMemcpyAsync(K->stage.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d color");
+        ck(cudaMemcpyAsync(K->stage.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st),
+           "h2d depth");
+        launch_from_hwc_double(K->stage.as<double>(), h, w, 3, K->color[level].as<float>(), st);
+        launch_from_hwc_double(K->stage.as<double>() + 3 * P, h, w, 1, K->depth[level].as<float>(), st);
+        K->ctx->launched(2);
+        if (K->ready.size() < K->hs.size()) {
+            K->ready.resize(K->hs.size(), nullptr);
+            K->pending.resize(K->hs.size(), 0);
+        }
+        if (!K->ready[level]) ck(cudaEventCreateWithFlags(&K->ready[level], cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(K->ready[level], st), "record upload");
+        K->pending[level] = 1;
+    }
+}
+
+// the step after this one, named by gs_train_step_prefetch
+struct Prefetch {
+    gs_keyframe* K = nullptr;
+    int32_t level = 0;
+    const double *color = nullptr, *depth = nullptr;
+};
+
+bool same_camera(const gs_camera& a, const gs_camera& b) {
+    return a.fx == b.fx && a.fy == b.fy && a.cx == b.cx && a.cy == b.cy && a.width == b.width && a.height == b.height;
+}
+
+void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
+                     gs_step_report* report, const Prefetch* pf) {
+    {
+        gs_context* C = M->ctx;
+        C->use();
+        *report = gs_step_report{};
+        if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
+        auto upload = [&] {
+            if (pf && pf->color) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
+        };
+        if (K->consumed >= K->initial_iters) {  // std::nullopt (mapper.cpp:219)
+            upload();
+            return;
+        }
+        gs_grads* G = scratch_grads(C);
+        const int level = schedule_level(K, *cfg);
+        const gs_camera lc = scaled(*cam, level);
+        // this step's render was enqueued speculatively by the previous call when it predicted
+        // this (keyframe, level, camera) and the map has not changed since
+        auto& sp = C->spec;
+        const bool have = sp.valid && sp.map == M && sp.kf == K && sp.level == level && sp.version == M->version &&
+                          same_camera(sp.cam, *cam) && std::memcmp(&sp.pose, &K->pose, sizeof(gs_pose)) == 0;
+        const int fi = have ? sp.frame : C->train_parity;
+        sp.valid = false;
+        C->spec_used += have;
+        gs_frame* F = train_frame(C, fi);
+        // with a named next step, its render goes to the other frame; without one, steps stay on
+        // one frame (its remembered capacities then track a growing map step by step)
+        C->train_parity = pf ? fi ^ 1 : fi;
+        gs_loss_result lr{};
+        bool prefetched = false;
+        // a level this very step reads is uploaded only after the step is final (an overflow
+        // re-run must not see the next input)
+        const bool late_upload = pf && pf->K == K && pf->level == level;
+        // the next step's render, enqueued while this step's read-back is in flight: the host's
+        // return, report and next call then overlap device work instead of idling it
+        auto speculate = [&] {
+            if (!pf || !pf->K || pf->K->hs.empty() || pf->level < 0 ||
+                pf->level >= static_cast<int>(pf->K->hs.size()) || M->n == 0)
+                return;
+            const gs_camera nc = scaled(*cam, pf->level);
+            gs_frame* B = train_frame(C, fi ^ 1);
+            const gs_frame::Caps& cs = B->cap_slot(nc.width, nc.height);
+            if (cs.pairs == 0) return;  // first render at this size needs exact counts (a sync)
+            render_impl(M, pf->K->pose, nc, B, false, false);
+            sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, pf->K->pose, fi ^ 1};
+            ++C->spec_enqueued;
+        };
+        // one host round trip per step (the loss read); a step whose render overflowed the
+        // remembered pair capacity changed nothing on the device and is re-run at exact size
+        for (int attempt = 0;; ++attempt) {
+            grads_zero(G, M);
+            if (!(have && attempt == 0)) render_impl(M, K->pose, lc, F, attempt > 0, false);
+            loss_impl(F, K, level, *cfg);
+            backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
+                          &F->loss.as<LossScalars>()->depth_scale, G);
+            adam_impl(M, G, cfg->lr, dev_counters(F));
+            // the next step's input upload is issued behind this step's enqueued work, on the
+            // copy stream (it waits for this step's last read of that level buffer)
+            if (!prefetched && !late_upload) {
+                upload();
+                prefetched = true;
+            }
+            if (C->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
+                lr.total = lr.psnr = std::nan("");
+                break;
+            }
+            if (attempt == 0 && pf) lr = read_loss(F, speculate);
+            else lr = read_loss(F);
+            if (!F->overflow) break;
+            sp.valid = false;  // rendered from the map before this step's (re-run) update
+            --M->adam_count;
+            --M->global_step;
+            if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
+        }
+        if (!prefetched) upload();
+        ++K->consumed;
+        report->ran = 1;
+        report->level = level;
+        report->loss = lr.total;
+        report->psnr = lr.psnr;
+    }
+}
+
 }  // namespace gsb_host
 
 // ============================================================================ C-ABI
@@ -1146,36 +1269,8 @@ int gs_keyframe_consumed(gs_keyframe* K, int32_t* c) { return guard([&] { *c = K
 int gs_keyframe_set_consumed(gs_keyframe* K, int32_t c) { return guard([&] { K->consumed = c; }); }
 int gs_keyframe_levels(gs_keyframe* K, int32_t* n) { return guard([&] { *n = static_cast<int32_t>(K->hs.size()); }); }
 
-void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const double* depth);
-
 int gs_keyframe_upload_level(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
     return guard([&] { upload_level_impl(K, level, color, depth); });
-}
-
-void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const double* depth) {
-    {
-        if (level < 0 || level >= static_cast<int>(K->hs.size())) fail(GS_EINVAL, "level out of range");
-        const int h = K->hs[level], w = K->ws[level];
-        const size_t P = static_cast<size_t>(h) * w;
-        // asynchronous on the copy stream (host buffers must stay valid until the next
-        // synchronising call on this keyframe's context): overlaps the compute stream's work
-        cudaStream_t st = K->ctx->copies();
-        if (K->used_valid) ck(cudaStreamWaitEvent(st, K->used, 0), "wait last use");
-        K->stage.ensure(sizeof(double) * 4 * P);
-        ck(cudaMemcpyAsync(K->stage.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d color");
-        ck(cudaMemcpyAsync(K->stage.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st),
-           "h2d depth");
-        launch_from_hwc_double(K->stage.as<double>(), h, w, 3, K->color[level].as<float>(), st);
-        launch_from_hwc_double(K->stage.as<double>() + 3 * P, h, w, 1, K->depth[level].as<float>(), st);
-        K->ctx->launched(2);
-        if (K->ready.size() < K->hs.size()) {
-            K->ready.resize(K->hs.size(), nullptr);
-            K->pending.resize(K->hs.size(), 0);
-        }
-        if (!K->ready[level]) ck(cudaEventCreateWithFlags(&K->ready[level], cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaEventRecord(K->ready[level], st), "record upload");
-        K->pending[level] = 1;
-    }
 }
 
 int gs_keyframe_read_level(gs_keyframe* K, int32_t level, double* color, double* depth) {
@@ -1235,14 +1330,6 @@ int gs_render_backward_frame(gs_map* M, const gs_pose* pose, const gs_camera* ca
     });
 }
 
-struct Prefetch {
-    gs_keyframe* K = nullptr;
-    int32_t level = 0;
-    const double *color = nullptr, *depth = nullptr;
-};
-void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
-                     gs_step_report* report, const Prefetch* pf);
-
 int gs_train_step(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_step_report* report) {
     return guard([&] { train_step_impl(M, K, cfg, cam, report, nullptr); });
 }
@@ -1256,94 +1343,6 @@ int gs_train_step_prefetch(gs_map* M, gs_keyframe* K, const gs_train_config* cfg
         Prefetch pf{next_kf, next_level, next_color, next_depth};
         train_step_impl(M, K, cfg, cam, report, next_kf ? &pf : nullptr);
     });
-}
-
-bool same_camera(const gs_camera& a, const gs_camera& b) {
-    return a.fx == b.fx && a.fy == b.fy && a.cx == b.cx && a.cy == b.cy && a.width == b.width && a.height == b.height;
-}
-
-void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam,
-                     gs_step_report* report, const Prefetch* pf) {
-    {
-        gs_context* C = M->ctx;
-        C->use();
-        *report = gs_step_report{};
-        if (K->hs.empty()) fail(GS_EINVAL, "train_keyframe_step: keyframe pyramid not built");
-        auto upload = [&] {
-            if (pf && pf->color) upload_level_impl(pf->K, pf->level, pf->color, pf->depth);
-        };
-        if (K->consumed >= K->initial_iters) {  // std::nullopt (mapper.cpp:219)
-            upload();
-            return;
-        }
-        gs_grads* G = scratch_grads(C);
-        const int level = schedule_level(K, *cfg);
-        const gs_camera lc = scaled(*cam, level);
-        // this step's render was enqueued speculatively by the previous call when it predicted
-        // this (keyframe, level, camera) and the map has not changed since
-        auto& sp = C->spec;
-        const bool have = sp.valid && sp.map == M && sp.kf == K && sp.level == level && sp.version == M->version &&
-                          same_camera(sp.cam, *cam) && std::memcmp(&sp.pose, &K->pose, sizeof(gs_pose)) == 0;
-        const int fi = have ? sp.frame : C->train_parity;
-        sp.valid = false;
-        C->spec_used += have;
-        gs_frame* F = train_frame(C, fi);
-        // with a named next step, its render goes to the other frame; without one, steps stay on
-        // one frame (its remembered capacities then track a growing map step by step)
-        C->train_parity = pf ? fi ^ 1 : fi;
-        gs_loss_result lr{};
-        bool prefetched = false;
-        // a level this very step reads is uploaded only after the step is final (an overflow
-        // re-run must not see the next input)
-        const bool late_upload = pf && pf->K == K && pf->level == level;
-        // the next step's render, enqueued while this step's read-back is in flight: the host's
-        // return, report and next call then overlap device work instead of idling it
-        auto speculate = [&] {
-            if (!pf || !pf->K || pf->K->hs.empty() || pf->level < 0 ||
-                pf->level >= static_cast<int>(pf->K->hs.size()) || M->n == 0)
-                return;
-            const gs_camera nc = scaled(*cam, pf->level);
-            gs_frame* B = train_frame(C, fi ^ 1);
-            const gs_frame::Caps& cs = B->cap_slot(nc.width, nc.height);
-            if (cs.pairs == 0) return;  // first render at this size needs exact counts (a sync)
-            render_impl(M, pf->K->pose, nc, B, false, false);
-            sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, pf->K->pose, fi ^ 1};
-            ++C->spec_enqueued;
-        };
-        // one host round trip per step (the loss read); a step whose render overflowed the
-        // remembered pair capacity changed nothing on the device and is re-run at exact size
-        for (int attempt = 0;; ++attempt) {
-            grads_zero(G, M);
-            if (!(have && attempt == 0)) render_impl(M, K->pose, lc, F, attempt > 0, false);
-            loss_impl(F, K, level, *cfg);
-            backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
-                          &F->loss.as<LossScalars>()->depth_scale, G);
-            adam_impl(M, G, cfg->lr, dev_counters(F));
-            // the next step's input upload is issued behind this step's enqueued work, on the
-            // copy stream (it waits for this step's last read of that level buffer)
-            if (!prefetched && !late_upload) {
-                upload();
-                prefetched = true;
-            }
-            if (C->defer_sync) {  // no read-back: no loss, no overflow re-run (diagnostics)
-                lr.total = lr.psnr = std::nan("");
-                break;
-            }
-            if (attempt == 0 && pf) lr = read_loss(F, speculate);
-            else lr = read_loss(F);
-            if (!F->overflow) break;
-            sp.valid = false;  // rendered from the map before this step's (re-run) update
-            --M->adam_count;
-            --M->global_step;
-            if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
-        }
-        if (!prefetched) upload();
-        ++K->consumed;
-        report->ran = 1;
-        report->level = level;
-        report->loss = lr.total;
-        report->psnr = lr.psnr;
-    }
 }
 
 int gs_train_accumulate(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, const gs_camera* cam, gs_frame* F,
