@@ -634,3 +634,42 @@ def test_speculative_next_render_changes_nothing():  # gs_train_step_prefetch wi
             m2.gaussians = gg
     np.testing.assert_allclose(l_e, ref, rtol=1e-12)
     np.testing.assert_array_equal(p_e, m2.gaussians["p"])
+
+
+def test_speculation_survives_capacity_overflow():
+    """A speculative next-step render that outgrows its frame's remembered pair capacity is
+    caught by the step that uses it (overflow flag) and re-run at exact size: training with
+    hints across a capacity jump equals plain training."""
+    import ctypes
+    cam = O.camera(400, 400, 319.5, 239.5, 640, 480)
+    g = random_scene(31, 6000, cam, O.pose(), 0.0, 2.0)
+    small, big = g.copy(), g.copy()
+    small["p"][:, 7:10] = np.log(0.002)
+    big["p"][:, 7:10] = np.log(0.2)
+    gen = np.random.default_rng(2)
+    color = f32(gen.uniform(0, 1, (480, 640, 3)))
+    sparse = f32(np.where(gen.uniform(size=(480, 640)) < 0.1, gen.uniform(1, 8, (480, 640)), 0.0))
+    cfg = G().TrainConfig.make(0.2, 0.5, 0)
+    pose = G().Pose(1, 0, 0, 0, 0, 0, 0)
+
+    ctx1 = G().Context(0)
+    ms = G().GaussianMap(ctx1, round32(small))
+    ks = G().Keyframe(pose, color, sparse, 10, 0, ctx=ctx1)
+    for _ in range(4):  # both train frames learn the small capacity
+        G().train_keyframe_step(ms, ks, cfg, gpu_cam(cam), prefetch=(ks, 0))
+    mb1 = G().GaussianMap(ctx1, round32(big))
+    kb1 = G().Keyframe(pose, color, sparse, 10, 0, ctx=ctx1)
+    r1 = [G().train_keyframe_step(mb1, kb1, cfg, gpu_cam(cam), prefetch=(kb1, 0) if i < 3 else None)["loss"]
+          for i in range(4)]
+    cnt = np.zeros(2, np.int64)
+    G().lib().gs_debug_speculation(ctypes.c_void_p(ctx1.h), cnt.ctypes.data_as(ctypes.c_void_p))
+    assert cnt[1] >= 2  # speculative renders were used, overflowing ones included
+
+    ctx2 = G().Context(0)
+    mb2 = G().GaussianMap(ctx2, round32(big))
+    kb2 = G().Keyframe(pose, color, sparse, 10, 0, ctx=ctx2)
+    r2 = [G().train_keyframe_step(mb2, kb2, cfg, gpu_cam(cam))["loss"] for _ in range(4)]
+    np.testing.assert_allclose(r1, r2, rtol=1e-9)
+    assert mb1.global_step == mb2.global_step == 4
+    d = np.abs(mb1.gaussians["p"] - mb2.gaussians["p"])
+    assert np.mean(d <= 1e-6) > 0.999 and d.max() < 0.2
