@@ -213,26 +213,31 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
         }
         {
             Scope sc_keys(C, "tile_keys_sort_ranges");
-            F->pair_keys.ensure(sizeof(uint32_t) * cap);
-            F->pair_keys2.ensure(sizeof(uint32_t) * cap);
             F->pair_vals.ensure(sizeof(uint32_t) * cap);
             F->pair_vals2.ensure(sizeof(uint32_t) * cap);
-            ck(cudaMemsetAsync(F->pair_keys.p, 0xff, sizeof(uint32_t) * cap, st), "memset pair keys");
-            launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, nv, cap, v.tiles_x,
-                              F->pair_keys.as<uint32_t>(), F->pair_vals.as<uint32_t>(), st);
-            C->launched();
             int bits = 1;  // the sentinel's low bits (2^bits - 1) must sort after every tile id
             while ((1u << bits) <= static_cast<uint32_t>(T)) ++bits;
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, F->pair_keys.as<uint32_t>(), F->pair_keys2.as<uint32_t>(),
-                                            F->pair_vals.as<uint32_t>(), F->pair_vals2.as<uint32_t>(),
-                                            static_cast<int>(cap), 0, bits, st);
-            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->pair_keys.as<uint32_t>(),
-                                               F->pair_keys2.as<uint32_t>(), F->pair_vals.as<uint32_t>(),
-                                               F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st),
-               "tile sort");
-            launch_tile_ranges(F->pair_keys2.as<uint32_t>(), cnt, cap, T, F->ranges.as<uint2>(), st);
-            C->launched();
+            // 16-bit tile keys while the tile count fits below the 0xffff sentinel
+            auto bin = [&](auto key_tag) {
+                using KeyT = decltype(key_tag);
+                F->pair_keys.ensure(sizeof(KeyT) * cap);
+                F->pair_keys2.ensure(sizeof(KeyT) * cap);
+                KeyT* k1 = F->pair_keys.as<KeyT>();
+                KeyT* k2 = F->pair_keys2.as<KeyT>();
+                ck(cudaMemsetAsync(k1, 0xff, sizeof(KeyT) * cap, st), "memset pair keys");
+                launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, nv, cap, v.tiles_x, k1,
+                                  F->pair_vals.as<uint32_t>(), st);
+                size_t tb = 0;
+                cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, F->pair_vals.as<uint32_t>(),
+                                                F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st);
+                ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, k1, k2, F->pair_vals.as<uint32_t>(),
+                                                   F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st),
+                   "tile sort");
+                launch_tile_ranges(k2, cnt, cap, T, F->ranges.as<uint2>(), st);
+            };
+            if (T < 0xffff) bin(uint16_t{});
+            else bin(uint32_t{});
+            C->launched(2);
         }
     }
     {

@@ -81,10 +81,13 @@ void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsig
 // tile ids; values are depth ranks, so a stable sort by tile yields each tile's list in
 // (depth, index) order, exactly the reference's push_back order (ty outer, tx inner).
 // Pairs beyond the capacity raise the overflow flag instead (nothing is written).
+// KeyT: uint16_t while the tile count fits (every (tile, rank) pair then moves 6 bytes per sort
+// pass instead of 8), uint32_t otherwise.
+template <typename KeyT>
 __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restrict__ emit_off,
                                                          const Splat* __restrict__ rec,
                                                          unsigned long long* __restrict__ cnt, uint32_t cap,
-                                                         int tiles_x, uint32_t* __restrict__ keys,
+                                                         int tiles_x, KeyT* __restrict__ keys,
                                                          uint32_t* __restrict__ vals) {
     const int n_vis = static_cast<int>(cnt[kCntVisible]);
     if (cnt[kCntPairs] > cap) {
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
         const uint32_t mg = __shfl_sync(0xffffffffu, magic, i);
         for (int l = lane; l < c; l += 32) {
             const int row = nx == 1 ? l : static_cast<int>(__umulhi(static_cast<uint32_t>(l), mg));
-            keys[o + l] = static_cast<uint32_t>(base_key + row * tiles_x + (l - row * nx));
+            keys[o + l] = static_cast<KeyT>(base_key + row * tiles_x + (l - row * nx));
             vals[o + l] = rbase + i;
         }
     }
@@ -126,37 +129,53 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(const uint32_t* __restr
 void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* cnt, int max_n, uint32_t cap,
                        int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
     if (max_n > 0)
-        emit_pairs_kernel<<<div_up(max_n, 256), 256, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, keys, vals);
+        emit_pairs_kernel<uint32_t><<<div_up(max_n, 256), 256, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, keys, vals);
+}
+
+void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* cnt, int max_n, uint32_t cap,
+                       int tiles_x, uint16_t* keys, uint32_t* vals, cudaStream_t st) {
+    if (max_n > 0)
+        emit_pairs_kernel<uint16_t><<<div_up(max_n, 256), 256, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, keys, vals);
 }
 
 // keys are sorted at capacity: the pairs past the device count carry the sentinel key. A
-// thread covers 4 consecutive keys (one 16-byte load plus the two neighbours).
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ cnt,
+// thread covers the keys of one 16-byte load (4 uint32 or 8 uint16) plus the two neighbours.
+template <typename KeyT>
+__global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, const unsigned long long* __restrict__ cnt,
                                    uint32_t cap, uint32_t tiles, uint2* __restrict__ ranges) {
+    constexpr int KV = 16 / sizeof(KeyT);
     const unsigned long long n64 = cnt[kCntPairs];
     if (n64 > cap) return;
     const uint32_t n = static_cast<uint32_t>(n64);
-    const uint32_t i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    const uint32_t i0 = KV * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i0 >= n) return;
-    const uint4 k4 = *reinterpret_cast<const uint4*>(keys + i0);  // cap is a multiple of 4
-    const uint32_t k[4] = {k4.x, k4.y, k4.z, k4.w};
+    KeyT k[KV];
+    *reinterpret_cast<uint4*>(k) = *reinterpret_cast<const uint4*>(keys + i0);  // cap is a multiple of 64
     uint32_t prev = i0 > 0 ? keys[i0 - 1] : 0xffffffffu;
-    const uint32_t next = i0 + 4 < n ? keys[i0 + 4] : 0xffffffffu;
+    const uint32_t next = i0 + KV < n ? keys[i0 + KV] : 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < KV; ++j) {
         const uint32_t i = i0 + j;
-        if (i >= n || k[j] >= tiles) break;  // sentinels (a truncated, flagged render) end the list
-        const uint32_t nk = (j < 3 && i + 1 < n) ? k[j + 1] : (j == 3 ? next : 0xffffffffu);
-        if (i == 0 || prev != k[j]) ranges[k[j]].x = i;
-        if (i == n - 1 || nk != k[j]) ranges[k[j]].y = i + 1;
-        prev = k[j];
+        const uint32_t kj = k[j];
+        if (i >= n || kj >= tiles) break;  // sentinels (a truncated, flagged render) end the list
+        const uint32_t nk = (j < KV - 1 && i + 1 < n) ? static_cast<uint32_t>(k[j + 1]) : (j == KV - 1 ? next : 0xffffffffu);
+        if (i == 0 || prev != kj) ranges[kj].x = i;
+        if (i == n - 1 || nk != kj) ranges[kj].y = i + 1;
+        prev = kj;
     }
 }
 
 void launch_tile_ranges(const uint32_t* keys, const unsigned long long* cnt, uint32_t cap, int tiles,
                         uint2* ranges, cudaStream_t st) {
     if (cap > 0)
-        tile_ranges_kernel<<<div_up(div_up(static_cast<int>(cap), 4), 256), 256, 0, st>>>(
+        tile_ranges_kernel<uint32_t><<<div_up(div_up(static_cast<int>(cap), 4), 256), 256, 0, st>>>(
+            keys, cnt, cap, static_cast<uint32_t>(tiles), ranges);
+}
+
+void launch_tile_ranges(const uint16_t* keys, const unsigned long long* cnt, uint32_t cap, int tiles,
+                        uint2* ranges, cudaStream_t st) {
+    if (cap > 0)
+        tile_ranges_kernel<uint16_t><<<div_up(div_up(static_cast<int>(cap), 8), 256), 256, 0, st>>>(
             keys, cnt, cap, static_cast<uint32_t>(tiles), ranges);
 }
 
