@@ -914,8 +914,7 @@ void launch_knn_init(const double* pts, int64_t n, int k, const KnnGrid& g, cons
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
                            const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,
-                           bool accumulate, bool by_gid, int32_t* rank_of, int n_map, const int32_t* vis_gid,
-                           cudaStream_t st) {
+                           bool accumulate, int32_t* rank_of, int n_map, const int32_t* vis_gid, cudaStream_t st) {
     if (max_ranks <= 0 || n_map <= 0) return;
     const int blocks = div_up(max_ranks, kBwdRanks);
     reduce_partials_kernel<<<blocks, kBwdRanks, 0, st>>>(emit_off, partials, cnt, sums);
@@ -923,7 +922,6 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
     // read-modify-write of the gradient entries
     // visible-list order measured best at every SH degree (C3, B200): rank order 0.113 / 0.515 ms,
     // map order 0.139 / 0.175 ms, visible list 0.108 / 0.158 ms at degree 0 / 3
-    (void)by_gid;
     const int order = g_k8_order >= 0 ? g_k8_order : kByVisList;
     if (order != kByRank) {
         cudaMemsetAsync(rank_of, 0xff, sizeof(int32_t) * static_cast<size_t>(n_map), st);

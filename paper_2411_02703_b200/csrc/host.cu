@@ -314,12 +314,11 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     }
     {
         Scope sc(C, "preprocess_bwd");
-        const bool by_gid = true;  // K8b in visible-list order (coalesced plane traffic), see geometry.cu
         F->rank_of.ensure(sizeof(int32_t) * std::max<int64_t>(M->n, 1));
         launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
                               F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
-                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, by_gid,
-                              F->rank_of.as<int32_t>(), static_cast<int>(M->n), F->vis_gid.as<int32_t>(), st);
+                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, F->rank_of.as<int32_t>(),
+                              static_cast<int>(M->n), F->vis_gid.as<int32_t>(), st);
         G->clean = false;
         C->launched(3);  // K8a reduce, rank scatter, K8b
     }

@@ -17,7 +17,7 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
                            const Splat* rec, const uint32_t* emit_off, const float* partials,
                            double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
-                           int max_ranks, float* grads, int64_t gcap, bool accumulate, bool by_gid,
+                           int max_ranks, float* grads, int64_t gcap, bool accumulate,
                            int32_t* rank_of /* [n_map] scratch */, int n_map, const int32_t* vis_gid,
                            cudaStream_t st);
 void set_k8_order(int order);  // diagnostics: 0 rank order, 1 map order, 2 visible-list order, -1 auto
