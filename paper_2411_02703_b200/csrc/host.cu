@@ -456,9 +456,12 @@ gs_frame* scratch_frame(gs_context* C) {
 }
 
 gs_frame* train_frame(gs_context* C, int i) {
-    if (!C->train_frames[i]) {
-        C->train_frames[i] = new gs_frame();
-        C->train_frames[i]->ctx = C;
+    if (!C->train_frames[0]) {
+        for (gs_frame*& f : C->train_frames) {
+            f = new gs_frame();
+            f->ctx = C;
+        }
+        C->train_frames[1]->shared_caps = &C->train_frames[0]->caps;
     }
     return C->train_frames[i];
 }

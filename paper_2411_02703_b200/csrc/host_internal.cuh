@@ -314,12 +314,16 @@ struct gs_frame {
         int vis = 0;         // visible Gaussians
     };
     std::vector<std::pair<int64_t, Caps>> caps;  // (width << 32 | height) -> capacities
+    // the two train frames share one table, so a capacity one learns (an overflow re-run)
+    // also sizes the other's next render of that level
+    std::vector<std::pair<int64_t, Caps>>* shared_caps = nullptr;
     Caps& cap_slot(int w, int h) {
+        auto& table = shared_caps ? *shared_caps : caps;
         const int64_t key = (static_cast<int64_t>(w) << 32) | static_cast<uint32_t>(h);
-        for (auto& c : caps)
+        for (auto& c : table)
             if (c.first == key) return c.second;
-        caps.emplace_back(key, Caps{});
-        return caps.back().second;
+        table.emplace_back(key, Caps{});
+        return table.back().second;
     }
     // per-Gaussian / per-rank / per-pair scratch
     DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,

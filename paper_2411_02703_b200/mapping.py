@@ -56,6 +56,7 @@ class MappingLoop:
         self.added: list[int] = []
         self.pruned = 0
         self.n_keyframes = 0
+        self._pending: _Entry | None = None  # the next sampled step (drawn one ahead)
 
     def _clock(self, name, fn, *a):
         if not self.timed:
@@ -69,8 +70,17 @@ class MappingLoop:
         self.calls[name] = self.calls.get(name, 0) + 1
         return r
 
-    def _step(self, e: _Entry):
-        rep = self._clock("train_step", G.train_keyframe_step, self.m, e.kf, self.cfg.train, self.cam)
+    def _level_after(self, e: _Entry, extra: int) -> int:
+        """schedule_level (mapper.cpp:221-224) of e's keyframe after `extra` more steps on it."""
+        t = self.cfg.train
+        n = t.pyramid_levels
+        ipl = t.iters_per_level if t.iters_per_level > 0 else max(1, self.cfg.iter_budget // (n + 1))
+        return n - min(n, (e.kf.consumed_iters + extra) // ipl)
+
+    def _step(self, e: _Entry, nxt: _Entry | None = None):
+        # naming the next step lets its render overlap this step's read-back (bitwise-equal results)
+        hint = (nxt.kf, self._level_after(nxt, 1 if nxt is e else 0)) if nxt is not None else None
+        rep = self._clock("train_step", G.train_keyframe_step, self.m, e.kf, self.cfg.train, self.cam, None, hint)
         if rep is not None:
             self.reports.append((e.index, rep))
             self.housekeeping()
@@ -97,17 +107,28 @@ class MappingLoop:
             self.active.append(e)
         return kf
 
-    def optimize_once(self) -> bool:
+    def _draw(self) -> _Entry | None:
+        """KeyframeQueue::sample_for_optimization (keyframe.cpp:122-138): a uniform pick among the
+        keyframes with budget left; its budget is taken and a spent keyframe retires."""
         eligible = [i for i, e in enumerate(self.active) if e.remaining > 0]
         if not eligible:
-            return False
+            return None
         i = eligible[int(self.rng.integers(len(eligible)))]
         e = self.active[i]
         e.remaining -= 1
         if e.remaining == 0:
             del self.active[i]
-        self._step(e)
-        if e.remaining == 0:  # retired (keyframe.cpp:133-136): its device pyramid is freed now
+        return e
+
+    def optimize_once(self) -> bool:
+        # the sampler runs one step ahead (same draws, same eligible sets: nothing between two
+        # steps changes eligibility), so each step can name its successor
+        e = self._pending if self._pending is not None else self._draw()
+        if e is None:
+            return False
+        self._pending = self._draw()
+        self._step(e, self._pending)
+        if e.remaining == 0 and e is not self._pending:  # retired (keyframe.cpp:133-136)
             self._clock("retire_keyframe", e.kf.close)
         return True
 
