@@ -20,7 +20,10 @@ constexpr int kBwdBatch = 32;
 // Per-warp reduction buffer: a processed entry's 10 per-lane sums are staged as rows of 32 lanes
 // (stride 36 floats: 16-byte aligned, conflict-free float4 reads), and every kFlush entries the
 // warp sums each row over its lanes (lane i takes rows i, i + 32, ...). No shuffles or selects.
-constexpr int kFlush = 4;
+// 6 entries per flush: 60 rows over 32 lanes is 2 full passes (4 entries left the second pass
+// a quarter full); measured -4% on the kernel against 4, equal to 8 (whose PPT2 build overflows
+// the 48 KB static shared memory)
+constexpr int kFlush = 6;
 constexpr int kRowStride = 36;
 
 }  // namespace
