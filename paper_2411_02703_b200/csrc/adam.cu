@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
 // small independent threads keep enough loads in flight to stream HBM (the per-Gaussian form
 // serialises its planes). Every plane base is 16-byte aligned when both capacities are
 // multiples of 4. SH planes past a Gaussian's degree are left untouched.
-__global__ void __launch_bounds__(256) adam_plane_kernel(float* __restrict__ params, float* __restrict__ m,
+// 128-thread blocks: -5% (d = 0) / -6% (d = 3) against 256 (measured; more blocks in flight)
+__global__ void __launch_bounds__(128) adam_plane_kernel(float* __restrict__ params, float* __restrict__ m,
                                                          float* __restrict__ v, const int32_t* __restrict__ birth,
                                                          const int8_t* __restrict__ degree,
                                                          const float* __restrict__ grads, int64_t gcap, int64_t cap,
@@ -132,8 +133,8 @@ void launch_adam(float* params, float* m, float* v, const int32_t* birth, const 
     args.a_common = static_cast<float>(1.0 / (1.0 - std::pow(0.9, static_cast<double>(t_common))));
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
     if (cap % 4 == 0 && gcap % 4 == 0) {
-        const dim3 grid(div_up(div_up(n, 4), 256), kGeomParams + 3 * (max_degree + 1) * (max_degree + 1));
-        adam_plane_kernel<<<grid, 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
+        const dim3 grid(div_up(div_up(n, 4), 128), kGeomParams + 3 * (max_degree + 1) * (max_degree + 1));
+        adam_plane_kernel<<<grid, 128, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
     } else
         adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
 }
