@@ -244,6 +244,7 @@ def run_ours(args, rank, world):
     if prof_range:
         torch.cuda.cudart().cudaProfilerStart()
     launches0 = ctx.launches
+    cap0 = ctx.capacity_stats()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.freeze()  # setup objects leave the collector's generations: no multi-ms gen-2 pauses in the timed loop
@@ -268,6 +269,8 @@ def run_ours(args, rank, world):
                            "mpix_per_s": round(shapes[l][0] * shapes[l][1] * views_per_rank * world / (np.mean(v) / 1e3) / 1e6, 2)}
                  for l, v in sorted(lvl_ms.items())}
     launches = ctx.launches - launches0
+    cap1 = ctx.capacity_stats()
+    capacity = {k: cap1[k] - cap0[k] for k in cap1}
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()
     ms_max = ms
@@ -297,7 +300,8 @@ def run_ours(args, rank, world):
                          "sh_degree": args.sh_degree, "lambda": 0.2, "lambda_d": 0.5, "keyframes": N_FRAMES,
                          "l2": "inputs larger than L2 (params+Adam+grads > 126 MB)",
                          "parallelism": f"dp{world}" if batch else "single-view"},
-              "gpu_launches": launches, "clocks": clk.summary(), "fixture_s": round(t_fix, 2)}
+              "gpu_launches": launches, "clocks": clk.summary(), "fixture_s": round(t_fix, 2),
+              "timed_region_capacity_events": capacity}
 
     # ---------------- per-kernel profile pass (separate from the headline timing)
     ctx.profile(True)

@@ -141,6 +141,10 @@ int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64
 int gs_debug_set_k8_order(int order);
 /* diagnostics: speculative next-step renders enqueued / used on this context (gs_train_step_prefetch) */
 int gs_debug_speculation(gs_context* ctx, int64_t* out2);
+/* diagnostics of the pair-capacity policy on this context: [0] capacity growths after a
+   read-back, [1] train steps re-run because a render overflowed its capacity, [2] renders that
+   read their pair count back before binning (first render of a resolution, exact re-runs) */
+int gs_debug_capacity(gs_context* ctx, int64_t* out3);
 /* checkpoint format v1 (io/checkpoint.cpp:17-73): text header + 476-byte fp64 AoS records.
    save_checkpoint writes the device map's parameters (exact fp64 widening of the fp32 store);
    load_checkpoint returns a NEW map (fresh Adam state, GaussianMap::append) or GS_ERUNTIME for

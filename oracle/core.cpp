@@ -32,8 +32,9 @@ CameraModel CameraModel::scaled(int level) const {  // core/types.hpp:34-44
 }
 
 Pose::Pose(double w, double x, double y, double z, const Vec3& tr) : t(tr) {
-    // types.hpp:53-54 rotation(q.normalized()): q / sqrt(|q|^2)
-    const double n2 = ((x * x + y * y) + z * z) + w * w;
+    // types.hpp:53-54 rotation(q.normalized()): q / sqrt(|q|^2), the squared norm over the
+    // quaternion's coefficient storage (x, y, z, w)
+    const double n2 = esum4_vec(x * x, y * y, z * z, w * w);
     const double n = std::sqrt(n2);
     if (n2 > 0.0) {
         qw = w / n; qx = x / n; qy = y / n; qz = z / n;
@@ -103,12 +104,12 @@ static Mat3 rotation_partial(const Vec4& u, int k) {  // covariance.cpp:17-43
     return r;
 }
 
-double norm4(const Vec4& q) {
-    return std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+double norm4(const Vec4& q) {  // Vector4d::norm
+    return std::sqrt(esum4_vec(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]));
 }
 
 Vec4 normalized4(const Vec4& q) {  // Eigen normalized(): n / sqrt(squaredNorm) if > 0
-    const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    const double n2 = esum4_vec(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
     if (!(n2 > 0.0)) return q;
     const double n = std::sqrt(n2);
     Vec4 u;
@@ -124,19 +125,32 @@ Mat3 build_covariance(const Vec4& q, const Vec3& ls) {  // covariance.cpp:51-56
     Mat3 rd, sigma, out;
     for (int i = 0; i < 3; ++i)
         for (int k = 0; k < 3; ++k) rd.m[i][k] = r.m[i][k] * s2[k];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
+    for (int j = 0; j < 3; ++j) {  // (R D) R^T: rows 0-1 sequential, row 2 halving (Eigen)
+        for (int i = 0; i < 2; ++i)
             sigma.m[i][j] = (rd.m[i][0] * r.m[j][0] + rd.m[i][1] * r.m[j][1]) + rd.m[i][2] * r.m[j][2];
+        sigma.m[2][j] = rd.m[2][0] * r.m[j][0] + (rd.m[2][1] * r.m[j][1] + rd.m[2][2] * r.m[j][2]);
+    }
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) out.m[i][j] = 0.5 * (sigma.m[i][j] + sigma.m[j][i]);
     return out;
 }
 
-static Mat3 mul33(const Mat3& a, const Mat3& b) {
+// A^T B (lhs a transpose: every coefficient is a contiguous redux, 3 terms sequential)
+static Mat3 mul33_tn(const Mat3& a, const Mat3& b) {
     Mat3 c;
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
+            c.m[i][j] = (a.m[0][i] * b.m[0][j] + a.m[1][i] * b.m[1][j]) + a.m[2][i] * b.m[2][j];
+    return c;
+}
+// A B of plain matrices: rows 0-1 sequential (packets), row 2 halving (Eigen)
+static Mat3 mul33(const Mat3& a, const Mat3& b) {
+    Mat3 c;
+    for (int j = 0; j < 3; ++j) {
+        for (int i = 0; i < 2; ++i)
             c.m[i][j] = (a.m[i][0] * b.m[0][j] + a.m[i][1] * b.m[1][j]) + a.m[i][2] * b.m[2][j];
+        c.m[2][j] = a.m[2][0] * b.m[0][j] + (a.m[2][1] * b.m[1][j] + a.m[2][2] * b.m[2][j]);
+    }
     return c;
 }
 static Mat3 transpose3(const Mat3& a) {
@@ -156,7 +170,7 @@ void build_covariance_vjp(const Vec4& q, const Vec3& ls, const Mat3& d_sigma, Ve
     Mat3 g_sym;
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) g_sym.m[i][j] = d_sigma.m[i][j] + d_sigma.m[j][i];
-    const Mat3 rtgr = mul33(mul33(transpose3(r), d_sigma), r);
+    const Mat3 rtgr = mul33(mul33_tn(r, d_sigma), r);
     for (int k = 0; k < 3; ++k) d_ls[k] = 2.0 * s2[k] * rtgr.m[k][k];
     Mat3 d_r = mul33(g_sym, r);
     for (int i = 0; i < 3; ++i)
@@ -164,12 +178,12 @@ void build_covariance_vjp(const Vec4& q, const Vec3& ls, const Mat3& d_sigma, Ve
     Vec4 d_u;
     for (int k = 0; k < 4; ++k) {
         const Mat3 p = rotation_partial(u, k);
-        double s = 0.0;
-        for (int j = 0; j < 3; ++j)      // Eigen column-major redux order
-            for (int i = 0; i < 3; ++i) s += d_r.m[i][j] * p.m[i][j];
-        d_u[k] = s;
+        double e[9];  // (d_r.array() * P.array()).sum(): column-major storage, packet tree
+        for (int j = 0; j < 3; ++j)
+            for (int i = 0; i < 3; ++i) e[3 * j + i] = d_r.m[i][j] * p.m[i][j];
+        d_u[k] = esum9_vec(e);
     }
-    const double ud = ((u[0] * d_u[0] + u[1] * d_u[1]) + u[2] * d_u[2]) + u[3] * d_u[3];
+    const double ud = esum4_vec(u[0] * d_u[0], u[1] * d_u[1], u[2] * d_u[2], u[3] * d_u[3]);
     for (int k = 0; k < 4; ++k) d_q[k] = (d_u[k] - u[k] * ud) / nrm;
 }
 

@@ -56,6 +56,17 @@ inline Vec3 cross(const Vec3& a, const Vec3& b) {
     return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
+// Eigen 3.4 (SSE2) evaluation orders where they decide bits; oracle/ref_eigen/Eigen/EigenSubset.h
+// restates the rules and oracle/_ref (the reference compiled against it) pins them:
+//   - a reduction over contiguous storage (dot, squaredNorm, sum of a plain matrix) adds packets
+//     of 2 as a tree: 4 terms (e0 + e2) + (e1 + e3), 9 terms ((e0+e2)+(e4+e6) + (e1+e3)+(e5+e7)) + e8;
+//   - a 3x3 * 3x3 product of plain (column-major) matrices computes rows 0-1 as the sequential
+//     sum over k (packets) and row 2 as a halving tree e0 + (e1 + e2) (strided redux).
+inline double esum4_vec(double e0, double e1, double e2, double e3) { return (e0 + e2) + (e1 + e3); }
+inline double esum9_vec(const double* e) {
+    return (((e[0] + e[2]) + (e[4] + e[6])) + ((e[1] + e[3]) + (e[5] + e[7]))) + e[8];
+}
+
 inline double sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }  // core/types.hpp:11
 inline double logit(double p) { return std::log(p / (1.0 - p)); }         // core/types.hpp:12
 

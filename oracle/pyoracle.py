@@ -17,7 +17,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_build", "liborc.so")
+_LIB_PATH = os.path.join(_HERE, "_build", "liborc.so")  # oracle/pyref.py rebinds this to oracle/_ref
 
 GAUSS_DTYPE = np.dtype([("p", "<f8", (59,)), ("degree", "<i4"), ("pad", "<i4")])
 
@@ -82,7 +82,20 @@ def lib():
     return _lib
 
 
-def _declare(L):
+class _Sym:
+    """Attribute sink for a symbol the loaded build does not export (the reference build,
+    oracle/_ref/libgsref.so, lacks the restatement-only helpers): declaring it is a no-op."""
+
+    def __setattr__(self, k, v):
+        pass
+
+
+def _declare(real):
+    class _Tolerant:
+        def __getattr__(self, name):
+            return getattr(real, name) if hasattr(real, name) else _Sym()
+
+    L = _Tolerant()
     P = C.c_void_p
     dp = C.POINTER(C.c_double)
     L.orc_last_error.restype = C.c_char_p
@@ -103,7 +116,7 @@ def _declare(L):
                  "orc_maybe_upgrade_sh", "orc_out_free", "orc_out_images", "orc_out_csr",
                  "orc_out_projected", "orc_out_bins", "orc_keyframe_free", "orc_pool_free",
                  "orc_rng_free", "orc_map_get_adam", "orc_map_set_adam", "orc_keyframe_set_consumed"):
-        getattr(L, name).argtypes = None
+        setattr(getattr(L, name), "argtypes", None)
     L.orc_map_raise_sh_degree.argtypes = [P, C.c_int]
     L.orc_map_max_active_degree.argtypes = [P]
     L.orc_maybe_upgrade_sh.argtypes = [P, C.c_int]

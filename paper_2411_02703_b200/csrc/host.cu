@@ -102,6 +102,45 @@ void frame_pixels(gs_frame* F, const ViewParams& v) {
     F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * sizeof(uint2));
 }
 
+// every device buffer a render + loss + backward of view v needs (map size n, pair capacity
+// cap): sized up front, so no allocation (cudaMalloc / cudaFree synchronise the device) happens
+// inside a step once a frame has seen the resolution. The train frames reserve each other too.
+void reserve_frame(gs_frame* F, const ViewParams& v, int64_t n, uint32_t cap) {
+    frame_pixels(F, v);
+    const size_t P = static_cast<size_t>(v.width) * v.height;
+    F->counters.ensure(kNumCounters * sizeof(unsigned long long));
+    if (v.width >= 11 && v.height >= 11) F->wbuf.ensure(sizeof(float) * 9 * static_cast<size_t>(v.height - 10) * (v.width - 10));
+    const int nseg = blend_segments(v);
+    if (nseg > 1) {
+        F->checkpoints.ensure(sizeof(float) * (nseg - 1) * kCkFields * P);
+        F->seg_scratch.ensure(sizeof(float) * (9 * nseg + 2) * P);
+    }
+    if (n <= 0) return;
+    F->rec_by_gid.ensure(sizeof(Splat) * n);
+    F->vis_flag.ensure(sizeof(int32_t) * n);  // K1a candidate list
+    F->key_by_gid.ensure(sizeof(unsigned long long) * n);
+    F->vis_gid.ensure(sizeof(int32_t) * n);
+    F->keys_a.ensure(sizeof(uint32_t) * n);
+    F->keys_b.ensure(sizeof(uint32_t) * n);
+    F->gid_sorted.ensure(sizeof(int32_t) * n);
+    F->gid_tmp.ensure(sizeof(int32_t) * n);
+    F->rec_sorted.ensure(sizeof(Splat) * n);
+    F->depth_sorted.ensure(sizeof(unsigned long long) * n);
+    F->ntiles.ensure(sizeof(uint32_t) * (n + 1));
+    F->emit_off.ensure(sizeof(uint32_t) * (n + 1));
+    F->sort_block.ensure(sizeof(SortBlock));
+    F->rank_sums.ensure(sizeof(double) * kNumPartials * n);
+    F->rank_of.ensure(sizeof(int32_t) * n);
+    if (cap == 0) return;
+    F->sort_status.ensure(sizeof(unsigned long long) * sort_status_words(std::max<int64_t>(n, cap)));
+    const size_t kb = v.tiles_x * v.tiles_y <= 0xffff ? sizeof(uint16_t) : sizeof(uint32_t);
+    F->pair_keys.ensure(kb * cap);
+    F->pair_keys2.ensure(kb * cap);
+    F->pair_vals.ensure(sizeof(uint32_t) * cap);
+    F->pair_vals2.ensure(sizeof(uint32_t) * cap);
+    F->partials.ensure(sizeof(float) * kNumPartials * cap);
+}
+
 unsigned long long* dev_counters(gs_frame* F) { return F->counters.as<unsigned long long>(); }
 
 void take_counts(gs_frame* F, const unsigned long long* cnt) {
@@ -110,6 +149,15 @@ void take_counts(gs_frame* F, const unsigned long long* cnt) {
     F->overflow = cnt[kCntOverflow] != 0;
     F->counts_known = true;
     if (F->n_pairs > 0xffffffffLL) fail(GS_ELOGIC, "render: more than 2^32 (tile, gaussian) pairs");
+    // keep the resolution's pair capacity >= 4/3 of the latest count (a growing map then never
+    // overflows a render: the buffers grow before they are needed)
+    if (F->rendered) {
+        gs_frame::Caps& cs = F->cap_slot(F->view.width, F->view.height);
+        if (cs.pairs > 0 && 4 * F->n_pairs > 3 * static_cast<int64_t>(cs.pairs)) {
+            cs.pairs = std::max(cs.pairs, grown_cap(F->n_pairs));
+            ++F->ctx->cap_growths;
+        }
+    }
 }
 
 // one host round trip for the frame's device counts (no-op when already read)
@@ -124,7 +172,7 @@ void ensure_counts(gs_frame* F) {
 }
 
 uint32_t grown_cap(int64_t pairs) {
-    const int64_t c = (pairs + pairs / 8 + 65536 + 63) / 64 * 64;  // multiple of 64 (vector loads)
+    const int64_t c = (2 * pairs + 65536 + 63) / 64 * 64;  // multiple of 64 (vector loads)
     return static_cast<uint32_t>(std::min<int64_t>(c, 0xffffffc0LL));
 }
 
@@ -145,9 +193,9 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     F->map_n = M->n;
     F->rendered = false;
     F->has_cotangent = false;
-    frame_pixels(F, v);
     const int n = static_cast<int>(M->n);
     const int T = v.tiles_x * v.tiles_y;
+    reserve_frame(F, v, 0, 0);
     ck(cudaMemsetAsync(F->ranges.p, 0, sizeof(uint2) * T, st), "memset ranges");
     F->counters.ensure(kNumCounters * sizeof(unsigned long long));
     ck(cudaMemsetAsync(F->counters.p, 0, kNumCounters * sizeof(unsigned long long), st), "memset counters");
@@ -159,19 +207,8 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     F->vis_cap = 0;
     unsigned long long* cnt = dev_counters(F);
     if (n > 0) {
-        F->rec_by_gid.ensure(sizeof(Splat) * n);
-        F->vis_flag.ensure(sizeof(int32_t) * n);  // K1a candidate list
-        F->key_by_gid.ensure(sizeof(unsigned long long) * n);
-        F->vis_gid.ensure(sizeof(int32_t) * n);
-        F->keys_a.ensure(sizeof(uint32_t) * n);
-        F->keys_b.ensure(sizeof(uint32_t) * n);
-        F->gid_sorted.ensure(sizeof(int32_t) * n);
-        F->rec_sorted.ensure(sizeof(Splat) * n);
-        F->depth_sorted.ensure(sizeof(unsigned long long) * n);
-        F->ntiles.ensure(sizeof(uint32_t) * (n + 1));
-        F->emit_off.ensure(sizeof(uint32_t) * (n + 1));
-        // sentinel depth keys past the visible count (real keys are positive fp32 bits)
-        ck(cudaMemsetAsync(F->keys_a.p, 0xff, sizeof(uint32_t) * n, st), "memset keys");
+        reserve_frame(F, v, n, 0);
+        ck(cudaMemsetAsync(F->sort_block.p, 0, sizeof(SortBlock), st), "memset sort block");
         {
             Scope sc(C, "preprocess_fwd");
             launch_cull(M->params, M->cap, n, v, F->vis_flag.as<int32_t>(), cnt, st);
@@ -180,71 +217,49 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
                                   F->vis_gid.as<int32_t>(), F->keys_a.as<uint32_t>(), cnt, st);
             C->launched(2);
         }
+        // the pair capacity of this resolution: learned from the first render's exact count,
+        // kept at >= 4/3 of the last count seen (take_counts); the sorts cost what the device
+        // count says, not what the buffers hold
         gs_frame::Caps& cs = F->cap_slot(v.width, v.height);
         if (cs.pairs == 0 || exact_counts) {
+            ++C->count_syncs;
             ensure_counts(F);
             cs.pairs = std::max(cs.pairs, grown_cap(F->n_pairs));
-            cs.vis = std::max(cs.vis, static_cast<int>((F->n_vis + F->n_vis / 8 + 4096 + 63) / 64 * 64));
         }
         const uint32_t cap = cs.pairs;
-        const int nv = std::min(n, cs.vis);  // a larger visible count raises the overflow flag
         F->pair_cap = cap;
-        F->vis_cap = nv;
+        F->vis_cap = n;
+        reserve_frame(F, v, n, cap);
+        if (F->sibling) reserve_frame(F->sibling, v, n, cap);
+        SortBlock* sb = F->sort_block.as<SortBlock>();
+        unsigned long long* status = F->sort_status.as<unsigned long long>();
         {
-            // (depth, index) order (rasterizer.cpp:69-72): stable radix sort on the fp32-rounded
-            // depth, then exact (fp64 depth, index) order inside runs of equal fp32 keys
+            // (depth, index) order (rasterizer.cpp:69-72): radix sort on the 24-bit depth key,
+            // then exact (fp64 depth, index) order inside runs of equal keys; rank-ordered
+            // records and the scan of their tile counts
             Scope sc_sort(C, "depth_sort_pack_scan");
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                            F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, kDepthKeyBits, st);
-            ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(),
-                                               F->vis_gid.as<int32_t>(), F->gid_sorted.as<int32_t>(), nv, 0, kDepthKeyBits, st),
-               "depth sort");
-            launch_fix_ties(F->keys_b.as<uint32_t>(), F->gid_sorted.as<int32_t>(),
-                            F->key_by_gid.as<unsigned long long>(), cnt, nv, st);
-            launch_pack(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(), F->key_by_gid.as<unsigned long long>(),
-                        cnt, nv, F->rec_sorted.as<Splat>(), F->ntiles.as<uint32_t>(),
-                        F->depth_sorted.as<unsigned long long>(), st);
-            C->launched(2);
-            tb = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(), nv + 1, st);
-            ck(cub::DeviceScan::ExclusiveSum(C->cub(tb), tb, F->ntiles.as<uint32_t>(), F->emit_off.as<uint32_t>(),
-                                             nv + 1, st), "scan");
+            launch_depth_sort(F->keys_a.as<uint32_t>(), F->keys_b.as<uint32_t>(), F->vis_gid.as<int32_t>(),
+                              F->gid_tmp.as<int32_t>(), F->gid_sorted.as<int32_t>(),
+                              F->key_by_gid.as<unsigned long long>(), cnt, n, sb, status, C->epochs(3), st);
+            launch_pack_scan(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(),
+                             F->key_by_gid.as<unsigned long long>(), cnt, n, F->rec_sorted.as<Splat>(),
+                             F->depth_sorted.as<unsigned long long>(), F->emit_off.as<uint32_t>(), sb, status,
+                             C->epochs(1), st);
+            C->launched(6);
         }
         {
             Scope sc_keys(C, "tile_keys_sort_ranges");
-            F->pair_vals.ensure(sizeof(uint32_t) * cap);
-            F->pair_vals2.ensure(sizeof(uint32_t) * cap);
-            int bits = 1;  // the sentinel's low bits (2^bits - 1) must sort after every tile id
-            while ((1u << bits) <= static_cast<uint32_t>(T)) ++bits;
-            // 16-bit tile keys while the tile count fits below the 0xffff sentinel
-            auto bin = [&](auto key_tag) {
-                using KeyT = decltype(key_tag);
-                F->pair_keys.ensure(sizeof(KeyT) * cap);
-                F->pair_keys2.ensure(sizeof(KeyT) * cap);
-                KeyT* k1 = F->pair_keys.as<KeyT>();
-                KeyT* k2 = F->pair_keys2.as<KeyT>();
-                ck(cudaMemsetAsync(k1, 0xff, sizeof(KeyT) * cap, st), "memset pair keys");
-                launch_emit_pairs(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, nv, cap, v.tiles_x, k1,
-                                  F->pair_vals.as<uint32_t>(), st);
-                size_t tb = 0;
-                cub::DeviceRadixSort::SortPairs(nullptr, tb, k1, k2, F->pair_vals.as<uint32_t>(),
-                                                F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st);
-                ck(cub::DeviceRadixSort::SortPairs(C->cub(tb), tb, k1, k2, F->pair_vals.as<uint32_t>(),
-                                                   F->pair_vals2.as<uint32_t>(), static_cast<int>(cap), 0, bits, st),
-                   "tile sort");
-                launch_tile_ranges(k2, cnt, cap, T, F->ranges.as<uint2>(), st);
-            };
-            if (T < 0xffff) bin(uint16_t{});
-            else bin(uint32_t{});
-            C->launched(2);
+            C->launched(launch_tile_sort(F->emit_off.as<uint32_t>(), F->rec_sorted.as<Splat>(), cnt, n, cap, v.tiles_x,
+                                         T, F->pair_keys.p, F->pair_keys2.p, F->pair_vals.as<uint32_t>(),
+                                         F->pair_vals2.as<uint32_t>(), F->ranges.as<uint2>(), sb, status,
+                                         C->epochs(2), st));
         }
     }
     {
         Scope sc(C, "blend_fwd");
         F->nseg = blend_segments(v);
         const size_t P = static_cast<size_t>(v.width) * v.height;
-        if (F->nseg > 1) {
+        if (F->nseg > 1) {  // (reserve_frame sized them)
             F->checkpoints.ensure(sizeof(float) * (F->nseg - 1) * kCkFields * P);
             F->seg_scratch.ensure(sizeof(float) * (9 * F->nseg + 2) * P);
         }
@@ -462,6 +477,8 @@ gs_frame* train_frame(gs_context* C, int i) {
             f->ctx = C;
         }
         C->train_frames[1]->shared_caps = &C->train_frames[0]->caps;
+        C->train_frames[0]->sibling = C->train_frames[1];
+        C->train_frames[1]->sibling = C->train_frames[0];
     }
     return C->train_frames[i];
 }
@@ -594,6 +611,7 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
             else lr = read_loss(F);
             if (!F->overflow) break;
             sp.valid = false;  // rendered from the map before this step's (re-run) update
+            ++C->overflow_reruns;
             --M->adam_count;
             --M->global_step;
             if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
@@ -933,6 +951,14 @@ int gs_debug_speculation(gs_context* C, int64_t* out2) {
     });
 }
 
+int gs_debug_capacity(gs_context* C, int64_t* out3) {
+    return guard([&] {
+        out3[0] = C->cap_growths;
+        out3[1] = C->overflow_reruns;
+        out3[2] = C->count_syncs;
+    });
+}
+
 int gs_debug_set_k8_order(int order) {
     return guard([&] { set_k8_order(order); });
 }
@@ -965,7 +991,9 @@ int gs_frame_destroy(gs_frame* F) {
                           &F->pair_keys,
                           &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->rank_sums, &F->color,
                           &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
-                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints, &F->seg_scratch})
+                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints, &F->seg_scratch, &F->gid_tmp,
+                          &F->sort_block, &F->sort_status, &F->rank_of, &F->eval_quant, &F->eval_gt, &F->eval_stage,
+                          &F->counters})
             b->release();
         delete F;
     });

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "blend_common.cuh"
+#include "sort.cuh"
 
 using namespace gsb;
 
@@ -180,6 +181,18 @@ struct gs_context {
     int train_parity = 0;
     cudaEvent_t loss_ready = nullptr;  // the step's read-back copies (waited on instead of the stream)
     int64_t spec_enqueued = 0, spec_used = 0;  // diagnostics
+    // diagnostics of the capacity policy: pair-capacity growths after a read-back, and train
+    // steps re-run because a render overflowed its capacity
+    int64_t cap_growths = 0, overflow_reruns = 0, count_syncs = 0;
+    // look-back epochs of the hand-written sorts (sort.cu): every pass gets a fresh value in
+    // [1, 2^30), so the status arrays never need clearing
+    uint32_t epoch = 0;
+    uint32_t epochs(uint32_t k) {
+        if (epoch + k + 1 >= (1u << 30)) epoch = 0;
+        const uint32_t e = epoch + 1;
+        epoch += k;
+        return e;
+    }
     struct Speculation {
         bool valid = false;
         const gs_map* map = nullptr;
@@ -317,6 +330,7 @@ struct gs_frame {
     // the two train frames share one table, so a capacity one learns (an overflow re-run)
     // also sizes the other's next render of that level
     std::vector<std::pair<int64_t, Caps>>* shared_caps = nullptr;
+    gs_frame* sibling = nullptr;  // the other train frame (buffers reserved together)
     Caps& cap_slot(int w, int h) {
         auto& table = shared_caps ? *shared_caps : caps;
         const int64_t key = (static_cast<int64_t>(w) << 32) | static_cast<uint32_t>(h);
@@ -327,7 +341,8 @@ struct gs_frame {
     }
     // per-Gaussian / per-rank / per-pair scratch
     DevBuf rec_by_gid, vis_flag, key_by_gid, vis_gid, keys_a, keys_b, gid_sorted, rec_sorted, ntiles, emit_off,
-        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, rank_sums, depth_sorted;
+        num_sel, pair_keys, pair_keys2, pair_vals, pair_vals2, ranges, partials, rank_sums, depth_sorted, gid_tmp,
+        sort_block, sort_status;
     // per-pixel
     DevBuf color, depth, vis, t_final, n_proc, n_contrib, dl_dcolor, depth_cot, wbuf, host_stage;
     DevBuf checkpoints;  // backward list-segment checkpoints [nseg - 1][5][pixels]

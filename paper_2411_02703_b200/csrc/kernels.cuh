@@ -49,19 +49,6 @@ void launch_knn_init(const double* pts6, int64_t n, int k, const KnnGrid& g, con
                      cudaStream_t st);
 
 // raster.cu
-void launch_fix_ties(const uint32_t* key32_sorted, int32_t* gid_sorted, const unsigned long long* depth_by_gid,
-                     unsigned long long* counters, int max_n, cudaStream_t st);
-void launch_pack(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
-                 const unsigned long long* counters, int max_n, Splat* rec_sorted, uint32_t* ntiles_sorted,
-                 unsigned long long* depth_sorted, cudaStream_t st);
-void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* counters, int max_n,
-                       uint32_t pair_cap, int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_emit_pairs(const uint32_t* emit_off, const Splat* rec, unsigned long long* counters, int max_n,
-                       uint32_t pair_cap, int tiles_x, uint16_t* keys, uint32_t* vals, cudaStream_t st);
-void launch_tile_ranges(const uint32_t* keys_sorted, const unsigned long long* counters, uint32_t pair_cap,
-                        int tiles, uint2* ranges, cudaStream_t st);
-void launch_tile_ranges(const uint16_t* keys_sorted, const unsigned long long* counters, uint32_t pair_cap,
-                        int tiles, uint2* ranges, cudaStream_t st);
 void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib /* written only when stats */, bool stats,

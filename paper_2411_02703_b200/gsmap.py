@@ -149,6 +149,13 @@ class Context:
         _check(lib().gs_context_launch_count(_vp(self.h), C.byref(n)))
         return n.value
 
+    def capacity_stats(self) -> dict:
+        """Pair-capacity policy counters (gs_debug_capacity): growths after a read-back, train
+        steps re-run after an overflow, renders that read their pair count before binning."""
+        out = np.zeros(3, np.int64)
+        _check(lib().gs_debug_capacity(_vp(self.h), _p(out)))
+        return {"cap_growths": int(out[0]), "overflow_reruns": int(out[1]), "count_syncs": int(out[2])}
+
     def profile(self, enable: bool = True):
         """Per-kernel CUDA-event timing on the context stream (resets the table)."""
         _check(lib().gs_context_profile(_vp(self.h), int(enable)))
