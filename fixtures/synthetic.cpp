@@ -39,8 +39,8 @@ inline V3 rot(const Quat& q, V3 v) {  // Eigen _transformVector
     const V3 c = cross(qv, uv);
     return {(v.x + q.w * uv.x) + c.x, (v.y + q.w * uv.y) + c.y, (v.z + q.w * uv.z) + c.z};
 }
-inline Quat normalized(Quat q) {
-    const double n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
+inline Quat normalized(Quat q) {  // Quaterniond::normalized: coefficients (x, y, z, w), packet sums
+    const double n2 = (q.x * q.x + q.z * q.z) + (q.y * q.y + q.w * q.w);
     const double n = std::sqrt(n2);
     return {q.w / n, q.x / n, q.y / n, q.z / n};
 }
@@ -83,8 +83,11 @@ void random_unit_quaternion(std::mt19937& rng, double out[4]) {
         q[3] = n(rng); q[2] = n(rng); q[1] = n(rng); q[0] = n(rng);
     };
     draw();
-    while (std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]) < 1e-6) draw();
-    const double nn = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+    // Vector4d::norm sums the squares as packets of 2: (q0^2 + q2^2) + (q1^2 + q3^2) (Eigen 3.4,
+    // pinned against the reference's generator in tests/test_ref_pin_cpu.py)
+    auto norm4 = [&] { return std::sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3])); };
+    while (norm4() < 1e-6) draw();
+    const double nn = norm4();
     for (int i = 0; i < 4; ++i) out[i] = q[i] / nn;
 }
 

@@ -626,12 +626,12 @@ double check_build_covariance(std::mt19937& rng) {  // gradcheck.cpp:32-64
     Vec4 d_q;
     Vec3 d_s;
     build_covariance_vjp(q, s, w, d_q, d_s);
-    auto loss = [&](const Vec4& qq, const Vec3& ss) {
+    auto loss = [&](const Vec4& qq, const Vec3& ss) {  // (w.array() * C.array()).sum()
         const Mat3 c = build_covariance(qq, ss);
-        double acc = 0.0;
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j) acc += w.m[i][j] * c.m[i][j];
-        return acc;
+        double e[9];
+        for (int j = 0; j < 3; ++j)
+            for (int i = 0; i < 3; ++i) e[3 * j + i] = w.m[i][j] * c.m[i][j];
+        return esum9_vec(e);
     };
     double worst = 0.0;
     for (int i = 0; i < 4; ++i) {
@@ -656,9 +656,11 @@ Gaussian2D must_project(const Gaussian3D& g, const Pose& p, const CameraModel& c
 
 double check_project(std::mt19937& rng) {  // gradcheck.cpp:66-117
     Gaussian3D g;
+    // Pose(Quaterniond(..).normalized(), Vector3d(..)): the call's arguments are evaluated
+    // right to left (g++), the translation's draws before the rotation's
+    const double tz = uni(rng, -1, 1), ty = uni(rng, -1, 1), tx = uni(rng, -1, 1);
     const double qz = uni(rng, -1, 1), qy = uni(rng, -1, 1), qx = uni(rng, -1, 1),
                  qw = uni(rng, -1, 1);
-    const double tz = uni(rng, -1, 1), ty = uni(rng, -1, 1), tx = uni(rng, -1, 1);
     const Pose n0(qw, qx, qy, qz, {0, 0, 0});
     const Pose pose(n0.qw, n0.qx, n0.qy, n0.qz, {tx, ty, tz});
     CameraModel cam{50.0, 55.0, 31.5, 31.5, 64, 64};
@@ -678,10 +680,10 @@ double check_project(std::mt19937& rng) {  // gradcheck.cpp:66-117
     project_gaussian_vjp(g, pose, cam, w_mean, w_cov, w_depth, d_pos, d_rot, d_scale);
     auto loss = [&](const Gaussian3D& gg) {
         const Gaussian2D p2 = must_project(gg, pose, cam);
-        double acc = w_mean.x * p2.mean.x + w_mean.y * p2.mean.y;
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 2; ++j) acc += w_cov.m[i][j] * p2.cov2d.m[i][j];
-        return acc + w_depth * p2.depth;
+        // w_mean.dot(mean) + (w_cov.array() * cov2d.array()).sum() + w_depth * depth
+        const double cs = esum4_vec(w_cov.m[0][0] * p2.cov2d.m[0][0], w_cov.m[1][0] * p2.cov2d.m[1][0],
+                                    w_cov.m[0][1] * p2.cov2d.m[0][1], w_cov.m[1][1] * p2.cov2d.m[1][1]);
+        return ((w_mean.x * p2.mean.x + w_mean.y * p2.mean.y) + cs) + w_depth * p2.depth;
     };
     double worst = 0.0;
     for (int i = 0; i < 3; ++i) {
@@ -806,8 +808,8 @@ struct RenderConfig {  // gradcheck.cpp:205-211
 RenderConfig draw_render_config(std::mt19937& rng, int n_gaussians, int image_size) {  // :213-247
     RenderConfig rc;
     rc.cam = CameraModel{40.0, 42.0, (image_size - 1) / 2.0, (image_size - 1) / 2.0, image_size, image_size};
-    const double qz = uni(rng, -1, 1), qy = uni(rng, -1, 1), qx = uni(rng, -1, 1), qw = uni(rng, -1, 1);
     const double tz = uni(rng, -0.5, 0.5), ty = uni(rng, -0.5, 0.5), tx = uni(rng, -0.5, 0.5);
+    const double qz = uni(rng, -1, 1), qy = uni(rng, -1, 1), qx = uni(rng, -1, 1), qw = uni(rng, -1, 1);
     const Pose n0(qw, qx, qy, qz, {0, 0, 0});
     rc.pose = Pose(n0.qw, n0.qx, n0.qy, n0.qz, {tx, ty, tz});
     const int n = std::max(1, n_gaussians);

@@ -1,9 +1,9 @@
 // K1 preprocess_fwd and K8 preprocess_bwd: per-Gaussian FP64 geometry.
 //
 // This translation unit is compiled with --fmad=false. The fp64 operation sequence for the
-// camera transform, mean, depth, 2D covariance and radius follows the oracle's canonical order
-// (oracle/core.cpp, which in turn restates proj/src/core/projection.cpp:17-40 and
-// covariance.cpp:51-56 with Eigen's evaluation formulas), so mean / depth / radius / pixel
+// camera transform, mean, depth, 2D covariance and radius follows the reference's order under
+// Eigen 3.4 (proj/src/core/projection.cpp:17-40, covariance.cpp:51-56; the oracle restates it and
+// oracle/_ref — the reference itself — pins it bitwise), so mean / depth / radius / pixel
 // rect / tile keys come out bit-identical to the fp64 reference on the same inputs. Only the
 // data the blend needs at fp32 (conic, opacity, colour, depth) is rounded after the fact.
 #include "common.cuh"
@@ -39,9 +39,11 @@ __device__ __forceinline__ void pose_matrix(const ViewParams& v, double W[3][3])
     W[2][0] = txz - twy; W[2][1] = tyz + twx; W[2][2] = 1.0 - (txx + tyy);
 }
 
-// covariance.cpp:7-14 on the normalised quaternion (Eigen normalized(): q / sqrt(|q|^2))
+// covariance.cpp:7-14 on the normalised quaternion (Eigen normalized(): q / sqrt(|q|^2), the
+// squared norm of a Vector4d summed as packets: (q0^2 + q2^2) + (q1^2 + q3^2), see
+// oracle/ref_eigen/Eigen/EigenSubset.h)
 __device__ __forceinline__ void unit_quat(const double q[4], double u[4], double* nrm) {
-    const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    const double n2 = (q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]);
     const double n = sqrt(n2);
     *nrm = n;
     if (n2 > 0.0) {
@@ -68,9 +70,11 @@ __device__ __forceinline__ void build_covariance(const double q[4], const double
     double rd[3][3], sg[3][3];
     for (int i = 0; i < 3; ++i)
         for (int k = 0; k < 3; ++k) rd[i][k] = r[i][k] * s2[k];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            sg[i][j] = (rd[i][0] * r[j][0] + rd[i][1] * r[j][1]) + rd[i][2] * r[j][2];
+    // Eigen's (R D) R^T: rows 0-1 are packet (sequential) sums, row 2 a halving-tree redux
+    for (int j = 0; j < 3; ++j) {
+        for (int i = 0; i < 2; ++i) sg[i][j] = (rd[i][0] * r[j][0] + rd[i][1] * r[j][1]) + rd[i][2] * r[j][2];
+        sg[2][j] = rd[2][0] * r[j][0] + (rd[2][1] * r[j][1] + rd[2][2] * r[j][2]);
+    }
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) out[i][j] = 0.5 * (sg[i][j] + sg[j][i]);
 }

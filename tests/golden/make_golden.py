@@ -1,14 +1,23 @@
-"""Freezes oracle outputs as this repo's golden fixtures (the reference stores no
-golden vectors, so the new build freezes its oracle's).
+"""Freezes the REFERENCE's outputs as this repo's golden fixtures (the reference
+stores no golden vectors). They are produced by the reference itself — its own sources under
+/root/reference/proj/src compiled unchanged into oracle/_ref/libgsref.so (oracle/ref/Makefile,
+against the Eigen 3.4 subset restatement oracle/ref_eigen) — through oracle/pyref.py. The
+tests then require the oracle restatement (tests/test_golden_cpu.py) and the device
+(tests/test_gpu_golden.py) to reproduce them.
 
-    python tests/golden/make_golden.py        # rewrites tests/golden/lvigs_crop.npz
+    python tests/golden/make_golden.py        # rewrites tests/golden/lvigs_crop.npz (needs
+                                              # /root/reference: run in the build container)
+
+generate(O) with O = oracle.pyoracle runs the same workload on the restatement.
 
 Workload: a crop of the bench's synthetic scene (the reference's generate_synthetic_scene
 restated in fixtures/: walls + speckle, line trajectory, LiDAR clouds) at 4000 Gaussians and
-160x128, with the colourised-LiDAR training map (3-NN init). Everything below is the fp64
-oracle (oracle/, -O3 -ffp-contract=off) on fp32-representable parameters (the device's storage):
+160x128, with the colourised-LiDAR training map (3-NN init). Everything below is fp64 on
+fp32-representable parameters (the device's storage):
   - frame 0 render: colour / depth / visibility, contributor counts, depth order and the tile
-    lists (bin_tiles order, as map indices);
+    lists (bin_tiles order as map indices; bin_tiles is internal to rasterizer.cpp, so the lists
+    are derived from the reference's projected means and radii by tile_lists() below, which
+    restates rasterizer.cpp:76-91);
   - the C1 loss (L1 only) against the GT render, its dL/dC and the backward's gradients;
   - 3 C1 training steps (level 0, L1 only) and 6 pyramid steps (3 levels, L1 + SSIM + depth).
 Image-valued outputs are stored as float32 (the comparison bars are >= 1e-5); integer outputs
@@ -23,7 +32,6 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from fixtures import pyfixture as F  # noqa: E402
-from oracle import pyoracle as O  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lvigs_crop.npz")
 N, W, H = 4000, 160, 128
@@ -39,7 +47,29 @@ def f32(a):
     return np.asarray(a, np.float32)
 
 
-def generate():
+def tile_lists(pr, width, height, tile=16):
+    """bin_tiles (rasterizer.cpp:76-91) from the projected list: (tile offsets, ranks)."""
+    tx_n, ty_n = (width + tile - 1) // tile, (height + tile - 1) // tile
+    bins = [[] for _ in range(tx_n * ty_n)]
+    for r, ((mx, my), rad) in enumerate(zip(pr["mean"], pr["radius"])):
+        x0 = max(0, int(np.ceil(mx - rad))); x1 = min(width - 1, int(np.floor(mx + rad)))
+        y0 = max(0, int(np.ceil(my - rad))); y1 = min(height - 1, int(np.floor(my + rad)))
+        if x0 > x1 or y0 > y1:
+            continue
+        for ty in range(y0 // tile, y1 // tile + 1):
+            for tx in range(x0 // tile, x1 // tile + 1):
+                bins[ty * tx_n + tx].append(r)
+    off = np.zeros(len(bins) + 1, np.int64)
+    off[1:] = np.cumsum([len(b) for b in bins])
+    ent = np.array([r for b in bins for r in b], np.int64)
+    return off, ent
+
+
+def generate(O=None):
+    """The golden workload on O (default: the reference through oracle/pyref.py)."""
+    if O is None:
+        from oracle import pyref
+        O = pyref.load()
     scene = F.Scene(n_gaussians=N, width=W, height=H, n_frames=2, seed=1)
     cam = O.camera(*scene.camera)
     poses = [O.pose(p[0], p[1], p[2], p[3], t=p[4:7]) for p in scene.poses]
@@ -50,8 +80,8 @@ def generate():
 
     m = O.OracleMap(train)
     out = O.render(m, poses[0], cam)
-    off, ent = out.bins()
     pr = out.projected()
+    off, ent = tile_lists(pr, W, H)
     tile_gid = pr["index"][ent].astype(np.int32)
 
     c1 = O.make_cfg(0.0, 0.0, 0)
