@@ -407,10 +407,22 @@ def run_ours(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- CPU (oracle) arm
-def cpu_sample(scene, train, gt_levels, threads=0):
-    """The oracle restatement of train_keyframe_step (fp64, ThreadPool with every host thread)
-    over one coarse-to-fine cycle of keyframe 0 (levels 2, 1, 0): 3 iterations."""
+def reference_cpu():
+    """The reference's own CPU implementation: oracle/_ref/libgsref.so (the reference sources
+    compiled unchanged, built here and shipped with the repo) when present, else the oracle
+    restatement. Returns (module with the oracle's wrappers, cpu_baseline kind, description)."""
+    from oracle import pyref
+    if pyref.available():
+        return pyref.load(), "reference", ("the reference itself: /root/reference/proj/src compiled unchanged "
+                                           "(-O3 -DNDEBUG, oracle/ref/Makefile) into oracle/_ref/libgsref.so")
     from oracle import pyoracle as O
+    return O, "port", "oracle restatement (oracle/, fp64, -O3 -ffp-contract=off)"
+
+
+def cpu_sample(scene, train, gt_levels, threads=0):
+    """The reference's train_keyframe_step (fp64, ThreadPool with every host thread) over one
+    coarse-to-fine cycle of keyframe 0 (levels 2, 1, 0): 3 iterations."""
+    O, kind, what = reference_cpu()
     fx, fy, cx, cy, W, H = scene.camera
     cam = O.camera(fx, fy, cx, cy, W, H)
     p = scene.poses[0]
@@ -427,10 +439,10 @@ def cpu_sample(scene, train, gt_levels, threads=0):
         h, w = level_shapes()[r["level"]]
         px += h * w
     dt = time.time() - t
-    return {"value": round(3 / dt, 5), "unit": "iters/s", "cores": pool.threads, "kind": "port",
+    return {"value": round(3 / dt, 5), "unit": "iters/s", "cores": pool.threads, "kind": kind,
             "mpix_per_s": round(px / dt / 1e6, 4),
-            "sample": "oracle restatement (oracle/, fp64, -O3 -ffp-contract=off) of train_keyframe_step: one "
-                      "L2->L1->L0 cycle (3 iterations) of keyframe 0 of the same 1M-Gaussian workload",
+            "sample": f"{what}, train_keyframe_step: one L2->L1->L0 cycle (3 iterations) of keyframe 0 of the "
+                      "same 1M-Gaussian workload",
             "seconds": round(dt, 2)}
 
 
@@ -535,11 +547,11 @@ def run_c5(args):
 
 
 def run_reference(args, rank):
-    """--impl reference: the reference's CPU path (oracle restatement; the C++ reference itself
-    cannot be built here: no Eigen/libpng/doctest) on this host's cores."""
+    """--impl reference: the reference's own CPU path (oracle/_ref: its sources compiled
+    unchanged; the oracle restatement only if that build is missing) on this host's cores."""
     if rank != 0:
         return None
-    from oracle import pyoracle as O
+    O, kind, what = reference_cpu()
     scene, train, t_fix = build_fixture(args.n_gaussians)
     fx, fy, cx, cy, W, H = scene.camera
     cam = O.camera(fx, fy, cx, cy, W, H)
@@ -565,7 +577,7 @@ def run_reference(args, rank):
         px += h * w
     dt = time.time() - t
     v = timed / dt
-    sample = (f"oracle restatement of train_keyframe_step (fp64, ThreadPool({pool.threads})), {timed} iterations "
+    sample = (f"{what}: train_keyframe_step (fp64, ThreadPool({pool.threads})), {timed} iterations "
               f"(levels 2,1,0) of keyframe 0 after {warm} warm-up; same fixture as --impl ours")
     return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "iters/s", "n_gpus": 0,
             "steps": timed, "warmup": warm, "ms_per_step": round(dt / timed * 1e3, 2), "higher_is_better": True,
@@ -573,7 +585,7 @@ def run_reference(args, rank):
             "mpix_per_s": round(px / dt / 1e6, 4),
             "config": {"workload": "C3: 1M Gaussians 1280x1024, 3-level pyramid, L1+SSIM+depth loss",
                        "n_gaussians": len(train), "width": W0, "height": H0},
-            "cpu_baseline": {"kind": "port", "cores": pool.threads, "sample": sample, "value": round(v, 5),
+            "cpu_baseline": {"kind": kind, "cores": pool.threads, "sample": sample, "value": round(v, 5),
                              "unit": "iters/s"},
             "e2e": {"value": round(v, 5), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
