@@ -307,8 +307,16 @@ def run_ours(args, rank, world):
     ctx.profile(True)
     for s in range(args.steps):
         step(args.warmup + args.steps + s)
-    prof = ctx.profile_read()
+    prof_lv = ctx.profile_read()
     ctx.profile(False)
+    # scopes of a train step carry its level ("name@L<l>"): per-level table + the aggregate
+    prof, per_level_kernels = {}, {}
+    for key, (tot_ms, cnt) in prof_lv.items():
+        name, _, lv = key.partition("@")
+        acc = prof.setdefault(name, [0.0, 0])
+        acc[0] += tot_ms; acc[1] += cnt
+        if lv:
+            per_level_kernels.setdefault(lv, {})[name] = round(tot_ms / max(cnt, 1), 4)
     # per-level workload counters for the algorithmic model
     stats = {}
     fr = G.RenderOutput(ctx)
@@ -362,6 +370,7 @@ def run_ours(args, rank, world):
     roof["model"] = "SURVEY §8d algorithmic bytes/flops per launch, averaged over the 3 pyramid levels"
     result["roofline"] = roof
     result["kernels"] = kernels
+    result["per_level_kernel_ms"] = per_level_kernels
     result["workload_counters"] = {f"L{l}": dict(zip(["n_visible", "pairs", "pixels", "contribs", "tiles"], v))
                                    for l, v in stats.items()}
 
@@ -622,7 +631,8 @@ def main():
         a3 = copy.copy(args)
         a3.sh_degree, a3.no_e2e = 3, True
         r3, _ = run_ours(a3, rank, world)
-        result["sh_degree_3"] = {k: r3[k] for k in ("value", "ms_per_step", "mpix_per_s", "per_level", "kernels")}
+        result["sh_degree_3"] = {k: r3[k] for k in ("value", "ms_per_step", "mpix_per_s", "per_level", "kernels",
+                                                    "per_level_kernel_ms")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         scene, train, kfs, host_levels = ctxdata
         c0, d0 = host_levels[0][0]

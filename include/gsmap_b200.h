@@ -63,6 +63,7 @@ typedef struct gs_map gs_map;
 typedef struct gs_frame gs_frame;
 typedef struct gs_grads gs_grads;
 typedef struct gs_keyframe gs_keyframe;
+typedef struct gs_comm gs_comm;
 
 const char* gs_last_error(void);
 const char* gs_version(void);
@@ -276,6 +277,33 @@ int gs_train_step_prefetch(gs_map* map, gs_keyframe* kf, const gs_train_config* 
 int gs_train_accumulate(gs_map* map, gs_keyframe* kf, const gs_train_config* cfg,
                         const gs_camera* cam, gs_frame* frame, gs_grads* grads, int32_t sync,
                         gs_step_report* report);
+
+/* ---- keyframe-batch training over NCCL (no reference counterpart; the batch is the
+   sum of per-view RenderGradients, GaussianGrad::add gaussian.hpp:51-57, then ONE
+   GaussianMap::apply_gradients, gaussian_map.cpp:37-54). NCCL is bound at run time (dlopen of
+   libnccl.so.2); failures return GS_ENCCL. ---- */
+/* ncclGetUniqueId: 128 bytes for every rank's gs_comm_create (exchange them out of band) */
+int gs_comm_unique_id(uint8_t* id128);
+/* ncclCommInitRank on the context's device (collective over the nranks callers) */
+int gs_comm_create(gs_context* ctx, const uint8_t* id128, int32_t nranks, int32_t rank, gs_comm** out);
+/* borrow an existing ncclComm_t (the caller keeps ownership; gs_comm_destroy only drops the wrapper) */
+int gs_comm_wrap(gs_context* ctx, void* nccl_comm, gs_comm** out);
+int gs_comm_destroy(gs_comm* comm);
+int gs_comm_size(gs_comm* comm, int32_t* nranks, int32_t* rank);
+/* One batch step over this rank's n views (each at its keyframe's scheduled level, like
+   train_keyframe_step; a keyframe with no budget left reports ran = 0): render -> loss ->
+   backward summed on the device, then
+     mode 0: ncclAllReduce of the active gradient planes + the same Adam step on every replica;
+     mode 1: ncclReduceScatter by Gaussian range + Adam on the own range + ncclAllGather of the
+             parameters (the optimizer state stays sharded, see gs_comm_gather_optimizer_state).
+   comm = NULL: a single-rank batch (no collective). reports[n]: per-view level / loss / psnr. */
+int gs_train_batch(gs_map* map, gs_keyframe** kfs, int32_t n, const gs_train_config* cfg, const gs_camera* cam,
+                   gs_comm* comm, int32_t mode, gs_step_report* reports);
+/* re-replicate a mode-1 map's Adam m / v over the ranks (collective). Every call that reads or
+   re-lays out the optimizer state (apply_gradients, train steps, append, prune, init, integrate,
+   get/set_adam, training-state IO) returns GS_ELOGIC on a sharded map until this is called. */
+int gs_comm_gather_optimizer_state(gs_map* map, gs_comm* comm);
+int gs_map_optimizer_sharded(const gs_map* map, int32_t* sharded);
 
 #ifdef __cplusplus
 }

@@ -42,12 +42,23 @@ def rank_views(n_views: int, rank: int, world: int) -> range:
     return range(rank * per, (rank + 1) * per)
 
 
-def reduce_gradient_planes(buf: torch.Tensor, n_planes: int, cap: int, group=None) -> None:
-    """Sum the first n_planes planes of a flat [59][cap] gradient buffer over the ranks, in place."""
+def reduce_gradient_planes(buf: torch.Tensor, n_planes: int, cap: int, group=None, device_sync=None) -> None:
+    """Sum the first n_planes planes of a flat [59][cap] gradient buffer over the ranks, in place:
+    NCCL on the device buffer; with a host backend (gloo: one GPU shared by several ranks in
+    tests, or CPU-only ranks) the planes go through host memory."""
     if buf.numel() < N_PARAMS * cap or not 0 < n_planes <= N_PARAMS:
         raise ValueError("reduce_gradient_planes: buffer/plane count mismatch")
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(buf[: n_planes * cap], group=group)
+        part = buf[: n_planes * cap]
+        if part.is_cuda and dist.get_backend(group) != "nccl":
+            if device_sync is not None:
+                device_sync()  # the gradients were written on the library's stream
+            host = part.cpu()
+            dist.all_reduce(host, group=group)
+            part.copy_(host)
+            torch.cuda.current_stream(part.device).synchronize()  # before Adam reads it
+        else:
+            dist.all_reduce(part, group=group)
 
 
 class BatchTrainer:
@@ -77,6 +88,7 @@ class BatchTrainer:
             self.G.train_accumulate(self.m, keyframes[k], cfg, cam, self.grads, self.frame, sync=False)
         if after_accumulate is not None:
             after_accumulate()
-        reduce_gradient_planes(self.buf, active_planes(self.m.max_active_degree()), self.cap, self.group)
+        reduce_gradient_planes(self.buf, active_planes(self.m.max_active_degree()), self.cap, self.group,
+                               device_sync=self.ctx.synchronize)
         self.m.apply_gradients(self.grads, lr if lr is not None else cfg.lr)
         return len(views)

@@ -98,7 +98,7 @@ void frame_pixels(gs_frame* F, const ViewParams& v) {
     F->n_contrib.ensure(P * sizeof(int32_t));
     F->dl_dcolor.ensure(3 * P * sizeof(float));
     F->depth_cot.ensure(P * sizeof(float));
-    F->loss.ensure(sizeof(LossScalars));
+    F->loss.ensure(loss_buffer_bytes(v.height, v.width));
     F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * sizeof(uint2));
 }
 
@@ -342,6 +342,7 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
 // counters: the frame whose gradients these are (the update is skipped if it overflowed)
 void adam_impl(gs_map* M, gs_grads* G, const gs_learning_rates& lr, const unsigned long long* counters) {
     if (G->n != M->n) fail(GS_EINVAL, "apply_gradients: gradient count does not match map size");
+    need_replicated_optimizer(M, "apply_gradients");
     const double l[5] = {lr.position, lr.rotation, lr.log_scale, lr.opacity, lr.sh};
     Scope sc(M->ctx, "adam");
     launch_adam(M->params, M->m, M->v, M->birth, M->degree, G->planes, G->cap, M->cap, static_cast<int>(M->n), l,
@@ -362,23 +363,24 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     gs_context* C = F->ctx;
     cudaStream_t st = C->stream;
     K->acquire(level, st);
-    ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset loss");
+    ck(cudaMemsetAsync(F->loss.p, 0, loss_buffer_bytes(h, w), st), "memset loss");
     Scope sc(C, "loss_l1_ssim_depth");
+    LossLayout layout{};
     if (cfg.lambda != 0.0) {
         if (h < 11 || w < 11) fail(GS_EINVAL, "ssim: image smaller than the 11x11 window");
         F->wbuf.ensure(sizeof(float) * 9 * static_cast<size_t>(h - 10) * (w - 10));
         // SSIM forward, then its adjoint fused with the per-pixel L1 / psnr / depth terms
-        launch_ssim(F->color.as<float>(), K->color[level].as<float>(), h, w, cfg.lambda, F->wbuf.as<float>(),
+        layout = launch_ssim(F->color.as<float>(), K->color[level].as<float>(), h, w, cfg.lambda, F->wbuf.as<float>(),
                     F->dl_dcolor.as<float>(), F->loss.as<LossScalars>(), F->depth.as<float>(), F->vis.as<float>(),
                     K->depth[level].as<float>(), F->depth_cot.as<float>(), st);
         C->launched(2);
     } else {
-        launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
+        layout = launch_loss_pixel(F->color.as<float>(), F->depth.as<float>(), F->vis.as<float>(), K->color[level].as<float>(),
                           K->depth[level].as<float>(), h, w, cfg.lambda, F->dl_dcolor.as<float>(),
                           F->depth_cot.as<float>(), F->loss.as<LossScalars>(), st);
         C->launched();
     }
-    launch_loss_finalize(F->loss.as<LossScalars>(), cfg.lambda_d, st);
+    launch_loss_finalize(F->loss.as<LossScalars>(), layout, cfg.lambda_d, st);
     C->launched();
     K->release_reads(st);
     F->has_cotangent = true;
@@ -439,9 +441,11 @@ void keyframe_build(gs_keyframe* K, const float* color0, const float* depth0, in
     K->color.resize(levels + 1);
     K->depth.resize(levels + 1);
     for (auto* v : {&K->color, &K->depth})
-        for (DevBuf& b : *v) b.pool = st;
-    K->stage.pool = st;
-    if (!device_src) K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(h) * w);  // host-upload staging
+        for (DevBuf& b : *v) b.pool = &K->ctx->stream;
+    K->stage.pool = &K->ctx->stream;
+    // host-upload staging at the level-0 size once: an upload of any level then never grows it
+    // (a growth would free a buffer an in-flight copy-stream upload may still be writing)
+    if (!device_src) K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(h) * w);
     int ch = h, cw = w;
     for (int l = 0; l <= levels; ++l) {
         K->hs[l] = ch;
@@ -512,7 +516,12 @@ void upload_level_impl(gs_keyframe* K, int32_t level, const double* color, const
         // synchronising call on this keyframe's context): overlaps the compute stream's work
         cudaStream_t st = K->ctx->copies();
         if (K->used_valid) ck(cudaStreamWaitEvent(st, K->used, 0), "wait last use");
-        K->stage.ensure(sizeof(double) * 4 * P);
+        if (K->stage.bytes < sizeof(double) * 4 * P) {
+            // first host upload of a device-built keyframe: size the stage for level 0 with no
+            // copy-stream work in flight on the old buffer
+            ck(cudaStreamSynchronize(st), "sync copy stream");
+            K->stage.ensure(sizeof(double) * 4 * static_cast<size_t>(K->hs[0]) * K->ws[0]);
+        }
         ck(cudaMemcpyAsync(K->stage.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d color");
         ck(cudaMemcpyAsync(K->stage.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st),
            "h2d depth");
@@ -584,7 +593,9 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
             gs_frame* B = train_frame(C, fi ^ 1);
             const gs_frame::Caps& cs = B->cap_slot(nc.width, nc.height);
             if (cs.pairs == 0) return;  // first render at this size needs exact counts (a sync)
+            C->prof_level = pf->level;
             render_impl(M, pf->K->pose, nc, B, false, false);
+            C->prof_level = level;
             sp = gs_context::Speculation{true, M, pf->K, pf->level, M->version, *cam, pf->K->pose, fi ^ 1};
             ++C->spec_enqueued;
         };
@@ -592,6 +603,7 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
         // remembered pair capacity changed nothing on the device and is re-run at exact size
         for (int attempt = 0;; ++attempt) {
             grads_zero(G, M);
+            C->prof_level = level;
             if (!(have && attempt == 0)) render_impl(M, K->pose, lc, F, attempt > 0, false);
             loss_impl(F, K, level, *cfg);
             backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
@@ -616,6 +628,7 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
             --M->global_step;
             if (attempt > 0) fail(GS_ELOGIC, "render: pair capacity overflow after exact sizing");
         }
+        C->prof_level = -1;
         if (!prefetched) upload();
         ++K->consumed;
         report->ran = 1;
@@ -651,7 +664,7 @@ int gs_context_create(int device, void* stream, gs_context** out) {
                 ck(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking), "cudaStreamCreate");
                 C->own_stream = true;
             }
-            for (DevBuf& b : C->scratch) b.pool = C->stream;
+            for (DevBuf& b : C->scratch) b.pool = &C->stream;
         } catch (...) {
             delete C;
             throw;
@@ -665,10 +678,12 @@ int gs_context_destroy(gs_context* C) {
         if (!C) return;
         C->use();
         cudaStreamSynchronize(C->stream);
-        delete C->scratch_frame;
-        delete C->train_frames[0];
-        delete C->train_frames[1];
+        for (gs_frame* F : {C->scratch_frame, C->train_frames[0], C->train_frames[1]}) {
+            if (F) F->release_all();
+            delete F;
+        }
         if (C->loss_ready) cudaEventDestroy(C->loss_ready);
+        for (cudaEvent_t e : C->ev_pool) cudaEventDestroy(e);
         if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external)
             pool_free(C->scratch_grads->planes, C->stream);
         delete C->scratch_grads;
@@ -677,6 +692,8 @@ int gs_context_destroy(gs_context* C) {
             cudaStreamDestroy(C->copy_stream);
         }
         C->cub_tmp.release();
+        C->batch_stats.release();
+        C->shard_grads.release();
         for (DevBuf& b : C->scratch) b.release();
         if (C->own_stream) cudaStreamDestroy(C->stream);
         delete C;
@@ -692,10 +709,20 @@ int gs_context_synchronize(gs_context* C) {
 
 int gs_context_set_stream(gs_context* C, void* stream) {
     return guard([&] {
+        C->use();
+        // nothing may still run on the old stream: its pooled buffers are re-pointed (they hold
+        // &C->stream) and the stream itself may be destroyed
+        if (C->copy_stream) ck(cudaStreamSynchronize(C->copy_stream), "sync copy stream");
         ck(cudaStreamSynchronize(C->stream), "sync");
+        C->spec.valid = false;
         if (C->own_stream) cudaStreamDestroy(C->stream);
-        C->own_stream = false;
-        C->stream = static_cast<cudaStream_t>(stream);
+        if (stream) {
+            C->stream = static_cast<cudaStream_t>(stream);
+            C->own_stream = false;
+        } else {
+            ck(cudaStreamCreateWithFlags(&C->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            C->own_stream = true;
+        }
     });
 }
 
@@ -780,10 +807,12 @@ int gs_context_profile_read(gs_context* C, char* names, int32_t names_len, doubl
         for (const auto& r : C->prof) {
             float t = 0.f;
             ck(cudaEventElapsedTime(&t, r.a, r.b), "cudaEventElapsedTime");
+            // scopes enqueued by a train step carry its pyramid level: "name@L<level>"
+            const std::string key = r.level >= 0 ? std::string(r.name) + "@L" + std::to_string(r.level) : r.name;
             size_t k = 0;
-            while (k < keys.size() && keys[k] != r.name) ++k;
+            while (k < keys.size() && keys[k] != key) ++k;
             if (k == keys.size()) {
-                keys.emplace_back(r.name);
+                keys.emplace_back(key);
                 ms.push_back(0.0);
                 cnt.push_back(0);
             }
@@ -834,6 +863,7 @@ int gs_map_append(gs_map* M, const gs_gaussian* g, int64_t n) {
     return guard([&] {
         M->ctx->use();
         if (n < 0) fail(GS_EINVAL, "append: negative count");
+        need_replicated_optimizer(M, "append");
         map_reserve(M, M->n + n);
         // fresh optimizer state for the new range (gaussian_map.cpp:33)
         cudaStream_t st = M->ctx->stream;
@@ -879,6 +909,7 @@ int gs_map_get_adam(gs_map* M, double* m59, double* v59, int64_t* step, int64_t 
     return guard([&] {
         M->ctx->use();
         if (n != M->n) fail(GS_EINVAL, "get_adam: count does not match map size");
+        need_replicated_optimizer(M, "get_adam");
         if (n == 0) return;
         std::vector<float> a(static_cast<size_t>(kNumParams) * n), b(a.size());
         std::vector<int32_t> s(n);
@@ -903,6 +934,7 @@ int gs_map_set_adam(gs_map* M, const double* m59, const double* v59, const int64
     return guard([&] {
         M->ctx->use();
         if (n != M->n) fail(GS_EINVAL, "set_adam: count does not match map size");
+        need_replicated_optimizer(M, "set_adam");
         if (n == 0) return;
         std::vector<float> a(static_cast<size_t>(kNumParams) * n), b(a.size());
         std::vector<int32_t> s(n);
@@ -986,15 +1018,7 @@ int gs_frame_destroy(gs_frame* F) {
         if (!F) return;
         F->ctx->use();
         cudaStreamSynchronize(F->ctx->stream);
-        for (DevBuf* b : {&F->rec_by_gid, &F->vis_flag, &F->key_by_gid, &F->vis_gid, &F->keys_a, &F->keys_b,
-                          &F->gid_sorted, &F->rec_sorted, &F->ntiles, &F->emit_off, &F->num_sel, &F->depth_sorted,
-                          &F->pair_keys,
-                          &F->pair_keys2, &F->pair_vals, &F->pair_vals2, &F->ranges, &F->partials, &F->rank_sums, &F->color,
-                          &F->depth, &F->vis, &F->t_final, &F->n_proc, &F->n_contrib, &F->dl_dcolor, &F->depth_cot,
-                          &F->wbuf, &F->host_stage, &F->loss, &F->checkpoints, &F->seg_scratch, &F->gid_tmp,
-                          &F->sort_block, &F->sort_status, &F->rank_of, &F->eval_quant, &F->eval_gt, &F->eval_stage,
-                          &F->counters})
-            b->release();
+        F->release_all();
         delete F;
     });
 }

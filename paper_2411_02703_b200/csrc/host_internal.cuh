@@ -67,12 +67,13 @@ int guard(F&& f) {
 
 // Grow-only device buffer (no per-iteration cudaMalloc on the hot path). Buffers of objects
 // created and destroyed in the mapping loop (keyframes) come from the device's stream-ordered
-// memory pool instead (`pool` = the stream they are used on): their frees return memory to the
-// pool without the device-wide synchronisation and unmapping of cudaFree (~50 ms per keyframe).
+// memory pool instead (`pool` = the context's stream member, so a gs_context_set_stream moves
+// their allocations and frees along): their frees return memory to the pool without the
+// device-wide synchronisation and unmapping of cudaFree (~50 ms per keyframe).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
-    cudaStream_t pool = nullptr;
+    const cudaStream_t* pool = nullptr;
     bool pooled = false;
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -81,9 +82,9 @@ struct DevBuf {
         release();
         const size_t alloc = std::max<size_t>(need + need / 4, 256);
         if (pool) {
-            ck(cudaMallocAsync(&p, alloc, pool), "cudaMallocAsync");
+            ck(cudaMallocAsync(&p, alloc, *pool), "cudaMallocAsync");
             // usable by every stream from here on (keyframe uploads run on the copy stream)
-            ck(cudaStreamSynchronize(pool), "sync");
+            ck(cudaStreamSynchronize(*pool), "sync");
             pooled = true;
         } else {
             ck(cudaMalloc(&p, alloc), "cudaMalloc");
@@ -93,7 +94,7 @@ struct DevBuf {
     }
     void release() {
         if (p) {
-            if (pooled) cudaFreeAsync(p, pool);
+            if (pooled) cudaFreeAsync(p, *pool);
             else cudaFree(p);
         }
         p = nullptr;
@@ -204,10 +205,13 @@ struct gs_context {
         int frame = 0;
     } spec;
     gs_grads* scratch_grads = nullptr;
+    DevBuf batch_stats, shard_grads;  // gs_train_batch: per-view loss records, reduce-scattered gradients
     // optional per-kernel event timing (bench roofline); events are pooled
     bool profile = false;
+    int prof_level = -1;  // pyramid level of the train step being enqueued (-1: none), tags scopes
     struct ProfRec {
         const char* name;
+        int level;
         cudaEvent_t a, b;
         double host_us;  // host time spent enqueueing the scope
     };
@@ -253,7 +257,7 @@ struct Scope {
             cudaEvent_t b = C->ev();
             cudaEventRecord(b, C->stream);
             const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
-            C->prof.push_back({name, a, b, us});
+            C->prof.push_back({name, C->prof_level, a, b, us});
         }
     }
 };
@@ -290,6 +294,10 @@ struct gs_map {
     DevBuf minmax;
 
     int min_degree = 0;
+    // sharded optimizer state (gs_train_batch mode 1): each rank's m / v are current only on its
+    // own Gaussian range [rank * chunk, (rank + 1) * chunk); 0 = replicated
+    int64_t opt_shard_chunk = 0;
+    int opt_shard_ranks = 0;
     void free_all() {
         cudaStream_t st = ctx->stream;
         for (void* p : {static_cast<void*>(params), static_cast<void*>(m), static_cast<void*>(v),
@@ -353,6 +361,15 @@ struct gs_frame {
     DevBuf eval_quant, eval_gt, eval_stage;  // evaluate_view scratch
     bool has_cotangent = false;
     bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)
+    // every device buffer of the frame (gs_frame_destroy and the context's internal frames)
+    void release_all() {
+        for (DevBuf* b : {&counters, &rec_by_gid, &vis_flag, &key_by_gid, &vis_gid, &keys_a, &keys_b, &gid_sorted,
+                          &rec_sorted, &ntiles, &emit_off, &num_sel, &pair_keys, &pair_keys2, &pair_vals, &pair_vals2,
+                          &ranges, &partials, &rank_sums, &depth_sorted, &gid_tmp, &sort_block, &sort_status, &color,
+                          &depth, &vis, &t_final, &n_proc, &n_contrib, &dl_dcolor, &depth_cot, &wbuf, &host_stage,
+                          &checkpoints, &seg_scratch, &loss, &rank_of, &eval_quant, &eval_gt, &eval_stage})
+            b->release();
+    }
     int loss_level = -1;
     double loss_lambda = 0.0, loss_lambda_d = 0.0;
 };
@@ -440,6 +457,8 @@ gs_frame* train_frame(gs_context* C, int i);
 gs_grads* scratch_grads(gs_context* C);
 void train_view(gs_map* M, gs_keyframe* K, const gs_train_config& cfg, const gs_camera& cam, gs_frame* F,
                 gs_grads* G, int* level_out, bool exact_counts);
+// comm.cu
+void need_replicated_optimizer(const gs_map* M, const char* what);
 // host_mapping.cu
 void init_points_device(gs_map* M, const double* dpts, int64_t n);
 int64_t filter_points_device(gs_map* M, const double* dpts, int64_t n, const gs_pose& pose, const gs_camera& cam,

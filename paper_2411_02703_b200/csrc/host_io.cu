@@ -91,6 +91,7 @@ int gs_load_checkpoint(gs_context* C, const char* path, gs_map** out) {
 int gs_save_training_state(gs_map* M, const char* path) {
     return guard([&] {
         M->ctx->use();
+        need_replicated_optimizer(M, "save_training_state");
         const int64_t n = M->n;
         std::vector<double> m(static_cast<size_t>(kNumParams) * n), v(m.size());
         std::vector<int64_t> step(n);
@@ -116,6 +117,7 @@ int gs_save_training_state(gs_map* M, const char* path) {
 int gs_load_training_state(gs_map* M, const char* path) {
     return guard([&] {
         M->ctx->use();
+        need_replicated_optimizer(M, "load_training_state");
         std::ifstream in(path, std::ios::binary);
         if (!in) fail(GS_ERUNTIME, std::string("load_training_state: cannot open ") + path);
         std::string line, magic;
@@ -178,10 +180,13 @@ int gs_evaluate_view(gs_map* M, const gs_pose* pose, const gs_camera* cam, const
             ck(cudaMemcpyAsync(stage + 3 * P, gt_depth, sizeof(double) * P, cudaMemcpyHostToDevice, st), "h2d gt depth");
             launch_from_hwc_double(stage + 3 * P, h, w, 1, gt + 3 * P, st);
         }
-        ck(cudaMemsetAsync(F->loss.p, 0, sizeof(LossScalars), st), "memset");
-        launch_eval(F->color.as<float>(), F->depth.as<float>(), gt, gt_depth ? gt + 3 * P : nullptr, h, w,
-                    F->eval_quant.as<float>(), F->wbuf.as<float>(), F->loss.as<LossScalars>(), st);
-        C->launched(gt_depth ? 4 : 3);
+        F->loss.ensure(loss_buffer_bytes(h, w));
+        ck(cudaMemsetAsync(F->loss.p, 0, loss_buffer_bytes(h, w), st), "memset");
+        const LossLayout layout = launch_eval(F->color.as<float>(), F->depth.as<float>(), gt,
+                                              gt_depth ? gt + 3 * P : nullptr, h, w, F->eval_quant.as<float>(),
+                                              F->wbuf.as<float>(), F->loss.as<LossScalars>(), st);
+        launch_loss_finalize(F->loss.as<LossScalars>(), layout, 0.0, st);
+        C->launched(gt_depth ? 5 : 4);
         LossScalars r;
         ck(cudaMemcpyAsync(&r, F->loss.p, sizeof(r), cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");

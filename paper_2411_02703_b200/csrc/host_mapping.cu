@@ -166,6 +166,7 @@ int gs_maybe_upgrade_sh(gs_map* M, int32_t sh_interval, int32_t* degree) {  // m
 int gs_map_init_from_points(gs_map* M, const double* pts6, int64_t n, int64_t* added) {  // mapper.cpp:43-61
     return guard([&] {
         *added = 0;
+        need_replicated_optimizer(M, "init_gaussians_from_points");
         if (n <= 0) return;  // points.empty() -> 0
         if (n > 0x7fffffff) fail(GS_EINVAL, "init_from_points: too many points");
         M->ctx->use();
@@ -220,6 +221,7 @@ int gs_integrate_keyframe(gs_map* M, const gs_pose* pose, const gs_camera* cam, 
                           const double* points6, int64_t n, double tau_alpha, int32_t initial_iters, int32_t levels,
                           gs_keyframe** out_kf, int64_t* added) {
     return guard([&] {  // pipeline.cpp:148-155 (+ the keyframe's sparse depth, pipeline.cpp:108)
+        need_replicated_optimizer(M, "integrate_keyframe");
         validate_camera(*cam);
         gs_context* C = M->ctx;
         C->use();
@@ -282,6 +284,7 @@ int gs_map_prune(gs_map* M, double opacity_threshold, int64_t* removed) {  // ga
     return guard([&] {
         if (opacity_threshold <= 0.0 || opacity_threshold >= 1.0)
             fail(GS_EINVAL, "prune: threshold must be in (0, 1)");
+        need_replicated_optimizer(M, "prune");
         M->ctx->use();
         *removed = 0;
         const int n = static_cast<int>(M->n);

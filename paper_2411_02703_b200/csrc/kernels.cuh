@@ -5,6 +5,13 @@
 
 namespace gsb {
 
+// loss buffer layout (loss.cu): which per-block partial slots a loss launch filled
+enum LossField : int { kLossL1 = 0, kLossSq = 1, kLossSsim = 2, kLossDabs = 3, kLossNv = 4, kLossFields = 5 };
+struct LossLayout {
+    int n[kLossFields];  // blocks that wrote each field's slots
+    int stride;          // slots per field
+};
+
 // geometry.cu (FP64, --fmad=false)
 // counters (Counter in common.cuh): [0] visible, [1] (tile, gaussian) pairs, [2] K1a
 // candidates, [3] overflow. Kernels after K1 read their counts from there; max_* arguments
@@ -34,8 +41,8 @@ struct KnnGrid {
 };
 void launch_knn_bbox(const double* pts6, int64_t n, unsigned long long* out6 /* ordered min xyz, max xyz */,
                      cudaStream_t st);
-void launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h, int w,
-                 float* quant, float* wbuf, LossScalars* acc, cudaStream_t st);
+LossLayout launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h,
+                       int w, float* quant, float* wbuf, LossScalars* acc, cudaStream_t st);
 void launch_vis_filter(const double* pts6, int64_t n, const ViewParams& v, const float* vis, double tau,
                        int32_t* keep, cudaStream_t st);
 void launch_compact_points(const double* src6, int64_t n, const int32_t* keep, const int32_t* pos, double* dst6,
@@ -67,15 +74,19 @@ void set_blend_seg_forward(int on);
 void launch_materialize(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                         const uint32_t* offsets, int32_t* out_gid, double* out_alpha, cudaStream_t st);
 
-// loss.cu
-void launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
-                       const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
-                       float* depth_cot, LossScalars* acc, cudaStream_t st);
+// loss.cu. The loss buffer is a LossScalars header followed by per-block partial slots
+// (loss_buffer_bytes); the launchers return which slots they filled and loss_finalize sums them
+// in a fixed order into the header (deterministic, no atomics).
+int loss_slot_stride(int h, int w);
+size_t loss_buffer_bytes(int h, int w);
+LossLayout launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
+                             const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
+                             float* depth_cot, LossScalars* acc, cudaStream_t st);
 // depth != nullptr: also computes loss_pixel's terms (L1 / psnr / masked depth) in the adjoint pass
-void launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
-                 float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis, const float* gt_depth,
-                 float* depth_cot, cudaStream_t st);
-void launch_loss_finalize(LossScalars* acc, double lambda_d, cudaStream_t st);
+LossLayout launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
+                       float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis,
+                       const float* gt_depth, float* depth_cot, cudaStream_t st);
+void launch_loss_finalize(LossScalars* acc, const LossLayout& layout, double lambda_d, cudaStream_t st);
 void launch_downsample(const float* in, int h, int w, int channels, bool depth, float* out, cudaStream_t st);
 
 // adam.cu

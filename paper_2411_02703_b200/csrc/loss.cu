@@ -4,24 +4,37 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
 namespace gsb {
 
 namespace {
-__constant__ float c_taps[11];  // metrics.cpp:20-30, normalised 11-tap Gaussian, sigma 1.5
-bool g_taps_ready = false;
+// metrics.cpp:20-30: the normalised 11-tap Gaussian (sigma 1.5), exp(-d^2 / 4.5) / sum in fp64,
+// rounded to fp32. A static initialiser: every device gets it when the module loads (a runtime
+// cudaMemcpyToSymbol would reach only the device current at the first call).
+__constant__ float c_taps[11] = {1.028380124e-03f, 7.598758209e-03f, 3.600077331e-02f, 1.093606874e-01f,
+                                 2.130055428e-01f, 2.660117149e-01f, 2.130055428e-01f, 1.093606874e-01f,
+                                 3.600077331e-02f, 7.598758209e-03f, 1.028380124e-03f};
 
+// host check that the literals are the reference's taps (once per process)
 void ensure_taps() {
-    if (g_taps_ready) return;
-    double g[11], sum = 0.0;
-    for (int i = 0; i < 11; ++i) {
-        const double d = i - 5;
-        g[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
-        sum += g[i];
-    }
-    float f[11];
-    for (int i = 0; i < 11; ++i) f[i] = static_cast<float>(g[i] / sum);
-    cudaMemcpyToSymbol(c_taps, f, sizeof(f));
-    g_taps_ready = true;
+    static const bool ok = [] {
+        double g[11], sum = 0.0;
+        for (int i = 0; i < 11; ++i) {
+            const double d = i - 5;
+            g[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+            sum += g[i];
+        }
+        const float lit[11] = {1.028380124e-03f, 7.598758209e-03f, 3.600077331e-02f, 1.093606874e-01f,
+                               2.130055428e-01f, 2.660117149e-01f, 2.130055428e-01f, 1.093606874e-01f,
+                               3.600077331e-02f, 7.598758209e-03f, 1.028380124e-03f};
+        for (int i = 0; i < 11; ++i)
+            if (static_cast<float>(g[i] / sum) != lit[i]) return false;
+        return true;
+    }();
+    if (!ok) throw std::logic_error("ssim: tap table differs from metrics.cpp's window");
 }
 
 template <typename T>
@@ -30,8 +43,18 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// block of 256 threads: sum a double into *dst with one atomic per block
-__device__ __forceinline__ void block_add(double v, double* dst, double* scratch) {
+// Deterministic reductions: every block stores its total (a fixed butterfly over the warp, then
+// over the warps) in its own slot of the frame's loss buffer, and loss_finalize_kernel sums the
+// slots in a fixed order — no atomics, so the loss and psnr are bitwise reproducible run to run
+// (the reference's are for a fixed thread count, test_rasterizer.cpp:137-176).
+// Slot layout after the LossScalars header: field f, block b at slots[f * stride + b].
+__device__ __forceinline__ int linear_block() {
+    return static_cast<int>(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+}
+__device__ __forceinline__ double* slot_base(LossScalars* acc) { return reinterpret_cast<double*>(acc + 1); }
+
+// block of 256 threads: its sum of v (all threads call it) into slot b of field f
+__device__ __forceinline__ void block_store(double v, LossScalars* acc, int f, int stride, int b, double* scratch) {
     v = warp_sum(v);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) scratch[warp] = v;
@@ -39,7 +62,7 @@ __device__ __forceinline__ void block_add(double v, double* dst, double* scratch
     if (warp == 0) {
         double t = lane < (blockDim.x >> 5) ? scratch[lane] : 0.0;
         t = warp_sum(t);
-        if (lane == 0 && t != 0.0) atomicAdd(dst, t);
+        if (lane == 0) slot_base(acc)[f * stride + b] = t;
     }
     __syncthreads();
 }
@@ -52,7 +75,7 @@ __device__ __forceinline__ float sgnf(double d) { return d > 0.0 ? 1.f : (d < 0.
 __global__ void __launch_bounds__(256) loss_pixel_kernel(
     const float* __restrict__ color, const float* __restrict__ depth, const float* __restrict__ vis,
     const float* __restrict__ gt_color, const float* __restrict__ gt_depth, int P, float l1_grad,
-    float* __restrict__ dl_dcolor, float* __restrict__ depth_cot, LossScalars* __restrict__ acc) {
+    float* __restrict__ dl_dcolor, float* __restrict__ depth_cot, LossScalars* __restrict__ acc, int stride) {
     __shared__ double scratch[8];
     double l1 = 0.0, sq = 0.0, dabs = 0.0;
     unsigned long long nv = 0;
@@ -75,21 +98,33 @@ __global__ void __launch_bounds__(256) loss_pixel_kernel(
         }
         depth_cot[p] = cot;
     }
-    block_add(l1, &acc->l1_sum, scratch);
-    block_add(sq, &acc->sq_sum, scratch);
-    block_add(dabs, &acc->depth_abs_sum, scratch);
-    nv = warp_sum(nv);
-    if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&acc->n_valid, nv);
+    const int b = linear_block();
+    block_store(l1, acc, kLossL1, stride, b, scratch);
+    block_store(sq, acc, kLossSq, stride, b, scratch);
+    block_store(dabs, acc, kLossDabs, stride, b, scratch);
+    block_store(static_cast<double>(nv), acc, kLossNv, stride, b, scratch);
 }
 
-void launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
-                       const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
-                       float* depth_cot, LossScalars* acc, cudaStream_t st) {
+namespace {
+int pixel_blocks(int P) { return std::min(div_up(P, 256), 148 * 8); }
+}  // namespace
+
+size_t loss_buffer_bytes(int h, int w) {
+    return sizeof(LossScalars) + sizeof(double) * kLossFields * static_cast<size_t>(loss_slot_stride(h, w));
+}
+
+LossLayout launch_loss_pixel(const float* color, const float* depth, const float* vis, const float* gt_color,
+                             const float* gt_depth, int h, int w, double lambda, float* dl_dcolor,
+                             float* depth_cot, LossScalars* acc, cudaStream_t st) {
     const int P = h * w;
     const float l1_grad = static_cast<float>((1.0 / (static_cast<double>(h) * w * 3)) * (1.0 - lambda));
-    const int blocks = std::min(div_up(P, 256), 148 * 8);
+    const int blocks = pixel_blocks(P);
+    LossLayout L{};
+    L.stride = loss_slot_stride(h, w);
     loss_pixel_kernel<<<blocks, 256, 0, st>>>(color, depth, vis, gt_color, gt_depth, P, l1_grad, dl_dcolor,
-                                              depth_cot, acc);
+                                              depth_cot, acc, L.stride);
+    L.n[kLossL1] = L.n[kLossSq] = L.n[kLossDabs] = L.n[kLossNv] = blocks;
+    return L;
 }
 
 // ---------------------------------------------------------------------------------- SSIM
@@ -104,7 +139,7 @@ constexpr float kShift = 0.5f;
 
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, float inv_n, float* __restrict__ wbuf,
-                                                       LossScalars* __restrict__ acc) {
+                                                       LossScalars* __restrict__ acc, int stride) {
     __shared__ float sa[kInY][kInX + 2], sb[kInY][kInX + 2];
     __shared__ float hs[5][kInY][kSx + 1];
     __shared__ double scratch[8];
@@ -198,7 +233,7 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__
             wc[2 * VP + oo] = ds_dsab * inv_n;
         }
     }
-    block_add(ssum, &acc->ssim_sum, scratch);
+    block_store(ssum, acc, kLossSsim, stride, linear_block(), scratch);
 }
 
 // Adjoint of the valid correlation (metrics.cpp:55-73) for the three weight maps, combined as
@@ -213,6 +248,7 @@ struct PixelLoss {
     float* depth_cot;
     float l1_grad;
     LossScalars* acc;
+    int stride;
 };
 
 template <bool FUSED>
@@ -310,34 +346,46 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__
     }
     if (FUSED) {
         __shared__ double scratch[8];
-        block_add(l1, &pl.acc->l1_sum, scratch);
-        block_add(sq, &pl.acc->sq_sum, scratch);
-        if (c == 0) {
-            block_add(dabs, &pl.acc->depth_abs_sum, scratch);
-            nv = warp_sum(nv);
-            if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&pl.acc->n_valid, nv);
+        const int b = linear_block();
+        block_store(l1, pl.acc, kLossL1, pl.stride, b, scratch);
+        block_store(sq, pl.acc, kLossSq, pl.stride, b, scratch);
+        if (c == 0) {  // depth terms from the channel-0 blocks: slots [0, gridDim.x * gridDim.y)
+            block_store(dabs, pl.acc, kLossDabs, pl.stride, b, scratch);
+            block_store(static_cast<double>(nv), pl.acc, kLossNv, pl.stride, b, scratch);
         }
     }
 }
 
-void launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
-                 float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis, const float* gt_depth,
-                 float* depth_cot, cudaStream_t st) {
+LossLayout launch_ssim(const float* color, const float* gt_color, int h, int w, double lambda, float* wbuf,
+                       float* dl_dcolor, LossScalars* acc, const float* depth, const float* vis,
+                       const float* gt_depth, float* depth_cot, cudaStream_t st) {
     ensure_taps();
+    LossLayout L{};
+    L.stride = loss_slot_stride(h, w);
     const int vh = h - kHalo, vw = w - kHalo;
     const float inv_n = static_cast<float>(1.0 / (static_cast<double>(vh) * vw * 3));
     dim3 gf(div_up(vw, kSx), div_up(vh, kSy), 3);
-    ssim_fwd_kernel<<<gf, 256, 0, st>>>(color, gt_color, h, w, inv_n, wbuf, acc);
+    ssim_fwd_kernel<<<gf, 256, 0, st>>>(color, gt_color, h, w, inv_n, wbuf, acc, L.stride);
+    L.n[kLossSsim] = static_cast<int>(gf.x * gf.y * gf.z);
     dim3 gb(div_up(w, kSx), div_up(h, kSy), 3);
     if (depth) {  // fused pixel loss (loss_pixel_kernel is not launched)
         PixelLoss pl{depth, vis, gt_depth, depth_cot,
-                     static_cast<float>((1.0 / (static_cast<double>(h) * w * 3)) * (1.0 - lambda)), acc};
+                     static_cast<float>((1.0 / (static_cast<double>(h) * w * 3)) * (1.0 - lambda)), acc, L.stride};
         ssim_bwd_kernel<true><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda), dl_dcolor,
                                                    pl);
+        L.n[kLossL1] = L.n[kLossSq] = static_cast<int>(gb.x * gb.y * gb.z);
+        L.n[kLossDabs] = L.n[kLossNv] = static_cast<int>(gb.x * gb.y);
     } else {
         ssim_bwd_kernel<false><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda),
                                                     dl_dcolor, PixelLoss{});
     }
+    return L;
+}
+
+int loss_slot_stride(int h, int w) {
+    const int fwd = h > kHalo && w > kHalo ? div_up(w - kHalo, kSx) * div_up(h - kHalo, kSy) * 3 : 0;
+    const int bwd = div_up(w, kSx) * div_up(h, kSy) * 3;
+    return std::max({pixel_blocks(h * w), fwd, bwd, 1});
 }
 
 // ---------------------------------------------------------------------------- evaluation
@@ -346,7 +394,7 @@ void launch_ssim(const float* color, const float* gt_color, int h, int w, double
 // depth_rmse over gt > 0 (metrics.cpp:183-197). The quantized planes feed the SSIM forward.
 __global__ void __launch_bounds__(256) eval_pixel_kernel(
     const float* __restrict__ color, const float* __restrict__ depth, const float* __restrict__ gt_color,
-    const float* __restrict__ gt_depth, int P, float* __restrict__ quant, LossScalars* __restrict__ acc) {
+    const float* __restrict__ gt_depth, int P, float* __restrict__ quant, LossScalars* __restrict__ acc, int stride) {
     __shared__ double scratch[8];
     double sq = 0.0, dsq = 0.0;
     unsigned long long nv = 0;
@@ -368,33 +416,64 @@ __global__ void __launch_bounds__(256) eval_pixel_kernel(
             }
         }
     }
-    block_add(sq, &acc->sq_sum, scratch);
-    block_add(dsq, &acc->depth_abs_sum, scratch);
-    nv = warp_sum(nv);
-    if ((threadIdx.x & 31) == 0 && nv) atomicAdd(&acc->n_valid, nv);
+    const int b = linear_block();
+    block_store(sq, acc, kLossSq, stride, b, scratch);
+    block_store(dsq, acc, kLossDabs, stride, b, scratch);
+    block_store(static_cast<double>(nv), acc, kLossNv, stride, b, scratch);
 }
 
-void launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h, int w,
-                 float* quant, float* wbuf, LossScalars* acc, cudaStream_t st) {
+LossLayout launch_eval(const float* color, const float* depth, const float* gt_color, const float* gt_depth, int h,
+                       int w, float* quant, float* wbuf, LossScalars* acc, cudaStream_t st) {
     const int P = h * w;
-    eval_pixel_kernel<<<std::min(div_up(P, 256), 148 * 8), 256, 0, st>>>(color, depth, gt_color, gt_depth, P, quant,
-                                                                         acc);
+    LossLayout L{};
+    L.stride = loss_slot_stride(h, w);
+    const int blocks = pixel_blocks(P);
+    eval_pixel_kernel<<<blocks, 256, 0, st>>>(color, depth, gt_color, gt_depth, P, quant, acc, L.stride);
+    L.n[kLossSq] = L.n[kLossDabs] = L.n[kLossNv] = blocks;
     if (h >= 11 && w >= 11) {
         ensure_taps();
         const int vh = h - kHalo, vw = w - kHalo;
         const float inv_n = static_cast<float>(1.0 / (static_cast<double>(vh) * vw * 3));
         dim3 gf(div_up(vw, kSx), div_up(vh, kSy), 3);
-        ssim_fwd_kernel<<<gf, 256, 0, st>>>(quant, gt_color, h, w, inv_n, wbuf, acc);
+        ssim_fwd_kernel<<<gf, 256, 0, st>>>(quant, gt_color, h, w, inv_n, wbuf, acc, L.stride);
+        L.n[kLossSsim] = static_cast<int>(gf.x * gf.y * gf.z);
+    }
+    return L;
+}
+
+// Sums every field's block slots in a fixed order (thread t takes slots t, t + 256, ... in turn,
+// then a fixed tree over the threads) into the LossScalars header; then depth_scale.
+__global__ void __launch_bounds__(256) loss_finalize_kernel(LossScalars* acc, LossLayout L, double lambda_d) {
+    __shared__ double scratch[8];
+    __shared__ double tot[kLossFields];
+    const double* slots = slot_base(acc);
+    for (int f = 0; f < kLossFields; ++f) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < L.n[f]; b += blockDim.x) s += slots[f * L.stride + b];
+        s = warp_sum(s);
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) scratch[warp] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += scratch[w];
+            tot[f] = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        acc->l1_sum = tot[kLossL1];
+        acc->sq_sum = tot[kLossSq];
+        acc->ssim_sum = tot[kLossSsim];
+        acc->depth_abs_sum = tot[kLossDabs];
+        const unsigned long long n = static_cast<unsigned long long>(tot[kLossNv]);
+        acc->n_valid = n;
+        acc->depth_scale = n > 0 ? static_cast<float>(lambda_d / static_cast<double>(n)) : 0.f;
     }
 }
 
-__global__ void loss_finalize_kernel(LossScalars* acc, double lambda_d) {
-    const unsigned long long n = acc->n_valid;
-    acc->depth_scale = n > 0 ? static_cast<float>(lambda_d / static_cast<double>(n)) : 0.f;
-}
-
-void launch_loss_finalize(LossScalars* acc, double lambda_d, cudaStream_t st) {
-    loss_finalize_kernel<<<1, 1, 0, st>>>(acc, lambda_d);
+void launch_loss_finalize(LossScalars* acc, const LossLayout& L, double lambda_d, cudaStream_t st) {
+    loss_finalize_kernel<<<1, 256, 0, st>>>(acc, L, lambda_d);
 }
 
 // ---------------------------------------------------------------------------------- pyramid

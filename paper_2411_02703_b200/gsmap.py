@@ -619,14 +619,37 @@ class Keyframe:
     def consumed_iters(self, c: int):
         _check(lib().gs_keyframe_set_consumed(_vp(self.h), c))
 
-    def upload_level(self, l: int, color: np.ndarray, depth: np.ndarray):
-        """Overwrite pyramid level ``l`` from host fp64 HWC images (pinned memory recommended)."""
-        _check(lib().gs_keyframe_upload_level(_vp(self.h), l, _p(color), _p(depth)))
-
-    def level(self, l: int):
+    def level_shape(self, l: int):
+        if not 0 <= l:
+            raise ValueError("level out of range")
         H, W = self.shape
         for _ in range(l):
             H, W = (H + 1) // 2, (W + 1) // 2
+        return H, W
+
+    def host_level(self, l: int, color: np.ndarray, depth: np.ndarray):
+        """(colour, depth) checked for gs_keyframe_upload_level: C-contiguous fp64 of the level's
+        (H, W, 3) / (H, W) shape. The C side reads exactly that many doubles, so anything else
+        is converted (a copy) or rejected here; the caller must keep the returned arrays alive
+        until the upload is consumed (the copy is asynchronous)."""
+        H, W = self.level_shape(l)
+        color = np.ascontiguousarray(color, np.float64)
+        depth = np.ascontiguousarray(depth, np.float64)
+        if color.shape != (H, W, 3) or depth.shape != (H, W):
+            raise ValueError(f"upload_level: level {l} needs colour ({H}, {W}, 3) and depth ({H}, {W}), "
+                             f"got {color.shape} and {depth.shape}")
+        return color, depth
+
+    def upload_level(self, l: int, color: np.ndarray, depth: np.ndarray):
+        """Overwrite pyramid level ``l`` from host fp64 HWC images (pinned memory recommended;
+        the copy is asynchronous, so a converted copy is kept alive on the keyframe until the next
+        upload of any level)."""
+        color, depth = self.host_level(l, color, depth)
+        self._pending_upload = (color, depth)
+        _check(lib().gs_keyframe_upload_level(_vp(self.h), l, _p(color), _p(depth)))
+
+    def level(self, l: int):
+        H, W = self.level_shape(l)
         c = np.zeros((H, W, 3)); d = np.zeros((H, W))
         _check(lib().gs_keyframe_read_level(_vp(self.h), l, _p(c), _p(d)))
         return c, d
@@ -654,9 +677,13 @@ def train_keyframe_step(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Cam
     rep = StepReport()
     if prefetch is not None:
         nk, nl, nc, nd = (tuple(prefetch) + (None, None))[:4]  # (keyframe, level[, colour, depth])
-        for a in (nc, nd):
-            if a is not None and (a.dtype != np.float64 or not a.flags.c_contiguous):
-                raise ValueError("train_keyframe_step: prefetch images must be C-contiguous float64")
+        if (nc is None) != (nd is None):
+            raise ValueError("train_keyframe_step: pass both prefetch images or neither")
+        if nc is not None:
+            # checked / converted like upload_level; kept alive on the next keyframe until its
+            # next upload (the copy runs asynchronously behind this step)
+            nc, nd = nk.host_level(int(nl), nc, nd)
+            nk._pending_upload = (nc, nd)
         _check(lib().gs_train_step_prefetch(_vp(m.h), _vp(kf.h), C.byref(cfg), C.byref(cam), _vp(nk.h), int(nl),
                                             _p(nc), _p(nd), C.byref(rep)))
     else:
@@ -676,3 +703,71 @@ def train_accumulate(m: GaussianMap, kf: Keyframe, cfg: TrainConfig, cam: Camera
     if not rep.ran:
         return None
     return dict(level=rep.level, loss=rep.loss, psnr=rep.psnr)
+
+
+# --------------------------------------------------------------------------- multi-GPU batch
+class Comm:
+    """An NCCL communicator of the context's device (gs_comm_*). Every rank calls
+    ``Comm(ctx, uid, nranks, rank)`` with the same ``uid = comm_unique_id()`` (shared out of
+    band); ``Comm.wrap(ctx, nccl_comm_ptr)`` borrows an existing ncclComm_t instead."""
+
+    def __init__(self, ctx: Context, uid: bytes | None = None, nranks: int = 1, rank: int = 0, _handle=None):
+        self.ctx = ctx
+        if _handle is not None:
+            self.h = _handle
+        else:
+            uid = comm_unique_id() if uid is None else uid
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            h = C.c_void_p()
+            _check(lib().gs_comm_create(_vp(ctx.h), buf, nranks, rank, C.byref(h)))
+            self.h = h.value
+        n, r = C.c_int32(), C.c_int32()
+        _check(lib().gs_comm_size(_vp(self.h), C.byref(n), C.byref(r)))
+        self.nranks, self.rank = n.value, r.value
+
+    @classmethod
+    def wrap(cls, ctx: Context, nccl_comm: int):
+        h = C.c_void_p()
+        _check(lib().gs_comm_wrap(_vp(ctx.h), C.c_void_p(nccl_comm), C.byref(h)))
+        return cls(ctx, _handle=h.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            h, self.h = self.h, None
+            _check(lib().gs_comm_destroy(_vp(h)))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().gs_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def train_batch(m: GaussianMap, keyframes, cfg: TrainConfig, cam: Camera, comm: Comm | None = None,
+                sharded: bool = False):
+    """gs_train_batch: this rank's views (each keyframe at its scheduled level) -> gradients
+    summed on the device -> NCCL reduce -> ONE Adam step. Returns the per-view reports (None for
+    a keyframe whose budget is spent)."""
+    n = len(keyframes)
+    arr = (C.c_void_p * max(n, 1))(*[k.h for k in keyframes])
+    reps = (StepReport * max(n, 1))()
+    _check(lib().gs_train_batch(_vp(m.h), arr, n, C.byref(cfg), C.byref(cam), _vp(comm.h) if comm else None,
+                                1 if sharded else 0, reps))
+    return [dict(level=r.level, loss=r.loss, psnr=r.psnr) if r.ran else None for r in reps[:n]]
+
+
+def gather_optimizer_state(m: GaussianMap, comm: Comm):
+    """Re-replicate the Adam state a sharded train_batch left on each rank's own range."""
+    _check(lib().gs_comm_gather_optimizer_state(_vp(m.h), _vp(comm.h)))
+
+
+def optimizer_sharded(m: GaussianMap) -> bool:
+    s = C.c_int32()
+    _check(lib().gs_map_optimizer_sharded(_vp(m.h), C.byref(s)))
+    return bool(s.value)

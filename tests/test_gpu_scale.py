@@ -3,10 +3,13 @@
 C1 (100k Gaussians, 640x512, L1-only loss) and C2 (300k, 1280x1024, L1 + SSIM + depth) run
 through both the GPU and the multi-threaded fp64 oracle: projected order, tile keys and ranges bit-exact; images within 1e-4 on pixels with
 the same contributor count (mismatching pixels counted and bounded); gradients per parameter
-group within 1e-3 on >= 99.9% of the Gaussians. At C3 scale (1M Gaussians, 1280x1024) the
-oracle is too slow for a test, so size-independent properties are checked instead: V + T = 1,
-run-to-run determinism, insertion-order invariance, Adam's per-step bound.
+group within 1e-3 on >= 99.9% of the Gaussians. C3 — the benchmarked configuration (1M
+Gaussians, 1280x1024 pyramid) — runs every level at SH degree 0 and 3 against the oracle
+(test_c3_parity_vs_oracle; the oracle is pinned bitwise to the reference build), plus
+size-independent properties: V + T = 1, run-to-run determinism, insertion-order invariance,
+Adam's per-step bound.
 """
+import json
 import os
 
 import numpy as np
@@ -140,6 +143,105 @@ def c3():
     scene = F.Scene(n_gaussians=1_000_000, width=1280, height=1024, n_frames=8, seed=1)
     train = scene.training_map(seed=2, noise=0.06)
     return scene, train
+
+
+def _group_bad(gg, og, mask, rowmax):
+    bad = np.zeros(len(og), bool)
+    for s_, t_ in GROUPS:
+        d = np.linalg.norm(gg[:, s_:t_] - og[:, s_:t_], axis=1)
+        n = np.maximum.reduce([np.linalg.norm(gg[:, s_:t_], axis=1), np.linalg.norm(og[:, s_:t_], axis=1),
+                               1e-3 * rowmax, np.full(len(og), 1e-6)])
+        bad |= (d / n > 1e-3) & mask[:, s_]
+    return bad
+
+
+@pytest.mark.parametrize("degree", [0, 3])
+def test_c3_parity_vs_oracle(c3, degree):
+    """C3 at full size (BASELINE configs[2], the bench workload: 1M Gaussians of the
+    colourised-LiDAR training map, keyframe 0, levels 2 / 1 / 0 = 320x256 / 640x512 /
+    1280x1024), GPU against the multi-threaded oracle on the same fp32-representable map:
+      - projected order, fp64 means / depths, pixel rects, tile lists and ranges bit-exact;
+      - colour / depth / visibility within 1e-4 on pixels whose contributor count matches,
+        mismatching pixels <= 1e-4 of P;
+      - gradients (the backward fed the oracle's fp32-rounded cotangents of the full
+        L1 + SSIM + depth loss) per parameter group within 1e-3 on >= 99.9% of the touched
+        Gaussians; the reference's scalar gradcheck metric is reported per level and bounded;
+      - one train_keyframe_step (L2, render -> loss -> backward -> Adam): loss within 1e-4 rel.
+    At degree 3 every Gaussian carries random higher-order SH coefficients."""
+    from tests._common import rel_err
+    scene, train = c3
+    g = train.copy()
+    if degree:
+        gen = np.random.default_rng(3)
+        g["degree"] = 3
+        g["p"][:, 14:59] = gen.uniform(-0.05, 0.05, (len(g), 45))
+    fx, fy, cx, cy, W, H = scene.camera
+    cam0 = O.camera(fx, fy, cx, cy, W, H)
+    pose = O.Pose(*scene.poses[0])
+    om, gm = pair(g)
+    gt0 = O.render(O.OracleMap(scene.gaussians), pose, cam0, threads=THREADS).color
+    gt0 = gt0.astype(np.float32).astype(np.float64)
+    sparse0 = scene.sparse_depth(0).astype(np.float32).astype(np.float64)
+    okf = O.Keyframe(pose, gt0, sparse0, 3, 2)
+    report = {"degree": degree, "levels": {}}
+    mask = active_columns(om.gaussians)
+    for level in (2, 1, 0):
+        cam = O.camera_scaled(cam0, level)
+        oo = O.render(om, pose, cam, threads=THREADS)
+        go = G().render(gm, gpu_pose(pose), gpu_cam(cam))
+        op, gp = oo.projected(), go.projected()
+        np.testing.assert_array_equal(gp["index"], op["index"])
+        np.testing.assert_array_equal(gp["mean"], op["mean"])
+        np.testing.assert_array_equal(gp["depth"], op["depth"])
+        np.testing.assert_array_equal(gp["rect"], rect_of(op["mean"], op["radius"], cam.width, cam.height))
+        ooff, oent = oo.bins()
+        goff, gent = go.tiles()
+        np.testing.assert_array_equal(goff, ooff)
+        np.testing.assert_array_equal(gent, op["index"][oent])
+        gnc, _ = go.pixel_state()
+        same = gnc == oo.n_contrib()
+        mism = int((~same).sum())
+        assert mism <= 1e-4 * same.size, (level, mism)
+        img_err = 0.0
+        for a, b in ((go.color, oo.color), (go.depth, oo.depth), (go.visibility, oo.visibility)):
+            err = np.abs(a - b)
+            err = err.max(axis=2) if err.ndim == 3 else err
+            img_err = max(img_err, float(err[same].max()))
+        assert img_err <= 1e-4, (level, img_err)
+        gtl, gdl = O.build_pyramid(gt0, 2)[level], O.build_pyramid(sparse0, 2, depth=True)[level]
+        loss = O.compute_loss(oo.color, oo.depth, oo.visibility, gtl, gdl, O.make_cfg(0.2, 0.5, 0))
+        dc = loss["dl_dcolor"].astype(np.float32).astype(np.float64)
+        dd = loss["dl_ddepth"].astype(np.float32).astype(np.float64)
+        og = O.render_backward(om, pose, cam, oo, dc, dd, threads=THREADS)
+        gg = G().render_backward(gm, gpu_pose(pose), gpu_cam(cam), go, dc, dd).read()
+        rowmax = np.abs(og).max(axis=1)
+        touched = rowmax > 0
+        bad = _group_bad(gg, og, mask, rowmax)
+        frac = float(bad[touched].mean())
+        e = rel_err(gg, og)[mask & touched[:, None]]
+        scalar_fail = float((e > 1e-3).mean())
+        report["levels"][f"L{level}"] = {
+            "n_visible": int(len(op["index"])), "pairs": int(goff[-1]), "pixels": int(same.size),
+            "contributor_count_mismatches": mism, "max_image_err_on_matching": img_err,
+            "touched_gaussians": int(touched.sum()), "group_bar_failures": int(bad[touched].sum()),
+            "group_bar_failure_fraction": frac, "scalar_rel_err_failure_fraction": scalar_fail,
+            "scalar_rel_err_p50": float(np.percentile(e, 50)), "scalar_rel_err_p99": float(np.percentile(e, 99)),
+            "scalar_rel_err_p999": float(np.percentile(e, 99.9))}
+        assert frac <= 1e-3, (level, frac)
+        assert scalar_fail <= 5e-3, (level, scalar_fail)
+    # one full training step at the coarsest level: loss within 1e-4 relative
+    gkf = G().Keyframe(gpu_pose(pose), gt0, sparse0, 3, 2)
+    rep_o = O.train_keyframe_step(om, okf, O.make_cfg(0.2, 0.5, 2, 1), cam0, O.ThreadPool(THREADS))
+    rep_g = G().train_keyframe_step(gm, gkf, G().TrainConfig.make(0.2, 0.5, 2, 1), gpu_cam(cam0))
+    assert rep_g["level"] == rep_o["level"] == 2
+    assert rep_g["loss"] == pytest.approx(rep_o["loss"], rel=1e-4)
+    report["train_step"] = {"level": 2, "loss_gpu": rep_g["loss"], "loss_oracle": rep_o["loss"],
+                            "psnr_gpu": rep_g["psnr"], "psnr_oracle": rep_o["psnr"]}
+    print("C3 parity", json.dumps(report))
+    out = os.environ.get("GS_PARITY_LOG")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps(report) + "\n")
 
 
 def test_c3_properties(c3):
