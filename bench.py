@@ -82,45 +82,69 @@ def schedule(step):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled through NVML every ~2 ms on a background thread while
+    the timed region runs (nvidia-smi's own start-up takes longer than a 20-step region). One
+    sample is taken on entry and one on exit, so even the shortest region has readings."""
+    NAMES = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+             ("hw_power_brake_slowdown", 0x80), ("sw_power_cap", 0x4))
+
     def __init__(self, device_index=0):
-        self.proc = None
         self.dev = device_index
+        self.h = None
+        self.samples = []
+        self.mx = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:  # the NVML device of this CUDA device (CUDA_VISIBLE_DEVICES may renumber)
+            import torch
+            p = torch.cuda.get_device_properties(self.dev)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _sample(self):
+        import pynvml
+        try:
+            sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append((sm, r))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self.stop.wait(0.002):
+            self._sample()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            self.h = self._handle()
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.h = None
+            return self
+        self.stop = threading.Event()
+        self._sample()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.proc:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-                self.lines = [l for l in out.splitlines() if l.strip()]
-            except Exception:
-                pass
+        if self.h is None:
+            return
+        self._sample()
+        self.stop.set()
+        self.th.join()
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[0])); mx = max(mx, float(f[1]))
-                for n, v in zip(names, f[2:6]):
-                    if v.lower().startswith("active"):
-                        reasons.add(n)
-            except (ValueError, IndexError):
-                continue
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.NAMES if r & bit})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.mx,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, ~2 ms period during the timed region"}
 
 
 # ----------------------------------------------------------------------------- roofline model

@@ -44,7 +44,10 @@ for stage in range(int(os.environ.get("DIAG_STAGES", "3"))):
             ctx.profile(True)
             L.gs_debug_counters(C.c_void_p(ctx.h), cnt.ctypes.data_as(C.c_void_p), 1)
             G.train_keyframe_step(m, kf, cfg, cam)
-            prof = ctx.profile_read()
+            prof = {}
+            for key, (ms_, n_) in ctx.profile_read().items():  # keys "name@L<l>"
+                a = prof.setdefault(key.partition("@")[0], [0.0, 0])
+                a[0] += ms_; a[1] += n_
             L.gs_debug_counters(C.c_void_p(ctx.h), cnt.ctypes.data_as(C.c_void_p), 1)
             ctx.profile(False)
             m.gaussians = mstate[0]

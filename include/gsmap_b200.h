@@ -137,9 +137,6 @@ int gs_maybe_upgrade_sh(gs_map* map, int32_t sh_interval, int32_t* degree);
    distance to the 3 nearest other points, exact grid search; opacity 0.1; SH0 from the colour;
    degree 0; fresh optimizer state). *added = n. */
 int gs_map_init_from_points(gs_map* map, const double* points6, int64_t n, int64_t* added);
-/* diagnostics: thread order of the per-Gaussian VJP kernel (0 depth rank, 1 map index, 2 the
-   visible list; -1 = automatic: the visible list) */
-int gs_debug_set_k8_order(int order);
 /* diagnostics: speculative next-step renders enqueued / used on this context (gs_train_step_prefetch) */
 int gs_debug_speculation(gs_context* ctx, int64_t* out2);
 /* diagnostics of the pair-capacity policy on this context: [0] capacity growths after a

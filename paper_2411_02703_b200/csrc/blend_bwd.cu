@@ -12,6 +12,10 @@
 #include "blend_common.cuh"
 #include "kernels.cuh"
 
+#ifndef GSB_BWD_MIN_BLOCKS
+#define GSB_BWD_MIN_BLOCKS 1
+#endif
+
 namespace gsb {
 
 namespace {
@@ -29,7 +33,7 @@ constexpr int kRowStride = 36;
 }  // namespace
 
 template <int PPT>
-__global__ void __launch_bounds__(kTileThreads / PPT) blend_bwd_kernel(
+__global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_bwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     const uint32_t* __restrict__ emit_off, ViewParams v, const float* __restrict__ t_final,
     const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,

@@ -14,6 +14,16 @@
 #include "blend_common.cuh"
 #include "kernels.cuh"
 
+// build knobs (diag/build_variant.sh experiments; the defaults are the product build)
+#ifndef GSB_FWD_MIN_BLOCKS
+#define GSB_FWD_MIN_BLOCKS 1
+#endif
+#ifdef GSB_NEAR_NOINLINE
+#define GSB_NEAR_INLINE __noinline__
+#else
+#define GSB_NEAR_INLINE __forceinline__
+#endif
+
 namespace gsb {
 
 __device__ unsigned long long g_blend_stats[2];  // [0] near-threshold checks, [1] fp64 replays
@@ -90,7 +100,7 @@ struct FwdState {
 // decide T64 < 1e-4 exactly. Called by the whole warp; kw = entries this warp has walked so far
 // (every pixel of the warp has taken at most kw factors).
 template <int PPT>
-__device__ __forceinline__ void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
+__device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
                                           int kw, float fx, const uint32_t* __restrict__ vals,
                                           const Splat* __restrict__ rec, uint2 range, double ox, double oy) {
     const double beta = kBetaPerFactor * kw;
@@ -127,7 +137,7 @@ __device__ __forceinline__ void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigne
 // DF mode: sign of (Th + Tl) - 1e-4 per near pixel; the sequential fp64 replay only if even the
 // df32 value is within its rounding bound of the threshold (not observed in practice).
 template <int PPT>
-__device__ __forceinline__ void df_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
+__device__ GSB_NEAR_INLINE void df_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
                                         float fx, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
                                         uint2 range, double ox, double oy) {
 #pragma unroll
@@ -309,7 +319,7 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
 }
 
 template <int PPT, bool STATS>
-__global__ void __launch_bounds__(kTileThreads / PPT) blend_fwd_kernel(
+__global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
@@ -564,7 +574,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
 }
 
 static int g_ppt_override[2] = {0, 0};  // [forward, backward]; 0 = automatic
-// tiles with longer lists use the df32 transmittance (measured crossover, tests/diag_fwd.py)
+// tiles with longer lists use the df32 transmittance (measured crossover, diag/diag_fwd.py)
 static int g_df_list = 1100;
 
 void set_blend_df_list(int n) { g_df_list = n < 0 ? 1100 : n; }
@@ -579,7 +589,7 @@ void set_blend_seg_forward(int max_tiles) { g_seg_forward_tiles = max_tiles < 0 
 int blend_segments(const ViewParams& v) {
     if (g_nseg_override > 0) return g_nseg_override;
     // few tiles (long lists): split each list so the backward fills the GPU (measured with
-    // tests/diag_fwd.py on the 1M-Gaussian 1280x1024 pyramid: 16 segments at the 320-tile level,
+    // diag/diag_fwd.py on the 1M-Gaussian 1280x1024 pyramid: 16 segments at the 320-tile level,
     // 8 at the 1280-tile level; none at full resolution)
     const int tiles = v.tiles_x * v.tiles_y;
     return tiles <= 512 ? 16 : tiles <= 2048 ? 8 : 1;
@@ -593,7 +603,7 @@ void set_blend_ppt(int fwd, int bwd) {
 int blend_ppt(const ViewParams& v, bool backward) {
     const int o = g_ppt_override[backward ? 1 : 0];
     if (o == 1 || o == 2 || o == 4 || o == 8) return o;
-    // measured on B200 (1M Gaussians, 1280x1024 pyramid, tests/diag_fwd.py): the forward wants
+    // measured on B200 (1M Gaussians, 1280x1024 pyramid, diag/diag_fwd.py): the forward wants
     // 2 pixels per thread at every level; the backward amortises its per-entry warp reduction
     // over 4 pixels (its parallelism at the coarse levels comes from the list segments)
     return backward ? 4 : 2;

@@ -414,30 +414,31 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
 }
 
 // ------------------------------------------------------------------------------------------
-// K8: one thread per projected Gaussian (rank). Reduces the (tile, gaussian) partials of its
-// emission segment in fp64, then runs the per-Gaussian VJP chain (rasterizer.cpp:323-353):
-// colour clamp mask -> eval_sh_vjp -> view-direction chain, sigmoid, project_gaussian_vjp
-// (projection.cpp:42-74) -> build_covariance_vjp (covariance.cpp:58-79). Accumulates into the
-// gradient planes (batch semantics = GaussianGrad::add, gaussian.hpp:51-57).
-// Two kernels: K8a reduces each rank's (tile, gaussian) partial rows to fp64 sums in a
-// rank-ordered buffer; K8b runs the fp64 VJP per rank with its map-indexed parameter loads
-// issued up front. Splitting keeps the streaming kernel at low register count (occupancy).
-constexpr int kBwdRanks = 64;  // 2 warps per block: -9% on K8 against 128 (more resident blocks)
+// K8: per visible Gaussian, the fp64 sum of its (tile, gaussian) partial rows, then the VJP chain
+// (rasterizer.cpp:323-353): colour clamp mask -> eval_sh_vjp -> view-direction chain, sigmoid,
+// project_gaussian_vjp (projection.cpp:42-74) -> build_covariance_vjp (covariance.cpp:58-79).
+// Accumulates into the gradient planes (batch semantics = GaussianGrad::add, gaussian.hpp:51-57).
+// Two kernels: K8a reduces each rank's rows (streaming, low register count) into a rank-ordered
+// fp32 [N_vis][10] buffer; K8b runs the fp64 VJP with threads over K1's visible list (runs of
+// ascending map indices: the 14-59 parameter planes are read and the gradient planes written
+// mostly coalesced), the rank looked up in rank_of (written by pack).
+constexpr int kBwdThreads = 64;  // 2 warps per block: -9% on K8 against 128 (more resident blocks)
 
-// K8a: a warp owns 32 consecutive ranks, whose partial rows are one contiguous range. It
-// streams them 32 rows at a time (lane l reads row base + l: 1280 B coalesced), finds each
-// row's rank with a 5-step shuffle search over the 33 segment offsets, sums runs of equal rank
+// K8a: a warp owns 32 consecutive ranks, whose partial rows are one contiguous range (rank
+// order: the sums do not depend on K1's run-to-run append order). It streams them 32 rows at a
+// time (lane l reads row base + l: 1280 B coalesced), finds each row's rank with a 5-step
+// shuffle search over the 33 segment offsets, sums runs of equal rank
 // with a segmented shuffle reduction (fixed tree: deterministic), and the owning lane adds the
 // run total into its fp64 accumulator. No block barriers; load balance is per row, not per rank.
-__global__ void __launch_bounds__(kBwdRanks) reduce_partials_kernel(const uint32_t* __restrict__ emit_off,
+__global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint32_t* __restrict__ emit_off,
                                                                     const float* __restrict__ partials,
                                                                     const unsigned long long* __restrict__ cnt,
-                                                                    double* __restrict__ sums) {
-    __shared__ float seg[kBwdRanks / 32][32][kNumPartials + 1];
-    __shared__ int stamp[kBwdRanks / 32][32];  // pass in which rank l's run total was written
+                                                                    float* __restrict__ sums) {
+    __shared__ float seg[kBwdThreads / 32][32][kNumPartials + 1];
+    __shared__ int stamp[kBwdThreads / 32][32];  // pass in which rank l's run total was written
     const int n_vis = static_cast<int>(cnt[kCntVisible]);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q0 = blockIdx.x * kBwdRanks + warp * 32;
+    const int q0 = blockIdx.x * kBwdThreads + warp * 32;
     if (q0 >= n_vis || overflowed(cnt)) return;  // warp-uniform; no block barrier below
     const int nr = min(32, n_vis - q0);
     const uint32_t off = emit_off[q0 + min(lane, nr)];  // lane l: first row of rank q0 + l
@@ -500,67 +501,38 @@ __global__ void __launch_bounds__(kBwdRanks) reduce_partials_kernel(const uint32
         __syncwarp();
     }
     if (lane >= nr) return;
-    double2* out = reinterpret_cast<double2*>(sums + static_cast<size_t>(q0 + lane) * kNumPartials);
+    // stored as fp32 (half the round trip to K8b; the rounding, 2^-24 relative, is far below the
+    // fp32 partials' own error)
+    float2* out = reinterpret_cast<float2*>(sums + static_cast<size_t>(q0 + lane) * kNumPartials);
 #pragma unroll
-    for (int k = 0; k < kNumPartials / 2; ++k) out[k] = make_double2(acc[2 * k], acc[2 * k + 1]);
+    for (int k = 0; k < kNumPartials / 2; ++k)
+        out[k] = make_float2(static_cast<float>(acc[2 * k]), static_cast<float>(acc[2 * k + 1]));
 }
 
-// rank_of[gid] = depth rank of every visible Gaussian (the rest stay -1 from the memset)
-__global__ void rank_scatter_kernel(const Splat* __restrict__ rec, const unsigned long long* __restrict__ cnt,
-                                   int32_t* __restrict__ rank_of) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < static_cast<int>(cnt[kCntVisible]) && !overflowed(cnt)) rank_of[rec[r].gid] = r;
-}
-
-// K8b, one thread per visible Gaussian; ORDER picks which thread takes which Gaussian.
-//   kByRank: depth-rank order (map index from the record): the parameter and gradient plane
-//            accesses scatter, one 32-byte sector per 4-byte value;
-//   kByMap: map order over every Gaussian (rank looked up, culled ones exit): coalesced planes
-//           but ~70% idle lanes;
-//   kByVisList: the visible list K1 appended (ascending map-index runs, rank looked up): full
-//           warps and mostly coalesced planes — the default (3.3x faster than rank order at SH
-//           degree 3, where 48 more planes move each way).
-enum K8Order : int { kByRank = 0, kByMap = 1, kByVisList = 2 };
-int g_k8_order = -1;  // diagnostics override (-1 = automatic)
-
-template <bool ACC, int ORDER>
-__global__ void __launch_bounds__(kBwdRanks) preprocess_bwd_kernel(
+template <bool ACC>
+__global__ void __launch_bounds__(kBwdThreads) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
-    const Splat* __restrict__ rec, const uint32_t* __restrict__ emit_off,
-    const double* __restrict__ sums, const unsigned long long* __restrict__ cnt, float* __restrict__ grads,
-    int64_t gcap, const int32_t* __restrict__ rank_of, int n_map, const int32_t* __restrict__ vis_gid) {
-    const int t = blockIdx.x * kBwdRanks + threadIdx.x;
-    if (overflowed(cnt)) return;
-    int r, i;
-    if (ORDER == kByMap) {
-        if (t >= n_map) return;
-        i = t;
-        r = rank_of[i];
-        if (r < 0) return;  // culled: never touched
-    } else if (ORDER == kByVisList) {
-        // the visible list in append order: runs of ascending map indices (one run per K1 warp)
-        if (t >= static_cast<int>(cnt[kCntVisible])) return;
-        i = vis_gid[t];
-        r = rank_of[i];
-    } else {
-        if (t >= static_cast<int>(cnt[kCntVisible])) return;
-        r = t;
-        i = rec[r].gid;
-    }
+    const uint32_t* __restrict__ emit_off, const float* __restrict__ sums, const unsigned long long* __restrict__ cnt,
+    float* __restrict__ grads, int64_t gcap, const int32_t* __restrict__ rank_of, const int32_t* __restrict__ vis_gid) {
+    const int t = blockIdx.x * kBwdThreads + threadIdx.x;
+    if (t >= static_cast<int>(cnt[kCntVisible]) || overflowed(cnt)) return;
+    const int i = vis_gid[t];
+    const int r = rank_of[i];
     if (emit_off[r] == emit_off[r + 1]) return;  // no tile: never touched (rasterizer.cpp:327)
-    const float opf = rec[r].opacity;
     float gp[kGeomParams];  // map-indexed: all loads in flight at once
 #pragma unroll
     for (int k = 0; k < kGeomParams; ++k) gp[k] = __ldg(params + static_cast<int64_t>(k) * cap + i);
     const int deg = degree[i];
     double acc[kNumPartials];
-    const double2* in = reinterpret_cast<const double2*>(sums + static_cast<size_t>(r) * kNumPartials);
+    const float2* in = reinterpret_cast<const float2*>(sums + static_cast<size_t>(r) * kNumPartials);
 #pragma unroll
     for (int k = 0; k < kNumPartials / 2; ++k) {
-        const double2 t = in[k];
-        acc[2 * k] = t.x;
-        acc[2 * k + 1] = t.y;
+        const float2 q = in[k];
+        acc[2 * k] = q.x;
+        acc[2 * k + 1] = q.y;
     }
+    // the opacity exactly as K1 rounded it into the record (same expression, same translation unit)
+    const float opf = static_cast<float>(1.0 / (1.0 + exp(-static_cast<double>(gp[P_OP]))));
     bool any = false;
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) any |= (acc[k] != 0.0);
@@ -916,37 +888,20 @@ void launch_knn_init(const double* pts, int64_t n, int k, const KnnGrid& g, cons
 }
 
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
-                           const Splat* rec, const uint32_t* emit_off, const float* partials, double* sums,
-                           const unsigned long long* cnt, int max_ranks, float* grads, int64_t gcap,
-                           bool accumulate, int32_t* rank_of, int n_map, const int32_t* vis_gid, cudaStream_t st) {
-    if (max_ranks <= 0 || n_map <= 0) return;
-    const int blocks = div_up(max_ranks, kBwdRanks);
-    reduce_partials_kernel<<<blocks, kBwdRanks, 0, st>>>(emit_off, partials, cnt, sums);
+                           const uint32_t* emit_off, const float* partials, float* sums, const unsigned long long* cnt,
+                           int max_ranks, float* grads, int64_t gcap, bool accumulate, const int32_t* rank_of,
+                           const int32_t* vis_gid, cudaStream_t st) {
+    if (max_ranks <= 0) return;
+    const int blocks = div_up(max_ranks, kBwdThreads);
+    reduce_partials_kernel<<<blocks, kBwdThreads, 0, st>>>(emit_off, partials, cnt, sums);
     // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
     // read-modify-write of the gradient entries
-    // visible-list order measured best at every SH degree (C3, B200): rank order 0.113 / 0.515 ms,
-    // map order 0.139 / 0.175 ms, visible list 0.108 / 0.158 ms at degree 0 / 3
-    const int order = g_k8_order >= 0 ? g_k8_order : kByVisList;
-    if (order != kByRank) {
-        cudaMemsetAsync(rank_of, 0xff, sizeof(int32_t) * static_cast<size_t>(n_map), st);
-        rank_scatter_kernel<<<div_up(max_ranks, 256), 256, 0, st>>>(rec, cnt, rank_of);
-    }
-    const int gblocks = order == kByMap ? div_up(n_map, kBwdRanks) : blocks;
-#define GS_K8(ACC_, ORD_)                                                                              \
-    preprocess_bwd_kernel<ACC_, ORD_><<<gblocks, kBwdRanks, 0, st>>>(params, cap, degree, v, rec, emit_off, \
-                                                                    sums, cnt, grads, gcap, rank_of, n_map, vis_gid)
-    if (accumulate) {
-        if (order == kByMap) GS_K8(true, kByMap);
-        else if (order == kByVisList) GS_K8(true, kByVisList);
-        else GS_K8(true, kByRank);
-    } else {
-        if (order == kByMap) GS_K8(false, kByMap);
-        else if (order == kByVisList) GS_K8(false, kByVisList);
-        else GS_K8(false, kByRank);
-    }
-#undef GS_K8
+    if (accumulate)
+        preprocess_bwd_kernel<true><<<blocks, kBwdThreads, 0, st>>>(params, cap, degree, v, emit_off, sums, cnt,
+                                                                   grads, gcap, rank_of, vis_gid);
+    else
+        preprocess_bwd_kernel<false><<<blocks, kBwdThreads, 0, st>>>(params, cap, degree, v, emit_off, sums, cnt,
+                                                                    grads, gcap, rank_of, vis_gid);
 }
-
-void set_k8_order(int order) { g_k8_order = order; }
 
 }  // namespace gsb

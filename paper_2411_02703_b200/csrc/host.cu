@@ -105,6 +105,25 @@ void frame_pixels(gs_frame* F, const ViewParams& v) {
 // every device buffer a render + loss + backward of view v needs (map size n, pair capacity
 // cap): sized up front, so no allocation (cudaMalloc / cudaFree synchronise the device) happens
 // inside a step once a frame has seen the resolution. The train frames reserve each other too.
+namespace {
+std::atomic<uint32_t> g_sort_epoch{0};
+std::atomic<uint32_t> g_sort_era{0};
+}  // namespace
+
+uint32_t sort_epochs(uint32_t k) {
+    for (;;) {
+        uint32_t cur = g_sort_epoch.load();
+        uint32_t base = cur;
+        if (base + k + 1 >= (1u << 30)) base = 0;  // wrap: every status array is cleared before reuse
+        if (g_sort_epoch.compare_exchange_weak(cur, base + k)) {
+            if (base != cur) g_sort_era.fetch_add(1);
+            return base + 1;
+        }
+    }
+}
+
+uint32_t sort_epoch_era() { return g_sort_era.load(); }
+
 void reserve_frame(gs_frame* F, const ViewParams& v, int64_t n, uint32_t cap) {
     frame_pixels(F, v);
     const size_t P = static_cast<size_t>(v.width) * v.height;
@@ -129,10 +148,19 @@ void reserve_frame(gs_frame* F, const ViewParams& v, int64_t n, uint32_t cap) {
     F->ntiles.ensure(sizeof(uint32_t) * (n + 1));
     F->emit_off.ensure(sizeof(uint32_t) * (n + 1));
     F->sort_block.ensure(sizeof(SortBlock));
-    F->rank_sums.ensure(sizeof(double) * kNumPartials * n);
     F->rank_of.ensure(sizeof(int32_t) * n);
+    F->rank_sums.ensure(sizeof(float) * kNumPartials * n);
     if (cap == 0) return;
-    F->sort_status.ensure(sizeof(unsigned long long) * sort_status_words(std::max<int64_t>(n, cap)));
+    {
+        const void* before = F->sort_status.p;
+        const size_t words = sort_status_words(std::max<int64_t>(n, cap));
+        F->sort_status.ensure(sizeof(unsigned long long) * words);
+        if (F->sort_status.p != before || F->status_era != sort_epoch_era()) {
+            // fresh (possibly recycled) memory, or the epoch counter wrapped: no stale epochs
+            ck(cudaMemsetAsync(F->sort_status.p, 0, F->sort_status.bytes, F->ctx->stream), "memset sort status");
+            F->status_era = sort_epoch_era();
+        }
+    }
     const size_t kb = v.tiles_x * v.tiles_y <= 0xffff ? sizeof(uint16_t) : sizeof(uint32_t);
     F->pair_keys.ensure(kb * cap);
     F->pair_keys2.ensure(kb * cap);
@@ -243,7 +271,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
                               F->key_by_gid.as<unsigned long long>(), cnt, n, sb, status, C->epochs(3), st);
             launch_pack_scan(F->gid_sorted.as<int32_t>(), F->rec_by_gid.as<Splat>(),
                              F->key_by_gid.as<unsigned long long>(), cnt, n, F->rec_sorted.as<Splat>(),
-                             F->depth_sorted.as<unsigned long long>(), F->emit_off.as<uint32_t>(), sb, status,
+                             F->depth_sorted.as<unsigned long long>(), F->rank_of.as<int32_t>(), F->emit_off.as<uint32_t>(), sb, status,
                              C->epochs(1), st);
             C->launched(6);
         }
@@ -318,7 +346,6 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     if (M->n == 0 || F->pair_cap == 0) return;
     if (F->counts_known && (F->n_vis == 0 || F->n_pairs == 0)) return;
     F->partials.ensure(sizeof(float) * kNumPartials * F->pair_cap);
-    F->rank_sums.ensure(sizeof(double) * kNumPartials * F->vis_cap);
     {
         Scope sc(C, "blend_bwd");
         launch_blend_bwd(F->ranges.as<uint2>(), F->pair_vals2.as<uint32_t>(), F->rec_sorted.as<Splat>(),
@@ -329,13 +356,11 @@ void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* 
     }
     {
         Scope sc(C, "preprocess_bwd");
-        F->rank_of.ensure(sizeof(int32_t) * std::max<int64_t>(M->n, 1));
-        launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->rec_sorted.as<Splat>(),
-                              F->emit_off.as<uint32_t>(), F->partials.as<float>(), F->rank_sums.as<double>(),
-                              dev_counters(F), F->vis_cap, G->planes, G->cap, !G->clean, F->rank_of.as<int32_t>(),
-                              static_cast<int>(M->n), F->vis_gid.as<int32_t>(), st);
+        launch_preprocess_bwd(M->params, M->cap, M->degree, F->view, F->emit_off.as<uint32_t>(),
+                              F->partials.as<float>(), F->rank_sums.as<float>(), dev_counters(F), F->vis_cap,
+                              G->planes, G->cap, !G->clean, F->rank_of.as<int32_t>(), F->vis_gid.as<int32_t>(), st);
         G->clean = false;
-        C->launched(3);  // K8a reduce, rank scatter, K8b
+        C->launched(2);  // K8a reduce, K8b VJP
     }
 }
 
@@ -989,10 +1014,6 @@ int gs_debug_capacity(gs_context* C, int64_t* out3) {
         out3[1] = C->overflow_reruns;
         out3[2] = C->count_syncs;
     });
-}
-
-int gs_debug_set_k8_order(int order) {
-    return guard([&] { set_k8_order(order); });
 }
 
 int gs_map_device_planes(gs_map* M, float** params, float** m, float** v, int64_t* cap) {

@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <functional>
@@ -70,6 +71,15 @@ int guard(F&& f) {
 // memory pool instead (`pool` = the context's stream member, so a gs_context_set_stream moves
 // their allocations and frees along): their frees return memory to the pool without the
 // device-wide synchronisation and unmapping of cudaFree (~50 ms per keyframe).
+// Look-back epochs of the hand-written sorts (sort.cu): every sort pass in the process gets a
+// fresh value in [1, 2^30), so a status array never needs clearing between passes. The counter
+// is process-wide, not per context: status arrays come from the device's shared memory pool,
+// and a recycled block may hold words another context published under a per-context epoch that
+// this context would reach later (a false "published" match in the look-back). A status array
+// is zeroed when it is (re)allocated and again whenever the counter wraps (sort_epoch_era).
+uint32_t sort_epochs(uint32_t k);
+uint32_t sort_epoch_era();
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -185,15 +195,8 @@ struct gs_context {
     // diagnostics of the capacity policy: pair-capacity growths after a read-back, and train
     // steps re-run because a render overflowed its capacity
     int64_t cap_growths = 0, overflow_reruns = 0, count_syncs = 0;
-    // look-back epochs of the hand-written sorts (sort.cu): every pass gets a fresh value in
-    // [1, 2^30), so the status arrays never need clearing
-    uint32_t epoch = 0;
-    uint32_t epochs(uint32_t k) {
-        if (epoch + k + 1 >= (1u << 30)) epoch = 0;
-        const uint32_t e = epoch + 1;
-        epoch += k;
-        return e;
-    }
+    // look-back epochs of the hand-written sorts (sort.cu): see sort_epochs()
+    uint32_t epochs(uint32_t k) { return sort_epochs(k); }
     struct Speculation {
         bool valid = false;
         const gs_map* map = nullptr;
@@ -328,6 +331,7 @@ struct gs_frame {
     // when counts_known. Pair buffers are sized by a capacity remembered per resolution.
     DevBuf counters;
     bool counts_known = false, overflow = false;
+    uint32_t status_era = ~0u;  // sort_epoch_era() when sort_status was last cleared
     uint32_t pair_cap = 0;
     int vis_cap = 0;  // ranks the depth sort and the rank-indexed kernels cover
     struct Caps {
@@ -357,7 +361,7 @@ struct gs_frame {
     DevBuf seg_scratch;  // segmented forward: per-segment local states, Tl and stop segment
     int nseg = 1;
     DevBuf loss;  // LossScalars
-    DevBuf rank_of;  // K8b: depth rank per map index (-1 = culled)
+    DevBuf rank_of;  // K8: depth rank per visible map index (written by pack)
     DevBuf eval_quant, eval_gt, eval_stage;  // evaluate_view scratch
     bool has_cotangent = false;
     bool has_contrib = false;  // n_contrib written (the training path's scratch frame skips it)

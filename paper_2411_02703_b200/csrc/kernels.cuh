@@ -21,13 +21,13 @@ void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, i
 void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degree, const int32_t* cand,
                            int max_cand, const ViewParams& v, Splat* rec_by_gid, unsigned long long* depth_key,
                            int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st);
+// K8 (partial reduction -> per-Gaussian VJP); sums = [max_ranks][10] fp32 scratch; rank_of =
+// depth rank per visible map index (written by pack), vis_gid = K1's visible list
 void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degree, const ViewParams& v,
-                           const Splat* rec, const uint32_t* emit_off, const float* partials,
-                           double* sums /* [max_ranks][10] scratch */, const unsigned long long* counters,
-                           int max_ranks, float* grads, int64_t gcap, bool accumulate,
-                           int32_t* rank_of /* [n_map] scratch */, int n_map, const int32_t* vis_gid,
-                           cudaStream_t st);
-void set_k8_order(int order);  // diagnostics: 0 rank order, 1 map order, 2 visible-list order, -1 auto
+                           const uint32_t* emit_off, const float* partials, float* sums,
+                           const unsigned long long* counters,
+                           int max_ranks, float* grads, int64_t gcap, bool accumulate, const int32_t* rank_of,
+                           const int32_t* vis_gid, cudaStream_t st);
 
 // project_sparse_depth: points [n][stride] (x, y, z first, fp64, device) -> depth [h][w] fp64
 void launch_sparse_depth(const double* pts, int stride, int64_t n, const ViewParams& v, double* depth,

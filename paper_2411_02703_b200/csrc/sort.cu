@@ -41,7 +41,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 
 // Sum of the values of tiles [0, tile) for one lane of the status array (`stride` words per
 // tile), after publishing this tile's own `value` as an aggregate; then publishes the inclusive
-// prefix. Waits only on lower tiles, which were ticketed earlier by running CTAs.
+// prefix. Waits only on lower tiles, which were ticketed earlier by running CTAs. The walk reads
+// a window of kLookWin predecessors per round trip (independent loads in flight together), so
+// the chain of dependent L2 round trips is ~tile / kLookWin long instead of ~tile.
+constexpr int kLookWin = 8;
+
 __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32_t tile, int stride, uint32_t epoch,
                                               uint32_t value) {
     unsigned long long* my = status + static_cast<size_t>(tile) * stride;
@@ -51,14 +55,63 @@ __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32
     }
     st_relaxed(my, pack_status(epoch, kFlagAgg, value));
     uint32_t excl = 0;
-    for (int j = static_cast<int>(tile) - 1;;) {
-        const unsigned long long s = ld_relaxed(status + static_cast<size_t>(j) * stride);
-        if (static_cast<uint32_t>(s >> 34) != epoch) continue;  // not yet published in this pass
-        excl += static_cast<uint32_t>(s);
-        if (((s >> 32) & 3u) == kFlagPrefix) break;
-        --j;
+    int j = static_cast<int>(tile) - 1;
+    for (;;) {
+        unsigned long long s[kLookWin];
+#pragma unroll
+        for (int w = 0; w < kLookWin; ++w)
+            s[w] = j - w >= 0 ? ld_relaxed(status + static_cast<size_t>(j - w) * stride) : 0ull;
+        // take the published predecessors nearest first, up to the first inclusive prefix; stop
+        // at the first one not yet published in this pass and poll again from there
+        int adv = 0;
+        bool done = false, stall = false;
+#pragma unroll
+        for (int w = 0; w < kLookWin; ++w) {
+            if (done || stall) continue;
+            const unsigned long long x = s[w];
+            if (j - w < 0 || static_cast<uint32_t>(x >> 34) != epoch) {
+                stall = true;
+            } else {
+                excl += static_cast<uint32_t>(x);
+                ++adv;
+                done = ((x >> 32) & 3u) == kFlagPrefix;
+            }
+        }
+        if (done) break;
+        j -= adv;
     }
     st_relaxed(my, pack_status(epoch, kFlagPrefix, excl + value));
+    return excl;
+}
+
+// The same for one status word per tile, walked by a whole warp: lane l reads predecessor
+// j - l, so one round trip covers 32 tiles. Every lane returns the exclusive prefix.
+__device__ __forceinline__ uint32_t look_back_warp(unsigned long long* status, uint32_t tile, uint32_t epoch,
+                                                   uint32_t value) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(status, pack_status(epoch, kFlagPrefix, value));
+        return 0u;
+    }
+    if (lane == 0) st_relaxed(status + tile, pack_status(epoch, kFlagAgg, value));
+    uint32_t excl = 0;
+    int j = static_cast<int>(tile) - 1;
+    for (;;) {
+        const int idx = j - lane;
+        const unsigned long long x = idx >= 0 ? ld_relaxed(status + idx) : pack_status(epoch, kFlagPrefix, 0u);
+        const bool ready = static_cast<uint32_t>(x >> 34) == epoch;
+        const unsigned nr = __ballot_sync(0xffffffffu, !ready);
+        const unsigned pre = __ballot_sync(0xffffffffu, ready && ((x >> 32) & 3u) == kFlagPrefix);
+        const int first_nr = nr ? __ffs(nr) - 1 : 32;
+        const int first_pre = pre ? __ffs(pre) - 1 : 32;
+        if (first_pre < first_nr) {
+            excl += __reduce_add_sync(0xffffffffu, lane <= first_pre ? static_cast<uint32_t>(x) : 0u);
+            break;
+        }
+        excl += __reduce_add_sync(0xffffffffu, lane < first_nr ? static_cast<uint32_t>(x) : 0u);
+        j -= first_nr;
+    }
+    if (lane == 0) st_relaxed(status + tile, pack_status(epoch, kFlagPrefix, excl + value));
     return excl;
 }
 
@@ -211,38 +264,44 @@ __global__ void __launch_bounds__(NT) radix_hist_kernel(const uint32_t* __restri
 
 // ------------------------------------------------------------------------------------------
 // Exact (fp64 depth, map index) order inside runs of equal 24-bit keys (the key is a monotone
-// function of the fp64 depth, so only equal-key runs can be out of order). Grid-stride over
-// the device count.
-__global__ void __launch_bounds__(NT) fix_ties_kernel(const uint32_t* __restrict__ key, int32_t* __restrict__ gid,
+// function of the fp64 depth, so only equal-key runs can be out of order). Runs are common
+// (fp32 positions under an axis-aligned pose give exactly equal depths; C3 has runs of up to
+// ~40), so every element of a run computes its own rank in the run by comparing against all
+// members (independent loads, the same addresses across the run's lanes) and scatters itself to
+// run start + rank; elements outside runs are copied. Out of place: gid_in -> gid_out.
+__global__ void __launch_bounds__(NT) fix_ties_kernel(const uint32_t* __restrict__ key,
+                                                      const int32_t* __restrict__ gid_in,
                                                       const unsigned long long* __restrict__ depth,
-                                                      const unsigned long long* __restrict__ cnt) {
+                                                      const unsigned long long* __restrict__ cnt,
+                                                      int32_t* __restrict__ gid_out) {
     const int n = static_cast<int>(cnt[kCntVisible]);
-    for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
-        const uint32_t k = key[i];
-        if ((i > 0 && key[i - 1] == k) || i + 1 >= n || key[i + 1] != k) continue;  // not a run start
-        int end = i + 1;
-        while (end < n && key[end] == k) ++end;
-        for (int a = i + 1; a < end; ++a) {
-            const int g = gid[a];
-            const unsigned long long d = depth[g];
-            int b = a - 1;
-            while (b >= i) {
-                const int gb = gid[b];
-                const unsigned long long db = depth[gb];
-                if (db < d || (db == d && gb < g)) break;
-                gid[b + 1] = gb;
-                --b;
-            }
-            gid[b + 1] = g;
+    for (int p = blockIdx.x * NT + threadIdx.x; p < n; p += gridDim.x * NT) {
+        const uint32_t k = key[p];
+        const int g = gid_in[p];
+        if (!((p > 0 && key[p - 1] == k) || (p + 1 < n && key[p + 1] == k))) {
+            gid_out[p] = g;
+            continue;
         }
+        int s = p, e = p + 1;
+        while (s > 0 && key[s - 1] == k) --s;
+        while (e < n && key[e] == k) ++e;
+        const unsigned long long d = depth[g];
+        int r = 0;
+#pragma unroll 4
+        for (int q = s; q < e; ++q) {
+            const int gq = gid_in[q];
+            const unsigned long long dq = depth[gq];
+            r += (dq < d || (dq == d && gq < g)) ? 1 : 0;
+        }
+        gid_out[s + r] = g;
     }
 }
 
 // ------------------------------------------------------------------------------------------
 // Rank-ordered copy of the projected records (the reference's sorted `projected` vector) fused
 // with the exclusive scan of their tile counts: emit_off[r] = first (tile, Gaussian) pair of
-// rank r, emit_off[n_vis] = total pairs. Tiles of IT*NT ranks (striped: coalesced writes), one
-// look-back word per tile.
+// rank r, emit_off[n_vis] = total pairs; also rank_of[map index] = rank for K8. Tiles of
+// 4 x NT ranks (4 consecutive per thread), one look-back word per tile (walked by a warp).
 constexpr int kPackItems = 4;
 
 __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict__ gid_sorted,
@@ -251,9 +310,11 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
                                                        const unsigned long long* __restrict__ cnt,
                                                        Splat* __restrict__ rec_sorted,
                                                        unsigned long long* __restrict__ depth_sorted,
+                                                       int32_t* __restrict__ rank_of,
                                                        uint32_t* __restrict__ emit_off, uint32_t* __restrict__ ticket,
                                                        unsigned long long* __restrict__ status, uint32_t epoch) {
     constexpr int PT = kPackItems * NT;
+    static_assert(kPackItems == 4, "one 16-byte load / store of ranks per thread");
     __shared__ uint32_t s_warp[NW];
     __shared__ uint32_t s_tile, s_before;
     const int tid = threadIdx.x;
@@ -265,42 +326,61 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
-        uint32_t loc[kPackItems], nt[kPackItems];
-        uint32_t carry = 0u;
+        // blocked: thread t owns ranks r0 .. r0 + 3 (one 16-byte load of the sorted map indices);
+        // the four record gathers are independent and in flight together
+        const uint32_t r0 = tile * PT + kPackItems * tid;
+        int g[kPackItems];
+        if (r0 + kPackItems <= nv) {
+            const int4 q = *reinterpret_cast<const int4*>(gid_sorted + r0);
+            g[0] = q.x; g[1] = q.y; g[2] = q.z; g[3] = q.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < kPackItems; ++i) g[i] = r0 + i < nv ? gid_sorted[r0 + i] : -1;
+        }
+        uint32_t nt[kPackItems];
+        uint32_t mine = 0u;
 #pragma unroll
         for (int i = 0; i < kPackItems; ++i) {
-            const uint32_t r = tile * PT + i * NT + tid;
             nt[i] = 0u;
-            if (r < nv) {
-                const int g = gid_sorted[r];
-                const Splat s = rec_by_gid[g];
-                rec_sorted[r] = s;
-                depth_sorted[r] = depth_by_gid[g];
-                nt[i] = s.ntiles;
+            if (g[i] >= 0) {
+                const Splat sp = rec_by_gid[g[i]];
+                rec_sorted[r0 + i] = sp;
+                depth_sorted[r0 + i] = depth_by_gid[g[i]];
+                rank_of[g[i]] = static_cast<int32_t>(r0 + i);
+                nt[i] = sp.ntiles;
             }
-            uint32_t tot;
-            loc[i] = carry + block_excl_scan(nt[i], s_warp, &tot);
-            carry += tot;
+            mine += nt[i];
         }
-        if (tid == 0) s_before = look_back(status, tile, 1, epoch, carry);
+        uint32_t carry;
+        const uint32_t loc = block_excl_scan(mine, s_warp, &carry);
+        if (tid < 32) {
+            const uint32_t b = look_back_warp(status, tile, epoch, carry);  // (carry is CTA-uniform)
+            if (tid == 0) s_before = b;
+        }
         __syncthreads();
-        const uint32_t before = s_before;
+        uint32_t o[kPackItems + 1];
+        o[0] = s_before + loc;
 #pragma unroll
-        for (int i = 0; i < kPackItems; ++i) {
-            const uint32_t r = tile * PT + i * NT + tid;
-            if (r < nv) {
-                emit_off[r] = before + loc[i];
-                if (r == nv - 1) emit_off[nv] = before + loc[i] + nt[i];
-            }
+        for (int i = 0; i < kPackItems; ++i) o[i + 1] = o[i] + nt[i];
+        if (r0 + kPackItems <= nv) {
+            *reinterpret_cast<uint4*>(emit_off + r0) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kPackItems; ++i)
+                if (r0 + i < nv) emit_off[r0 + i] = o[i];
         }
+#pragma unroll
+        for (int i = 0; i < kPackItems; ++i)
+            if (r0 + i == nv - 1) emit_off[nv] = o[i + 1];
         __syncthreads();
     }
 }
 
 // ------------------------------------------------------------------------------------------
 // Duplicate-key emission (bin_tiles, rasterizer.cpp:76-91): a warp owns 32 consecutive depth
-// ranks, whose pairs are contiguous in the scan, and writes them rank by rank with all lanes
-// (row/column of the tile rect by a magic-number multiply). Keys are tile ids, values depth
+// ranks, whose pairs are contiguous in the scan, and writes them 32 pairs at a time, one per
+// lane (each lane finds its pair's rank by a shuffle search; row/column of the tile rect by a
+// magic-number multiply). Keys are tile ids, values depth
 // ranks, so the stable sort by tile yields each tile's list in (depth, index) order — the
 // reference's push_back order. Persistent grid; also builds the digit histograms of the tile
 // sort's passes (low `b0` bits, then the rest). Pairs beyond the capacity raise the overflow
@@ -324,30 +404,41 @@ __global__ void __launch_bounds__(NT) emit_pairs_kernel(const uint32_t* __restri
     const int warps = gridDim.x * NW;
     for (int grp = blockIdx.x * NW + (threadIdx.x >> 5); grp * 32 < n_vis; grp += warps) {
         const int r = grp * 32 + lane;
-        int off = 0, len = 0, tx0 = 0, ty0 = 0, ntx = 1;
-        uint32_t magic = 0;
+        // lane l: rank grp*32 + l's first pair (ranks past the count: past every pair), its
+        // tile-rect origin key, rect width and the reciprocal for row / column
+        uint32_t off = 0xffffffffu, magic = 0u;
+        int base_key = 0, ntx = 1;
         if (r < n_vis) {
-            off = static_cast<int>(emit_off[r]);
-            len = static_cast<int>(emit_off[r + 1]) - off;
+            off = emit_off[r];
             const Splat& s = rec[r];
-            tx0 = s.x0 >> 4;
-            ty0 = s.y0 >> 4;
+            const int tx0 = s.x0 >> 4, ty0 = s.y0 >> 4;
+            base_key = ty0 * tiles_x + tx0;
             ntx = (s.x1 >> 4) - tx0 + 1;
             magic = 0xffffffffu / static_cast<uint32_t>(ntx) + 1u;  // (wraps to 0 for ntx = 1: not used)
         }
+        const uint32_t beg = __shfl_sync(0xffffffffu, off, 0);
+        const uint32_t end = emit_off[min(grp * 32 + 32, n_vis)];
         const uint32_t rbase = static_cast<uint32_t>(grp * 32);
-        for (int i = 0; i < 32; ++i) {
-            const int c = __shfl_sync(0xffffffffu, len, i);
-            if (c == 0) continue;
-            const int o = __shfl_sync(0xffffffffu, off, i);
-            const int base_key = __shfl_sync(0xffffffffu, ty0 * tiles_x + tx0, i);
-            const int nx = __shfl_sync(0xffffffffu, ntx, i);
-            const uint32_t mg = __shfl_sync(0xffffffffu, magic, i);
-            for (int l = lane; l < c; l += 32) {
-                const int row = nx == 1 ? l : static_cast<int>(__umulhi(static_cast<uint32_t>(l), mg));
-                const uint32_t k = static_cast<uint32_t>(base_key + row * tiles_x + (l - row * nx));
-                keys[o + l] = static_cast<KeyT>(k);
-                vals[o + l] = rbase + i;
+        // the group's pairs are contiguous: lane l writes pair base + l (coalesced) and finds its
+        // rank as the largest l' with off_l' <= pair (offsets non-decreasing: 5 shuffle steps)
+        for (uint32_t base = beg; base < end; base += 32) {
+            const uint32_t e = base + lane;
+            int rl = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t oc = __shfl_sync(0xffffffffu, off, rl + step);
+                if (oc <= e) rl += step;
+            }
+            const uint32_t o = __shfl_sync(0xffffffffu, off, rl);
+            const int bk = __shfl_sync(0xffffffffu, base_key, rl);
+            const int nx = __shfl_sync(0xffffffffu, ntx, rl);
+            const uint32_t mg = __shfl_sync(0xffffffffu, magic, rl);
+            if (e < end) {
+                const uint32_t l = e - o;
+                const uint32_t row = nx == 1 ? l : __umulhi(l, mg);
+                const uint32_t k = static_cast<uint32_t>(bk) + row * static_cast<uint32_t>(tiles_x) + (l - row * nx);
+                keys[e] = static_cast<KeyT>(k);
+                vals[e] = rbase + rl;
                 atomicAdd(&s_hist[0][k & m0], 1u);
                 if (passes > 1) atomicAdd(&s_hist[1][k >> b0], 1u);
             }
@@ -414,26 +505,28 @@ void launch_depth_sort(uint32_t* keys_a, uint32_t* keys_b, int32_t* vis_gid, int
     const unsigned long long* nvis = cnt + kCntVisible;
     radix_hist_kernel<<<persistent_grid(div_up(max_n, NT * 8), 2), NT, 0, st>>>(keys_a, nvis, cap, 3, sb->hist[0]);
     const int grid = persistent_grid(div_up(max_n, TILE), 4);
-    // (keys_a, vis_gid) -> (keys_b, gid_sorted) -> (keys_a, gid_tmp) -> (keys_b, gid_sorted); vis_gid
-    // (K1's append order) is kept for K8b
+    // (keys_a, vis_gid) -> (keys_b, gid_tmp) -> (keys_a, gid_sorted) -> (keys_b, gid_tmp) -> exact tie
+    // order into gid_sorted; vis_gid (K1's append order) is kept for K8
     onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_a, reinterpret_cast<const uint32_t*>(vis_gid), keys_b,
-                                                         reinterpret_cast<uint32_t*>(gid_sorted), nvis, cap, 0, 8,
+                                                         reinterpret_cast<uint32_t*>(gid_tmp), nvis, cap, 0, 8,
                                                          sb->hist[0], &sb->ticket[0], status, epoch);
-    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_b, reinterpret_cast<const uint32_t*>(gid_sorted), keys_a,
-                                                         reinterpret_cast<uint32_t*>(gid_tmp), nvis, cap, 8, 8,
+    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_b, reinterpret_cast<const uint32_t*>(gid_tmp), keys_a,
+                                                         reinterpret_cast<uint32_t*>(gid_sorted), nvis, cap, 8, 8,
                                                          sb->hist[1], &sb->ticket[1], status, epoch + 1);
-    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_a, reinterpret_cast<const uint32_t*>(gid_tmp), keys_b,
-                                                         reinterpret_cast<uint32_t*>(gid_sorted), nvis, cap, 16, 8,
+    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_a, reinterpret_cast<const uint32_t*>(gid_sorted), keys_b,
+                                                         reinterpret_cast<uint32_t*>(gid_tmp), nvis, cap, 16, 8,
                                                          sb->hist[2], &sb->ticket[2], status, epoch + 2);
-    fix_ties_kernel<<<persistent_grid(div_up(max_n, NT), 4), NT, 0, st>>>(keys_b, gid_sorted, depth_by_gid, cnt);
+    fix_ties_kernel<<<persistent_grid(div_up(max_n, NT), 4), NT, 0, st>>>(keys_b, gid_tmp, depth_by_gid, cnt,
+                                                                          gid_sorted);
 }
 
 void launch_pack_scan(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
                       const unsigned long long* cnt, int max_n, Splat* rec_sorted, unsigned long long* depth_sorted,
+                      int32_t* rank_of,
                       uint32_t* emit_off, SortBlock* sb, unsigned long long* status, uint32_t epoch, cudaStream_t st) {
     if (max_n <= 0) return;
     pack_scan_kernel<<<persistent_grid(div_up(max_n, kPackItems * NT), 4), NT, 0, st>>>(
-        gid_sorted, rec_by_gid, depth_by_gid, cnt, rec_sorted, depth_sorted, emit_off, &sb->ticket[3], status, epoch);
+        gid_sorted, rec_by_gid, depth_by_gid, cnt, rec_sorted, depth_sorted, rank_of, emit_off, &sb->ticket[3], status, epoch);
 }
 
 template <typename KeyT>

@@ -30,6 +30,7 @@ void launch_depth_sort(uint32_t* keys_a, uint32_t* keys_b, int32_t* vis_gid, int
 // rank-ordered records + exclusive scan of their tile counts (emit_off[0 .. n_vis])
 void launch_pack_scan(const int32_t* gid_sorted, const Splat* rec_by_gid, const unsigned long long* depth_by_gid,
                       const unsigned long long* cnt, int max_n, Splat* rec_sorted, unsigned long long* depth_sorted,
+                      int32_t* rank_of /* [map size]: depth rank of each visible map index */,
                       uint32_t* emit_off, SortBlock* sb, unsigned long long* status, uint32_t epoch, cudaStream_t st);
 
 // emission of the (tile, rank) pairs + stable sort by tile + ranges; the sorted ranks land in

@@ -17,6 +17,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgsmap_b200.so")
+# diagnostics only (diag/build_variant.sh): time an experimental build of the same sources
+if os.environ.get("GSMAP_B200_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(_HERE), "diag", "_variants", os.environ["GSMAP_B200_VARIANT"],
+                            "libgsmap_b200.so")
 
 GAUSS_DTYPE = np.dtype([("p", "<f8", (59,)), ("degree", "<i4"), ("pad", "<i4")])
 

@@ -173,3 +173,27 @@ def test_non_multiple_of_tile_image():
     om, gm = pair(random_scene(5, 180, cam, pose))
     oo, go = check_keys(om, gm, pose, cam)
     assert check_images(oo, go) == 0
+
+
+@pytest.mark.parametrize("sizes", [(1, 2, 3, 5, 16), (17, 40), (2,) * 30])
+def test_depth_ties_ordered_exactly(sizes):
+    """Runs of equal depth keys (rasterizer.cpp:69-72: ties by map index; fp64 depths that differ
+    below the key's resolution) — the register-network runs (<= 16) and the insertion fallback."""
+    cam = O.camera(60, 60, 31.5, 31.5, 64, 64)
+    pose = O.pose(1.0, 1e-7, 0.0, 0.0)  # a tiny tilt: same 24-bit key, distinct fp64 depths
+    g = random_scene(11, sum(sizes), cam, pose)
+    gen = np.random.default_rng(len(sizes))
+    k = 0
+    for j, m in enumerate(sizes):
+        z = 1.0 + 0.37 * j
+        for a in range(m):
+            if a % 3 == 2:
+                g["p"][k, :3] = g["p"][k - 1, :3]  # an exact duplicate depth: ordered by index
+            else:
+                g["p"][k, :2] = gen.uniform(-0.4, 0.4, 2) * z
+                g["p"][k, 2] = z
+            k += 1
+    g = g[gen.permutation(len(g))]
+    om, gm = pair(g)
+    oo, go = check_keys(om, gm, pose, cam)
+    assert check_images(oo, go) == 0
