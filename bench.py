@@ -380,7 +380,9 @@ def run_ours(args, rank, world):
     # measured DRAM bytes per launch of the same kernel (ncu dram__bytes_read + _write, one
     # capture per pyramid level, averaged like `achieved`), committed under profiles/
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r1_traffic.json")
     if os.path.exists(tpath):
         tk = json.load(open(tpath)).get("kernels", {}).get(dom)
         traffic = tk.get("dram_bytes_per_launch") if tk else None
@@ -393,6 +395,26 @@ def run_ours(args, rank, world):
                            else "gs_microbench on this device (FP32 FMA / MUFU.EX2 issue rate)")
     roof["model"] = "SURVEY §8d algorithmic bytes/flops per launch, averaged over the 3 pyramid levels"
     result["roofline"] = roof
+    # SURVEY §8d step-level figure: sum over the step's kernels of t_roof = max(bytes / HBM,
+    # flop / FP32, ex2 / MUFU) against the measured step time
+    t_roof = sum(max(b_ / (hbm * 1e9), f_ / fp32.value, x_ / ex2.value) for b_, f_, x_ in alg.values())
+    result["step_roofline"] = {"sum_t_roof_ms": round(t_roof * 1e3, 4), "measured_ms": round(ms_max / args.steps, 4),
+                               "frac": round(t_roof * 1e3 / (ms_max / args.steps), 4),
+                               "model": "SURVEY §8d: per kernel t_roof = max(B / hbm_gbs, F / FP32 FFMA rate, "
+                                        "X / MUFU.EX2 rate), workload counters from the device, averaged over levels"}
+    # per-level step time = the level's kernel times from the profile pass (device time of that
+    # level's render + loss + backward + Adam); the interval between step reports is kept beside
+    # it (each interval also holds the next step's speculative render)
+    for lv, ks in per_level_kernels.items():
+        if lv in per_level:
+            kt = sum(ks.values())
+            per_level[lv]["interval_ms"] = per_level[lv]["ms_per_step"]
+            per_level[lv]["ms_per_step"] = round(kt, 4)
+            h_, w_ = shapes[int(lv[1:])]
+            per_level[lv]["mpix_per_s"] = round(h_ * w_ / (kt / 1e3) / 1e6, 2)
+    result["per_level_note"] = ("ms_per_step: the level's kernel times (profile pass, CUDA events on the context "
+                                "stream); interval_ms: time between consecutive step reports in the timed region, "
+                                "which also holds the next step's speculative render")
     result["kernels"] = kernels
     result["per_level_kernel_ms"] = per_level_kernels
     result["workload_counters"] = {f"L{l}": dict(zip(["n_visible", "pairs", "pixels", "contribs", "tiles"], v))

@@ -186,9 +186,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
             const float2 m = sb.mean[k];
             const float4 cn = sb.con[k];
             const float4 col = sb.col[k];
-            float2 acc[kNumPartials];
-#pragma unroll
-            for (int c = 0; c < kNumPartials; ++c) acc[c] = f2(0.f);
+            float2 acc[kNumPartials];  // the first pixel pair initialises (no additions of 0)
             bool any = false;
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
@@ -212,23 +210,36 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
                 B[q] = __ffma2_rn(w, A, B[q]);
                 // an inactive half has al = 0 -> om = 1 -> rcp.approx(1) = 1 exactly -> ti = T
                 T[q] = ti;
-                acc[0] = __ffma2_rn(w, g0[q], acc[0]);
-                acc[1] = __ffma2_rn(w, g1[q], acc[1]);
-                acc[2] = __ffma2_rn(w, g2[q], acc[2]);
-                acc[3] = __ffma2_rn(w, gz[q], acc[3]);
                 // rasterizer.cpp:297: the clamp is flat -> no opacity / mean / covariance terms
                 const float2 gdr = __fmul2_rn(e.g, dalpha);
                 const float2 gd = make_float2(a0 && e.a_raw.x < kAlphaMaxF ? gdr.x : 0.f,
                                               a1 && e.a_raw.y < kAlphaMaxF ? gdr.y : 0.f);
-                acc[4] = __fadd2_rn(acc[4], gd);
                 // mean / covariance terms without the opacity (K8 applies op and op / 2)
                 const float2 h0 = __fmul2_rn(gd, e.u0);
                 const float2 h1 = __fmul2_rn(gd, e.u1);
-                acc[5] = __fadd2_rn(acc[5], h0);
-                acc[6] = __fadd2_rn(acc[6], h1);
-                acc[7] = __ffma2_rn(h0, e.u0, acc[7]);
-                acc[8] = __ffma2_rn(h0, e.u1, acc[8]);
-                acc[9] = __ffma2_rn(h1, e.u1, acc[9]);
+                if (q == 0) {
+                    acc[0] = __fmul2_rn(w, g0[q]);
+                    acc[1] = __fmul2_rn(w, g1[q]);
+                    acc[2] = __fmul2_rn(w, g2[q]);
+                    acc[3] = __fmul2_rn(w, gz[q]);
+                    acc[4] = gd;
+                    acc[5] = h0;
+                    acc[6] = h1;
+                    acc[7] = __fmul2_rn(h0, e.u0);
+                    acc[8] = __fmul2_rn(h0, e.u1);
+                    acc[9] = __fmul2_rn(h1, e.u1);
+                } else {
+                    acc[0] = __ffma2_rn(w, g0[q], acc[0]);
+                    acc[1] = __ffma2_rn(w, g1[q], acc[1]);
+                    acc[2] = __ffma2_rn(w, g2[q], acc[2]);
+                    acc[3] = __ffma2_rn(w, gz[q], acc[3]);
+                    acc[4] = __fadd2_rn(acc[4], gd);
+                    acc[5] = __fadd2_rn(acc[5], h0);
+                    acc[6] = __fadd2_rn(acc[6], h1);
+                    acc[7] = __ffma2_rn(h0, e.u0, acc[7]);
+                    acc[8] = __ffma2_rn(h0, e.u1, acc[8]);
+                    acc[9] = __ffma2_rn(h1, e.u1, acc[9]);
+                }
             }
             if (!__any_sync(0xffffffffu, any)) continue;
 #pragma unroll

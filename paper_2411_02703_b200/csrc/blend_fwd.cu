@@ -1,7 +1,8 @@
 // K5: front-to-back blend (rasterizer.cpp:118-162). Box test = integer pixel rect; alpha clamped
 // at 0.99; the contributor is accumulated BEFORE the T < 1e-4 break; V = sum of weights. Per
-// pixel it keeps n_proc (list position + 1 of the last contributor) and T_final for the
-// backward instead of the reference's CSR table (rasterizer.cpp:164-197).
+// pixel it keeps n_proc (list position + 1 of the terminating contributor, the list length when
+// the pixel never terminates) and T_final for the backward instead of the reference's CSR table
+// (rasterizer.cpp:164-197).
 //
 // Exact termination with fp32 arithmetic: the transmittance is carried in fp32 together with a
 // rigorous bound on its distance from the reference's fp64 product. Each fp32 factor
@@ -16,7 +17,7 @@
 
 // build knobs (diag/build_variant.sh experiments; the defaults are the product build)
 #ifndef GSB_FWD_MIN_BLOCKS
-#define GSB_FWD_MIN_BLOCKS 1
+#define GSB_FWD_MIN_BLOCKS 6  // 80 registers, 6 CTAs per SM: -13% at full resolution (diag/variant_levels.sh)
 #endif
 #ifdef GSB_NEAR_NOINLINE
 #define GSB_NEAR_INLINE __noinline__
@@ -110,8 +111,12 @@ __device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigne
         if (!((near >> p) & 1u)) continue;
         atomicAdd(&g_blend_stats[0], 1ull);
         const double t = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x;
-        if (t / (1.0 - beta) < kTMin) s.live &= ~(1u << p);  // T64 <= T32 / (1 - beta) < 1e-4
-        else if (!(t / (1.0 + beta) >= kTMin)) amb |= 1u << p;  // else T64 >= T32 / (1 + beta) >= 1e-4
+        if (t / (1.0 - beta) < kTMin) {  // T64 <= T32 / (1 - beta) < 1e-4
+            s.live &= ~(1u << p);
+            s.nproc[p] = pos + 1;
+        } else if (!(t / (1.0 + beta) >= kTMin)) {
+            amb |= 1u << p;  // else T64 >= T32 / (1 + beta) >= 1e-4
+        }
     }
     unsigned need = __ballot_sync(0xffffffffu, amb != 0u);
     while (need) {
@@ -129,7 +134,12 @@ __device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigne
             double T = warp_replay(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
             if (fabs(T / kTMin - 1.0) <= 2.5 * (pos + 1) * 1.1102230246251565e-16 && (threadIdx.x & 31) == src)
                 T = replay_transmittance(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
-            if ((threadIdx.x & 31) == src && T < kTMin) s.live &= ~(1u << p);
+            if ((threadIdx.x & 31) == src && T < kTMin) {
+                s.live &= ~(1u << p);
+#pragma unroll
+                for (int q = 0; q < 2 * ((PPT + 1) / 2); ++q)  // (static indices: nproc stays in registers)
+                    if (q == p) s.nproc[q] = pos + 1;
+            }
         }
     }
 }
@@ -154,7 +164,10 @@ __device__ GSB_NEAR_INLINE void df_near(FwdState<(PPT + 1) / 2>& s, unsigned nea
             term = replay_transmittance(vals, rec, range, pos, sc.px, sc.py0 + p, ox, oy, fx,
                                         static_cast<float>(sc.ly0 + p)) < kTMin;
         }
-        if (term) s.live &= ~(1u << p);
+        if (term) {
+            s.live &= ~(1u << p);
+            s.nproc[p] = pos + 1;
+        }
     }
 }
 
@@ -208,13 +221,11 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             s.T[q] = __fadd2_rn(pr, t);
             s.Tl[q] = __fadd2_rn(t, neg2(__fadd2_rn(s.T[q], neg2(pr))));
         } else {
-            float2 f = __fadd2_rn(f2(1.f), neg2(al));
-            if (a0 && e.a_raw.x >= kAlphaMaxF) f.x = kClampFac;
-            if (a1 && e.a_raw.y >= kAlphaMaxF) f.y = kClampFac;
-            s.T[q] = __fmul2_rn(s.T[q], f);
+            // 1 - al, with a clamp (al = 0.99f, 1 - al = 0.0099999905f) replaced by 0.01f: every
+            // unclamped al < 0.99f gives 1 - al >= 0.0100000501f, so a max does it (inactive: 1)
+            const float2 f = __fadd2_rn(f2(1.f), neg2(al));
+            s.T[q] = __fmul2_rn(s.T[q], make_float2(fmaxf(f.x, kClampFac), fmaxf(f.y, kClampFac)));
         }
-        if (a0) s.nproc[p0] = pos + 1;
-        if (a1) s.nproc[p0 + 1] = pos + 1;
         if (STATS) {
             s.ncontrib[p0] += a0;
             s.ncontrib[p0 + 1] += a1;
@@ -341,9 +352,13 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_
         s.T[q] = f2(1.f);
         s.Tl[q] = s.c0[q] = s.c1[q] = s.c2[q] = s.dd[q] = s.vis[q] = f2(0.f);
     }
+    // n_proc: list position + 1 of the terminating contributor; a pixel that never terminates
+    // keeps the list length (its later entries do not contain it, so the backward's replay from
+    // there is the same)
 #pragma unroll
     for (int p = 0; p < 2 * NP; ++p) {
-        s.nproc[p] = s.ncontrib[p] = 0;
+        s.nproc[p] = static_cast<int>(range.y - range.x);
+        s.ncontrib[p] = 0;
         if (p < PPT && sc.px < v.width && sc.py0 + p < v.height) s.live |= 1u << p;
     }
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
@@ -377,7 +392,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_
 // boundaries and walked in three passes, so the latency-bound sequential walk is spread over
 // (tile, segment) CTAs. Exactness: every termination decision is taken either on a df32 product
 // certainly above 1e-4 or by the exact df32 walk of pass 3.
-constexpr int kSegFields = 9;  // Th, Tl, C_r, C_g, C_b, D, V, last contributor + 1, contributions
+constexpr int kSegFields = 9;  // Th, Tl, C_r, C_g, C_b, D, V, (unused), contributions
 
 template <int PPT>
 __device__ __forceinline__ void init_state(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, int width, int height) {
@@ -430,8 +445,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
         base[4 * P + o] = hi ? s.c2[q].y : s.c2[q].x;
         base[5 * P + o] = hi ? s.dd[q].y : s.dd[q].x;
         base[6 * P + o] = hi ? s.vis[q].y : s.vis[q].x;
-        base[7 * P + o] = __int_as_float(s.nproc[p]);
-        base[8 * P + o] = __int_as_float(s.ncontrib[p]);
+        base[8 * P + o] = __int_as_float(s.ncontrib[p]);  // (field 7 unused: n_proc comes from pass 3)
     }
 }
 
@@ -452,7 +466,9 @@ __global__ void fwd_seg_chain_kernel(const uint2* __restrict__ ranges, ViewParam
     const int n_list = static_cast<int>(range.y - range.x);
     const int L = seg_len(n_list, nseg);
     float th = 1.f, tl = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, dd = 0.f, vis = 0.f;
-    int nproc = 0, ncontrib = 0, star = -1;
+    // no termination before the stopping segment: n_proc = the list length unless pass 3 finds it
+    const int nproc = n_list;
+    int ncontrib = 0, star = -1;
     for (int s = 0; s < nseg && s * L < n_list; ++s) {
         if (s >= 1) {
             float* cp = ck + static_cast<size_t>(s - 1) * kCkFields * P;
@@ -481,8 +497,6 @@ __global__ void fwd_seg_chain_kernel(const uint2* __restrict__ ranges, ViewParam
         c2 = __fmaf_rn(th, sg[4 * P + o], c2);
         dd = __fmaf_rn(th, sg[5 * P + o], dd);
         vis = __fmaf_rn(th, sg[6 * P + o], vis);
-        const int last = __float_as_int(sg[7 * P + o]);
-        if (last) nproc = last;
         ncontrib += __float_as_int(sg[8 * P + o]);
         th = nh;
         tl = nl;
