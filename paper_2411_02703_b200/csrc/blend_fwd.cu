@@ -95,6 +95,13 @@ struct FwdState {
     float2 T[NP], Tl[NP], c0[NP], c1[NP], c2[NP], dd[NP], vis[NP];  // Tl: df32 low part (DF mode)
     int nproc[2 * NP], ncontrib[2 * NP];
     unsigned live;
+    // pixel p stops after the entry at list position pos
+    __device__ __forceinline__ void stop(int p, int pos) {
+        live &= ~(1u << p);
+#pragma unroll
+        for (int q = 0; q < 2 * NP; ++q)  // static indices: the arrays stay in registers
+            if (q == p) nproc[q] = pos + 1;
+    }
 };
 
 // Pixels whose fp32 transmittance fell below t_near after the entry at `pos` (bits in `near`):
@@ -112,8 +119,7 @@ __device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigne
         atomicAdd(&g_blend_stats[0], 1ull);
         const double t = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x;
         if (t / (1.0 - beta) < kTMin) {  // T64 <= T32 / (1 - beta) < 1e-4
-            s.live &= ~(1u << p);
-            s.nproc[p] = pos + 1;
+            s.stop(p, pos);
         } else if (!(t / (1.0 + beta) >= kTMin)) {
             amb |= 1u << p;  // else T64 >= T32 / (1 + beta) >= 1e-4
         }
@@ -134,12 +140,7 @@ __device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigne
             double T = warp_replay(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
             if (fabs(T / kTMin - 1.0) <= 2.5 * (pos + 1) * 1.1102230246251565e-16 && (threadIdx.x & 31) == src)
                 T = replay_transmittance(vals, rec, range, pos, px, py0 + p, ox, oy, sfx, fy);
-            if ((threadIdx.x & 31) == src && T < kTMin) {
-                s.live &= ~(1u << p);
-#pragma unroll
-                for (int q = 0; q < 2 * ((PPT + 1) / 2); ++q)  // (static indices: nproc stays in registers)
-                    if (q == p) s.nproc[q] = pos + 1;
-            }
+            if ((threadIdx.x & 31) == src && T < kTMin) s.stop(p, pos);
         }
     }
 }
@@ -164,10 +165,7 @@ __device__ GSB_NEAR_INLINE void df_near(FwdState<(PPT + 1) / 2>& s, unsigned nea
             term = replay_transmittance(vals, rec, range, pos, sc.px, sc.py0 + p, ox, oy, fx,
                                         static_cast<float>(sc.ly0 + p)) < kTMin;
         }
-        if (term) {
-            s.live &= ~(1u << p);
-            s.nproc[p] = pos + 1;
-        }
+        if (term) s.stop(p, pos);
     }
 }
 
@@ -189,11 +187,14 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
                                           uint2 range, double ox, double oy) {
     constexpr int NP = (PPT + 1) / 2;
     const bool colin = COVER || (sc.px >= rc.x && sc.px <= rc.z);
-    unsigned near = 0;
+    // pixels whose fp32 transmittance fell below t_near at this entry: kept as predicates, the
+    // bitmask is built only on the (rare) slow path
+    bool nb[2 * NP];
+    bool anyn = false;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const int p0 = 2 * q, y0 = sc.py0 + p0;
-        bool a0 = (s.live >> p0) & 1u, a1 = (s.live >> (p0 + 1)) & 1u;
+        bool a0 = (s.live & (1u << p0)) != 0u, a1 = (s.live & (2u << p0)) != 0u;
         if (!COVER) {
             a0 = a0 && colin && y0 >= rc.y && y0 <= rc.w;
             a1 = a1 && colin && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
@@ -230,20 +231,29 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             s.ncontrib[p0] += a0;
             s.ncontrib[p0 + 1] += a1;
         }
-        near |= (static_cast<unsigned>(a0 && s.T[q].x < t_near) << p0) |
-                (static_cast<unsigned>(a1 && s.T[q].y < t_near) << (p0 + 1));
+        nb[p0] = a0 && s.T[q].x < t_near;
+        nb[p0 + 1] = a1 && s.T[q].y < t_near;
+        anyn = anyn || nb[p0] || nb[p0 + 1];
     }
     if (MODE == kDf) {
-        if (near) df_near<PPT>(s, near, sc, pos, fx, vals, rec, range, ox, oy);
+        if (anyn) {
+            unsigned near = 0;
+#pragma unroll
+            for (int p = 0; p < 2 * NP; ++p) near |= static_cast<unsigned>(nb[p]) << p;
+            df_near<PPT>(s, near, sc, pos, fx, vals, rec, range, ox, oy);
+        }
     } else if (MODE == kLocal) {
 #pragma unroll
         for (int p = 0; p < 2 * NP; ++p) {
-            if (!((near >> p) & 1u)) continue;
+            if (!nb[p]) continue;
             const float th = (p & 1) ? s.T[p >> 1].y : s.T[p >> 1].x, tl = (p & 1) ? s.Tl[p >> 1].y : s.Tl[p >> 1].x;
             const float d = __fadd_rn(th, -kTMinHi) + __fadd_rn(tl, -kTMinLo);
-            if (d < -1e-4f * 5.7e-14f * static_cast<float>(pos + 16)) s.live &= ~(1u << p);  // certainly below
+            if (d < -1e-4f * 5.7e-14f * static_cast<float>(pos + 16)) s.stop(p, pos);  // certainly below
         }
-    } else if (__any_sync(0xffffffffu, near != 0u)) {
+    } else if (__any_sync(0xffffffffu, anyn)) {
+        unsigned near = 0;
+#pragma unroll
+        for (int p = 0; p < 2 * NP; ++p) near |= static_cast<unsigned>(nb[p]) << p;
         resolve_near<PPT>(s, near, sc, pos, kw, fx, vals, rec, range, ox, oy);
     }
 }
