@@ -197,6 +197,11 @@ int gs_render(gs_map* map, const gs_pose* pose, const gs_camera* cam, gs_frame* 
 int gs_frame_stats_get(gs_frame* frame, gs_frame_stats* out);
 /* RenderOutput color/depth/visibility as host fp64 HWC (any pointer may be NULL) */
 int gs_frame_read(gs_frame* frame, double* color, double* depth, double* visibility);
+/* a RenderOutput from host images (compute_loss takes any rendered images, mapper.hpp:61-62):
+   fp64 HWC color / depth / visibility; the frame has no contributor lists, so
+   gs_render_backward on it returns GS_ELOGIC (the reference's inconsistent-CSR error) */
+int gs_frame_set_images(gs_frame* frame, const double* color, const double* depth, const double* visibility,
+                        int32_t h, int32_t w);
 /* device planes: color [3][H][W], depth [H][W], visibility [H][W] (fp32) */
 int gs_frame_device_images(gs_frame* frame, float** color, float** depth, float** visibility);
 /* per-pixel list length and final transmittance (H*W each) */

@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstddef>
 #include <type_traits>
 
@@ -171,6 +172,13 @@ public:
     Matrix(const ArrayVal<R, C>& a);
 
     static Matrix Zero() { return Constant(0.0); }
+    // Eigen 3.4 internal::random<double>() = -1 + 2 * rand() / RAND_MAX (random_default_impl),
+    // coefficients in storage order (the reference's unit tests draw scenes with it)
+    static Matrix Random() {
+        Matrix m;
+        for (int i = 0; i < R * C; ++i) m.m_d[i] = -1.0 + 2.0 * static_cast<double>(std::rand()) / RAND_MAX;
+        return m;
+    }
     static Matrix Constant(double v) {
         Matrix m;
         for (int i = 0; i < R * C; ++i) m.m_d[i] = v;
@@ -569,6 +577,15 @@ public:
         m_c = Vector4d(s * aa.axis()(0), s * aa.axis()(1), s * aa.axis()(2), std::cos(ha));
     }
     static Quaternion Identity() { return Quaternion(1.0, 0.0, 0.0, 0.0); }
+    // Eigen 3.4 Quaternion::UnitRandom (Geometry/Quaternion.h): u1 in [0, 1], u2, u3 in [0, 2 pi]
+    // from internal::random<double>(lo, hi) = lo + (hi - lo) * rand() / RAND_MAX
+    static Quaternion UnitRandom() {
+        const double u1 = 0.0 + (1.0 - 0.0) * static_cast<double>(std::rand()) / RAND_MAX;
+        const double u2 = 0.0 + (2 * 3.14159265358979323846 - 0.0) * static_cast<double>(std::rand()) / RAND_MAX;
+        const double u3 = 0.0 + (2 * 3.14159265358979323846 - 0.0) * static_cast<double>(std::rand()) / RAND_MAX;
+        const double a = std::sqrt(1.0 - u1), b = std::sqrt(u1);
+        return Quaternion(a * std::sin(u2), a * std::cos(u2), b * std::sin(u3), b * std::cos(u3));
+    }
 
     double& x() { return m_c[0]; }
     double& y() { return m_c[1]; }

@@ -1067,6 +1067,45 @@ int gs_frame_stats_get(gs_frame* F, gs_frame_stats* out) {
     });
 }
 
+// A RenderOutput that did not come from a device render (compute_loss takes any images,
+// mapper.hpp:61-62): host fp64 HWC images into the frame's planes. The frame then has images
+// but no contributor lists, so render_backward on it fails like the reference's CSR check.
+int gs_frame_set_images(gs_frame* F, const double* color, const double* depth, const double* vis, int32_t h,
+                        int32_t w) {
+    return guard([&] {
+        if (h <= 0 || w <= 0) fail(GS_EINVAL, "frame_set_images: image size must be positive");
+        if (!color || !depth || !vis) fail(GS_EINVAL, "frame_set_images: null image");
+        F->ctx->use();
+        ViewParams v{};
+        v.width = w;
+        v.height = h;
+        v.tiles_x = div_up(w, kTile);
+        v.tiles_y = div_up(h, kTile);
+        frame_pixels(F, v);
+        const size_t P = static_cast<size_t>(h) * w;
+        cudaStream_t st = F->ctx->stream;
+        DevBuf tmp;
+        tmp.ensure(sizeof(double) * 5 * P);
+        ck(cudaMemcpyAsync(tmp.p, color, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(tmp.as<double>() + 3 * P, depth, sizeof(double) * P, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(tmp.as<double>() + 4 * P, vis, sizeof(double) * P, cudaMemcpyHostToDevice, st), "h2d");
+        launch_from_hwc_double(tmp.as<double>(), h, w, 3, F->color.as<float>(), st);
+        launch_from_hwc_double(tmp.as<double>() + 3 * P, h, w, 1, F->depth.as<float>(), st);
+        launch_from_hwc_double(tmp.as<double>() + 4 * P, h, w, 1, F->vis.as<float>(), st);
+        F->ctx->launched(3);
+        ck(cudaStreamSynchronize(st), "sync");
+        tmp.release();
+        F->view = v;
+        F->rendered = true;
+        F->has_cotangent = false;
+        F->has_contrib = false;
+        F->map_n = -1;  // no lists: render_backward refuses this frame
+        F->n_vis = F->n_pairs = 0;
+        F->counts_known = true;
+        F->overflow = false;
+    });
+}
+
 int gs_frame_read(gs_frame* F, double* color, double* depth, double* vis) {
     return guard([&] {
         need_rendered(F);
