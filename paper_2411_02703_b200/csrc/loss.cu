@@ -441,27 +441,43 @@ LossLayout launch_eval(const float* color, const float* depth, const float* gt_c
     return L;
 }
 
-// Sums every field's block slots in a fixed order (thread t takes slots t, t + 256, ... in turn,
-// then a fixed tree over the threads) into the LossScalars header; then depth_scale.
-__global__ void __launch_bounds__(256) loss_finalize_kernel(LossScalars* acc, LossLayout L, double lambda_d) {
-    __shared__ double scratch[8];
-    __shared__ double tot[kLossFields];
+// Sums every field's block slots in a fixed order (thread t takes slots t, t + T, ... in turn,
+// the five fields' loads of one slot index issued together; then a fixed tree over the lanes and
+// a fixed sum over the warps) into the LossScalars header; then depth_scale. One block of 1024
+// threads: ~4 dependent round trips at full resolution instead of ~75.
+constexpr int kFinalizeThreads = 1024;
+
+__global__ void __launch_bounds__(kFinalizeThreads) loss_finalize_kernel(LossScalars* acc, LossLayout L,
+                                                                          double lambda_d) {
+    __shared__ double scratch[kLossFields][kFinalizeThreads / 32];
     const double* slots = slot_base(acc);
+    int nmax = 0;
+#pragma unroll
+    for (int f = 0; f < kLossFields; ++f) nmax = max(nmax, L.n[f]);
+    double s[kLossFields];
+#pragma unroll
+    for (int f = 0; f < kLossFields; ++f) s[f] = 0.0;
+    for (int b = threadIdx.x; b < nmax; b += kFinalizeThreads) {
+        double v[kLossFields];
+#pragma unroll
+        for (int f = 0; f < kLossFields; ++f) v[f] = b < L.n[f] ? slots[f * L.stride + b] : 0.0;
+#pragma unroll
+        for (int f = 0; f < kLossFields; ++f) s[f] += v[f];
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
     for (int f = 0; f < kLossFields; ++f) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < L.n[f]; b += blockDim.x) s += slots[f * L.stride + b];
-        s = warp_sum(s);
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (lane == 0) scratch[warp] = s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        const double t = warp_sum(s[f]);
+        if (lane == 0) scratch[f][warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot[kLossFields];
+        for (int f = 0; f < kLossFields; ++f) {
             double t = 0.0;
-            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += scratch[w];
+            for (int w = 0; w < kFinalizeThreads / 32; ++w) t += scratch[f][w];
             tot[f] = t;
         }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
         acc->l1_sum = tot[kLossL1];
         acc->sq_sum = tot[kLossSq];
         acc->ssim_sum = tot[kLossSsim];
@@ -473,7 +489,7 @@ __global__ void __launch_bounds__(256) loss_finalize_kernel(LossScalars* acc, Lo
 }
 
 void launch_loss_finalize(LossScalars* acc, const LossLayout& L, double lambda_d, cudaStream_t st) {
-    loss_finalize_kernel<<<1, 256, 0, st>>>(acc, L, lambda_d);
+    loss_finalize_kernel<<<1, kFinalizeThreads, 0, st>>>(acc, L, lambda_d);
 }
 
 // ---------------------------------------------------------------------------------- pyramid

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
     static_assert(kPackItems == 4, "one 16-byte load / store of ranks per thread");
     __shared__ uint32_t s_warp[NW];
     __shared__ uint32_t s_tile, s_before;
+    __shared__ uint32_t s_nt[NW][32 * kPackItems];  // tile counts of each warp's records
     const int tid = threadIdx.x;
     const uint32_t nv = static_cast<uint32_t>(cnt[kCntVisible]);
     const uint32_t ntiles = (nv + PT - 1) / PT;
@@ -326,8 +327,7 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
-        // blocked: thread t owns ranks r0 .. r0 + 3 (one 16-byte load of the sorted map indices);
-        // the four record gathers are independent and in flight together
+        // blocked: thread t owns ranks r0 .. r0 + 3 (one 16-byte load of the sorted map indices)
         const uint32_t r0 = tile * PT + kPackItems * tid;
         int g[kPackItems];
         if (r0 + kPackItems <= nv) {
@@ -337,17 +337,45 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
 #pragma unroll
             for (int i = 0; i < kPackItems; ++i) g[i] = r0 + i < nv ? gid_sorted[r0 + i] : -1;
         }
+        // the warp's 128 records are copied cooperatively: per instruction 8 records, 4 lanes per
+        // record (16 bytes each) -> each 64-byte record read whole and 512 contiguous bytes written
+        // (a per-thread copy of its own 4 records scatters every store instruction over 32 rows)
+        {
+            const int lane = tid & 31;
+            const uint32_t wr0 = tile * PT + kPackItems * (tid & ~31);  // the warp's first rank
+            const int item = (lane >> 2) & 3, chunk = lane & 3;
+            uint4 buf[16];
+            int dst[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int owner = 2 * j + (lane >> 4);  // record k = 8 j + lane / 4 = 4 owner + item
+                int gi = __shfl_sync(0xffffffffu, g[0], owner);
+                const int g1 = __shfl_sync(0xffffffffu, g[1], owner);
+                const int g2 = __shfl_sync(0xffffffffu, g[2], owner);
+                const int g3 = __shfl_sync(0xffffffffu, g[3], owner);
+                gi = item == 1 ? g1 : item == 2 ? g2 : item == 3 ? g3 : gi;
+                dst[j] = gi;
+                if (gi >= 0) buf[j] = reinterpret_cast<const uint4*>(rec_by_gid + gi)[chunk];
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t k = 8 * j + (lane >> 2);
+                if (dst[j] >= 0) {
+                    reinterpret_cast<uint4*>(rec_sorted + wr0 + k)[chunk] = buf[j];
+                    if (chunk == 3) s_nt[tid >> 5][k] = buf[j].w;  // Splat::ntiles
+                }
+            }
+            __syncwarp();
+        }
         uint32_t nt[kPackItems];
         uint32_t mine = 0u;
 #pragma unroll
         for (int i = 0; i < kPackItems; ++i) {
             nt[i] = 0u;
             if (g[i] >= 0) {
-                const Splat sp = rec_by_gid[g[i]];
-                rec_sorted[r0 + i] = sp;
                 depth_sorted[r0 + i] = depth_by_gid[g[i]];
                 rank_of[g[i]] = static_cast<int32_t>(r0 + i);
-                nt[i] = sp.ntiles;
+                nt[i] = s_nt[tid >> 5][kPackItems * (tid & 31) + i];
             }
             mine += nt[i];
         }
