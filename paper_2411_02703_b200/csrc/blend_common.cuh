@@ -85,6 +85,9 @@ struct AlphaP {
     float2 u0, u1, g, a_raw, alpha;
 };
 
+// CLAMP = false: the entry's opacity is below 0.99f, so o * g (g <= 1) never reaches the clamp
+// and alpha = a_raw exactly (the blends pick the variant per entry, warp-uniformly)
+template <bool CLAMP = true>
 __device__ __forceinline__ AlphaP alpha_pair(float2 m, float4 cn, float fx, float2 fy) {
     const float dx = __fadd_rn(fx, -m.x);
     const float2 dy = __fadd2_rn(fy, f2(-m.y));
@@ -95,7 +98,7 @@ __device__ __forceinline__ AlphaP alpha_pair(float2 m, float4 cn, float fx, floa
     const float2 q = __ffma2_rn(dy, a.u1, __fmul2_rn(f2(dx), a.u0));
     a.g = make_float2(ex2(q.x), ex2(q.y));
     a.a_raw = __fmul2_rn(f2(cn.w), a.g);
-    a.alpha = make_float2(fminf(a.a_raw.x, kAlphaMaxF), fminf(a.a_raw.y, kAlphaMaxF));
+    a.alpha = CLAMP ? make_float2(fminf(a.a_raw.x, kAlphaMaxF), fminf(a.a_raw.y, kAlphaMaxF)) : a.a_raw;
     return a;
 }
 

@@ -180,7 +180,7 @@ enum FwdMode : int { kBand = 0, kDf = 1, kLocal = 2 };
 // One tile-list entry over the thread's pixels. COVER: the entry's rect contains every live
 // pixel of the warp (warp-uniform), so the per-pixel box test reduces to the live bits.
 // STATS: maintain n_contrib (only the public render reports it).
-template <int PPT, bool COVER, bool STATS, int MODE>
+template <int PPT, bool COVER, bool STATS, int MODE, bool CLAMP>
 __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, const int4& rc,
                                           float2 m, float4 cn, float4 col, int pos, int kw, float fx, float t_near,
                                           const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
@@ -201,7 +201,7 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
         }
         // no branch on (a0 || a1): an inactive half has al = 0 -> w = 0 and factor exactly 1
         const float fy = static_cast<float>(sc.ly0 + p0);
-        const AlphaP e = alpha_pair(m, cn, fx, make_float2(fy, fy + 1.f));
+        const AlphaP e = alpha_pair<CLAMP>(m, cn, fx, make_float2(fy, fy + 1.f));
         const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
         const float2 w = __fmul2_rn(al, s.T[q]);
         s.c0[q] = __ffma2_rn(w, f2(col.x), s.c0[q]);
@@ -213,8 +213,8 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             // exact factor 1 - alpha = fh + fl (Fast2Sum(1, -alpha)); clamp -> 1 - 0.99 (fp64)
             float2 fh = __fadd2_rn(f2(1.f), neg2(al));
             float2 fl = __fadd2_rn(neg2(al), neg2(__fadd2_rn(fh, f2(-1.f))));
-            if (a0 && e.a_raw.x >= kAlphaMaxF) { fh.x = kClampFacHi; fl.x = kClampFacLo; }
-            if (a1 && e.a_raw.y >= kAlphaMaxF) { fh.y = kClampFacHi; fl.y = kClampFacLo; }
+            if (CLAMP && a0 && e.a_raw.x >= kAlphaMaxF) { fh.x = kClampFacHi; fl.x = kClampFacLo; }
+            if (CLAMP && a1 && e.a_raw.y >= kAlphaMaxF) { fh.y = kClampFacHi; fl.y = kClampFacLo; }
             // (Th + Tl) * (fh + fl) with the exact product error of Th * fh
             const float2 pr = __fmul2_rn(s.T[q], fh);
             const float2 er = __ffma2_rn(s.T[q], fh, neg2(pr));
@@ -225,7 +225,7 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             // 1 - al, with a clamp (al = 0.99f, 1 - al = 0.0099999905f) replaced by 0.01f: every
             // unclamped al < 0.99f gives 1 - al >= 0.0100000501f, so a max does it (inactive: 1)
             const float2 f = __fadd2_rn(f2(1.f), neg2(al));
-            s.T[q] = __fmul2_rn(s.T[q], make_float2(fmaxf(f.x, kClampFac), fmaxf(f.y, kClampFac)));
+            s.T[q] = __fmul2_rn(s.T[q], CLAMP ? make_float2(fmaxf(f.x, kClampFac), fmaxf(f.y, kClampFac)) : f);
         }
         if (STATS) {
             s.ncontrib[p0] += a0;
@@ -326,12 +326,24 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
                 const int4 rc = sb.rect[j];
                 const int pos = static_cast<int>(base - full.x) + j;
                 ++kw;
-                if (rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w)
-                    fwd_entry<PPT, true, STATS, MODE>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx,
-                                                      t_near, vals, rec, full, ox, oy);
-                else
-                    fwd_entry<PPT, false, STATS, MODE>(s, sc, rc, sb.mean[j], sb.con[j], sb.col[j], pos, kw, fx,
-                                                       t_near, vals, rec, full, ox, oy);
+                const float4 cn = sb.con[j];
+                // warp-uniform variants: the rect covers every live pixel of the warp (no per-pixel
+                // box test); the opacity is below 0.99f (alpha can never clamp)
+                const bool cover = rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w;
+                if (cn.w < kAlphaMaxF) {
+                    if (cover)
+                        fwd_entry<PPT, true, STATS, MODE, false>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                                                                 t_near, vals, rec, full, ox, oy);
+                    else
+                        fwd_entry<PPT, false, STATS, MODE, false>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                                                                  t_near, vals, rec, full, ox, oy);
+                } else if (cover) {
+                    fwd_entry<PPT, true, STATS, MODE, true>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                                                            t_near, vals, rec, full, ox, oy);
+                } else {
+                    fwd_entry<PPT, false, STATS, MODE, true>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                                                             t_near, vals, rec, full, ox, oy);
+                }
             }
         }
     }

@@ -44,7 +44,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
 // prefix. Waits only on lower tiles, which were ticketed earlier by running CTAs. The walk reads
 // a window of kLookWin predecessors per round trip (independent loads in flight together), so
 // the chain of dependent L2 round trips is ~tile / kLookWin long instead of ~tile.
-constexpr int kLookWin = 8;
+#ifndef GSB_LOOKBACK_WIN
+#define GSB_LOOKBACK_WIN 8
+#endif
+constexpr int kLookWin = GSB_LOOKBACK_WIN;
 
 __device__ __forceinline__ uint32_t look_back(unsigned long long* status, uint32_t tile, int stride, uint32_t epoch,
                                               uint32_t value) {
