@@ -240,7 +240,8 @@ __device__ __forceinline__ void rotation_partial(const double u[4], int k, doubl
 // K1a: camera transform (exact fp64, as in K1b), near clip, and the off-screen test with a
 // conservative radius bound R >= the exact radius: lambda_max(Sigma_I) <= ||J||_F^2
 // max_k exp(2 ls_k) + 0.3 (W is a rotation). A Gaussian K1a culls is culled by the exact test
-// too, so the candidate list is a superset of the visible set. Candidates are appended with
+// too, so the candidate list is a superset of the visible set (the camera transform and near clip
+// in fp64 as K1b; the bound itself in fp32 with margins). Candidates are appended with
 // warp-aggregated atomics (their order does not matter: K1b writes by map index).
 __global__ void __launch_bounds__(256) cull_kernel(const float* __restrict__ params, int64_t cap, int n,
                                                    ViewParams v, int32_t* __restrict__ cand,
@@ -251,19 +252,22 @@ __global__ void __launch_bounds__(256) cull_kernel(const float* __restrict__ par
         const D3 pos{ldp(params, cap, P_POS, i), ldp(params, cap, P_POS + 1, i), ldp(params, cap, P_POS + 2, i)};
         D3 p = quat_rotate(v.qw, v.qx, v.qy, v.qz, pos);
         p = {p.x + v.tx, p.y + v.ty, p.z + v.tz};
-        if (!(p.z <= kNearClip)) {
-            const double mx = v.fx * p.x / p.z + v.cx;
-            const double my = v.fy * p.y / p.z + v.cy;
-            const double iz = 1.0 / p.z;
-            const double jf2 = (v.fx * iz) * (v.fx * iz) * (1.0 + (p.x * iz) * (p.x * iz)) +
-                               (v.fy * iz) * (v.fy * iz) * (1.0 + (p.y * iz) * (p.y * iz));
-            const double lsmax = fmax(fmax(ldp(params, cap, P_LS, i), ldp(params, cap, P_LS + 1, i)),
-                                      ldp(params, cap, P_LS + 2, i));
-            const double lam = (jf2 * exp(2.0 * lsmax) + kCovReg) * (1.0 + 1e-6);
-            const double R = ceil(3.0 * sqrt(lam)) + 1.0;
-            keep = !(mx + R < 0.0 || mx - R > static_cast<double>(v.width - 1) || my + R < 0.0 ||
-                     my - R > static_cast<double>(v.height - 1)) ||
-                   !(lam < 1e300);  // non-finite bound: leave the decision to the exact test
+        if (!(p.z <= kNearClip)) {  // the exact test's own near clip (same fp64 sequence)
+            // the rest in fp32 with margins that cover its rounding (relative ~1e-6 against the
+            // 1e-3 and 1e-4 |m| slack): the bound only has to stay conservative
+            const float px = static_cast<float>(p.x), py = static_cast<float>(p.y), pz = static_cast<float>(p.z);
+            const float fx = static_cast<float>(v.fx), fy = static_cast<float>(v.fy);
+            const float iz = 1.0f / pz;
+            const float ux = px * iz, uy = py * iz;
+            const float mx = fx * ux + static_cast<float>(v.cx), my = fy * uy + static_cast<float>(v.cy);
+            const float jf2 = (fx * iz) * (fx * iz) * (1.0f + ux * ux) + (fy * iz) * (fy * iz) * (1.0f + uy * uy);
+            const float lsmax = fmaxf(fmaxf(params[P_LS * cap + i], params[(P_LS + 1) * cap + i]),
+                                      params[(P_LS + 2) * cap + i]);
+            const float lam = (jf2 * __expf(2.0f * lsmax) + static_cast<float>(kCovReg)) * 1.001f;
+            const float R = ceilf(3.0f * sqrtf(lam)) + 2.0f + 1e-4f * (fabsf(mx) + fabsf(my));
+            keep = !(mx + R < 0.0f || mx - R > static_cast<float>(v.width - 1) || my + R < 0.0f ||
+                     my - R > static_cast<float>(v.height - 1)) ||
+                   !(lam < 1e30f);  // non-finite bound: leave the decision to the exact test
         }
     }
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
@@ -449,10 +453,22 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
     stamp[warp][lane] = -1;
     __syncwarp();
+    // the next pass's rows are loaded one pass ahead (their latency overlaps this pass's shuffles)
+    auto load_row = [&](uint32_t e, float2 r[kNumPartials / 2]) {
+        if (e < end) {
+            const float2* row = reinterpret_cast<const float2*>(partials + static_cast<size_t>(e) * kNumPartials);
+#pragma unroll
+            for (int k = 0; k < kNumPartials / 2; ++k) r[k] = __ldg(row + k);
+        }
+    };
+    float2 cur[kNumPartials / 2];
+    load_row(beg + lane, cur);
     int pass = 0;
     for (uint32_t base = beg; base < end; base += 32, ++pass) {
         const uint32_t e = base + lane;
         const bool valid = e < end;
+        float2 nxt[kNumPartials / 2];
+        load_row(e + 32, nxt);
         // rank (0..nr-1) of row e: largest l with off_l <= e (offsets are non-decreasing)
         int rl = 0;
 #pragma unroll
@@ -463,12 +479,10 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
         }
         float v[kNumPartials];
         if (valid) {
-            const float2* row = reinterpret_cast<const float2*>(partials + static_cast<size_t>(e) * kNumPartials);
 #pragma unroll
             for (int k = 0; k < kNumPartials / 2; ++k) {
-                const float2 t = __ldg(row + k);
-                v[2 * k] = t.x;
-                v[2 * k + 1] = t.y;
+                v[2 * k] = cur[k].x;
+                v[2 * k + 1] = cur[k].y;
             }
         } else {
 #pragma unroll
@@ -499,6 +513,8 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
             for (int k = 0; k < kNumPartials; ++k) acc[k] += static_cast<double>(seg[warp][lane][k]);
         }
         __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kNumPartials / 2; ++k) cur[k] = nxt[k];
     }
     if (lane >= nr) return;
     // stored as fp32 (half the round trip to K8b; the rounding, 2^-24 relative, is far below the
