@@ -125,10 +125,12 @@ struct Strip {
     static constexpr int kBH = 32 * PPT / kBW;
     static constexpr int kWarpsPerRow = kTile / kBW;
     int tx, ty, warp, lane, lx, ly0, px, py0, bx0, by0;
-    __device__ __forceinline__ Strip(int tiles_x) {
-        tx = blockIdx.x % tiles_x;
-        ty = blockIdx.x / tiles_x;
-        warp = threadIdx.x >> 5;
+    __device__ __forceinline__ Strip(int tiles_x) : Strip(tiles_x, blockIdx.x, threadIdx.x >> 5) {}
+    // tile `tile`, warp `w` of the tile's kThreads / 32 (a tile may be split over several CTAs)
+    __device__ __forceinline__ Strip(int tiles_x, int tile, int w) {
+        tx = tile % tiles_x;
+        ty = tile / tiles_x;
+        warp = w;
         lane = threadIdx.x & 31;
         const int wx = (warp % kWarpsPerRow) * kBW, wy = (warp / kWarpsPerRow) * kBH;
         lx = wx + lane % kBW;

@@ -282,12 +282,12 @@ __device__ __forceinline__ void write_checkpoint(const FwdState<(PPT + 1) / 2>& 
 // The walk over entries [start, end) of one tile's list `full` (staging batches of NT entries,
 // per-warp ballot against the live-pixel box, list order within the warp). Positions are
 // relative to the list start; checkpoints are written only by a whole-list walk (start = 0).
-template <int PPT, bool STATS, int MODE>
-__device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<kTileThreads / PPT>& sb,
+template <int PPT, bool STATS, int MODE, int NT = kTileThreads / PPT>
+__device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<NT>& sb,
                                            const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
                                            const Splat* __restrict__ rec, uint2 full, int start, int end, double ox,
                                            double oy, float fx, float* ck, int nseg, int width, int height) {
-    constexpr int NT = Strip<PPT>::kThreads;
+    // NT: threads of the CTA = the staging batch (a tile may be split over SUB CTAs)
     static_assert(kSegAlign % NT == 0, "segment boundaries must fall on staging batches");
     const int n_list = static_cast<int>(full.y - full.x);
     const int L = seg_len(n_list, nseg);
@@ -351,8 +351,11 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
     for (; next_ck < nseg && next_ck * L < n_list; ++next_ck) write_checkpoint<PPT>(s, sc, ck, next_ck, width, height);
 }
 
-template <int PPT, bool STATS>
-__global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_fwd_kernel(
+// SUB CTAs per tile, each with kThreads / SUB threads (its share of the tile's warps): finer work
+// units for the block scheduler (a level whose tile count is not a multiple of the resident CTA
+// slots leaves a part-empty last wave)
+template <int PPT, bool STATS, int SUB>
+__global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS * SUB) blend_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
@@ -360,10 +363,11 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
     // live, so its packed lane computes nothing that is kept.
-    constexpr int NT = S::kThreads, NP = (PPT + 1) / 2;
+    constexpr int NT = S::kThreads / SUB, NP = (PPT + 1) / 2;
     __shared__ StageBuf<NT> sb;
-    const S sc(v.tiles_x);
-    const uint2 range = ranges[blockIdx.x];
+    const int tile = blockIdx.x / SUB;
+    const S sc(v.tiles_x, tile, (blockIdx.x % SUB) * (NT / 32) + (threadIdx.x >> 5));
+    const uint2 range = ranges[tile];
     const double ox = sc.tx * kTile, oy = sc.ty * kTile;
     const float fx = static_cast<float>(sc.lx);
 
@@ -385,11 +389,11 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_FWD_MIN_BLOCKS) blend_
     }
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
     if (static_cast<int>(range.y - range.x) > df_list)
-        blend_walk<PPT, STATS, kDf>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
-                                    fx, ck, nseg, v.width, v.height);
+        blend_walk<PPT, STATS, kDf, NT>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
+                                        fx, ck, nseg, v.width, v.height);
     else
-        blend_walk<PPT, STATS, kBand>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
-                                      oy, fx, ck, nseg, v.width, v.height);
+        blend_walk<PPT, STATS, kBand, NT>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
+                                          oy, fx, ck, nseg, v.width, v.height);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
@@ -667,9 +671,12 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
                 ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
         return;
     }
-#define GSB_FWD(P, S) \
-    blend_fwd_kernel<P, S><<<n_tiles, kTileThreads / P, 0, st>>>(ranges, vals, rec, v, color, depth, vis, t_final, \
-                                                               n_proc, n_contrib, g_df_list, ck, nseg)
+#ifndef GSB_FWD_SUB
+#define GSB_FWD_SUB 1
+#endif
+#define GSB_FWD(P, S)                                                                                        \
+    blend_fwd_kernel<P, S, GSB_FWD_SUB><<<n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, 0, st>>>( \
+        ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);
