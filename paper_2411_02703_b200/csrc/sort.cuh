@@ -6,7 +6,10 @@ namespace gsb {
 
 constexpr int kRadix = 256;
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
+#ifndef GSB_SORT_ITEMS
+#define GSB_SORT_ITEMS 8
+#endif
+constexpr int kSortItems = GSB_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;
 
 // Per-render sort state, zeroed once per render: digit histograms (depth passes 0-2, tile
