@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ params, f
                                                    const int8_t* __restrict__ degree,
                                                    const float* __restrict__ grads, int64_t gcap, int64_t cap, int n,
                                                    AdamArgs args, const unsigned long long* __restrict__ cnt) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || overflowed(cnt)) return;
     const int t = args.t_common - birth[i];
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(128) adam_plane_kernel(float* __restrict__ par
                                                          const float* __restrict__ grads, int64_t gcap, int64_t cap,
                                                          int n, AdamArgs args,
                                                          const unsigned long long* __restrict__ cnt) {
+    pdl_enter();
     const int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     const int k = blockIdx.y;  // plane
     if (i >= n || overflowed(cnt)) return;
@@ -134,9 +136,9 @@ void launch_adam(float* params, float* m, float* v, const int32_t* birth, const 
     args.b_common = static_cast<float>(1.0 / (1.0 - std::pow(0.999, static_cast<double>(t_common))));
     if (cap % 4 == 0 && gcap % 4 == 0) {
         const dim3 grid(div_up(div_up(n, 4), 128), kGeomParams + 3 * (max_degree + 1) * (max_degree + 1));
-        adam_plane_kernel<<<grid, 128, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
+        launch_pdl(adam_plane_kernel, grid, 128, st, params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
     } else
-        adam_kernel<<<div_up(n, 256), 256, 0, st>>>(params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
+        launch_pdl(adam_kernel, div_up(n, 256), 256, st, params, m, v, birth, degree, grads, gcap, cap, n, args, cnt);
 }
 
 // GaussianMap::prune (gaussian_map.cpp:56-73): keep sigmoid(opacity_logit) >= threshold (fp64,

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
     const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials,
     const unsigned long long* __restrict__ cnt, const float* __restrict__ ck, int nseg,
     const float* __restrict__ color_final, const float* __restrict__ depth_final) {
+    pdl_enter();
     if (overflowed(cnt)) return;  // pair capacity exceeded: the host re-runs the step
     using S = Strip<PPT>;
     constexpr int NT = S::kThreads, NW = NT / 32, NP = (PPT + 1) / 2;  // PPT = 1: high half never live
@@ -287,10 +288,10 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
     const dim3 n_tiles(v.tiles_x * v.tiles_y, nseg);
     // 4 pixels per thread (2 warps per tile) unless overridden to 2 (4 warps per tile)
     if (blend_ppt(v, true) == 2)
-        blend_bwd_kernel<2><<<n_tiles, 128, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+        launch_pdl(blend_bwd_kernel<2>, n_tiles, 128, st, ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
                                                      dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
     else
-        blend_bwd_kernel<4><<<n_tiles, 64, 0, st>>>(ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
+        launch_pdl(blend_bwd_kernel<4>, n_tiles, 64, st, ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
                                                     dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
 }
 

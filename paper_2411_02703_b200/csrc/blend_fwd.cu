@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
     float* __restrict__ ck, int nseg) {
+    pdl_enter();
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
     // live, so its packed lane computes nothing that is kept.
@@ -441,6 +442,7 @@ template <int PPT, bool STATS>
 __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ seg, int nseg) {
+    pdl_enter();
     using S = Strip<PPT>;
     __shared__ StageBuf<S::kThreads> sb;
     const S sc(v.tiles_x);
@@ -484,6 +486,7 @@ __global__ void fwd_seg_chain_kernel(const uint2* __restrict__ ranges, ViewParam
                                      int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib,
                                      float* __restrict__ tl_plane, int32_t* __restrict__ star_plane,
                                      float* __restrict__ ck) {
+    pdl_enter();
     const int P = v.width * v.height;
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= P) return;
@@ -546,6 +549,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib,
     const float* __restrict__ tl_plane, const int32_t* __restrict__ star_plane, int nseg) {
+    pdl_enter();
     using S = Strip<PPT>;
     constexpr int NP = (PPT + 1) / 2;
     __shared__ StageBuf<S::kThreads> sb;
@@ -659,15 +663,15 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
         float* tl_plane = seg_scratch + static_cast<size_t>(nseg) * kSegFields * P;
         int32_t* star = reinterpret_cast<int32_t*>(tl_plane + P);
         const dim3 grid(n_tiles, nseg);
-        if (stats) fwd_seg_local_kernel<2, true><<<grid, kTileThreads / 2, 0, st>>>(ranges, vals, rec, v, seg, nseg);
-        else fwd_seg_local_kernel<2, false><<<grid, kTileThreads / 2, 0, st>>>(ranges, vals, rec, v, seg, nseg);
-        fwd_seg_chain_kernel<<<div_up(static_cast<int>(P), 256), 256, 0, st>>>(
+        if (stats) launch_pdl(fwd_seg_local_kernel<2, true>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg);
+        else launch_pdl(fwd_seg_local_kernel<2, false>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg);
+        launch_pdl(fwd_seg_chain_kernel, div_up(static_cast<int>(P), 256), 256, st, 
             ranges, v, seg, nseg, color, depth, vis, t_final, n_proc, stats ? n_contrib : nullptr, tl_plane, star, ck);
         if (stats)
-            fwd_seg_finish_kernel<2, true><<<grid, kTileThreads / 2, 0, st>>>(
+            launch_pdl(fwd_seg_finish_kernel<2, true>, grid, kTileThreads / 2, st, 
                 ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
         else
-            fwd_seg_finish_kernel<2, false><<<grid, kTileThreads / 2, 0, st>>>(
+            launch_pdl(fwd_seg_finish_kernel<2, false>, grid, kTileThreads / 2, st, 
                 ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
         return;
     }
@@ -675,8 +679,8 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
 #define GSB_FWD_SUB 1
 #endif
 #define GSB_FWD(P, S)                                                                                        \
-    blend_fwd_kernel<P, S, GSB_FWD_SUB><<<n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, 0, st>>>( \
-        ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg)
+    launch_pdl(blend_fwd_kernel<P, S, GSB_FWD_SUB>, n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, st,     \
+               ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);

@@ -6,6 +6,41 @@
 
 namespace gsb {
 
+// Programmatic dependent launch along the training step's kernel chain: a kernel launched with
+// launch_pdl first waits for its predecessor grid (griddepcontrol.wait: complete and its writes
+// visible; a no-op for an ordinary launch), then lets its own dependent grid launch, so the
+// next kernel's launch and CTA start-up overlap this one's work and tail. Only a kernel whose
+// predecessor on the stream is a kernel (not a memset or copy) is launched this way.
+#ifndef GSB_PDL
+#define GSB_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if GSB_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+#if GSB_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+#else
+    kernel<<<grid, block, 0, st>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+#endif
+}
+
 constexpr int kTile = 16;                 // rasterizer.hpp:17 kTileSize
 constexpr int kTileThreads = kTile * kTile;
 constexpr double kNearClip = 0.01;        // projection.hpp:11

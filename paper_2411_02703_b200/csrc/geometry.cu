@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(256, 3) preprocess_fwd_kernel(
     const int32_t* __restrict__ cand, ViewParams v, Splat* __restrict__ rec_by_gid,
     unsigned long long* __restrict__ depth_key, int32_t* __restrict__ vis_gid, uint32_t* __restrict__ key32,
     unsigned long long* __restrict__ counters) {
+    pdl_enter();
     const int n_cand = static_cast<int>(counters[2]);
     const int stride = gridDim.x * blockDim.x;
     const int first = blockIdx.x * blockDim.x + threadIdx.x;
@@ -413,7 +414,7 @@ void launch_preprocess_fwd(const float* params, int64_t cap, const int8_t* degre
                            int32_t* vis_gid, uint32_t* key32, unsigned long long* counters, cudaStream_t st) {
     if (max_cand <= 0) return;
     const int blocks = std::min(div_up(max_cand, 256), 148 * 8);
-    preprocess_fwd_kernel<<<blocks, 256, 0, st>>>(params, cap, degree, cand, v, rec_by_gid, depth_key, vis_gid,
+    launch_pdl(preprocess_fwd_kernel, blocks, 256, st, params, cap, degree, cand, v, rec_by_gid, depth_key, vis_gid,
                                                   key32, counters);
 }
 
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
                                                                     const float* __restrict__ partials,
                                                                     const unsigned long long* __restrict__ cnt,
                                                                     float* __restrict__ sums) {
+    pdl_enter();
     __shared__ float seg[kBwdThreads / 32][32][kNumPartials + 1];
     __shared__ int stamp[kBwdThreads / 32][32];  // pass in which rank l's run total was written
     const int n_vis = static_cast<int>(cnt[kCntVisible]);
@@ -530,6 +532,7 @@ __global__ void __launch_bounds__(kBwdThreads) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const uint32_t* __restrict__ emit_off, const float* __restrict__ sums, const unsigned long long* __restrict__ cnt,
     float* __restrict__ grads, int64_t gcap, const int32_t* __restrict__ rank_of, const int32_t* __restrict__ vis_gid) {
+    pdl_enter();
     const int t = blockIdx.x * kBwdThreads + threadIdx.x;
     if (t >= static_cast<int>(cnt[kCntVisible]) || overflowed(cnt)) return;
     const int i = vis_gid[t];
@@ -909,14 +912,14 @@ void launch_preprocess_bwd(const float* params, int64_t cap, const int8_t* degre
                            const int32_t* vis_gid, cudaStream_t st) {
     if (max_ranks <= 0) return;
     const int blocks = div_up(max_ranks, kBwdThreads);
-    reduce_partials_kernel<<<blocks, kBwdThreads, 0, st>>>(emit_off, partials, cnt, sums);
+    launch_pdl(reduce_partials_kernel, blocks, kBwdThreads, st, emit_off, partials, cnt, sums);
     // accumulate = false: the gradient planes were just zeroed, so plain stores replace the
     // read-modify-write of the gradient entries
     if (accumulate)
-        preprocess_bwd_kernel<true><<<blocks, kBwdThreads, 0, st>>>(params, cap, degree, v, emit_off, sums, cnt,
+        launch_pdl(preprocess_bwd_kernel<true>, blocks, kBwdThreads, st, params, cap, degree, v, emit_off, sums, cnt,
                                                                    grads, gcap, rank_of, vis_gid);
     else
-        preprocess_bwd_kernel<false><<<blocks, kBwdThreads, 0, st>>>(params, cap, degree, v, emit_off, sums, cnt,
+        launch_pdl(preprocess_bwd_kernel<false>, blocks, kBwdThreads, st, params, cap, degree, v, emit_off, sums, cnt,
                                                                     grads, gcap, rank_of, vis_gid);
 }
 

@@ -255,6 +255,7 @@ template <bool FUSED>
 __global__ void __launch_bounds__(256) ssim_bwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, const float* __restrict__ wbuf,
                                                        float neg_lambda, float* __restrict__ dl, PixelLoss pl) {
+    pdl_enter();
     __shared__ float sw[3][kInY][kInX + 2];
     __shared__ float hx[3][kInY][kSx + 1];
     const int c = blockIdx.z;
@@ -371,12 +372,12 @@ LossLayout launch_ssim(const float* color, const float* gt_color, int h, int w, 
     if (depth) {  // fused pixel loss (loss_pixel_kernel is not launched)
         PixelLoss pl{depth, vis, gt_depth, depth_cot,
                      static_cast<float>((1.0 / (static_cast<double>(h) * w * 3)) * (1.0 - lambda)), acc, L.stride};
-        ssim_bwd_kernel<true><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda), dl_dcolor,
+        launch_pdl(ssim_bwd_kernel<true>, gb, 256, st, color, gt_color, h, w, wbuf, static_cast<float>(-lambda), dl_dcolor,
                                                    pl);
         L.n[kLossL1] = L.n[kLossSq] = static_cast<int>(gb.x * gb.y * gb.z);
         L.n[kLossDabs] = L.n[kLossNv] = static_cast<int>(gb.x * gb.y);
     } else {
-        ssim_bwd_kernel<false><<<gb, 256, 0, st>>>(color, gt_color, h, w, wbuf, static_cast<float>(-lambda),
+        launch_pdl(ssim_bwd_kernel<false>, gb, 256, st, color, gt_color, h, w, wbuf, static_cast<float>(-lambda),
                                                     dl_dcolor, PixelLoss{});
     }
     return L;
@@ -449,6 +450,7 @@ constexpr int kFinalizeThreads = 1024;
 
 __global__ void __launch_bounds__(kFinalizeThreads) loss_finalize_kernel(LossScalars* acc, LossLayout L,
                                                                           double lambda_d) {
+    pdl_enter();
     __shared__ double scratch[kLossFields][kFinalizeThreads / 32];
     const double* slots = slot_base(acc);
     int nmax = 0;
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(kFinalizeThreads) loss_finalize_kernel(LossSca
 }
 
 void launch_loss_finalize(LossScalars* acc, const LossLayout& L, double lambda_d, cudaStream_t st) {
-    loss_finalize_kernel<<<1, kFinalizeThreads, 0, st>>>(acc, L, lambda_d);
+    launch_pdl(loss_finalize_kernel, 1, kFinalizeThreads, st, acc, L, lambda_d);
 }
 
 // ---------------------------------------------------------------------------------- pyramid

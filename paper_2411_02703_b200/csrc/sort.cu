@@ -25,6 +25,8 @@ static_assert(NT == kRadix, "one thread per digit in the look-back");
 
 constexpr uint32_t kFlagAgg = 1u, kFlagPrefix = 2u;
 
+// (the kernels below are chained with programmatic dependent launch: pdl_enter, common.cuh)
+
 __device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32_t flag, uint32_t value) {
     return (static_cast<unsigned long long>(epoch) << 34) | (static_cast<unsigned long long>(flag) << 32) | value;
 }
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(const KeyT* __restrict__ k
                                                       int shift, int bits, const uint32_t* __restrict__ hist,
                                                       uint32_t* __restrict__ ticket,
                                                       unsigned long long* __restrict__ status, uint32_t epoch) {
+    pdl_enter();
     __shared__ uint32_t s_base[kRadix], s_tstart[kRadix], s_run[kRadix];
     __shared__ uint32_t s_whist[NW][kRadix];
     __shared__ uint32_t s_warp[NW];
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(const KeyT* __restrict__ k
 __global__ void __launch_bounds__(NT) radix_hist_kernel(const uint32_t* __restrict__ keys,
                                                         const unsigned long long* __restrict__ count, uint32_t cap,
                                                         int passes, uint32_t* __restrict__ hist) {
+    pdl_enter();
     __shared__ uint32_t s[4][kRadix];
     for (int i = threadIdx.x; i < 4 * kRadix; i += NT) (&s[0][0])[i] = 0u;
     __syncthreads();
@@ -277,6 +281,7 @@ __global__ void __launch_bounds__(NT) fix_ties_kernel(const uint32_t* __restrict
                                                       const unsigned long long* __restrict__ depth,
                                                       const unsigned long long* __restrict__ cnt,
                                                       int32_t* __restrict__ gid_out) {
+    pdl_enter();
     const int n = static_cast<int>(cnt[kCntVisible]);
     for (int p = blockIdx.x * NT + threadIdx.x; p < n; p += gridDim.x * NT) {
         const uint32_t k = key[p];
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict
                                                        int32_t* __restrict__ rank_of,
                                                        uint32_t* __restrict__ emit_off, uint32_t* __restrict__ ticket,
                                                        unsigned long long* __restrict__ status, uint32_t epoch) {
+    pdl_enter();
     constexpr int PT = kPackItems * NT;
     static_assert(kPackItems == 4, "one 16-byte load / store of ranks per thread");
     __shared__ uint32_t s_warp[NW];
@@ -422,6 +428,7 @@ __global__ void __launch_bounds__(NT) emit_pairs_kernel(const uint32_t* __restri
                                                         unsigned long long* __restrict__ cnt, uint32_t cap,
                                                         int tiles_x, int b0, int passes, KeyT* __restrict__ keys,
                                                         uint32_t* __restrict__ vals, uint32_t* __restrict__ hist) {
+    pdl_enter();
     __shared__ uint32_t s_hist[2][kRadix];
     for (int i = threadIdx.x; i < 2 * kRadix; i += NT) (&s_hist[0][0])[i] = 0u;
     __syncthreads();
@@ -486,6 +493,7 @@ __global__ void __launch_bounds__(NT) emit_pairs_kernel(const uint32_t* __restri
 template <typename KeyT>
 __global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, const unsigned long long* __restrict__ cnt,
                                    uint32_t cap, uint2* __restrict__ ranges) {
+    pdl_enter();
     constexpr int KV = 16 / sizeof(KeyT);
     const uint32_t n = clamp_count(cnt + kCntPairs, cap);
     for (uint32_t i0 = KV * (blockIdx.x * blockDim.x + threadIdx.x); i0 < n; i0 += KV * gridDim.x * blockDim.x) {
@@ -524,6 +532,7 @@ int persistent_grid(int64_t max_tiles, int per_sm) {
 }
 }  // namespace
 
+
 size_t sort_status_words(int64_t max_elems) {
     return static_cast<size_t>((max_elems + kSortTile - 1) / kSortTile + 1) * kRadix;
 }
@@ -538,16 +547,16 @@ void launch_depth_sort(uint32_t* keys_a, uint32_t* keys_b, int32_t* vis_gid, int
     const int grid = persistent_grid(div_up(max_n, TILE), 4);
     // (keys_a, vis_gid) -> (keys_b, gid_tmp) -> (keys_a, gid_sorted) -> (keys_b, gid_tmp) -> exact tie
     // order into gid_sorted; vis_gid (K1's append order) is kept for K8
-    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_a, reinterpret_cast<const uint32_t*>(vis_gid), keys_b,
+    launch_pdl(onesweep_kernel<uint32_t, true>, grid, NT, st, keys_a, reinterpret_cast<const uint32_t*>(vis_gid), keys_b,
                                                          reinterpret_cast<uint32_t*>(gid_tmp), nvis, cap, 0, 8,
                                                          sb->hist[0], &sb->ticket[0], status, epoch);
-    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_b, reinterpret_cast<const uint32_t*>(gid_tmp), keys_a,
+    launch_pdl(onesweep_kernel<uint32_t, true>, grid, NT, st, keys_b, reinterpret_cast<const uint32_t*>(gid_tmp), keys_a,
                                                          reinterpret_cast<uint32_t*>(gid_sorted), nvis, cap, 8, 8,
                                                          sb->hist[1], &sb->ticket[1], status, epoch + 1);
-    onesweep_kernel<uint32_t, true><<<grid, NT, 0, st>>>(keys_a, reinterpret_cast<const uint32_t*>(gid_sorted), keys_b,
+    launch_pdl(onesweep_kernel<uint32_t, true>, grid, NT, st, keys_a, reinterpret_cast<const uint32_t*>(gid_sorted), keys_b,
                                                          reinterpret_cast<uint32_t*>(gid_tmp), nvis, cap, 16, 8,
                                                          sb->hist[2], &sb->ticket[2], status, epoch + 2);
-    fix_ties_kernel<<<persistent_grid(div_up(max_n, NT), 4), NT, 0, st>>>(keys_b, gid_tmp, depth_by_gid, cnt,
+    launch_pdl(fix_ties_kernel, persistent_grid(div_up(max_n, NT), 4), NT, st, keys_b, gid_tmp, depth_by_gid, cnt,
                                                                           gid_sorted);
 }
 
@@ -556,7 +565,7 @@ void launch_pack_scan(const int32_t* gid_sorted, const Splat* rec_by_gid, const 
                       int32_t* rank_of,
                       uint32_t* emit_off, SortBlock* sb, unsigned long long* status, uint32_t epoch, cudaStream_t st) {
     if (max_n <= 0) return;
-    pack_scan_kernel<<<persistent_grid(div_up(max_n, kPackItems * NT), 4), NT, 0, st>>>(
+    launch_pdl(pack_scan_kernel, persistent_grid(div_up(max_n, kPackItems * NT), 4), NT, st, 
         gid_sorted, rec_by_gid, depth_by_gid, cnt, rec_sorted, depth_sorted, rank_of, emit_off, &sb->ticket[3], status, epoch);
 }
 
@@ -572,21 +581,21 @@ static void tile_sort_impl(const uint32_t* emit_off, const Splat* rec, unsigned 
     // passes emit into (kb, vb) and go through (ka, va)
     KeyT* ke = passes == 1 ? ka : kb;
     uint32_t* ve = passes == 1 ? va : vb;
-    emit_pairs_kernel<KeyT><<<persistent_grid(div_up(max_n, NT), 2), NT, 0, st>>>(emit_off, rec, cnt, cap, tiles_x, b0,
+    launch_pdl(emit_pairs_kernel<KeyT>, persistent_grid(div_up(max_n, NT), 2), NT, st, emit_off, rec, cnt, cap, tiles_x, b0,
                                                                                  passes, ke, ve, sb->hist[3]);
     const int grid = persistent_grid(div_up(static_cast<int64_t>(cap), TILE), 4);
     const unsigned long long* npairs = cnt + kCntPairs;
     if (passes == 1) {
-        onesweep_kernel<KeyT, true><<<grid, NT, 0, st>>>(ka, va, kb, vb, npairs, cap, 0, b0, sb->hist[3],
+        launch_pdl(onesweep_kernel<KeyT, true>, grid, NT, st, ka, va, kb, vb, npairs, cap, 0, b0, sb->hist[3],
                                                          &sb->ticket[4], status, epoch);
     } else {
-        onesweep_kernel<KeyT, true><<<grid, NT, 0, st>>>(kb, vb, ka, va, npairs, cap, 0, b0, sb->hist[3],
+        launch_pdl(onesweep_kernel<KeyT, true>, grid, NT, st, kb, vb, ka, va, npairs, cap, 0, b0, sb->hist[3],
                                                          &sb->ticket[4], status, epoch);
-        onesweep_kernel<KeyT, true><<<grid, NT, 0, st>>>(ka, va, kb, vb, npairs, cap, b0, bits - b0, sb->hist[4],
+        launch_pdl(onesweep_kernel<KeyT, true>, grid, NT, st, ka, va, kb, vb, npairs, cap, b0, bits - b0, sb->hist[4],
                                                          &sb->ticket[5], status, epoch + 1);
     }
     constexpr int KV = 16 / sizeof(KeyT);
-    tile_ranges_kernel<KeyT><<<persistent_grid(div_up(static_cast<int64_t>(cap), KV * 256), 8), 256, 0, st>>>(
+    launch_pdl(tile_ranges_kernel<KeyT>, persistent_grid(div_up(static_cast<int64_t>(cap), KV * 256), 8), 256, st, 
         kb, cnt, cap, ranges);
 }
 
