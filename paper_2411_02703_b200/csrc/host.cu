@@ -337,6 +337,32 @@ void grads_zero(gs_grads* G, gs_map* M) {
     G->clean = true;
 }
 
+// grads_zero for a training step: the memset runs on the context's aux stream from the point the
+// compute stream has reached (every earlier read of the planes is done), overlapping the render;
+// the compute stream waits for it right before the backward (join_grads_zero)
+void grads_zero_async(gs_grads* G, gs_map* M) {
+#if defined(GSB_SYNC_GRADS_ZERO)
+    grads_zero(G, M);
+    return;
+#endif
+    G->ensure(std::max<int64_t>(M->n, 1));
+    gs_context* C = M->ctx;
+    if (M->n > 0) {
+        cudaStream_t ax = C->aux();
+        ck(cudaEventRecord(C->aux_in, C->stream), "event record");
+        ck(cudaStreamWaitEvent(ax, C->aux_in, 0), "stream wait");
+        const int planes = n_active_planes(M->max_degree);
+        ck(cudaMemset2DAsync(G->planes, sizeof(float) * G->cap, 0, sizeof(float) * M->n, planes, ax), "memset grads");
+        ck(cudaEventRecord(C->aux_out, ax), "event record");
+    }
+    G->n = M->n;
+    G->clean = true;
+}
+
+void join_grads_zero(gs_context* C) {
+    if (C->aux_stream) ck(cudaStreamWaitEvent(C->stream, C->aux_out, 0), "stream wait");
+}
+
 void backward_impl(gs_map* M, gs_frame* F, const float* dl_dcolor, const float* dl_ddepth,
                    const float* depth_scale, gs_grads* G) {
     gs_context* C = M->ctx;
@@ -627,10 +653,11 @@ void train_step_impl(gs_map* M, gs_keyframe* K, const gs_train_config* cfg, cons
         // one host round trip per step (the loss read); a step whose render overflowed the
         // remembered pair capacity changed nothing on the device and is re-run at exact size
         for (int attempt = 0;; ++attempt) {
-            grads_zero(G, M);
+            grads_zero_async(G, M);
             C->prof_level = level;
             if (!(have && attempt == 0)) render_impl(M, K->pose, lc, F, attempt > 0, false);
             loss_impl(F, K, level, *cfg);
+            join_grads_zero(C);
             backward_impl(M, F, F->dl_dcolor.as<float>(), F->depth_cot.as<float>(),
                           &F->loss.as<LossScalars>()->depth_scale, G);
             adam_impl(M, G, cfg->lr, dev_counters(F));
@@ -708,6 +735,12 @@ int gs_context_destroy(gs_context* C) {
             delete F;
         }
         if (C->loss_ready) cudaEventDestroy(C->loss_ready);
+        if (C->aux_stream) {
+            cudaStreamSynchronize(C->aux_stream);
+            cudaStreamDestroy(C->aux_stream);
+            cudaEventDestroy(C->aux_in);
+            cudaEventDestroy(C->aux_out);
+        }
         for (cudaEvent_t e : C->ev_pool) cudaEventDestroy(e);
         if (C->scratch_grads && C->scratch_grads->planes && !C->scratch_grads->external)
             pool_free(C->scratch_grads->planes, C->stream);

@@ -179,6 +179,18 @@ struct gs_context {
     DevBuf& sc(ScratchSlot s) { return scratch[s]; }
     PinnedBuf pinned;
     cudaStream_t copy_stream = nullptr;  // host uploads (overlap the compute stream)
+    // the training step's gradient zeroing runs here, beside the render (which does not touch the
+    // gradient planes); the backward waits for it
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t aux_in = nullptr, aux_out = nullptr;
+    cudaStream_t aux() {
+        if (!aux_stream) {
+            ck(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaEventCreateWithFlags(&aux_in, cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaEventCreateWithFlags(&aux_out, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        return aux_stream;
+    }
     bool defer_sync = false;             // diagnostics: train steps skip the loss read-back
     cudaStream_t copies() {
         if (!copy_stream) ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
