@@ -285,8 +285,10 @@ def run_ours(args, rank, world):
     ms = e0.elapsed_time(e1)
     # per-level step times (per-level rates)
     lvl_ms = {}
+    intervals = []
     for s in range(args.steps):
         d = step_ev[s - 1].elapsed_time(step_ev[s]) if s else e0.elapsed_time(step_ev[0])
+        intervals.append(round(d, 4))
         lvl = (LEVELS - ((args.warmup + s) % 3)) if batch else schedule(args.warmup + s)[1]
         lvl_ms.setdefault(lvl, []).append(d)
     per_level = {f"L{l}": {"ms_per_step": round(float(np.mean(v)), 4), "steps": len(v),
@@ -325,7 +327,9 @@ def run_ours(args, rank, world):
                          "l2": "inputs larger than L2 (params+Adam+grads > 126 MB)",
                          "parallelism": f"dp{world}" if batch else "single-view"},
               "gpu_launches": launches, "clocks": clk.summary(), "fixture_s": round(t_fix, 2),
-              "timed_region_capacity_events": capacity}
+              "timed_region_capacity_events": capacity,
+              # device time between consecutive step reports (per-step view of the timed region)
+              "step_intervals_ms": intervals if args.steps <= 300 else None}
 
     # ---------------- per-kernel profile pass (separate from the headline timing)
     ctx.profile(True)
