@@ -102,6 +102,35 @@ __device__ __forceinline__ AlphaP alpha_pair(float2 m, float4 cn, float fx, floa
     return a;
 }
 
+// The same with a per-pixel opacity pair (the forward masks stopped pixels by opacity 0):
+// op = cn.w * 1 is cn.w exactly, so a live pixel's alpha is bit-identical to alpha_pair's.
+template <bool CLAMP = true>
+__device__ __forceinline__ AlphaP alpha_pair_op(float2 m, float4 cn, float2 op, float fx, float2 fy) {
+    const float dx = __fadd_rn(fx, -m.x);
+    const float2 dy = __fadd2_rn(fy, f2(-m.y));
+    const float adx = __fmul_rn(cn.x, dx), bdx = __fmul_rn(cn.y, dx);
+    AlphaP a;
+    a.u0 = __ffma2_rn(f2(cn.y), dy, f2(adx));
+    a.u1 = __ffma2_rn(f2(cn.z), dy, f2(bdx));
+    const float2 q = __ffma2_rn(dy, a.u1, __fmul2_rn(f2(dx), a.u0));
+    a.g = make_float2(ex2(q.x), ex2(q.y));
+    a.a_raw = __fmul2_rn(op, a.g);
+    a.alpha = CLAMP ? make_float2(fminf(a.a_raw.x, kAlphaMaxF), fminf(a.a_raw.y, kAlphaMaxF)) : a.a_raw;
+    return a;
+}
+
+// 64-byte record copy global -> shared without staging registers (cp.async, L2 only): the
+// blends prefetch the next batch's records this way while walking the current one
+__device__ __forceinline__ void cp_async_splat(Splat* dst, const Splat* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const char* g = reinterpret_cast<const char*>(src);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * i), "l"(g + 16 * i) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // fp64 transmittance factor (1 - alpha): the clamp substitutes the exact double 0.99, so two
 // stacked clamped splats leave T = (1 - 0.99)^2 = 1.0000000000000018e-4 (no termination),
 // exactly as the fp64 reference (rasterizer.cpp:143-151).

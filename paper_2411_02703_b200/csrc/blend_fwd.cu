@@ -93,14 +93,29 @@ __device__ __noinline__ double warp_replay(const uint32_t* __restrict__ vals, co
 template <int NP>
 struct FwdState {
     float2 T[NP], Tl[NP], c0[NP], c1[NP], c2[NP], dd[NP], vis[NP];  // Tl: df32 low part (DF mode)
+    // per pixel, as packed multipliers of the walk: on = 1 while the pixel is live, else 0 (it
+    // scales the entry's opacity, so a stopped or absent pixel takes alpha = 0, weight 0, factor
+    // 1); tn = on * t_near (a stopped pixel never asks for a termination check)
+    float2 on[NP], tn[NP];
     int nproc[2 * NP], ncontrib[2 * NP];
     unsigned live;
     // pixel p stops after the entry at list position pos
     __device__ __forceinline__ void stop(int p, int pos) {
         live &= ~(1u << p);
 #pragma unroll
-        for (int q = 0; q < 2 * NP; ++q)  // static indices: the arrays stay in registers
-            if (q == p) nproc[q] = pos + 1;
+        for (int q = 0; q < 2 * NP; ++q) {  // static indices: the arrays stay in registers
+            if (q != p) continue;
+            nproc[q] = pos + 1;
+            if (q & 1) on[q >> 1].y = tn[q >> 1].y = 0.f;
+            else on[q >> 1].x = tn[q >> 1].x = 0.f;
+        }
+    }
+    __device__ __forceinline__ void arm(float t_near) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            on[q] = make_float2((live >> (2 * q)) & 1u ? 1.f : 0.f, (live >> (2 * q + 1)) & 1u ? 1.f : 0.f);
+            tn[q] = make_float2(on[q].x * t_near, on[q].y * t_near);
+        }
     }
 };
 
@@ -178,11 +193,11 @@ __device__ GSB_NEAR_INLINE void df_near(FwdState<(PPT + 1) / 2>& s, unsigned nea
 enum FwdMode : int { kBand = 0, kDf = 1, kLocal = 2 };
 
 // One tile-list entry over the thread's pixels. COVER: the entry's rect contains every live
-// pixel of the warp (warp-uniform), so the per-pixel box test reduces to the live bits.
+// pixel of the warp (warp-uniform), so no per-pixel box test (a stopped pixel has opacity 0).
 // STATS: maintain n_contrib (only the public render reports it).
 template <int PPT, bool COVER, bool STATS, int MODE, bool CLAMP>
 __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, const int4& rc,
-                                          float2 m, float4 cn, float4 col, int pos, int kw, float fx, float t_near,
+                                          float2 m, float4 cn, float4 col, int pos, int kw, float fx,
                                           const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
                                           uint2 range, double ox, double oy) {
     constexpr int NP = (PPT + 1) / 2;
@@ -194,15 +209,16 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const int p0 = 2 * q, y0 = sc.py0 + p0;
-        bool a0 = (s.live & (1u << p0)) != 0u, a1 = (s.live & (2u << p0)) != 0u;
+        // in the entry's rect (a stopped pixel is masked by its zero opacity instead)
+        bool a0 = true, a1 = true;
         if (!COVER) {
-            a0 = a0 && colin && y0 >= rc.y && y0 <= rc.w;
-            a1 = a1 && colin && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
+            a0 = colin && y0 >= rc.y && y0 <= rc.w;
+            a1 = colin && y0 + 1 >= rc.y && y0 + 1 <= rc.w;
         }
         // no branch on (a0 || a1): an inactive half has al = 0 -> w = 0 and factor exactly 1
         const float fy = static_cast<float>(sc.ly0 + p0);
-        const AlphaP e = alpha_pair<CLAMP>(m, cn, fx, make_float2(fy, fy + 1.f));
-        const float2 al = make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
+        const AlphaP e = alpha_pair_op<CLAMP>(m, cn, __fmul2_rn(f2(cn.w), s.on[q]), fx, make_float2(fy, fy + 1.f));
+        const float2 al = COVER ? e.alpha : make_float2(a0 ? e.alpha.x : 0.f, a1 ? e.alpha.y : 0.f);
         const float2 w = __fmul2_rn(al, s.T[q]);
         s.c0[q] = __ffma2_rn(w, f2(col.x), s.c0[q]);
         s.c1[q] = __ffma2_rn(w, f2(col.y), s.c1[q]);
@@ -228,11 +244,12 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
             s.T[q] = __fmul2_rn(s.T[q], CLAMP ? make_float2(fmaxf(f.x, kClampFac), fmaxf(f.y, kClampFac)) : f);
         }
         if (STATS) {
-            s.ncontrib[p0] += a0;
-            s.ncontrib[p0 + 1] += a1;
+            s.ncontrib[p0] += a0 && ((s.live >> p0) & 1u);
+            s.ncontrib[p0 + 1] += a1 && ((s.live >> (p0 + 1)) & 1u);
         }
-        nb[p0] = a0 && s.T[q].x < t_near;
-        nb[p0 + 1] = a1 && s.T[q].y < t_near;
+        // a pixel outside the rect kept T (already decided at its last contributor): no check
+        nb[p0] = a0 && s.T[q].x < s.tn[q].x;
+        nb[p0 + 1] = a1 && s.T[q].y < s.tn[q].y;
         anyn = anyn || nb[p0] || nb[p0 + 1];
     }
     if (MODE == kDf) {
@@ -282,8 +299,11 @@ __device__ __forceinline__ void write_checkpoint(const FwdState<(PPT + 1) / 2>& 
 // The walk over entries [start, end) of one tile's list `full` (staging batches of NT entries,
 // per-warp ballot against the live-pixel box, list order within the warp). Positions are
 // relative to the list start; checkpoints are written only by a whole-list walk (start = 0).
+// The next batch's records are copied into `raw` (cp.async, one 64-byte record per thread)
+// while the current batch is walked; the list index of the batch after that is kept in a
+// register so the copy's address is ready when it is issued.
 template <int PPT, bool STATS, int MODE, int NT = kTileThreads / PPT>
-__device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<NT>& sb,
+__device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<NT>& sb, Splat* raw,
                                            const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
                                            const Splat* __restrict__ rec, uint2 full, int start, int end, double ox,
                                            double oy, float fx, float* ck, int nseg, int width, int height) {
@@ -296,20 +316,27 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
     // rounded up; df32 modes a fixed guard
     const float t_near = MODE != kBand ? 1.0001e-4f
                                        : __double2float_ru(kTMin * (1.0 + kBetaPerFactor * (n_list + 1)));
+    s.arm(t_near);
     int4 lb = warp_bbox<PPT>(s.live, sc);
     unsigned seen = s.live;
     int kw = 0;  // entries this warp has walked (uniform)
     const uint32_t b_end = full.x + end;
-    // the next batch's record is loaded one batch ahead (its latency overlaps the current walk)
-    Splat nsp;
-    if (full.x + start + threadIdx.x < b_end) nsp = rec[vals[full.x + start + threadIdx.x]];
+    const uint32_t i0 = full.x + start + threadIdx.x;
+    if (i0 < b_end) cp_async_splat(&raw[threadIdx.x], &rec[vals[i0]]);
+    cp_async_commit();
+    uint32_t nvi = i0 + NT < b_end ? vals[i0 + NT] : 0u;
     for (uint32_t base = full.x + start; base < b_end; base += NT) {
         if (next_ck < nseg && static_cast<int>(base - full.x) == next_ck * L)
             write_checkpoint<PPT>(s, sc, ck, next_ck++, width, height);
         if (__syncthreads_count(s.live != 0) == 0) break;
         const uint32_t idx = base + threadIdx.x;
-        if (idx < b_end) sb.put(threadIdx.x, stage_of(nsp, ox, oy));
-        if (idx + NT < b_end) nsp = rec[vals[idx + NT]];
+        cp_async_wait_all();  // this thread's own record (each thread reads only its slot)
+        if (idx < b_end) sb.put(threadIdx.x, stage_of(raw[threadIdx.x], ox, oy));
+        if (idx + NT < b_end) {
+            cp_async_splat(&raw[threadIdx.x], &rec[nvi]);
+            if (idx + 2 * NT < b_end) nvi = vals[idx + 2 * NT];
+        }
+        cp_async_commit();
         __syncthreads();
         const int cnt = min(NT, static_cast<int>(b_end - base));
         for (int b0 = 0; b0 < cnt; b0 += 32) {
@@ -318,35 +345,46 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
                 lb = warp_bbox<PPT>(s.live, sc);
             }
             if (lb.x > lb.z) break;  // no live pixel left in this warp
+            // per chunk of 32 staged entries, lane l classifies entry b0 + l against the chunk's
+            // live box: meets it (walked), covers it (no per-pixel box test), opacity >= 0.99f
+            // (alpha may clamp). Pixels stopping inside the chunk only shrink the true box, so
+            // the chunk-start classification stays valid.
             const int jj = b0 + sc.lane;
-            unsigned todo = __ballot_sync(0xffffffffu, jj < cnt && rect_meets(sb.rect[jj], lb));
+            bool meets = false, covers = false, clamps = false;
+            if (jj < cnt) {
+                const int4 r = sb.rect[jj];
+                meets = rect_meets(r, lb);
+                covers = r.x <= lb.x && r.z >= lb.z && r.y <= lb.y && r.w >= lb.w;
+                clamps = sb.con[jj].w >= kAlphaMaxF;
+            }
+            unsigned todo = __ballot_sync(0xffffffffu, meets);
+            const unsigned cov = __ballot_sync(0xffffffffu, meets && covers);
+            const unsigned clp = __ballot_sync(0xffffffffu, meets && clamps);
             while (todo) {
-                const int j = b0 + __ffs(todo) - 1;
+                const int bit = __ffs(todo) - 1;
                 todo &= todo - 1;
-                const int4 rc = sb.rect[j];
+                const int j = b0 + bit;
                 const int pos = static_cast<int>(base - full.x) + j;
                 ++kw;
                 const float4 cn = sb.con[j];
-                // warp-uniform variants: the rect covers every live pixel of the warp (no per-pixel
-                // box test); the opacity is below 0.99f (alpha can never clamp)
-                const bool cover = rc.x <= lb.x && rc.z >= lb.z && rc.y <= lb.y && rc.w >= lb.w;
-                if (cn.w < kAlphaMaxF) {
-                    if (cover)
-                        fwd_entry<PPT, true, STATS, MODE, false>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
-                                                                 t_near, vals, rec, full, ox, oy);
+                if (!((clp >> bit) & 1u)) {
+                    if ((cov >> bit) & 1u)
+                        fwd_entry<PPT, true, STATS, MODE, false>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                                                                 vals, rec, full, ox, oy);
                     else
-                        fwd_entry<PPT, false, STATS, MODE, false>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
-                                                                  t_near, vals, rec, full, ox, oy);
-                } else if (cover) {
-                    fwd_entry<PPT, true, STATS, MODE, true>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
-                                                            t_near, vals, rec, full, ox, oy);
+                        fwd_entry<PPT, false, STATS, MODE, false>(s, sc, sb.rect[j], sb.mean[j], cn, sb.col[j], pos,
+                                                                  kw, fx, vals, rec, full, ox, oy);
+                } else if ((cov >> bit) & 1u) {
+                    fwd_entry<PPT, true, STATS, MODE, true>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, kw, fx, vals,
+                                                            rec, full, ox, oy);
                 } else {
-                    fwd_entry<PPT, false, STATS, MODE, true>(s, sc, rc, sb.mean[j], cn, sb.col[j], pos, kw, fx,
-                                                             t_near, vals, rec, full, ox, oy);
+                    fwd_entry<PPT, false, STATS, MODE, true>(s, sc, sb.rect[j], sb.mean[j], cn, sb.col[j], pos, kw,
+                                                             fx, vals, rec, full, ox, oy);
                 }
             }
         }
     }
+    cp_async_wait_all();  // no copy may land after the CTA's shared memory is reused
     // boundaries past an early exit (every pixel terminated) hold the final state
     for (; next_ck < nseg && next_ck * L < n_list; ++next_ck) write_checkpoint<PPT>(s, sc, ck, next_ck, width, height);
 }
@@ -366,6 +404,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     // live, so its packed lane computes nothing that is kept.
     constexpr int NT = S::kThreads / SUB, NP = (PPT + 1) / 2;
     __shared__ StageBuf<NT> sb;
+    __shared__ Splat raw[NT];
     const int tile = blockIdx.x / SUB;
     const S sc(v.tiles_x, tile, (blockIdx.x % SUB) * (NT / 32) + (threadIdx.x >> 5));
     const uint2 range = ranges[tile];
@@ -390,10 +429,10 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     }
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
     if (static_cast<int>(range.y - range.x) > df_list)
-        blend_walk<PPT, STATS, kDf, NT>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
+        blend_walk<PPT, STATS, kDf, NT>(s, sb, raw, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
                                         fx, ck, nseg, v.width, v.height);
     else
-        blend_walk<PPT, STATS, kBand, NT>(s, sb, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
+        blend_walk<PPT, STATS, kBand, NT>(s, sb, raw, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
                                           oy, fx, ck, nseg, v.width, v.height);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
@@ -445,6 +484,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
     pdl_enter();
     using S = Strip<PPT>;
     __shared__ StageBuf<S::kThreads> sb;
+    __shared__ Splat raw[S::kThreads];
     const S sc(v.tiles_x);
     const uint2 range = ranges[blockIdx.x];
     const int n_list = static_cast<int>(range.y - range.x);
@@ -455,7 +495,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
     const float fx = static_cast<float>(sc.lx);
     FwdState<(PPT + 1) / 2> s;
     init_state<PPT>(s, sc, v.width, v.height);
-    blend_walk<PPT, STATS, kLocal>(s, sb, sc, vals, rec, range, lo, min(lo + L, n_list), ox, oy, fx, nullptr, 1,
+    blend_walk<PPT, STATS, kLocal>(s, sb, raw, sc, vals, rec, range, lo, min(lo + L, n_list), ox, oy, fx, nullptr, 1,
                                    v.width, v.height);
     const size_t P = static_cast<size_t>(v.width) * v.height;
     float* base = seg + static_cast<size_t>(blockIdx.y) * kSegFields * P;
@@ -553,6 +593,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
     using S = Strip<PPT>;
     constexpr int NP = (PPT + 1) / 2;
     __shared__ StageBuf<S::kThreads> sb;
+    __shared__ Splat raw[S::kThreads];
     const S sc(v.tiles_x);
     const uint2 range = ranges[blockIdx.x];
     const int n_list = static_cast<int>(range.y - range.x);
@@ -598,7 +639,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
     if (__syncthreads_count(mine != 0u) == 0) return;
     const double ox = sc.tx * kTile, oy = sc.ty * kTile;
     const float fx = static_cast<float>(sc.lx);
-    blend_walk<PPT, STATS, kDf>(s, sb, sc, vals, rec, range, lo, n_list, ox, oy, fx, nullptr, 1, v.width, v.height);
+    blend_walk<PPT, STATS, kDf>(s, sb, raw, sc, vals, rec, range, lo, n_list, ox, oy, fx, nullptr, 1, v.width, v.height);
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
         if (!((mine >> p) & 1u)) continue;
