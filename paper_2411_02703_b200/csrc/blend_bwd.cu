@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
     const int32_t* __restrict__ n_proc, const float* __restrict__ dl_dcolor,
     const float* __restrict__ dl_ddepth, const float* __restrict__ depth_scale, float* __restrict__ partials,
     const unsigned long long* __restrict__ cnt, const float* __restrict__ ck, int nseg,
-    const float* __restrict__ color_final, const float* __restrict__ depth_final) {
+    const float* __restrict__ color_final, const float* __restrict__ depth_final, const uint32_t* __restrict__ order) {
     pdl_enter();
     if (overflowed(cnt)) return;  // pair capacity exceeded: the host re-runs the step
     using S = Strip<PPT>;
@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
     __shared__ int s_max[NW];
     __shared__ __align__(16) float s_pv[NW][kFlush][kNumPartials][kRowStride];
     __shared__ int s_pk[NW][kFlush];
-    const S sc(v.tiles_x);
+    const int tile = order ? static_cast<int>(order[blockIdx.x]) : static_cast<int>(blockIdx.x);
+    const S sc(v.tiles_x, tile, threadIdx.x >> 5);
     // sums the warp's staged rows over its lanes and stores them per (entry, partial)
     auto flush = [&](int nb) {
         __syncwarp();
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
         }
         __syncwarp();
     };
-    const uint2 range = ranges[blockIdx.x];
+    const uint2 range = ranges[tile];
     // this CTA's list segment [lo_s, hi_s) (blockIdx.y); the whole list when nseg = 1
     const int n_list = static_cast<int>(range.y - range.x);
     const int L = seg_len(n_list, nseg);
@@ -286,13 +287,14 @@ void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* re
                       float* partials, const unsigned long long* cnt, const float* ck, int nseg,
                       const float* color, const float* depth, cudaStream_t st) {
     const dim3 n_tiles(v.tiles_x * v.tiles_y, nseg);
+    const uint32_t* order = tile_order(ranges, v.tiles_x * v.tiles_y);
     // 4 pixels per thread (2 warps per tile) unless overridden to 2 (4 warps per tile)
     if (blend_ppt(v, true) == 2)
         launch_pdl(blend_bwd_kernel<2>, n_tiles, 128, st, ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                     dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
+                                                     dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth, order);
     else
         launch_pdl(blend_bwd_kernel<4>, n_tiles, 64, st, ranges, vals, rec, emit_off, v, t_final, n_proc, dl_dcolor,
-                                                    dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth);
+                                                    dl_ddepth, depth_scale, partials, cnt, ck, nseg, color, depth, order);
 }
 
 }  // namespace gsb

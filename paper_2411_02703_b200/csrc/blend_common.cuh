@@ -202,6 +202,17 @@ __host__ __device__ inline int seg_len(int n_list, int nseg) {
     return nseg <= 1 ? n_list : div_up(div_up(n_list, nseg), kSegAlign) * kSegAlign;
 }
 
+// Tile launch order of the blends: tiles sorted by descending list length (longest first), so
+// the longest tiles start in the first wave instead of forming the tail of the last one. The
+// order sits behind the tile ranges in the same buffer (ranges[T], then order[T]).
+#ifndef GSB_LPT
+#define GSB_LPT 1
+#endif
+__host__ __device__ inline const uint32_t* tile_order(const uint2* ranges, int tiles) {
+    return GSB_LPT ? reinterpret_cast<const uint32_t*>(ranges + tiles) : nullptr;
+}
+void launch_tile_order(const uint2* ranges, int tiles, cudaStream_t st);
+
 // pixels-per-thread chosen per level (host override for experiments; 0 = automatic)
 int blend_ppt(const ViewParams& v, bool backward);
 // backward list segments per tile, chosen per level (host override; 0 = automatic)

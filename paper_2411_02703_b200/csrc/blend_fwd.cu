@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
-    float* __restrict__ ck, int nseg) {
+    float* __restrict__ ck, int nseg, const uint32_t* __restrict__ order) {
     pdl_enter();
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     constexpr int NT = S::kThreads / SUB, NP = (PPT + 1) / 2;
     __shared__ StageBuf<NT> sb;
     __shared__ Splat raw[NT];
-    const int tile = blockIdx.x / SUB;
+    const int tile = order ? static_cast<int>(order[blockIdx.x / SUB]) : static_cast<int>(blockIdx.x / SUB);
     const S sc(v.tiles_x, tile, (blockIdx.x % SUB) * (NT / 32) + (threadIdx.x >> 5));
     const uint2 range = ranges[tile];
     const double ox = sc.tx * kTile, oy = sc.ty * kTile;
@@ -694,10 +694,13 @@ int blend_ppt(const ViewParams& v, bool backward) {
     return backward ? 4 : 2;
 }
 
-void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
+int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib, bool stats, float* ck, int nseg, float* seg_scratch, cudaStream_t st) {
     const int n_tiles = v.tiles_x * v.tiles_y;
+    // the order is computed for every forward: the backward of the frame reads it too
+    const uint32_t* order = tile_order(ranges, n_tiles);
+    if (order) launch_tile_order(ranges, n_tiles, st);
     if (nseg > 1 && n_tiles <= g_seg_forward_tiles && seg_scratch) {
         const size_t P = static_cast<size_t>(v.width) * v.height;
         float* seg = seg_scratch;
@@ -714,14 +717,14 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
         else
             launch_pdl(fwd_seg_finish_kernel<2, false>, grid, kTileThreads / 2, st, 
                 ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
-        return;
+        return order ? 4 : 3;
     }
 #ifndef GSB_FWD_SUB
 #define GSB_FWD_SUB 1
 #endif
 #define GSB_FWD(P, S)                                                                                        \
     launch_pdl(blend_fwd_kernel<P, S, GSB_FWD_SUB>, n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, st,     \
-               ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg)
+               ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg, order)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);
@@ -730,6 +733,47 @@ void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* re
             if (stats) GSB_FWD(2, true); else GSB_FWD(2, false);
     }
 #undef GSB_FWD
+    return order ? 2 : 1;  // launches
+}
+
+// Counting sort of the tiles by list length, descending, in buckets of 16 entries (ties in any
+// order: the launch order does not change any tile's result). One CTA.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int tiles,
+                                                          uint32_t* __restrict__ order) {
+    pdl_enter();
+    constexpr int kBuckets = 1024;
+    __shared__ uint32_t cnt[kBuckets];
+    __shared__ uint32_t warp_tot[32];
+    auto bucket = [&](int t) {
+        const uint2 r = ranges[t];
+        return kBuckets - 1 - static_cast<int>(min((r.y - r.x) >> 4, static_cast<uint32_t>(kBuckets - 1)));
+    };
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) atomicAdd(&cnt[bucket(t)], 1u);
+    __syncthreads();
+    // exclusive scan of the 1024 bucket counts (thread i owns bucket i)
+    const uint32_t c = cnt[threadIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    uint32_t base = 0;
+    for (int w = 0; w < warp; ++w) base += warp_tot[w];
+    __syncthreads();
+    cnt[threadIdx.x] = base + incl - c;
+    __syncthreads();
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) order[atomicAdd(&cnt[bucket(t)], 1u)] = static_cast<uint32_t>(t);
+}
+
+void launch_tile_order(const uint2* ranges, int tiles, cudaStream_t st) {
+    launch_pdl(tile_order_kernel, 1, 1024, st, ranges, tiles,
+               const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(ranges + tiles)));
 }
 
 }  // namespace gsb

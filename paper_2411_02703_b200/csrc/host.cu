@@ -99,7 +99,8 @@ void frame_pixels(gs_frame* F, const ViewParams& v) {
     F->dl_dcolor.ensure(3 * P * sizeof(float));
     F->depth_cot.ensure(P * sizeof(float));
     F->loss.ensure(loss_buffer_bytes(v.height, v.width));
-    F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * sizeof(uint2));
+    // tile ranges, then the blends' tile launch order (blend_common.cuh tile_order)
+    F->ranges.ensure(static_cast<size_t>(v.tiles_x) * v.tiles_y * (sizeof(uint2) + sizeof(uint32_t)));
 }
 
 // every device buffer a render + loss + backward of view v needs (map size n, pair capacity
@@ -291,12 +292,12 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
             F->checkpoints.ensure(sizeof(float) * (F->nseg - 1) * kCkFields * P);
             F->seg_scratch.ensure(sizeof(float) * (9 * F->nseg + 2) * P);
         }
-        launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
+        const int k = launch_blend_fwd(F->ranges.as<uint2>(), n > 0 ? F->pair_vals2.as<uint32_t>() : nullptr,
                          n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
                          F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, F->checkpoints.as<float>(),
                          F->nseg, n > 0 && F->nseg > 1 ? F->seg_scratch.as<float>() : nullptr, st);
-        C->launched();
+        C->launched(k);
     }
     F->rendered = true;
     F->has_contrib = stats;

@@ -56,7 +56,7 @@ void launch_knn_init(const double* pts6, int64_t n, int k, const KnnGrid& g, con
                      cudaStream_t st);
 
 // raster.cu
-void launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
+int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib /* written only when stats */, bool stats,
                       float* checkpoints /* [nseg - 1][5][pixels] */, int nseg,
