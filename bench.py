@@ -493,16 +493,30 @@ def cpu_sample(scene, train, gt_levels, threads=0):
     pool = O.ThreadPool(threads)
     t = time.time()
     px = 0
+    level_s = {}
     for it in range(3):
+        t0 = time.time()
         r = O.train_keyframe_step(om, kf, cfg, cam, pool)
+        level_s[f"L{r['level']}"] = round(time.time() - t0, 3)
         h, w = level_shapes()[r["level"]]
         px += h * w
     dt = time.time() - t
+    # a single-thread run beside the pool -- the first (coarsest-level) iteration of
+    # the same keyframe on a fresh copy of the map, ThreadPool(1)
+    kf1 = O.Keyframe(pose, color0, depth0, 3, LEVELS)
+    om1 = O.OracleMap(train)
+    t0 = time.time()
+    r1 = O.train_keyframe_step(om1, kf1, cfg, cam, O.ThreadPool(1))
+    t1 = time.time() - t0
+    lv = f"L{r1['level']}"
     return {"value": round(3 / dt, 5), "unit": "iters/s", "cores": pool.threads, "kind": kind,
             "mpix_per_s": round(px / dt / 1e6, 4),
             "sample": f"{what}, train_keyframe_step: one L2->L1->L0 cycle (3 iterations) of keyframe 0 of the "
                       "same 1M-Gaussian workload",
-            "seconds": round(dt, 2)}
+            "seconds": round(dt, 2), "seconds_per_level": level_s,
+            "single_thread": {"level": r1["level"], "seconds": round(t1, 3), "threads": 1,
+                              "pool_seconds_same_level": level_s.get(lv),
+                              "pool_speedup": round(t1 / level_s[lv], 2) if level_s.get(lv) else None}}
 
 
 # ----------------------------------------------------------------------------- C5 mapping loop
