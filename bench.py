@@ -426,8 +426,12 @@ def run_ours(args, rank, world):
 
     # ---------------- e2e: same metric through the C-ABI with host buffers each step
     if not args.no_e2e:
+        # the e2e leg continues the step sequence (keyframe consumption and level schedule stay
+        # consistent whatever the warm-up and step counts)
+        eb = args.warmup + 2 * args.steps
         for s in range(3):
-            step(s, e2e=True)
+            step(eb + s, e2e=True)
+        eb += 3
         barrier()
         t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
@@ -439,16 +443,16 @@ def run_ours(args, rank, world):
             # train call right behind its enqueued work (gs_train_step_prefetch), so the copies
             # and their API calls overlap compute; every step's copy is inside the timed region
             # (step 0's included) and each train step waits for its own level's upload
-            k0, l0 = schedule(0)
+            k0, l0 = schedule(eb)
             kfs[k0].upload_level(l0, *host_levels[k0][l0])
         else:
-            l0 = LEVELS - 0 % 3
+            l0 = LEVELS - eb % 3
             for k in my_views:
                 kfs[k].upload_level(l0, *host_levels[k][l0])
         for s in range(args.steps):
-            v, _ = step(s, e2e=False, prefetch=s + 1 if s + 1 < args.steps else None)
+            v, _ = step(eb + s, e2e=False, prefetch=eb + s + 1 if s + 1 < args.steps else None)
             views += v
-            lvl = LEVELS - (s % 3)
+            lvl = LEVELS - ((eb + s) % 3)
             h2d += 32 * shapes[lvl][0] * shapes[lvl][1] * (views_per_rank if batch else 1)
         t1.record(stream)
         barrier()

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
         __syncwarp();
     };
     const uint2 range = ranges[tile];
+    [[maybe_unused]] const unsigned long long* const counters = cnt;  // (the batch loop's `cnt` is its entry count)
+    GSB_CHECK(range.x <= range.y && range.y <= counters[kCntPairs]);
     // this CTA's list segment [lo_s, hi_s) (blockIdx.y); the whole list when nseg = 1
     const int n_list = static_cast<int>(range.y - range.x);
     const int L = seg_len(n_list, nseg);
@@ -137,7 +139,9 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
     // entries of the segment no pixel reached still own a partial slot: zero it
     for (int j = max_last + threadIdx.x; j < hi_s; j += NT) {
         const uint32_t r = vals[range.x + j];
+        GSB_CHECK(r < counters[kCntVisible]);
         const uint32_t slot = emission_index(rec[r], emit_off[r], sc.tx, sc.ty);
+        GSB_CHECK(slot >= emit_off[r] && slot < emit_off[r + 1] && slot < counters[kCntPairs]);
         float2* dst = reinterpret_cast<float2*>(partials + static_cast<size_t>(slot) * kNumPartials);
 #pragma unroll
         for (int k = 0; k < kNumPartials / 2; ++k) dst[k] = make_float2(0.f, 0.f);
@@ -159,11 +163,13 @@ __global__ void __launch_bounds__(kTileThreads / PPT, GSB_BWD_MIN_BLOCKS) blend_
         if (threadIdx.x < cnt) {
             sb.put(threadIdx.x, stage_of(nsp, ox, oy));
             s_slot[threadIdx.x] = emission_index(nsp, noff, sc.tx, sc.ty);
+            GSB_CHECK(s_slot[threadIdx.x] < counters[kCntPairs]);
         }
         {
             const int nlo = max(lo_s, lo - kBwdBatch);
             if (threadIdx.x < lo - nlo) {
                 const uint32_t r = vals[range.x + nlo + threadIdx.x];
+                GSB_CHECK(r < counters[kCntVisible]);
                 nsp = rec[r];
                 noff = emit_off[r];
             }

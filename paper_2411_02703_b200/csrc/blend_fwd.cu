@@ -306,7 +306,9 @@ template <int PPT, bool STATS, int MODE, int NT = kTileThreads / PPT>
 __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<NT>& sb, Splat* raw,
                                            const Strip<PPT>& sc, const uint32_t* __restrict__ vals,
                                            const Splat* __restrict__ rec, uint2 full, int start, int end, double ox,
-                                           double oy, float fx, float* ck, int nseg, int width, int height) {
+                                           double oy, float fx, float* ck, int nseg, int width, int height,
+                                           [[maybe_unused]] const unsigned long long* cnt) {
+    GSB_CHECK(full.x <= full.y && full.y <= cnt[kCntPairs] && end <= static_cast<int>(full.y - full.x));
     // NT: threads of the CTA = the staging batch (a tile may be split over SUB CTAs)
     static_assert(kSegAlign % NT == 0, "segment boundaries must fall on staging batches");
     const int n_list = static_cast<int>(full.y - full.x);
@@ -322,7 +324,10 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
     int kw = 0;  // entries this warp has walked (uniform)
     const uint32_t b_end = full.x + end;
     const uint32_t i0 = full.x + start + threadIdx.x;
-    if (i0 < b_end) cp_async_splat(&raw[threadIdx.x], &rec[vals[i0]]);
+    if (i0 < b_end) {
+        GSB_CHECK(vals[i0] < cnt[kCntVisible]);
+        cp_async_splat(&raw[threadIdx.x], &rec[vals[i0]]);
+    }
     cp_async_commit();
     uint32_t nvi = i0 + NT < b_end ? vals[i0 + NT] : 0u;
     for (uint32_t base = full.x + start; base < b_end; base += NT) {
@@ -333,6 +338,7 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
         cp_async_wait_all();  // this thread's own record (each thread reads only its slot)
         if (idx < b_end) sb.put(threadIdx.x, stage_of(raw[threadIdx.x], ox, oy));
         if (idx + NT < b_end) {
+            GSB_CHECK(nvi < cnt[kCntVisible]);
             cp_async_splat(&raw[threadIdx.x], &rec[nvi]);
             if (idx + 2 * NT < b_end) nvi = vals[idx + 2 * NT];
         }
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
-    float* __restrict__ ck, int nseg, const uint32_t* __restrict__ order) {
+    float* __restrict__ ck, int nseg, const uint32_t* __restrict__ order, const unsigned long long* __restrict__ cnt) {
     pdl_enter();
     using S = Strip<PPT>;
     // PPT = 1 runs one (real) pixel per lane in the low half of the pair; the high half is never
@@ -430,10 +436,10 @@ __global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS *
     // fp32 + band for short lists; df32 for lists longer than df_list (wide band, long replays)
     if (static_cast<int>(range.y - range.x) > df_list)
         blend_walk<PPT, STATS, kDf, NT>(s, sb, raw, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox, oy,
-                                        fx, ck, nseg, v.width, v.height);
+                                        fx, ck, nseg, v.width, v.height, cnt);
     else
         blend_walk<PPT, STATS, kBand, NT>(s, sb, raw, sc, vals, rec, range, 0, static_cast<int>(range.y - range.x), ox,
-                                          oy, fx, ck, nseg, v.width, v.height);
+                                          oy, fx, ck, nseg, v.width, v.height, cnt);
     const size_t P = static_cast<size_t>(v.width) * v.height;
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
@@ -480,7 +486,7 @@ __device__ __forceinline__ void init_state(FwdState<(PPT + 1) / 2>& s, const Str
 template <int PPT, bool STATS>
 __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
-    ViewParams v, float* __restrict__ seg, int nseg) {
+    ViewParams v, float* __restrict__ seg, int nseg, const unsigned long long* __restrict__ cnt) {
     pdl_enter();
     using S = Strip<PPT>;
     __shared__ StageBuf<S::kThreads> sb;
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_local_kernel(
     FwdState<(PPT + 1) / 2> s;
     init_state<PPT>(s, sc, v.width, v.height);
     blend_walk<PPT, STATS, kLocal>(s, sb, raw, sc, vals, rec, range, lo, min(lo + L, n_list), ox, oy, fx, nullptr, 1,
-                                   v.width, v.height);
+                                   v.width, v.height, cnt);
     const size_t P = static_cast<size_t>(v.width) * v.height;
     float* base = seg + static_cast<size_t>(blockIdx.y) * kSegFields * P;
 #pragma unroll
@@ -588,7 +594,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib,
-    const float* __restrict__ tl_plane, const int32_t* __restrict__ star_plane, int nseg) {
+    const float* __restrict__ tl_plane, const int32_t* __restrict__ star_plane, int nseg,
+    const unsigned long long* __restrict__ cnt) {
     pdl_enter();
     using S = Strip<PPT>;
     constexpr int NP = (PPT + 1) / 2;
@@ -639,7 +646,8 @@ __global__ void __launch_bounds__(kTileThreads / PPT) fwd_seg_finish_kernel(
     if (__syncthreads_count(mine != 0u) == 0) return;
     const double ox = sc.tx * kTile, oy = sc.ty * kTile;
     const float fx = static_cast<float>(sc.lx);
-    blend_walk<PPT, STATS, kDf>(s, sb, raw, sc, vals, rec, range, lo, n_list, ox, oy, fx, nullptr, 1, v.width, v.height);
+    blend_walk<PPT, STATS, kDf>(s, sb, raw, sc, vals, rec, range, lo, n_list, ox, oy, fx, nullptr, 1, v.width, v.height,
+                                cnt);
 #pragma unroll
     for (int p = 0; p < PPT; ++p) {
         if (!((mine >> p) & 1u)) continue;
@@ -696,7 +704,8 @@ int blend_ppt(const ViewParams& v, bool backward) {
 
 int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const ViewParams& v,
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
-                      int32_t* n_contrib, bool stats, float* ck, int nseg, float* seg_scratch, cudaStream_t st) {
+                      int32_t* n_contrib, bool stats, float* ck, int nseg, float* seg_scratch,
+                      const unsigned long long* cnt, cudaStream_t st) {
     const int n_tiles = v.tiles_x * v.tiles_y;
     // the order is computed for every forward: the backward of the frame reads it too
     const uint32_t* order = tile_order(ranges, n_tiles);
@@ -707,16 +716,16 @@ int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec
         float* tl_plane = seg_scratch + static_cast<size_t>(nseg) * kSegFields * P;
         int32_t* star = reinterpret_cast<int32_t*>(tl_plane + P);
         const dim3 grid(n_tiles, nseg);
-        if (stats) launch_pdl(fwd_seg_local_kernel<2, true>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg);
-        else launch_pdl(fwd_seg_local_kernel<2, false>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg);
+        if (stats) launch_pdl(fwd_seg_local_kernel<2, true>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg, cnt);
+        else launch_pdl(fwd_seg_local_kernel<2, false>, grid, kTileThreads / 2, st, ranges, vals, rec, v, seg, nseg, cnt);
         launch_pdl(fwd_seg_chain_kernel, div_up(static_cast<int>(P), 256), 256, st, 
             ranges, v, seg, nseg, color, depth, vis, t_final, n_proc, stats ? n_contrib : nullptr, tl_plane, star, ck);
         if (stats)
             launch_pdl(fwd_seg_finish_kernel<2, true>, grid, kTileThreads / 2, st, 
-                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
+                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg, cnt);
         else
             launch_pdl(fwd_seg_finish_kernel<2, false>, grid, kTileThreads / 2, st, 
-                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg);
+                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, tl_plane, star, nseg, cnt);
         return order ? 4 : 3;
     }
 #ifndef GSB_FWD_SUB
@@ -724,7 +733,7 @@ int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec
 #endif
 #define GSB_FWD(P, S)                                                                                        \
     launch_pdl(blend_fwd_kernel<P, S, GSB_FWD_SUB>, n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, st,     \
-               ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg, order)
+               ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg, order, cnt)
     switch (blend_ppt(v, false)) {
         case 4:
             if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);

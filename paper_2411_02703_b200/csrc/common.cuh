@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace gsb {
 
 // Programmatic dependent launch along the training step's kernel chain: a kernel launched with
@@ -40,6 +42,24 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
     return cudaGetLastError();
 #endif
 }
+
+// Device-side bounds assertions, compiled in only by the checked build (diag/build_variant.sh
+// checked -DGSB_CHECKS): compute-sanitizer is closed on this GPU pool, so the index invariants
+// of the hot kernels are asserted in-kernel instead and the GPU suite runs against that build.
+#ifdef GSB_CHECKS
+#define GSB_CHECK(cond)                                                                   \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("GSB_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #cond);   \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define GSB_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 constexpr int kTile = 16;                 // rasterizer.hpp:17 kTileSize
 constexpr int kTileThreads = kTile * kTile;

@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
     const uint32_t off = emit_off[q0 + min(lane, nr)];  // lane l: first row of rank q0 + l
     const uint32_t end = __shfl_sync(0xffffffffu, emit_off[q0 + nr], 0);
     const uint32_t beg = __shfl_sync(0xffffffffu, off, 0);
+    GSB_CHECK(beg <= end && end <= cnt[kCntPairs]);
     double acc[kNumPartials];
 #pragma unroll
     for (int k = 0; k < kNumPartials; ++k) acc[k] = 0.0;
@@ -536,7 +537,9 @@ __global__ void __launch_bounds__(kBwdThreads) preprocess_bwd_kernel(
     const int t = blockIdx.x * kBwdThreads + threadIdx.x;
     if (t >= static_cast<int>(cnt[kCntVisible]) || overflowed(cnt)) return;
     const int i = vis_gid[t];
+    GSB_CHECK(i >= 0 && i < gcap);
     const int r = rank_of[i];
+    GSB_CHECK(r >= 0 && r < static_cast<int>(cnt[kCntVisible]));
     if (emit_off[r] == emit_off[r + 1]) return;  // no tile: never touched (rasterizer.cpp:327)
     float gp[kGeomParams];  // map-indexed: all loads in flight at once
 #pragma unroll

@@ -296,7 +296,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
                          n > 0 ? F->rec_sorted.as<Splat>() : nullptr, v, F->color.as<float>(),
                          F->depth.as<float>(), F->vis.as<float>(), F->t_final.as<float>(),
                          F->n_proc.as<int32_t>(), F->n_contrib.as<int32_t>(), stats, F->checkpoints.as<float>(),
-                         F->nseg, n > 0 && F->nseg > 1 ? F->seg_scratch.as<float>() : nullptr, st);
+                         F->nseg, n > 0 && F->nseg > 1 ? F->seg_scratch.as<float>() : nullptr, dev_counters(F), st);
         C->launched(k);
     }
     F->rendered = true;

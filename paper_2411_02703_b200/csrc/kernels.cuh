@@ -60,7 +60,8 @@ int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec
                       float* color, float* depth, float* vis, float* t_final, int32_t* n_proc,
                       int32_t* n_contrib /* written only when stats */, bool stats,
                       float* checkpoints /* [nseg - 1][5][pixels] */, int nseg,
-                      float* seg_scratch /* [(9 nseg + 2) pixels]: segmented forward, nullable */, cudaStream_t st);
+                      float* seg_scratch /* [(9 nseg + 2) pixels]: segmented forward, nullable */,
+                      const unsigned long long* counters /* bounds of the checked build */, cudaStream_t st);
 void launch_blend_bwd(const uint2* ranges, const uint32_t* vals, const Splat* rec, const uint32_t* emit_off,
                       const ViewParams& v, const float* t_final, const int32_t* n_proc,
                       const float* dl_dcolor, const float* dl_ddepth, const float* depth_scale,

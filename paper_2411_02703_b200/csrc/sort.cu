@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(const KeyT* __restrict__ k
         for (int i = 0; i < IT; ++i) {
             if (dig[i] < kRadix) {
                 const uint32_t lp = s_tstart[dig[i]] + s_whist[warp][dig[i]] + rnk[i];
+                GSB_CHECK(lp < static_cast<uint32_t>(TILE));
                 s_keys[lp] = key[i];
                 s_vals[lp] = val[i];
             }
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(const KeyT* __restrict__ k
         for (uint32_t j = tid; j < tn; j += NT) {
             const KeyT k = s_keys[j];
             const uint32_t g = s_run[(static_cast<uint32_t>(k) >> shift) & mask] + j;
+            GSB_CHECK(g < n);
             if (KEYS_OUT) kout[g] = k;
             vout[g] = s_vals[j];
         }
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(NT) fix_ties_kernel(const uint32_t* __restrict
             const unsigned long long dq = depth[gq];
             r += (dq < d || (dq == d && gq < g)) ? 1 : 0;
         }
+        GSB_CHECK(s + r < e);  // the run members' ranks are a permutation of [0, e - s)
         gid_out[s + r] = g;
     }
 }
@@ -475,6 +478,7 @@ __global__ void __launch_bounds__(NT) emit_pairs_kernel(const uint32_t* __restri
                 const uint32_t l = e - o;
                 const uint32_t row = nx == 1 ? l : __umulhi(l, mg);
                 const uint32_t k = static_cast<uint32_t>(bk) + row * static_cast<uint32_t>(tiles_x) + (l - row * nx);
+                GSB_CHECK(e < cap && l - row * nx < static_cast<uint32_t>(nx) && rbase + rl < static_cast<uint32_t>(n_vis));
                 keys[e] = static_cast<KeyT>(k);
                 vals[e] = rbase + rl;
                 atomicAdd(&s_hist[0][k & m0], 1u);
