@@ -19,6 +19,9 @@
 #ifndef GSB_FWD_MIN_BLOCKS
 #define GSB_FWD_MIN_BLOCKS 6  // 80 registers, 6 CTAs per SM: -13% at full resolution (diag/variant_levels.sh)
 #endif
+// levels with more tiles than kFwdWideTiles run a 7-CTA build (72 registers): -2.5% on the
+// full-resolution forward, +6% at 1280 tiles (diag/variant_levels.sh)
+constexpr int kFwdWideTiles = 2048, kFwdWideBlocks = 7;
 #ifdef GSB_NEAR_NOINLINE
 #define GSB_NEAR_INLINE __noinline__
 #else
@@ -398,8 +401,8 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
 // SUB CTAs per tile, each with kThreads / SUB threads (its share of the tile's warps): finer work
 // units for the block scheduler (a level whose tile count is not a multiple of the resident CTA
 // slots leaves a part-empty last wave)
-template <int PPT, bool STATS, int SUB>
-__global__ void __launch_bounds__(kTileThreads / PPT / SUB, GSB_FWD_MIN_BLOCKS * SUB) blend_fwd_kernel(
+template <int PPT, bool STATS, int SUB, int MINB = GSB_FWD_MIN_BLOCKS>
+__global__ void __launch_bounds__(kTileThreads / PPT / SUB, MINB * SUB) blend_fwd_kernel(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
     ViewParams v, float* __restrict__ out_color, float* __restrict__ out_depth, float* __restrict__ out_vis,
     float* __restrict__ out_t, int32_t* __restrict__ out_nproc, int32_t* __restrict__ out_ncontrib, int df_list,
@@ -731,15 +734,17 @@ int launch_blend_fwd(const uint2* ranges, const uint32_t* vals, const Splat* rec
 #ifndef GSB_FWD_SUB
 #define GSB_FWD_SUB 1
 #endif
-#define GSB_FWD(P, S)                                                                                        \
-    launch_pdl(blend_fwd_kernel<P, S, GSB_FWD_SUB>, n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, st,     \
+#define GSB_FWD(P, S, B)                                                                                        \
+    launch_pdl(blend_fwd_kernel<P, S, GSB_FWD_SUB, B>, n_tiles * GSB_FWD_SUB, kTileThreads / P / GSB_FWD_SUB, st,  \
                ranges, vals, rec, v, color, depth, vis, t_final, n_proc, n_contrib, g_df_list, ck, nseg, order, cnt)
     switch (blend_ppt(v, false)) {
         case 4:
-            if (stats) GSB_FWD(4, true); else GSB_FWD(4, false);
+            if (stats) GSB_FWD(4, true, GSB_FWD_MIN_BLOCKS); else GSB_FWD(4, false, GSB_FWD_MIN_BLOCKS);
             break;
         default:
-            if (stats) GSB_FWD(2, true); else GSB_FWD(2, false);
+            if (stats) GSB_FWD(2, true, GSB_FWD_MIN_BLOCKS);
+            else if (n_tiles > kFwdWideTiles) GSB_FWD(2, false, kFwdWideBlocks);
+            else GSB_FWD(2, false, GSB_FWD_MIN_BLOCKS);
     }
 #undef GSB_FWD
     return order ? 2 : 1;  // launches
