@@ -294,7 +294,10 @@ void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, i
 // rasterizer.cpp:81-88 (pixel rect -> tile rect).
 // 3 CTAs per SM (80 registers, 80 B of L1-resident spills) beat the unconstrained 128-register
 // build: the fp64 chain is latency-bound and the extra warps hide it (measured -6%)
-__global__ void __launch_bounds__(256, 3) preprocess_fwd_kernel(
+#ifndef GSB_K1_MIN_BLOCKS
+#define GSB_K1_MIN_BLOCKS 4  // 64 registers (small spill): -3% on K1 against 3 (diag/variant_levels.sh)
+#endif
+__global__ void __launch_bounds__(256, GSB_K1_MIN_BLOCKS) preprocess_fwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree,
     const int32_t* __restrict__ cand, ViewParams v, Splat* __restrict__ rec_by_gid,
     unsigned long long* __restrict__ depth_key, int32_t* __restrict__ vis_gid, uint32_t* __restrict__ key32,
