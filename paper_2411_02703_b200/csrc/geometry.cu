@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(kBwdThreads) reduce_partials_kernel(const uint
 }
 
 template <bool ACC>
-__global__ void __launch_bounds__(kBwdThreads) preprocess_bwd_kernel(
+#ifndef GSB_K8B_MIN_BLOCKS
+#define GSB_K8B_MIN_BLOCKS 12  // 85 registers: -3% on K8 against the unconstrained 128 (diag/variant_levels.sh)
+#endif
+__global__ void __launch_bounds__(kBwdThreads, GSB_K8B_MIN_BLOCKS) preprocess_bwd_kernel(
     const float* __restrict__ params, int64_t cap, const int8_t* __restrict__ degree, ViewParams v,
     const uint32_t* __restrict__ emit_off, const float* __restrict__ sums, const unsigned long long* __restrict__ cnt,
     float* __restrict__ grads, int64_t gcap, const int32_t* __restrict__ rank_of, const int32_t* __restrict__ vis_gid) {

@@ -153,7 +153,10 @@ __device__ __forceinline__ uint32_t clamp_count(const unsigned long long* count,
 // ------------------------------------------------------------------------------------------
 // one LSD pass over digit (key >> shift) & (2^bits - 1); hist = this pass's digit histogram
 template <typename KeyT, bool KEYS_OUT>
-__global__ void __launch_bounds__(NT) onesweep_kernel(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+// the 32-bit (depth) passes with an explicit 1-CTA bound (ptxas then allocates for it: -5% on the
+// depth sort), the 16-bit (tile) passes unconstrained (the same bound costs them +10%); a 0
+// bound emits no .minnctapersm (diag/variant_levels.sh)
+__global__ void __launch_bounds__(NT, sizeof(KeyT) == 4 ? 1 : 0) onesweep_kernel(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       const unsigned long long* __restrict__ count, uint32_t cap,
                                                       int shift, int bits, const uint32_t* __restrict__ hist,
@@ -315,7 +318,10 @@ __global__ void __launch_bounds__(NT) fix_ties_kernel(const uint32_t* __restrict
 // 4 x NT ranks (4 consecutive per thread), one look-back word per tile (walked by a warp).
 constexpr int kPackItems = 4;
 
-__global__ void __launch_bounds__(NT) pack_scan_kernel(const int32_t* __restrict__ gid_sorted,
+#ifndef GSB_PACK_MIN_BLOCKS
+#define GSB_PACK_MIN_BLOCKS 2  // 2 resident CTAs per SM (from 118 to 96 registers): -6% on K2 + pack
+#endif
+__global__ void __launch_bounds__(NT, GSB_PACK_MIN_BLOCKS) pack_scan_kernel(const int32_t* __restrict__ gid_sorted,
                                                        const Splat* __restrict__ rec_by_gid,
                                                        const unsigned long long* __restrict__ depth_by_gid,
                                                        const unsigned long long* __restrict__ cnt,
