@@ -246,6 +246,7 @@ __device__ __forceinline__ void rotation_partial(const double u[4], int k, doubl
 __global__ void __launch_bounds__(256) cull_kernel(const float* __restrict__ params, int64_t cap, int n,
                                                    ViewParams v, int32_t* __restrict__ cand,
                                                    unsigned long long* __restrict__ counters) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool keep = false;
     if (i < n) {
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(256) cull_kernel(const float* __restrict__ par
 
 void launch_cull(const float* params, int64_t cap, int n, const ViewParams& v, int32_t* cand,
                  unsigned long long* counters, cudaStream_t st) {
-    if (n > 0) cull_kernel<<<div_up(n, 256), 256, 0, st>>>(params, cap, n, v, cand, counters);
+    if (n > 0) launch_pdl(cull_kernel, div_up(n, 256), 256, st, params, cap, n, v, cand, counters);
 }
 
 // K1b: exact projection of the candidates (grid-stride over the device-side candidate count).

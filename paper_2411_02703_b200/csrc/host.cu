@@ -225,9 +225,7 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     const int n = static_cast<int>(M->n);
     const int T = v.tiles_x * v.tiles_y;
     reserve_frame(F, v, 0, 0);
-    ck(cudaMemsetAsync(F->ranges.p, 0, sizeof(uint2) * T, st), "memset ranges");
     F->counters.ensure(kNumCounters * sizeof(unsigned long long));
-    ck(cudaMemsetAsync(F->counters.p, 0, kNumCounters * sizeof(unsigned long long), st), "memset counters");
     F->n_vis = 0;
     F->n_pairs = 0;
     F->overflow = false;
@@ -235,9 +233,10 @@ void render_impl(gs_map* M, const gs_pose& pose, const gs_camera& cam, gs_frame*
     F->pair_cap = 0;
     F->vis_cap = 0;
     unsigned long long* cnt = dev_counters(F);
+    if (n > 0) reserve_frame(F, v, n, 0);
+    launch_frame_init(F->ranges.as<uint2>(), T, cnt, n > 0 ? F->sort_block.as<SortBlock>() : nullptr, st);
+    C->launched();
     if (n > 0) {
-        reserve_frame(F, v, n, 0);
-        ck(cudaMemsetAsync(F->sort_block.p, 0, sizeof(SortBlock), st), "memset sort block");
         {
             Scope sc(C, "preprocess_fwd");
             launch_cull(M->params, M->cap, n, v, F->vis_flag.as<int32_t>(), cnt, st);
@@ -415,7 +414,8 @@ void loss_impl(gs_frame* F, gs_keyframe* K, int level, const gs_train_config& cf
     gs_context* C = F->ctx;
     cudaStream_t st = C->stream;
     K->acquire(level, st);
-    ck(cudaMemsetAsync(F->loss.p, 0, loss_buffer_bytes(h, w), st), "memset loss");
+    // (no zeroing of the loss buffer: every slot the finalize reads is written by this call's
+    // kernels, and the finalize writes every header field)
     Scope sc(C, "loss_l1_ssim_depth");
     LossLayout layout{};
     if (cfg.lambda != 0.0) {

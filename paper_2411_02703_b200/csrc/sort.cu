@@ -525,6 +525,19 @@ __global__ void tile_ranges_kernel(const KeyT* __restrict__ keys, const unsigned
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Start of a render: zero the tile ranges (tiles without pairs keep (0, 0)), the device counters
+// and the sort block in one PDL launch (three memsets used to break the kernel chain)
+__global__ void __launch_bounds__(1024) frame_init_kernel(uint2* __restrict__ ranges, int tiles,
+                                                          unsigned long long* __restrict__ counters,
+                                                          uint32_t* __restrict__ sb, int sb_words) {
+    pdl_enter();
+    for (int i = threadIdx.x; i < tiles; i += blockDim.x) ranges[i] = make_uint2(0u, 0u);
+    if (threadIdx.x < kNumCounters) counters[threadIdx.x] = 0ull;
+    if (sb)
+        for (int i = threadIdx.x; i < sb_words; i += blockDim.x) sb[i] = 0u;
+}
+
 // ============================================================================ host launchers
 namespace {
 int g_sm_count = 0;
@@ -607,6 +620,11 @@ static void tile_sort_impl(const uint32_t* emit_off, const Splat* rec, unsigned 
     constexpr int KV = 16 / sizeof(KeyT);
     launch_pdl(tile_ranges_kernel<KeyT>, persistent_grid(div_up(static_cast<int64_t>(cap), KV * 256), 8), 256, st, 
         kb, cnt, cap, ranges);
+}
+
+void launch_frame_init(uint2* ranges, int tiles, unsigned long long* counters, SortBlock* sb, cudaStream_t st) {
+    launch_pdl(frame_init_kernel, 1, 1024, st, ranges, tiles, counters, reinterpret_cast<uint32_t*>(sb),
+               sb ? static_cast<int>(sizeof(SortBlock) / sizeof(uint32_t)) : 0);
 }
 
 int launch_tile_sort(const uint32_t* emit_off, const Splat* rec, unsigned long long* cnt, int max_n, uint32_t cap,

@@ -39,6 +39,8 @@ void launch_pack_scan(const int32_t* gid_sorted, const Splat* rec_by_gid, const 
 // emission of the (tile, rank) pairs + stable sort by tile + ranges; the sorted ranks land in
 // vals_b (keys in keys_b: uint16 while tiles <= 0xffff, else uint32). Uses epochs epoch,
 // epoch + 1. Returns the number of kernel launches.
+// zero the tile ranges [tiles], the device counters and (if non-null) the sort block
+void launch_frame_init(uint2* ranges, int tiles, unsigned long long* counters, SortBlock* sb, cudaStream_t st);
 int launch_tile_sort(const uint32_t* emit_off, const Splat* rec, unsigned long long* cnt, int max_n, uint32_t cap,
                      int tiles_x, int tiles, void* keys_a, void* keys_b, uint32_t* vals_a, uint32_t* vals_b,
                      uint2* ranges, SortBlock* sb, unsigned long long* status, uint32_t epoch, cudaStream_t st);
