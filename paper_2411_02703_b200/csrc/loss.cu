@@ -140,6 +140,7 @@ constexpr float kShift = 0.5f;
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                        int h, int w, float inv_n, float* __restrict__ wbuf,
                                                        LossScalars* __restrict__ acc, int stride) {
+    pdl_enter();
     __shared__ float sa[kInY][kInX + 2], sb[kInY][kInX + 2];
     __shared__ float hs[5][kInY][kSx + 1];
     __shared__ double scratch[8];
@@ -366,7 +367,7 @@ LossLayout launch_ssim(const float* color, const float* gt_color, int h, int w, 
     const int vh = h - kHalo, vw = w - kHalo;
     const float inv_n = static_cast<float>(1.0 / (static_cast<double>(vh) * vw * 3));
     dim3 gf(div_up(vw, kSx), div_up(vh, kSy), 3);
-    ssim_fwd_kernel<<<gf, 256, 0, st>>>(color, gt_color, h, w, inv_n, wbuf, acc, L.stride);
+    launch_pdl(ssim_fwd_kernel, gf, 256, st, color, gt_color, h, w, inv_n, wbuf, acc, L.stride);
     L.n[kLossSsim] = static_cast<int>(gf.x * gf.y * gf.z);
     dim3 gb(div_up(w, kSx), div_up(h, kSy), 3);
     if (depth) {  // fused pixel loss (loss_pixel_kernel is not launched)

@@ -566,7 +566,8 @@ void launch_depth_sort(uint32_t* keys_a, uint32_t* keys_b, int32_t* vis_gid, int
     if (max_n <= 0) return;
     const uint32_t cap = static_cast<uint32_t>(max_n);
     const unsigned long long* nvis = cnt + kCntVisible;
-    radix_hist_kernel<<<persistent_grid(div_up(max_n, NT * 8), 2), NT, 0, st>>>(keys_a, nvis, cap, 3, sb->hist[0]);
+    launch_pdl(radix_hist_kernel, persistent_grid(div_up(max_n, NT * 8), 2), NT, st, static_cast<const uint32_t*>(keys_a),
+               nvis, cap, 3, sb->hist[0]);
     const int grid = persistent_grid(div_up(max_n, TILE), 4);
     // (keys_a, vis_gid) -> (keys_b, gid_tmp) -> (keys_a, gid_sorted) -> (keys_b, gid_tmp) -> exact tie
     // order into gid_sorted; vis_gid (K1's append order) is kept for K8
