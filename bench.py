@@ -88,8 +88,9 @@ class ClockSampler:
     NAMES = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
              ("hw_power_brake_slowdown", 0x80), ("sw_power_cap", 0x4))
 
-    def __init__(self, device_index=0):
+    def __init__(self, device_index=0, period=0.002):
         self.dev = device_index
+        self.period = float(os.environ.get("GS_CLOCK_PERIOD", period))
         self.h = None
         self.samples = []
         self.mx = None
@@ -115,7 +116,7 @@ class ClockSampler:
             pass
 
     def _run(self):
-        while not self.stop.wait(0.002):
+        while not self.stop.wait(self.period):
             self._sample()
 
     def __enter__(self):
@@ -554,6 +555,13 @@ def run_c5(args):
         G.render(gt_map, poses[f], cam, fr)
         colors.append(np.floor(np.clip(fr.color, 0.0, 1.0) * 255.0 + 0.5) / 255.0)  # stored as 8-bit images
     del gt_map, fr
+
+    def pinned(a):  # the sequence loader's frames staged in pinned host memory (as the C3 e2e leg)
+        out = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+        out[...] = a
+        return out
+    clouds = [pinned(c) for c in clouds]
+    colors = [pinned(c) for c in colors]
     t_fix = time.time() - t
     mk = lambda budget: MappingConfig(iter_budget=budget, train=G.TrainConfig.make(0.2, 0.5, LEVELS))
     # warm-up: a short loop on a throw-away map (allocations, CUB temp sizes, first launches)
@@ -564,6 +572,7 @@ def run_c5(args):
     if args.c5_phases:
         ctx.profile(True)  # per-phase CUDA-event table of the integration calls (train steps included)
     launches0 = ctx.launches
+    cap0 = ctx.capacity_stats()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     gc.collect()
     gc.freeze()  # setup objects leave the collector's generations: no multi-ms gen-2 pauses in the timed loop
@@ -577,10 +586,11 @@ def run_c5(args):
         wall = time.perf_counter() - w0
     dev_ms = e0.elapsed_time(e1)
     launches = ctx.launches - launches0
+    cap1 = ctx.capacity_stats()
+    capacity = {k: cap1[k] - cap0[k] for k in cap1}
     phases = None
     if args.c5_phases:
-        phases = {k: {"ms": round(v[0], 2), "calls": v[1]} for k, v in ctx.profile_read().items()
-                  if k.startswith("kf_") or k == "map_reserve"}
+        phases = {k: {"ms": round(v[0], 2), "calls": v[1]} for k, v in ctx.profile_read().items()}
         ctx.profile(False)
     # evaluate_sequence (gt depth = the projected cloud, as without a gt depth file)
     torch.cuda.synchronize()
@@ -612,9 +622,12 @@ def run_c5(args):
                        "gt_gaussians": args.c5_gaussians, "iter_budget": args.c5_budget, "tau_alpha": 0.5,
                        "prune_interval": 50, "sh_interval": 300, "cloud_points": [len(c) for c in clouds]},
             "device_ms": round(dev_ms, 2), "wall_ms": round(wall * 1e3, 2), "gpu_launches": launches,
+            "capacity_events": capacity,
             "map": {"final_gaussians": len(m), "added_per_keyframe": loop.added, "pruned": loop.pruned,
                     "max_sh_degree": m.max_active_degree()},
-            "rows": rows, "integrate_phases": phases,
+            "rows": rows, "rows_note": "host wall time per call (no device synchronisation around the calls: a train "
+                                       "step returns after its own loss read-back, the housekeeping calls once enqueued)",
+            "integrate_phases": phases,
             "evaluate": {"frames": len(recs), "ms_per_frame": round(t_eval * 1e3 / len(recs), 3),
                          "mean_psnr": round(float(np.mean(psnr)), 4),
                          "mean_ssim": round(float(np.mean([r["ssim"] for r in recs])), 5)},

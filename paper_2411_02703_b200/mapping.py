@@ -59,13 +59,14 @@ class MappingLoop:
         self._pending: _Entry | None = None  # the next sampled step (drawn one ahead)
 
     def _clock(self, name, fn, *a):
+        # host wall time per call, without device synchronisation (a sync here would also wait
+        # for the next step's speculative render and leave the device idle through the host's
+        # bookkeeping): a train step returns after its own loss read-back, the housekeeping
+        # calls after enqueuing their work
         if not self.timed:
             return fn(*a)
-        import torch
-        torch.cuda.synchronize()
         t = time.perf_counter()
         r = fn(*a)
-        torch.cuda.synchronize()
         self.times[name] = self.times.get(name, 0.0) + time.perf_counter() - t
         self.calls[name] = self.calls.get(name, 0) + 1
         return r
