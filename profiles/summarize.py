@@ -51,7 +51,7 @@ def full(path):
         print("  stalls per issued instruction: " + ", ".join(f"{k}={v:.2f}" for k, v in stalls[:8]))
 
 
-FAMILY = [("cull", "preprocess_fwd"), ("preprocess_fwd", "preprocess_fwd"), ("radix_hist", "depth_sort_pack_scan"),
+FAMILY = [("frame_init", "preprocess_fwd"), ("tile_order", "blend_fwd"), ("cull", "preprocess_fwd"), ("preprocess_fwd", "preprocess_fwd"), ("radix_hist", "depth_sort_pack_scan"),
           ("onesweep_kernel<unsigned int", "depth_sort_pack_scan"), ("fix_ties", "depth_sort_pack_scan"),
           ("pack_scan", "depth_sort_pack_scan"), ("emit_pairs", "tile_keys_sort_ranges"),
           ("onesweep_kernel<unsigned short", "tile_keys_sort_ranges"), ("tile_ranges", "tile_keys_sort_ranges"),
@@ -78,10 +78,13 @@ def table(path, traffic_out=None):
     fam_bytes = {}
     print(f"{'lvl':3s} {'kernel':34s} {'us':>8s} {'DRAM MB':>8s} {'GB/s':>7s} {'issue%':>6s} {'warps%':>6s} "
           f"{'FMA%':>5s} {'ALU%':>5s} {'XU%':>5s} {'regs':>4s}")
+    prev = ""
     for row in rows:
         name = row[col["Kernel Name"]].replace("void ", "").split("(")[0]
-        if name.startswith("cull"):
+        # a render starts with frame_init (then cull); older captures start at cull
+        if name.startswith("frame_init") or (name.startswith("cull") and not prev.startswith("frame_init")):
             step += 1
+        prev = name
         lv = levels[step] if 0 <= step < 3 else f"s{step}"
         t = num(row, "gpu__time_duration.sum", us[units[col["gpu__time_duration.sum"]]])
         d = (num(row, "dram__bytes_read.sum", mb[units[col["dram__bytes_read.sum"]]]) +
