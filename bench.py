@@ -172,11 +172,23 @@ def algorithmic(stats_by_level, n, sp):
 
 
 # ----------------------------------------------------------------------------- our arm
+def local_device() -> int:
+    """This rank's GPU: LOCAL_RANK (modulo the visible devices)."""
+    import torch
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+
+
+def coll_device(dev: int) -> str:
+    """Where a collective's tensor lives: the GPU under NCCL, the host under gloo."""
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else f"cuda:{dev}"
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_2411_02703_b200 import gsmap as G
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = local_device()
     torch.cuda.set_device(dev)
     # one explicit stream for everything: the C-ABI context launches on it and the timing
     # events are recorded on it (torch's default stream handle is 0, for which the context
@@ -303,7 +315,7 @@ def run_ours(args, rank, world):
     ms_max = ms
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], device=f"cuda:{dev}")
+        t = torch.tensor([ms], device=coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     total_views = views * world
@@ -460,7 +472,7 @@ def run_ours(args, rank, world):
         e_ms = t0.elapsed_time(t1)
         if world > 1:
             import torch.distributed as dist
-            t = torch.tensor([e_ms], device=f"cuda:{dev}")
+            t = torch.tensor([e_ms], device=coll_device(dev))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         result["e2e"] = {"value": round(views * world / (e_ms / 1e3), 3), "unit": "iters/s",
@@ -703,8 +715,10 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # GS_DIST_BACKEND=gloo: host-side collectives, for a functional run of the multi-rank
+        # path with several ranks on one GPU (never a measurement)
+        dist.init_process_group(os.environ.get("GS_DIST_BACKEND", "nccl"))
     result, ctxdata = run_ours(args, rank, world)
     if world == 1 and not args.batch and args.sh_degree == 0 and not args.profile_only:
         # d = 0 and d = 3 reported separately (same workload, every SH band active)
