@@ -123,13 +123,13 @@ struct FwdState {
 };
 
 // Pixels whose fp32 transmittance fell below t_near after the entry at `pos` (bits in `near`):
-// decide T64 < 1e-4 exactly. Called by the whole warp; kw = entries this warp has walked so far
-// (every pixel of the warp has taken at most kw factors).
+// decide T64 < 1e-4 exactly. Called by the whole warp; every pixel has taken at most pos + 1
+// factors (the list entries up to pos).
 template <int PPT>
 __device__ GSB_NEAR_INLINE void resolve_near(FwdState<(PPT + 1) / 2>& s, unsigned near, const Strip<PPT>& sc, int pos,
-                                          int kw, float fx, const uint32_t* __restrict__ vals,
+                                          float fx, const uint32_t* __restrict__ vals,
                                           const Splat* __restrict__ rec, uint2 range, double ox, double oy) {
-    const double beta = kBetaPerFactor * kw;
+    const double beta = kBetaPerFactor * (pos + 1);
     unsigned amb = 0;
 #pragma unroll
     for (int p = 0; p < 2 * ((PPT + 1) / 2); ++p) {
@@ -200,7 +200,7 @@ enum FwdMode : int { kBand = 0, kDf = 1, kLocal = 2 };
 // STATS: maintain n_contrib (only the public render reports it).
 template <int PPT, bool COVER, bool STATS, int MODE, bool CLAMP>
 __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Strip<PPT>& sc, const int4& rc,
-                                          float2 m, float4 cn, float4 col, int pos, int kw, float fx,
+                                          float2 m, float4 cn, float4 col, int pos, float fx,
                                           const uint32_t* __restrict__ vals, const Splat* __restrict__ rec,
                                           uint2 range, double ox, double oy) {
     constexpr int NP = (PPT + 1) / 2;
@@ -274,7 +274,7 @@ __device__ __forceinline__ void fwd_entry(FwdState<(PPT + 1) / 2>& s, const Stri
         unsigned near = 0;
 #pragma unroll
         for (int p = 0; p < 2 * NP; ++p) near |= static_cast<unsigned>(nb[p]) << p;
-        resolve_near<PPT>(s, near, sc, pos, kw, fx, vals, rec, range, ox, oy);
+        resolve_near<PPT>(s, near, sc, pos, fx, vals, rec, range, ox, oy);
     }
 }
 
@@ -324,7 +324,6 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
     s.arm(t_near);
     int4 lb = warp_bbox<PPT>(s.live, sc);
     unsigned seen = s.live;
-    int kw = 0;  // entries this warp has walked (uniform)
     const uint32_t b_end = full.x + end;
     const uint32_t i0 = full.x + start + threadIdx.x;
     if (i0 < b_end) {
@@ -374,20 +373,19 @@ __device__ __forceinline__ void blend_walk(FwdState<(PPT + 1) / 2>& s, StageBuf<
                 todo &= todo - 1;
                 const int j = b0 + bit;
                 const int pos = static_cast<int>(base - full.x) + j;
-                ++kw;
                 const float4 cn = sb.con[j];
                 if (!((clp >> bit) & 1u)) {
                     if ((cov >> bit) & 1u)
-                        fwd_entry<PPT, true, STATS, MODE, false>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, kw, fx,
+                        fwd_entry<PPT, true, STATS, MODE, false>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, fx,
                                                                  vals, rec, full, ox, oy);
                     else
                         fwd_entry<PPT, false, STATS, MODE, false>(s, sc, sb.rect[j], sb.mean[j], cn, sb.col[j], pos,
-                                                                  kw, fx, vals, rec, full, ox, oy);
+                                                                  fx, vals, rec, full, ox, oy);
                 } else if ((cov >> bit) & 1u) {
-                    fwd_entry<PPT, true, STATS, MODE, true>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, kw, fx, vals,
+                    fwd_entry<PPT, true, STATS, MODE, true>(s, sc, lb, sb.mean[j], cn, sb.col[j], pos, fx, vals,
                                                             rec, full, ox, oy);
                 } else {
-                    fwd_entry<PPT, false, STATS, MODE, true>(s, sc, sb.rect[j], sb.mean[j], cn, sb.col[j], pos, kw,
+                    fwd_entry<PPT, false, STATS, MODE, true>(s, sc, sb.rect[j], sb.mean[j], cn, sb.col[j], pos,
                                                              fx, vals, rec, full, ox, oy);
                 }
             }
